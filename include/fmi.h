@@ -1,0 +1,153 @@
+/*
+ * fmi.h — C ABI of the B200-native free-mesh interpolator (arXiv 1511.01353, Challacombe,
+ * "A N-Body Solver for Free Mesh Interpolation").
+ *
+ * The library implements the data-parallel hot path of the paper's Free Mesh Transform:
+ *   fmi_build — the top-down octree residual fit, Algorithm 1 (FMT_Mesh_to_Tree,
+ *               P:294-314) with Algorithm 2 (FMT_Mesh_to_Moments) at every node;
+ *   fmi_eval  — the interpolant f(r) = Λ(r)·F_p summed over each query's root-to-deepest-node
+ *               path (§2; "only downward recursion to accumulate local polynomial
+ *               representation of the residual", §4).
+ * Citations: P:<line> = PAPER.md line; G<k> = reading k of the paper-gap ledger.
+ *
+ * Every step runs in hand-written CUDA kernels for sm_100a; there is no CPU fallback.  All
+ * arithmetic is IEEE fp64.
+ *
+ * Conventions shared by all calls
+ *   - Pointers may be host or device pointers (detected with cudaPointerGetAttributes).  Host
+ *     inputs are copied to the device inside the call; host outputs are copied back.
+ *   - The caller owns every array it passes; the library never keeps or frees them and never
+ *     writes to input arrays (the paper overwrites x and f in place; we copy).
+ *   - Work is issued on the stream set with fmi_set_stream (default: the legacy default stream)
+ *     and every call returns after that stream is synchronised.
+ *   - Errors: functions returning int return 0 on success or a negative FMI_E* code; functions
+ *     returning a pointer return NULL.  fmi_last_error() returns the code and a message of the
+ *     last failure on the calling thread.
+ *   - Not thread-safe for concurrent calls on the same tree handle; distinct handles may be used
+ *     from distinct threads if each thread sets its own stream.
+ */
+#ifndef FMI_H_
+#define FMI_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FMI_OK 0
+#define FMI_EINPUT (-1)      /* null pointer, N < 0, M < 0, non-finite coordinate or value      */
+#define FMI_EPRECOND (-2)    /* N < 𝓛 (root underdetermined), degree/max_depth/tol range */
+#define FMI_EVERSION (-3)    /* reserved (tree import)                                           */
+#define FMI_ENUMERIC (-4)    /* non-finite coefficients (unreachable with the pivot guard)       */
+#define FMI_ECUDA (-5)       /* CUDA runtime error or no CUDA device                            */
+#define FMI_ENCCL (-6)       /* reserved (multi-GPU)                                             */
+#define FMI_ENOMEM (-7)      /* device allocation failed                                         */
+
+#define FMI_MAX_DEGREE 10    /* compiled degrees p = 0..10 (𝓛 up to 286)                        */
+#define FMI_MAX_DEPTH 20     /* keys carry max_depth+1 <= 21 levels (63-bit Morton keys)           */
+
+typedef struct fmi_tree fmi_tree; /* opaque; owned by the library until fmi_free */
+
+/*
+ * fmi_build — fit the octree interpolant to N scattered samples.
+ *   pts        N×3 row-major fp64 (x0,y0,z0,x1,...), host or device.
+ *   f          N fp64 sample values, host or device.
+ *   N          number of points, N >= 𝓛 = (p+1)(p+2)(p+3)/6 (G1).
+ *   degree     total degree p of the local polynomials, 0 <= p <= FMI_MAX_DEGREE.  The basis is the
+ *              geometric moments Λ_lmn(u) = u1^l u2^m u3^n/(l!m!n!) in Algorithm-2 loop order
+ *              (P:185-189).
+ *   tol        τ >= 0: an octant block becomes a child iff E_RMS > τ and n_o >= 𝓛
+ *              and depth+1 <= max_depth (G5).  E_RMS = sqrt(Σ r²/n_o) over the post-fit residual.
+ *   max_depth  0..FMI_MAX_DEPTH, root depth 0.
+ * Root frame (G6): the cube [0,1]^3 if every point lies in it, else the isotropic bounding cube.
+ * Node fit (G9): the least-squares fit of Algorithm 2 computed from the column-equilibrated
+ * moment Gram with a column-rejection Cholesky (a column whose residual norm against the kept
+ * columns is <= 1e-6 of its own norm is dropped, coefficient 0).
+ * Returns a tree handle or NULL (see fmi_last_error).
+ */
+fmi_tree* fmi_build(const double* pts, const double* f, int64_t N, int degree, double tol, int max_depth);
+
+/*
+ * fmi_eval — evaluate the interpolant at M query points.
+ *   q    M×3 row-major fp64, host or device.
+ *   out  M fp64, host or device, caller-allocated; written in q's order.
+ * A query outside the root cube receives the root polynomial only (extrapolation).
+ * Returns 0 or a negative FMI_E* code.
+ */
+int fmi_eval(const fmi_tree* tree, const double* q, int64_t M, double* out);
+
+/* fmi_free — release the tree and its device memory.  NULL-safe. */
+void fmi_free(fmi_tree* tree);
+
+/* fmi_last_error — code of the last failure on this thread (0 if none); *msg (optional) points to a
+ * thread-local message valid until the next library call on this thread. */
+int fmi_last_error(const char** msg);
+
+/* fmi_set_stream — CUDA stream (cudaStream_t passed as void*) for subsequent calls on this thread;
+ * NULL = legacy default stream. */
+int fmi_set_stream(void* stream);
+
+/* ------------------------------------------------------------------------------------------------
+ * Introspection (parity harness and benchmark; not on the timed path).
+ * ------------------------------------------------------------------------------------------------ */
+
+typedef struct {
+  int32_t depth;          /* root = 0                                                          */
+  int32_t cell[3];        /* integer cell (i,j,k) at this depth; centre (2i+1)/2^(d+1) in the   */
+                          /* root cube's unit coordinates, half-width 1/2^(d+1)  */
+  uint64_t prefix;        /* Morton label: level digits o = bx + 2by + 4bz, most significant    */
+                          /* first (G7)                                                  */
+  int64_t n_points;       /* points of the node                                                */
+  int32_t rank;           /* kept columns (𝓛 unless truncated, G9)                             */
+  int32_t parent;         /* index in the exported order of the parent, -1 for the root       */
+  int32_t flags;          /* bit 0: fitted by the Householder-QR path (ill-conditioned node)   */
+  int32_t reserved;
+  double residual_rms;    /* sqrt(Σ r²/n) over the node's points after its own fit            */
+  double min_pivot;       /* smallest kept Cholesky pivot sqrt(s_jj) of the equilibrated Gram */
+  int64_t child_count[8]; /* n_o of each octant block                                 */
+  double child_rms[8];    /* E_RMS of each octant block; NaN if n_o == 0              */
+  int32_t child[8];       /* exported index of the child node or -1                           */
+} fmi_node;
+
+/* Number of nodes of the tree (or a negative code). */
+int64_t fmi_node_count(const fmi_tree* tree);
+
+/* Coefficient count 𝓛 of the tree (or a negative code). */
+int fmi_rank(const fmi_tree* tree);
+
+/* Export up to cap nodes in canonical (depth, prefix) order.  coeffs (may be NULL) receives
+ * cap×𝓛 doubles: P_F of each node in the Λ basis and Algorithm-2 column order.
+ * Returns the number of nodes written or a negative code. */
+int64_t fmi_export_nodes(const fmi_tree* tree, fmi_node* out, double* coeffs, int64_t cap);
+
+/* Root cube of the tree: lo[3] and edge width (G6). */
+int fmi_root_cube(const fmi_tree* tree, double* lo3, double* width);
+
+/* Final residual r_i (after the deepest fit containing point i) in INPUT order; out is N fp64,
+ * host or device.  Bookkeeping identity: interpolant(x_i) + r_i = f_i. */
+int fmi_residual(const fmi_tree* tree, double* out);
+
+/* Build statistics: levels, and per level (up to cap entries) the active node count and the
+ * number of points in active nodes (point-levels). Returns the number of levels. */
+int fmi_level_stats(const fmi_tree* tree, int64_t* nodes, int64_t* points, int cap);
+
+/* ------------------------------------------------------------------------------------------------
+ * Profiling (bench.py).  When enabled, every kernel launch of the library is bracketed by CUDA
+ * events on the library stream; fmi_profile_get returns, per kernel name, the summed device time
+ * in ms and the launch count since the last fmi_profile_reset.
+ * ------------------------------------------------------------------------------------------------ */
+int fmi_profile_enable(int on);
+int fmi_profile_reset(void);
+/* kernel names: "keys", "sort", "gather", "moments", "moments_reduce", "solve", "children",
+ * "residual", "residual_reduce", "decide", "chunks", "scan", "eval", "misc", "project",
+ * "refine_solve" */
+int fmi_profile_get(const char* kernel, double* total_ms, int64_t* launches);
+/* Total kernel launches issued by the library since load (or since fmi_profile_reset). */
+int64_t fmi_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* FMI_H_ */

@@ -1,0 +1,676 @@
+// fmi_api.cu — the C ABI (include/fmi.h) and the host orchestration of the level-synchronous build.
+//
+// fmi_build runs PAPER.md Algorithm 1 breadth-first: all nodes of one depth form a level,
+// and every step of the level runs as a device kernel over all of its nodes at once:
+//   K3 octant block bounds -> K4 moments+projection (Alg. 2 Λ / QR / Qᵀf)
+//   -> K5 node solve -> K6 residual update + block energies
+//   -> decisions + compaction of the next level.
+// The only host synchronisation per level is one 16-byte read of the next level's size.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/fmi.h"
+#include "fmi_internal.cuh"
+
+namespace fmi {
+size_t solve_scratch_per_node(int p);
+
+__global__ void k_scatter_residual(const double* __restrict__ r, const uint32_t* __restrict__ perm, int64_t n,
+                                   double* __restrict__ out) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[perm[i]] = r[i];
+}
+}  // namespace fmi
+
+using namespace fmi;
+
+// ------------------------------------------------------------------------------------------------
+// thread-local state, errors
+// ------------------------------------------------------------------------------------------------
+namespace {
+thread_local int tl_err = 0;
+thread_local std::string tl_msg;
+thread_local cudaStream_t tl_stream = 0;
+
+void set_error(int code, const std::string& msg) {
+  tl_err = code;
+  tl_msg = msg;
+}
+}  // namespace
+
+namespace fmi {
+
+[[noreturn]] void fail(int code, const std::string& msg) { throw Error{code, msg}; }
+
+void check_cuda(cudaError_t e, const char* what, const char* file, int line) {
+  if (e == cudaSuccess) return;
+  std::string m = std::string(cudaGetErrorString(e)) + " in " + what + " (" + file + ":" + std::to_string(line) + ")";
+  if (e == cudaErrorMemoryAllocation) {
+    cudaGetLastError();
+    fail(FMI_ENOMEM, m);
+  }
+  fail(FMI_ECUDA, m);
+}
+
+// ------------------------------------------------------------------------------------------------
+// memory: stream-ordered pool allocations; the pool keeps freed memory for reuse across calls
+// ------------------------------------------------------------------------------------------------
+namespace {
+std::once_flag g_pool_once;
+}
+
+void* dmalloc(size_t bytes, cudaStream_t s) {
+  std::call_once(g_pool_once, [] {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t thr = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    cudaGetLastError();
+  });
+  void* p = nullptr;
+  cudaError_t e = cudaMallocAsync(&p, bytes, s);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    fail(FMI_ENOMEM, "device allocation of " + std::to_string(bytes) + " bytes failed: " + cudaGetErrorString(e));
+  }
+  return p;
+}
+
+void dfree(void* p, cudaStream_t s) {
+  if (p) cudaFreeAsync(p, s);
+}
+
+// ------------------------------------------------------------------------------------------------
+// launch counting and profiling
+// ------------------------------------------------------------------------------------------------
+namespace {
+std::atomic<int64_t> g_launches{0};
+std::atomic<bool> g_prof{false};
+std::mutex g_prof_mu;
+struct Pending {
+  int kid;
+  cudaEvent_t a, b;
+};
+std::vector<Pending> g_pending;
+std::vector<cudaEvent_t> g_event_pool;
+double g_prof_ms[KID_COUNT];
+int64_t g_prof_n[KID_COUNT];
+thread_local cudaEvent_t tl_open = nullptr;
+
+cudaEvent_t get_event() {
+  if (!g_event_pool.empty()) {
+    cudaEvent_t e = g_event_pool.back();
+    g_event_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  FMI_CK(cudaEventCreate(&e));
+  return e;
+}
+const char* kNames[KID_COUNT] = {"keys",     "sort",     "gather", "moments", "moments_reduce",
+                                 "solve",    "children", "residual", "residual_reduce",
+                                 "decide",   "chunks",   "scan",   "eval",    "misc",
+                                 "project",  "refine_solve"};
+}  // namespace
+
+const char* kernel_name(int kid) { return (kid >= 0 && kid < KID_COUNT) ? kNames[kid] : "?"; }
+
+void prof_begin(int kid, cudaStream_t s) {
+  (void)kid;
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  if (!g_prof.load(std::memory_order_relaxed)) return;
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  tl_open = get_event();
+  FMI_CK(cudaEventRecord(tl_open, s));
+}
+
+void prof_end(int kid, cudaStream_t s) {
+  if (!g_prof.load(std::memory_order_relaxed) || !tl_open) return;
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  cudaEvent_t b = get_event();
+  FMI_CK(cudaEventRecord(b, s));
+  g_pending.push_back({kid, tl_open, b});
+  tl_open = nullptr;
+}
+
+void prof_collect() {
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  for (auto& p : g_pending) {
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, p.a, p.b) == cudaSuccess) {
+      g_prof_ms[p.kid] += ms;
+      g_prof_n[p.kid] += 1;
+    }
+    cudaGetLastError();
+    g_event_pool.push_back(p.a);
+    g_event_pool.push_back(p.b);
+  }
+  g_pending.clear();
+}
+
+}  // namespace fmi
+
+// ------------------------------------------------------------------------------------------------
+// the tree
+// ------------------------------------------------------------------------------------------------
+struct fmi_tree {
+  int p = 0, L = 0, K = 0, D = 0, Dk = 0, depth_max = 0;
+  int refine = 2;  // max semi-normal refinement steps per level (env FMI_REFINE); adaptive per node
+  double tau = 0;
+  double lo[3] = {0, 0, 0};
+  double width = 1;
+  bool unit = true;
+  int64_t N = 0;
+  int64_t nodes = 0;
+  int64_t cap = 0;
+  NodeTable nt;
+  std::vector<int64_t> lvl_first, lvl_count, lvl_points;
+  double* residual = nullptr;  // Morton order
+  uint32_t* perm = nullptr;    // Morton position -> input index
+  cudaStream_t stream = 0;
+};
+
+namespace {
+
+void free_table(NodeTable& t, cudaStream_t s) {
+  dfree(t.start, s); dfree(t.end, s); dfree(t.cell, s); dfree(t.parent, s); dfree(t.child, s);
+  dfree(t.child_start, s); dfree(t.child_ss, s); dfree(t.coef, s); dfree(t.rms, s); dfree(t.minpiv, s);
+  dfree(t.rank, s); dfree(t.flag, s);
+  t = NodeTable{};
+}
+
+template <typename T>
+void grow_array(T*& p, int64_t old_n, int64_t new_n, cudaStream_t s) {
+  T* q = static_cast<T*>(dmalloc((size_t)new_n * sizeof(T), s));
+  if (p && old_n > 0) FMI_CK(cudaMemcpyAsync(q, p, (size_t)old_n * sizeof(T), cudaMemcpyDeviceToDevice, s));
+  dfree(p, s);
+  p = q;
+}
+
+void ensure_capacity(fmi_tree* T, int64_t need, cudaStream_t s) {
+  if (need <= T->cap) return;
+  int64_t nc = std::max<int64_t>(need, std::max<int64_t>(1024, T->cap * 2));
+  const int64_t keep = T->cap;  // copy every existing slot (children of the current level included)
+  NodeTable& t = T->nt;
+  grow_array(t.start, keep, nc, s);
+  grow_array(t.end, keep, nc, s);
+  grow_array(t.cell, keep, nc, s);
+  grow_array(t.parent, keep, nc, s);
+  grow_array(t.child, keep * 8, nc * 8, s);
+  grow_array(t.child_start, keep * 9, nc * 9, s);
+  grow_array(t.child_ss, keep * 8, nc * 8, s);
+  grow_array(t.coef, keep * T->L, nc * T->L, s);
+  grow_array(t.rms, keep, nc, s);
+  grow_array(t.minpiv, keep, nc, s);
+  grow_array(t.rank, keep, nc, s);
+  grow_array(t.flag, keep, nc, s);
+  T->cap = nc;
+}
+
+bool is_device_ptr(const void* p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+int64_t choose_chunk(int64_t points, int64_t min_ch, int64_t per_sm_chunks) {
+  int64_t target = (points + 148 * per_sm_chunks - 1) / (148 * per_sm_chunks);
+  return std::max(min_ch, target);
+}
+
+template <int P>
+void run_levels(fmi_tree* T, const uint64_t* keys, double* ux, double* uy, double* uz, double* r, cudaStream_t s) {
+  constexpr int L = rank3(P), K = rank3(2 * P);
+  // root node
+  ensure_capacity(T, 16, s);
+  {
+    int64_t st = 0, en = T->N;
+    int4 c = make_int4(0, 0, 0, 0);
+    int32_t par = -1;
+    std::vector<int32_t> ch(8, -1);
+    FMI_CK(cudaMemcpyAsync(T->nt.start, &st, sizeof st, cudaMemcpyHostToDevice, s));
+    FMI_CK(cudaMemcpyAsync(T->nt.end, &en, sizeof en, cudaMemcpyHostToDevice, s));
+    FMI_CK(cudaMemcpyAsync(T->nt.cell, &c, sizeof c, cudaMemcpyHostToDevice, s));
+    FMI_CK(cudaMemcpyAsync(T->nt.parent, &par, sizeof par, cudaMemcpyHostToDevice, s));
+    FMI_CK(cudaMemcpyAsync(T->nt.child, ch.data(), 8 * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+    FMI_CK(cudaStreamSynchronize(s));  // host staging values above live on this frame
+  }
+  T->nodes = 1;
+  int64_t first = 0, count = 1, points = T->N;
+  DBuf<int64_t> counts, begin4, begin6, flags, scan, dev_small(4, s);
+  DBuf<Chunk> chunks4, chunks6;
+  DBuf<double> partial, mom, segpart, scratch, proj, delta;
+  DBuf<uint8_t> skip;
+  int64_t* host_small = nullptr;
+  FMI_CK(cudaMallocHost(&host_small, 4 * sizeof(int64_t)));
+  const size_t scr_per_node = solve_scratch_per_node(P);
+  const int64_t scr_nodes = scr_per_node ? 2048 : 0;
+  if (scr_nodes) scratch.alloc((size_t)scr_nodes * scr_per_node / sizeof(double), s);
+  const int64_t qr_slots = 148;
+  DBuf<double> qr_scratch((size_t)qr_slots * solve_qr_scratch_per_cta(P) / sizeof(double), s);
+  try {
+    for (int depth = 0; count > 0; ++depth) {
+      T->lvl_first.push_back(first);
+      T->lvl_count.push_back(count);
+      T->lvl_points.push_back(points);
+      T->depth_max = depth;
+      ensure_capacity(T, first + count + 8 * count, s);
+      LevelCtx c{keys, ux, uy, uz, r, T->nt, first, count, depth, T->D, T->Dk, P, L, K, T->tau};
+      level_children(c, s);
+      // K4 chunk list over the level's nodes
+      const int64_t ch4 = choose_chunk(points, 256, 4);
+      const int64_t max4 = points / ch4 + count + 1;
+      counts.ensure(std::max<int64_t>(count * 8, 1), s);
+      begin4.ensure(count, s);
+      chunks4.ensure(max4, s);
+      make_chunks(T->nt.start + first, T->nt.end + first, count, ch4, counts.p, begin4.p, dev_small.p, chunks4.p,
+                  max4, s);
+      partial.ensure((size_t)max4 * (K + L), s);
+      mom.ensure((size_t)count * (K + L), s);
+      level_moments<P>(c, chunks4.p, dev_small.p, max4, begin4.p, partial.p, mom.p, s);
+      level_solve<P>(c, mom.p, nullptr, nullptr, nullptr, scratch.p, scr_nodes, s);
+      level_solve_qr<P>(c, mom.p, qr_scratch.p, qr_slots, s);
+      // K6 chunk list over the level's octant segments
+      const int64_t ch6 = choose_chunk(points, 1024, 8);
+      const int64_t max6 = points / ch6 + 8 * count + 1;
+      begin6.ensure(count * 8, s);
+      chunks6.ensure(max6, s);
+      make_chunks(T->nt.child_start + first * 9, nullptr, count * 8, ch6, counts.p, begin6.p, dev_small.p + 1,
+                  chunks6.p, max6, s);
+      segpart.ensure(max6, s);
+      level_residual<P>(c, T->nt.coef + first * L, nullptr, chunks6.p, dev_small.p + 1, max6, begin6.p, segpart.p, s);
+      // semi-normal iterative refinement (DESIGN.md §3 K5r): b1 = Λᵀ r1, G δ = b1 with the same
+      // factorization, r2 = r1 - Λ δ.  Restores QR-level accuracy where the Gram squares κ.
+      for (int it = 0; it < T->refine; ++it) {
+        proj.ensure((size_t)count * L, s);
+        delta.ensure((size_t)count * L, s);
+        skip.ensure((size_t)count, s);
+        level_project<P>(c, chunks4.p, dev_small.p, max4, begin4.p, partial.p, proj.p, s);
+        level_solve<P>(c, mom.p, proj.p, delta.p, skip.p, scratch.p, scr_nodes, s);
+        level_residual<P>(c, delta.p, skip.p, chunks6.p, dev_small.p + 1, max6, begin6.p, segpart.p, s);
+      }
+      flags.ensure(count * 8, s);
+      scan.ensure(count * 8, s);
+      level_decide(c, flags.p, scan.p, dev_small.p + 2, s);
+      FMI_CK(cudaMemcpyAsync(host_small, dev_small.p + 2, 2 * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+      FMI_CK(cudaStreamSynchronize(s));
+      const int64_t nnew = host_small[0], npts = host_small[1];
+      first += count;
+      T->nodes = first + nnew;
+      count = nnew;
+      points = npts;
+    }
+  } catch (...) {
+    cudaFreeHost(host_small);
+    throw;
+  }
+  cudaFreeHost(host_small);
+}
+
+template <int P>
+void run_eval(const fmi_tree* T, const double* q, const uint64_t* keys, const uint32_t* idx, int64_t M, int Dk,
+              double* out, cudaStream_t s) {
+  eval_sorted<P>(q, keys, idx, M, T->lo, T->width, T->unit, Dk, T->nt, out, s);
+}
+
+#define FMI_DISPATCH(p, FN, ...)                      \
+  switch (p) {                                        \
+    case 0: FN<0>(__VA_ARGS__); break;                \
+    case 1: FN<1>(__VA_ARGS__); break;                \
+    case 2: FN<2>(__VA_ARGS__); break;                \
+    case 3: FN<3>(__VA_ARGS__); break;                \
+    case 4: FN<4>(__VA_ARGS__); break;                \
+    case 5: FN<5>(__VA_ARGS__); break;                \
+    case 6: FN<6>(__VA_ARGS__); break;                \
+    case 7: FN<7>(__VA_ARGS__); break;                \
+    case 8: FN<8>(__VA_ARGS__); break;                \
+    case 9: FN<9>(__VA_ARGS__); break;                \
+    case 10: FN<10>(__VA_ARGS__); break;              \
+    default: fail(FMI_EPRECOND, "degree out of range"); \
+  }
+
+void require_device() {
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess || n == 0) {
+    cudaGetLastError();
+    fail(FMI_ECUDA, std::string("no CUDA device available: ") + cudaGetErrorString(e));
+  }
+}
+
+fmi_tree* build_impl(const double* pts, const double* f, int64_t N, int degree, double tol, int max_depth) {
+  if (!pts || !f) fail(FMI_EINPUT, "null pointer argument");
+  if (N < 0) fail(FMI_EINPUT, "N < 0");
+  if (degree < 0 || degree > FMI_MAX_DEGREE) fail(FMI_EPRECOND, "degree outside 0..10");
+  if (max_depth < 0 || max_depth > FMI_MAX_DEPTH) fail(FMI_EPRECOND, "max_depth outside 0..20");
+  if (!(tol >= 0.0)) fail(FMI_EPRECOND, "tol must be >= 0 (and not NaN)");
+  const int L = rank3(degree);
+  if (N < L) fail(FMI_EPRECOND, "N < rank: the root fit is underdetermined (S:348)");
+  if (N > (int64_t)UINT32_MAX) fail(FMI_EPRECOND, "N exceeds 2^32 - 1");
+  require_device();
+  cudaStream_t s = tl_stream;
+
+  // inputs on the device
+  DBuf<double> dpts_own, df_own;
+  const double* dpts = pts;
+  const double* df = f;
+  if (!is_device_ptr(pts)) {
+    dpts_own.alloc((size_t)N * 3, s);
+    FMI_CK(cudaMemcpyAsync(dpts_own.p, pts, (size_t)N * 3 * sizeof(double), cudaMemcpyHostToDevice, s));
+    dpts = dpts_own.p;
+  }
+  if (!is_device_ptr(f)) {
+    df_own.alloc((size_t)N, s);
+    FMI_CK(cudaMemcpyAsync(df_own.p, f, (size_t)N * sizeof(double), cudaMemcpyHostToDevice, s));
+    df = df_own.p;
+  }
+
+  // root frame (G6) + finiteness
+  DBuf<double> bb(8, s);
+  bbox_and_check(dpts, N, bb.p, df, s);
+  double hb[8];
+  FMI_CK(cudaMemcpyAsync(hb, bb.p, sizeof hb, cudaMemcpyDeviceToHost, s));
+  FMI_CK(cudaStreamSynchronize(s));
+  if (hb[6] != 0.0) fail(FMI_EINPUT, "non-finite coordinate or value");
+
+  fmi_tree* T = new fmi_tree();
+  try {
+    T->p = degree;
+    T->L = L;
+    T->K = rank3(2 * degree);
+    T->D = max_depth;
+    T->Dk = max_depth + 1;
+    T->tau = tol;
+    T->N = N;
+    T->stream = s;
+    if (const char* e = std::getenv("FMI_REFINE")) T->refine = std::max(0, std::atoi(e));
+    bool unit = hb[0] >= 0.0 && hb[1] >= 0.0 && hb[2] >= 0.0 && hb[3] <= 1.0 && hb[4] <= 1.0 && hb[5] <= 1.0;
+    if (unit) {
+      T->unit = true;
+      T->lo[0] = T->lo[1] = T->lo[2] = 0.0;
+      T->width = 1.0;
+    } else {
+      T->unit = false;
+      for (int a = 0; a < 3; ++a) T->lo[a] = hb[a];
+      double w = std::max(hb[3] - hb[0], std::max(hb[4] - hb[1], hb[5] - hb[2]));
+      T->width = w > 0.0 ? w : 1.0;
+    }
+    // K1 keys + K2 sort + gather
+    DBuf<uint64_t> keys(N, s), ktmp(N, s);
+    DBuf<uint32_t> perm(N, s), ptmp(N, s);
+    morton_keys(dpts, N, T->lo, T->width, T->unit, T->Dk, keys.p, perm.p, s);
+    radix_sort_pairs(keys.p, perm.p, ktmp.p, ptmp.p, N, 3 * T->Dk, s);
+    ktmp.release();
+    ptmp.release();
+    DBuf<double> ux(N, s), uy(N, s), uz(N, s), r(N, s);
+    gather_points(dpts, df, perm.p, N, T->lo, T->width, T->unit, ux.p, uy.p, uz.p, r.p, s);
+    dpts_own.release();
+    df_own.release();
+    FMI_DISPATCH(degree, run_levels, T, keys.p, ux.p, uy.p, uz.p, r.p, s);
+    T->residual = r.p;
+    r.p = nullptr;
+    T->perm = perm.p;
+    perm.p = nullptr;
+    FMI_CK(cudaStreamSynchronize(s));
+  } catch (...) {
+    free_table(T->nt, s);
+    dfree(T->residual, s);
+    dfree(T->perm, s);
+    delete T;
+    throw;
+  }
+  prof_collect();
+  return T;
+}
+
+int eval_impl(const fmi_tree* T, const double* q, int64_t M, double* out) {
+  if (!T) fail(FMI_EINPUT, "null tree");
+  if (M < 0) fail(FMI_EINPUT, "M < 0");
+  if (M == 0) return 0;
+  if (!q || !out) fail(FMI_EINPUT, "null pointer argument");
+  if (M > (int64_t)UINT32_MAX) fail(FMI_EPRECOND, "M exceeds 2^32 - 1");
+  cudaStream_t s = tl_stream;
+  DBuf<double> dq_own, dout_own;
+  const double* dq = q;
+  double* dout = out;
+  const bool host_out = !is_device_ptr(out);
+  if (!is_device_ptr(q)) {
+    dq_own.alloc((size_t)M * 3, s);
+    FMI_CK(cudaMemcpyAsync(dq_own.p, q, (size_t)M * 3 * sizeof(double), cudaMemcpyHostToDevice, s));
+    dq = dq_own.p;
+  }
+  if (host_out) {
+    dout_own.alloc((size_t)M, s);
+    dout = dout_own.p;
+  }
+  const int Dk = T->depth_max;
+  if (Dk == 0) {
+    FMI_DISPATCH(T->p, run_eval, T, dq, nullptr, nullptr, M, 0, dout, s);
+  } else {
+    DBuf<uint64_t> keys(M, s), ktmp(M, s);
+    DBuf<uint32_t> idx(M, s), itmp(M, s);
+    morton_keys(dq, M, T->lo, T->width, T->unit, Dk, keys.p, idx.p, s);
+    radix_sort_pairs(keys.p, idx.p, ktmp.p, itmp.p, M, 3 * Dk, s);
+    FMI_DISPATCH(T->p, run_eval, T, dq, keys.p, idx.p, M, Dk, dout, s);
+  }
+  if (host_out) FMI_CK(cudaMemcpyAsync(out, dout, (size_t)M * sizeof(double), cudaMemcpyDeviceToHost, s));
+  FMI_CK(cudaStreamSynchronize(s));
+  prof_collect();
+  return 0;
+}
+
+uint64_t morton_label(int depth, int i, int j, int k) {
+  uint64_t out = 0;
+  for (int t = 0; t < depth; ++t) {
+    int b = depth - 1 - t;
+    uint64_t o = ((i >> b) & 1) | (((j >> b) & 1) << 1) | (((k >> b) & 1) << 2);
+    out = (out << 3) | o;
+  }
+  return out;
+}
+
+template <typename F>
+int guard(F&& fn) {
+  try {
+    tl_err = 0;
+    return fn();
+  } catch (const Error& e) {
+    set_error(e.code, e.msg);
+    return e.code;
+  } catch (const std::exception& e) {
+    set_error(FMI_ECUDA, e.what());
+    return FMI_ECUDA;
+  }
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------------------------------------
+// C ABI
+// ------------------------------------------------------------------------------------------------
+extern "C" {
+
+fmi_tree* fmi_build(const double* pts, const double* f, int64_t N, int degree, double tol, int max_depth) {
+  fmi_tree* out = nullptr;
+  guard([&] {
+    out = build_impl(pts, f, N, degree, tol, max_depth);
+    return 0;
+  });
+  return out;
+}
+
+int fmi_eval(const fmi_tree* tree, const double* q, int64_t M, double* out) {
+  return guard([&] { return eval_impl(tree, q, M, out); });
+}
+
+void fmi_free(fmi_tree* T) {
+  if (!T) return;
+  cudaStream_t s = tl_stream;
+  free_table(T->nt, s);
+  dfree(T->residual, s);
+  dfree(T->perm, s);
+  cudaStreamSynchronize(s);
+  cudaGetLastError();
+  delete T;
+}
+
+int fmi_last_error(const char** msg) {
+  if (msg) *msg = tl_msg.c_str();
+  return tl_err;
+}
+
+int fmi_set_stream(void* stream) {
+  tl_stream = static_cast<cudaStream_t>(stream);
+  return 0;
+}
+
+int64_t fmi_node_count(const fmi_tree* T) {
+  if (!T) { set_error(FMI_EINPUT, "null tree"); return FMI_EINPUT; }
+  return T->nodes;
+}
+
+int fmi_rank(const fmi_tree* T) {
+  if (!T) { set_error(FMI_EINPUT, "null tree"); return FMI_EINPUT; }
+  return T->L;
+}
+
+int64_t fmi_export_nodes(const fmi_tree* T, fmi_node* out, double* coeffs, int64_t cap) {
+  int64_t written = 0;
+  int rc = guard([&] {
+    if (!T || !out) fail(FMI_EINPUT, "null argument");
+    const int64_t n = std::min<int64_t>(cap, T->nodes);
+    if (n <= 0) return 0;
+    const int L = T->L;
+    const int64_t nn = T->nodes;
+    std::vector<int64_t> st(nn), en(nn), cs(nn * 9);
+    std::vector<int4> cell(nn);
+    std::vector<int32_t> par(nn), child(nn * 8), rank(nn), flag(nn);
+    std::vector<double> ss(nn * 8), rms(nn), mp(nn), coef((size_t)nn * L);
+    cudaStream_t s = tl_stream;
+    FMI_CK(cudaMemcpyAsync(st.data(), T->nt.start, nn * 8, cudaMemcpyDeviceToHost, s));
+    FMI_CK(cudaMemcpyAsync(en.data(), T->nt.end, nn * 8, cudaMemcpyDeviceToHost, s));
+    FMI_CK(cudaMemcpyAsync(cs.data(), T->nt.child_start, nn * 9 * 8, cudaMemcpyDeviceToHost, s));
+    FMI_CK(cudaMemcpyAsync(cell.data(), T->nt.cell, nn * sizeof(int4), cudaMemcpyDeviceToHost, s));
+    FMI_CK(cudaMemcpyAsync(par.data(), T->nt.parent, nn * 4, cudaMemcpyDeviceToHost, s));
+    FMI_CK(cudaMemcpyAsync(child.data(), T->nt.child, nn * 8 * 4, cudaMemcpyDeviceToHost, s));
+    FMI_CK(cudaMemcpyAsync(rank.data(), T->nt.rank, nn * 4, cudaMemcpyDeviceToHost, s));
+    FMI_CK(cudaMemcpyAsync(flag.data(), T->nt.flag, nn * 4, cudaMemcpyDeviceToHost, s));
+    FMI_CK(cudaMemcpyAsync(ss.data(), T->nt.child_ss, nn * 8 * 8, cudaMemcpyDeviceToHost, s));
+    FMI_CK(cudaMemcpyAsync(rms.data(), T->nt.rms, nn * 8, cudaMemcpyDeviceToHost, s));
+    FMI_CK(cudaMemcpyAsync(mp.data(), T->nt.minpiv, nn * 8, cudaMemcpyDeviceToHost, s));
+    FMI_CK(cudaMemcpyAsync(coef.data(), T->nt.coef, (size_t)nn * L * 8, cudaMemcpyDeviceToHost, s));
+    FMI_CK(cudaStreamSynchronize(s));
+    // factorials of the basis (P_F = a_lmn · l! m! n!)
+    std::vector<double> fac(L);
+    {
+      double f1[32];
+      f1[0] = 1.0;
+      for (int i = 1; i < 32; ++i) f1[i] = f1[i - 1] * i;
+      int i = 0;
+      for (int l = 0; l <= T->p; ++l)
+        for (int m = 0; m <= T->p - l; ++m)
+          for (int k = 0; k <= T->p - l - m; ++k) fac[i++] = f1[l] * f1[m] * f1[k];
+    }
+    for (int64_t i = 0; i < n; ++i) {
+      fmi_node& o = out[i];
+      std::memset(&o, 0, sizeof o);
+      o.depth = cell[i].w;
+      o.cell[0] = cell[i].x; o.cell[1] = cell[i].y; o.cell[2] = cell[i].z;
+      o.prefix = morton_label(cell[i].w, cell[i].x, cell[i].y, cell[i].z);
+      o.n_points = en[i] - st[i];
+      o.rank = rank[i];
+      o.parent = par[i];
+      o.flags = flag[i];
+      o.residual_rms = rms[i];
+      o.min_pivot = mp[i];
+      for (int k = 0; k < 8; ++k) {
+        const int64_t no = cs[i * 9 + k + 1] - cs[i * 9 + k];
+        o.child_count[k] = no;
+        o.child_rms[k] = no > 0 ? std::sqrt(ss[i * 8 + k] / (double)no) : NAN;
+        o.child[k] = child[i * 8 + k];
+      }
+      if (coeffs)
+        for (int j = 0; j < L; ++j) coeffs[i * L + j] = coef[(size_t)i * L + j] * fac[j];
+    }
+    written = n;
+    return 0;
+  });
+  return rc ? rc : written;
+}
+
+int fmi_root_cube(const fmi_tree* T, double* lo3, double* width) {
+  if (!T || !lo3 || !width) { set_error(FMI_EINPUT, "null argument"); return FMI_EINPUT; }
+  for (int a = 0; a < 3; ++a) lo3[a] = T->lo[a];
+  *width = T->width;
+  return 0;
+}
+
+int fmi_residual(const fmi_tree* T, double* out) {
+  return guard([&] {
+    if (!T || !out) fail(FMI_EINPUT, "null argument");
+    cudaStream_t s = tl_stream;
+    DBuf<double> tmp;
+    double* d = out;
+    const bool host = !is_device_ptr(out);
+    if (host) { tmp.alloc(T->N, s); d = tmp.p; }
+    FMI_LAUNCH(KID_MISC, s, k_scatter_residual, (unsigned)((T->N + 255) / 256), 256, 0, T->residual, T->perm, T->N, d);
+    if (host) FMI_CK(cudaMemcpyAsync(out, d, T->N * sizeof(double), cudaMemcpyDeviceToHost, s));
+    FMI_CK(cudaStreamSynchronize(s));
+    return 0;
+  });
+}
+
+int fmi_level_stats(const fmi_tree* T, int64_t* nodes, int64_t* points, int cap) {
+  if (!T) { set_error(FMI_EINPUT, "null tree"); return FMI_EINPUT; }
+  int n = (int)T->lvl_count.size();
+  for (int i = 0; i < std::min(n, cap); ++i) {
+    if (nodes) nodes[i] = T->lvl_count[i];
+    if (points) points[i] = T->lvl_points[i];
+  }
+  return n;
+}
+
+int fmi_profile_enable(int on) {
+  g_prof.store(on != 0);
+  return 0;
+}
+
+int fmi_profile_reset(void) {
+  prof_collect();
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  for (int k = 0; k < KID_COUNT; ++k) { g_prof_ms[k] = 0.0; g_prof_n[k] = 0; }
+  g_launches.store(0);
+  return 0;
+}
+
+int fmi_profile_get(const char* kernel, double* total_ms, int64_t* launches) {
+  prof_collect();
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  for (int k = 0; k < KID_COUNT; ++k) {
+    if (kernel && std::strcmp(kernel, kNames[k]) == 0) {
+      if (total_ms) *total_ms = g_prof_ms[k];
+      if (launches) *launches = g_prof_n[k];
+      return 0;
+    }
+  }
+  set_error(FMI_EINPUT, "unknown kernel name");
+  return FMI_EINPUT;
+}
+
+int64_t fmi_launch_count(void) { return g_launches.load(); }
+
+}  // extern "C"

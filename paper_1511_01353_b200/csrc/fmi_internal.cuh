@@ -1,0 +1,194 @@
+// fmi_internal.cuh — internal declarations of the B200 free-mesh interpolator (not part of the ABI).
+//
+// Data layout in HBM:
+//   points, Morton order, SoA fp64: ux[N], uy[N], uz[N] (root-cube unit coordinates), r[N] (residual)
+//   keys[N] uint64 Morton keys (3·D bits), perm[N] uint32 (Morton position -> input index)
+//   node table (all levels, level-contiguous): NodeTable below
+//   per-level scratch: chunk lists, moment partials [chunks][K+𝓛], node moments [nodes][K+𝓛]
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+namespace fmi {
+
+constexpr int kMaxDegree = 10;
+constexpr int kMaxDepth = 20;  // keys carry max_depth + 1 <= 21 levels (63 bits)
+// Column-rejection threshold of the node solve (reading G9): a column whose Schur
+// complement diagonal of the equilibrated Gram is <= kDelta^2 is dropped.
+constexpr double kDelta = 1e-6;
+
+// ---------------------------------------------------------------------------------------------
+// multi-index arithmetic (Algorithm-2 loop order: l outer, m middle, n inner)
+// ---------------------------------------------------------------------------------------------
+__host__ __device__ constexpr int rank3(int k) { return k < 0 ? 0 : (k + 1) * (k + 2) * (k + 3) / 6; }
+// position of (l, m, n), l+m+n <= Q, in the Algorithm-2 order of total degree Q
+__host__ __device__ constexpr int basis_index(int Q, int l, int m, int n) {
+  return rank3(Q) - rank3(Q - l) + m * (Q - l + 1) - m * (m - 1) / 2 + n;
+}
+
+// ---------------------------------------------------------------------------------------------
+// error handling (C++ exceptions internally, converted to codes at the C ABI)
+// ---------------------------------------------------------------------------------------------
+struct Error {
+  int code;
+  std::string msg;
+};
+[[noreturn]] void fail(int code, const std::string& msg);
+void check_cuda(cudaError_t e, const char* what, const char* file, int line);
+#define FMI_CK(x) ::fmi::check_cuda((x), #x, __FILE__, __LINE__)
+
+// ---------------------------------------------------------------------------------------------
+// launch bookkeeping and optional per-kernel event timing (fmi_profile_*)
+// ---------------------------------------------------------------------------------------------
+enum KernelId {
+  KID_KEYS = 0, KID_SORT, KID_GATHER, KID_MOMENTS, KID_MOMENTS_REDUCE, KID_SOLVE, KID_CHILDREN,
+  KID_RESIDUAL, KID_RESIDUAL_REDUCE, KID_DECIDE, KID_CHUNKS, KID_SCAN, KID_EVAL, KID_MISC, KID_PROJECT,
+  KID_REFINE_SOLVE, KID_COUNT
+};
+const char* kernel_name(int kid);
+void prof_begin(int kid, cudaStream_t s);
+void prof_end(int kid, cudaStream_t s);
+void prof_collect();  // after a stream sync: accumulate elapsed times of completed launches
+
+#define FMI_LAUNCH(kid, stream, kernel, grid, block, smem, ...)                          \
+  do {                                                                                   \
+    ::fmi::prof_begin((kid), (stream));                                                  \
+    kernel<<<(grid), (block), (smem), (stream)>>>(__VA_ARGS__);                          \
+    FMI_CK(cudaGetLastError());                                                          \
+    ::fmi::prof_end((kid), (stream));                                                    \
+  } while (0)
+
+// ---------------------------------------------------------------------------------------------
+// stream-ordered device buffers
+// ---------------------------------------------------------------------------------------------
+void* dmalloc(size_t bytes, cudaStream_t s);
+void dfree(void* p, cudaStream_t s);
+
+template <typename T>
+struct DBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  cudaStream_t s = 0;
+  DBuf() = default;
+  DBuf(size_t count, cudaStream_t st) { alloc(count, st); }
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  DBuf(DBuf&& o) noexcept : p(o.p), n(o.n), s(o.s) { o.p = nullptr; o.n = 0; }
+  DBuf& operator=(DBuf&& o) noexcept {
+    if (this != &o) { release(); p = o.p; n = o.n; s = o.s; o.p = nullptr; o.n = 0; }
+    return *this;
+  }
+  void alloc(size_t count, cudaStream_t st) {
+    release();
+    s = st;
+    n = count;
+    p = count ? static_cast<T*>(dmalloc(count * sizeof(T), st)) : nullptr;
+  }
+  void ensure(size_t count, cudaStream_t st) { if (count > n) alloc(count, st); }
+  void release() { if (p) dfree(p, s); p = nullptr; n = 0; }
+  ~DBuf() { release(); }
+};
+
+// ---------------------------------------------------------------------------------------------
+// shared structures
+// ---------------------------------------------------------------------------------------------
+struct Chunk {
+  int32_t owner;   // node (level-local) or segment (node*8 + octant) index
+  int32_t pad;
+  int64_t start;   // [start, end) in Morton order
+  int64_t end;
+};
+
+// node table (all levels; nodes of one level are contiguous, in canonical (depth, prefix) order)
+struct NodeTable {
+  int64_t* start = nullptr;      // [cap]
+  int64_t* end = nullptr;        // [cap]
+  int4* cell = nullptr;          // [cap] (i, j, k, depth)
+  int32_t* parent = nullptr;     // [cap]
+  int32_t* child = nullptr;      // [cap*8]
+  int64_t* child_start = nullptr;// [cap*9] octant block bounds (G2)
+  double* child_ss = nullptr;    // [cap*8] Σ r² of each octant block after the node's fit
+  double* coef = nullptr;        // [cap*L] monomial-form coefficients a_lmn = P_F,lmn / (l!m!n!)
+  double* rms = nullptr;         // [cap]
+  double* minpiv = nullptr;      // [cap]
+  int32_t* rank = nullptr;       // [cap]
+  int32_t* flag = nullptr;       // [cap] bit0: re-fitted by the QR path (K5q); bit1: refinement converged
+};
+
+// ---------------------------------------------------------------------------------------------
+// kernels / launchers (defined in the .cu files)
+// ---------------------------------------------------------------------------------------------
+// scan.cu: exclusive prefix sum of int64 (in place allowed); returns nothing, total via `total` (device)
+void exclusive_scan_i64(const int64_t* in, int64_t* out, int64_t n, int64_t* total, cudaStream_t s);
+
+// keys.cu
+void bbox_and_check(const double* pts, int64_t n, double* out8 /*device: min3,max3,nonfinite,unused*/,
+                    const double* f, cudaStream_t s);
+void morton_keys(const double* pts, int64_t n, const double lo[3], double width, bool unit, int D,
+                 uint64_t* keys, uint32_t* idx, cudaStream_t s);
+void radix_sort_pairs(uint64_t* keys, uint32_t* vals, uint64_t* keys_tmp, uint32_t* vals_tmp, int64_t n,
+                      int nbits, cudaStream_t s);
+void gather_points(const double* pts, const double* f, const uint32_t* perm, int64_t n, const double lo[3],
+                   double width, bool unit, double* ux, double* uy, double* uz, double* r, cudaStream_t s);
+
+// chunks.cu (level bookkeeping)
+// Build a chunk list over `nr` ranges [rstart[i], rend[i]) with at most `ch` points per chunk.
+// chunk_begin[i] (exclusive scan of per-range chunk counts) and *nchunks (device) are written.
+void make_chunks(const int64_t* rstart, const int64_t* rend, int64_t nr, int64_t ch, int64_t* counts_tmp,
+                 int64_t* chunk_begin, int64_t* nchunks_dev, Chunk* chunks, int64_t max_chunks, cudaStream_t s);
+
+// level ops (level.cu)
+struct LevelCtx {
+  const uint64_t* keys;
+  const double* ux; const double* uy; const double* uz;
+  double* r;
+  NodeTable nt;
+  int64_t first;      // global index of the level's first node
+  int64_t count;      // active nodes at this level
+  int depth;          // depth of the level
+  int D;              // max_depth (depth guard, G5)
+  int Dk;             // key depth (bits per axis of the Morton keys) = max_depth + 1
+  int p, L, K;
+  double tau;
+};
+void level_children(const LevelCtx& c, cudaStream_t s);  // child_start for the level's nodes
+template <int P> void level_moments(const LevelCtx& c, const Chunk* chunks, const int64_t* nchunks_dev,
+                                    int64_t max_chunks, const int64_t* chunk_begin, double* partial,
+                                    double* mom, cudaStream_t s);
+// projection-only pass b_α = Σ u^α r (refinement), proj[node][𝓛]
+template <int P> void level_project(const LevelCtx& c, const Chunk* chunks, const int64_t* nchunks_dev,
+                                    int64_t max_chunks, const int64_t* chunk_begin, double* partial, double* proj,
+                                    cudaStream_t s);
+// rhs == nullptr: initial solve (rhs from mom, writes coef).  rhs != nullptr: refinement solve with the
+// same factorization; writes the correction to delta[node][𝓛] and adds it to coef (QR-path nodes: 0).
+// skip[node] (refinement only) = 1 when the node takes no correction this step.
+template <int P> void level_solve(const LevelCtx& c, const double* mom, const double* rhs, double* delta,
+                                  uint8_t* skip, double* scratch, int64_t scratch_nodes, cudaStream_t s);
+// a node stops refining once its correction is below this fraction of its coefficients (equilibrated)
+constexpr double kRefineConv = 1e-14;
+// coefs: row i = polynomial of the level's local node i (nt.coef + first*𝓛, or a refinement delta)
+// skip (refinement passes): nodes whose correction was not computed keep their residual and sums.
+template <int P> void level_residual(const LevelCtx& c, const double* coefs, const uint8_t* skip,
+                                     const Chunk* chunks, const int64_t* nchunks_dev, int64_t max_chunks,
+                                     const int64_t* chunk_begin, double* seg_part, cudaStream_t s);
+// decisions + compaction: writes the next level's nodes at [first+count, ...), returns via dev_out[0] the
+// number of new nodes and dev_out[1] their total points.
+void level_decide(const LevelCtx& c, int64_t* flags_tmp, int64_t* scan_tmp, int64_t* dev_out, cudaStream_t s);
+
+// solve_qr.cu (robust path for ill-conditioned nodes)
+size_t solve_qr_scratch_per_cta(int p);
+template <int P> void level_solve_qr(const LevelCtx& c, const double* mom, double* scratch, int64_t slots,
+                                     cudaStream_t s);
+// Gram pivot below which a node is re-fitted by K5q (DESIGN.md §2 G9, §3 K5q)
+constexpr double kQrFlagPivot2 = 1e-9;
+
+// eval.cu
+template <int P> void eval_sorted(const double* q, const uint64_t* keys, const uint32_t* idx, int64_t M,
+                                  const double lo[3], double width, bool unit, int Dk, const NodeTable& nt,
+                                  double* out, cudaStream_t s);
+
+}  // namespace fmi

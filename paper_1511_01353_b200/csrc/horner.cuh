@@ -1,0 +1,83 @@
+// horner.cuh — evaluation of a node polynomial Σ_α a_α u^α (monomial form, Algorithm-2 column order)
+// by nested Horner in z, y, x: 𝓛 fused multiply-adds, coefficient offsets known at compile time.
+// Used by K6 (residual update, "f <- f - Λ·P_F") and K7 (evaluation).
+#pragma once
+
+#include "fmi_internal.cuh"
+
+namespace fmi {
+
+// COEF(i) must yield coefficient i (e.g. a shared-memory read or an __ldg).
+template <int P, typename Coef>
+__device__ __forceinline__ double horner3(const Coef& coef, double x, double y, double z) {
+  double px = 0.0;
+#pragma unroll
+  for (int l = P; l >= 0; --l) {
+    double py = 0.0;
+#pragma unroll
+    for (int m = P - l; m >= 0; --m) {
+      double pz = 0.0;
+#pragma unroll
+      for (int n = P - l - m; n >= 0; --n) pz = fma(pz, z, coef(basis_index(P, l, m, n)));
+      py = fma(py, y, pz);
+    }
+    px = fma(px, x, py);
+  }
+  return px;
+}
+
+// Two points per call: every coefficient load feeds two FMAs.
+template <int P, typename Coef>
+__device__ __forceinline__ void horner3x2(const Coef& coef, double x0, double y0, double z0, double x1, double y1,
+                                          double z1, double& v0, double& v1) {
+  double px0 = 0.0, px1 = 0.0;
+#pragma unroll
+  for (int l = P; l >= 0; --l) {
+    double py0 = 0.0, py1 = 0.0;
+#pragma unroll
+    for (int m = P - l; m >= 0; --m) {
+      double pz0 = 0.0, pz1 = 0.0;
+#pragma unroll
+      for (int n = P - l - m; n >= 0; --n) {
+        const double a = coef(basis_index(P, l, m, n));
+        pz0 = fma(pz0, z0, a);
+        pz1 = fma(pz1, z1, a);
+      }
+      py0 = fma(py0, y0, pz0);
+      py1 = fma(py1, y1, pz1);
+    }
+    px0 = fma(px0, x0, py0);
+    px1 = fma(px1, x1, py1);
+  }
+  v0 = px0;
+  v1 = px1;
+}
+
+// Shared-memory coefficient reader that the compiler cannot hoist out of a point loop (a hoisted
+// copy of 𝓛 = 286 coefficients would not fit in registers).
+struct SmemCoef {
+  uint32_t base;  // shared-window address of coefficient 0
+  __device__ __forceinline__ explicit SmemCoef(const double* p)
+      : base((uint32_t)__cvta_generic_to_shared(p)) {}
+  __device__ __forceinline__ double operator()(int i) const {
+    double v;
+    asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(base + 8u * (uint32_t)i));
+    return v;
+  }
+};
+
+// node frame: centre (2i+1)·2^-(d+1), scale 2^(d+1) (FMT_New_Octant; local map P:299)
+struct Frame {
+  double cx, cy, cz, scale;
+};
+__device__ __forceinline__ Frame node_frame(int4 c) {
+  const double h = ldexp(1.0, -(c.w + 1));
+  Frame f;
+  f.scale = ldexp(1.0, c.w + 1);
+  f.cx = (2.0 * c.x + 1.0) * h;
+  f.cy = (2.0 * c.y + 1.0) * h;
+  f.cz = (2.0 * c.z + 1.0) * h;
+  return f;
+}
+
+}  // namespace fmi

@@ -1,0 +1,253 @@
+// keys.cu — K1 Morton keys, K2 LSD radix sort of (key, index) pairs and the SoA gather.
+//
+// A recursive stable octant partition (FMT_Ordered_by_Octant, Alg. 1) applied level by
+// level is exactly a stable sort by the interleaved cell key, so one global sort makes every octree
+// node a contiguous point range (DESIGN.md §3 K1/K2).
+//
+// Octant digit of level t (1..D): o = bx + 2·by + 4·bz (x fastest), b* = bit (D-t) of
+// q* = min(floor(u*·2^D), 2^D - 1).  u* is the root-cube unit coordinate; u* >= split plane <=> the
+// bit is set (tie -> upper side) because u·2^D is an exact power-of-two scaling (G7, G18).
+#include <algorithm>
+
+#include "fmi_internal.cuh"
+
+namespace fmi {
+
+namespace {
+
+// ------------------------------------------------------------------------------------------------
+// bounding box + finiteness check (root frame, reading G6)
+// ------------------------------------------------------------------------------------------------
+constexpr int BB_THREADS = 256;
+
+__global__ void __launch_bounds__(BB_THREADS) k_bbox_partial(const double* __restrict__ pts, int64_t n,
+                                                             const double* __restrict__ f,
+                                                             double* __restrict__ part) {
+  double mn[3] = {INFINITY, INFINITY, INFINITY}, mx[3] = {-INFINITY, -INFINITY, -INFINITY};
+  double bad = 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * BB_THREADS + threadIdx.x; i < n; i += (int64_t)gridDim.x * BB_THREADS) {
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      double v = pts[3 * i + a];
+      if (!isfinite(v)) bad = 1.0;
+      mn[a] = fmin(mn[a], v);
+      mx[a] = fmax(mx[a], v);
+    }
+    if (f && !isfinite(f[i])) bad = 1.0;
+  }
+  __shared__ double sm[7][BB_THREADS];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) { sm[a][threadIdx.x] = mn[a]; sm[3 + a][threadIdx.x] = mx[a]; }
+  sm[6][threadIdx.x] = bad;
+  __syncthreads();
+  for (int w = BB_THREADS / 2; w > 0; w >>= 1) {
+    if (threadIdx.x < w) {
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        sm[a][threadIdx.x] = fmin(sm[a][threadIdx.x], sm[a][threadIdx.x + w]);
+        sm[3 + a][threadIdx.x] = fmax(sm[3 + a][threadIdx.x], sm[3 + a][threadIdx.x + w]);
+      }
+      sm[6][threadIdx.x] = fmax(sm[6][threadIdx.x], sm[6][threadIdx.x + w]);
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x < 7) part[blockIdx.x * 8 + threadIdx.x] = sm[threadIdx.x][0];
+}
+
+__global__ void k_bbox_final(const double* __restrict__ part, int nb, double* __restrict__ out) {
+  if (threadIdx.x != 0) return;
+  double r[7] = {INFINITY, INFINITY, INFINITY, -INFINITY, -INFINITY, -INFINITY, 0.0};
+  for (int b = 0; b < nb; ++b) {
+    for (int a = 0; a < 3; ++a) {
+      r[a] = fmin(r[a], part[b * 8 + a]);
+      r[3 + a] = fmax(r[3 + a], part[b * 8 + 3 + a]);
+    }
+    r[6] = fmax(r[6], part[b * 8 + 6]);
+  }
+  for (int a = 0; a < 7; ++a) out[a] = r[a];
+  out[7] = 0.0;
+}
+
+// ------------------------------------------------------------------------------------------------
+// K1 Morton keys
+// ------------------------------------------------------------------------------------------------
+__device__ __forceinline__ uint64_t spread3(uint64_t v) {
+  v &= 0x1fffffull;
+  v = (v | (v << 32)) & 0x1f00000000ffffull;
+  v = (v | (v << 16)) & 0x1f0000ff0000ffull;
+  v = (v | (v << 8)) & 0x100f00f00f00f00full;
+  v = (v | (v << 4)) & 0x10c30c30c30c30c3ull;
+  v = (v | (v << 2)) & 0x1249249249249249ull;
+  return v;
+}
+
+// root-cube unit coordinate: (x - lo) / W, one IEEE subtraction and one division (same as the
+// oracle's to_unit); identity for the unit cube.
+__device__ __forceinline__ double to_unit(double x, double lo, double w, bool unit) {
+  return unit ? x : __ddiv_rn(__dsub_rn(x, lo), w);
+}
+
+__device__ __forceinline__ uint64_t quantize(double u, int D) {
+  const double scale = (double)(1ull << D);
+  double t = floor(__dmul_rn(u, scale));       // exact power-of-two scaling, no contraction
+  const double top = scale - 1.0;
+  t = fmin(fmax(t, 0.0), top);                 // u = 1 -> top cell; outside queries are clamped
+  return (uint64_t)t;
+}
+
+__global__ void __launch_bounds__(256) k_keys(const double* __restrict__ pts, int64_t n, double lo0, double lo1,
+                                              double lo2, double w, bool unit, int D, uint64_t* __restrict__ keys,
+                                              uint32_t* __restrict__ idx) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double ux = to_unit(pts[3 * i + 0], lo0, w, unit);
+  double uy = to_unit(pts[3 * i + 1], lo1, w, unit);
+  double uz = to_unit(pts[3 * i + 2], lo2, w, unit);
+  uint64_t k = spread3(quantize(ux, D)) | (spread3(quantize(uy, D)) << 1) | (spread3(quantize(uz, D)) << 2);
+  keys[i] = k;
+  idx[i] = (uint32_t)i;
+}
+
+// ------------------------------------------------------------------------------------------------
+// K2 LSD radix sort, 8-bit digits, stable.  Upsweep histogram -> exclusive scan (digit-major) ->
+// downsweep with warp-level stable ranking (match.any) and per-warp digit counters.
+// ------------------------------------------------------------------------------------------------
+constexpr int RS_THREADS = 256;
+constexpr int RS_WARPS = RS_THREADS / 32;
+constexpr int RS_ITEMS = 16;
+constexpr int RS_TILE = RS_THREADS * RS_ITEMS;  // 4096
+constexpr int RS_WARP_ITEMS = RS_TILE / RS_WARPS; // 512
+
+__global__ void __launch_bounds__(RS_THREADS) k_rs_hist(const uint64_t* __restrict__ keys, int64_t n, int shift,
+                                                        int64_t nblk, int64_t* __restrict__ counts) {
+  __shared__ int hist[256];
+  hist[threadIdx.x] = 0;
+  __syncthreads();
+  const int64_t base = (int64_t)blockIdx.x * RS_TILE;
+#pragma unroll 4
+  for (int i = 0; i < RS_ITEMS; ++i) {
+    int64_t idx = base + (int64_t)i * RS_THREADS + threadIdx.x;
+    if (idx < n) atomicAdd(&hist[(keys[idx] >> shift) & 255], 1);
+  }
+  __syncthreads();
+  counts[(int64_t)threadIdx.x * nblk + blockIdx.x] = hist[threadIdx.x];
+}
+
+__global__ void __launch_bounds__(RS_THREADS) k_rs_scatter(const uint64_t* __restrict__ kin,
+                                                           const uint32_t* __restrict__ vin, int64_t n, int shift,
+                                                           int64_t nblk, const int64_t* __restrict__ offs,
+                                                           uint64_t* __restrict__ kout, uint32_t* __restrict__ vout) {
+  __shared__ int whist[RS_WARPS][257];
+  __shared__ int64_t boff[256];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int t = threadIdx.x; t < RS_WARPS * 257; t += RS_THREADS) (&whist[0][0])[t] = 0;
+  boff[threadIdx.x] = offs[(int64_t)threadIdx.x * nblk + blockIdx.x];
+  __syncthreads();
+  const int64_t base = (int64_t)blockIdx.x * RS_TILE + (int64_t)warp * RS_WARP_ITEMS;
+  const unsigned lt_mask = (1u << lane) - 1u;
+  uint64_t k[RS_ITEMS];
+  uint32_t v[RS_ITEMS];
+  int rank[RS_ITEMS];
+  int dig[RS_ITEMS];
+#pragma unroll
+  for (int it = 0; it < RS_ITEMS; ++it) {
+    int64_t idx = base + it * 32 + lane;
+    bool valid = idx < n;
+    k[it] = valid ? kin[idx] : 0;
+    v[it] = valid ? vin[idx] : 0;
+    dig[it] = valid ? (int)((k[it] >> shift) & 255) : 256;
+  }
+#pragma unroll
+  for (int it = 0; it < RS_ITEMS; ++it) {
+    unsigned peers = __match_any_sync(0xffffffffu, dig[it]);
+    int before = whist[warp][dig[it]];
+    __syncwarp();
+    int leader = __ffs(peers) - 1;
+    if (lane == leader) whist[warp][dig[it]] = before + __popc(peers);
+    __syncwarp();
+    rank[it] = before + __popc(peers & lt_mask);
+  }
+  __syncthreads();
+  {  // exclusive prefix over warps for each digit
+    int d = threadIdx.x, run = 0;
+#pragma unroll
+    for (int w = 0; w < RS_WARPS; ++w) {
+      int t = whist[w][d];
+      whist[w][d] = run;
+      run += t;
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int it = 0; it < RS_ITEMS; ++it) {
+    if (dig[it] < 256) {
+      int64_t pos = boff[dig[it]] + whist[warp][dig[it]] + rank[it];
+      kout[pos] = k[it];
+      vout[pos] = v[it];
+    }
+  }
+}
+
+// ------------------------------------------------------------------------------------------------
+// SoA gather in Morton order
+// ------------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_gather(const double* __restrict__ pts, const double* __restrict__ f,
+                                                const uint32_t* __restrict__ perm, int64_t n, double lo0, double lo1,
+                                                double lo2, double w, bool unit, double* __restrict__ ux,
+                                                double* __restrict__ uy, double* __restrict__ uz,
+                                                double* __restrict__ r) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int64_t j = perm[i];
+  ux[i] = to_unit(pts[3 * j + 0], lo0, w, unit);
+  uy[i] = to_unit(pts[3 * j + 1], lo1, w, unit);
+  uz[i] = to_unit(pts[3 * j + 2], lo2, w, unit);
+  r[i] = f[j];
+}
+
+}  // namespace
+
+void bbox_and_check(const double* pts, int64_t n, double* out8, const double* f, cudaStream_t s) {
+  int nb = (int)std::min<int64_t>((n + BB_THREADS - 1) / BB_THREADS, 1184);
+  if (nb < 1) nb = 1;
+  DBuf<double> part((size_t)nb * 8, s);
+  FMI_LAUNCH(KID_MISC, s, k_bbox_partial, nb, BB_THREADS, 0, pts, n, f, part.p);
+  FMI_LAUNCH(KID_MISC, s, k_bbox_final, 1, 32, 0, part.p, nb, out8);
+}
+
+void morton_keys(const double* pts, int64_t n, const double lo[3], double width, bool unit, int D, uint64_t* keys,
+                 uint32_t* idx, cudaStream_t s) {
+  if (n <= 0) return;
+  unsigned grid = (unsigned)((n + 255) / 256);
+  FMI_LAUNCH(KID_KEYS, s, k_keys, grid, 256, 0, pts, n, lo[0], lo[1], lo[2], width, unit, D, keys, idx);
+}
+
+void radix_sort_pairs(uint64_t* keys, uint32_t* vals, uint64_t* keys_tmp, uint32_t* vals_tmp, int64_t n, int nbits,
+                      cudaStream_t s) {
+  if (n <= 1 || nbits <= 0) return;
+  const int64_t nblk = (n + RS_TILE - 1) / RS_TILE;
+  DBuf<int64_t> counts((size_t)nblk * 256, s);
+  uint64_t* ka = keys; uint32_t* va = vals; uint64_t* kb = keys_tmp; uint32_t* vb = vals_tmp;
+  int passes = 0;
+  for (int shift = 0; shift < nbits; shift += 8, ++passes) {
+    FMI_LAUNCH(KID_SORT, s, k_rs_hist, (unsigned)nblk, RS_THREADS, 0, ka, n, shift, nblk, counts.p);
+    exclusive_scan_i64(counts.p, counts.p, nblk * 256, nullptr, s);
+    FMI_LAUNCH(KID_SORT, s, k_rs_scatter, (unsigned)nblk, RS_THREADS, 0, ka, va, n, shift, nblk, counts.p, kb, vb);
+    std::swap(ka, kb);
+    std::swap(va, vb);
+  }
+  if (passes & 1) {  // result is in the tmp buffers: copy back
+    FMI_CK(cudaMemcpyAsync(keys, ka, n * sizeof(uint64_t), cudaMemcpyDeviceToDevice, s));
+    FMI_CK(cudaMemcpyAsync(vals, va, n * sizeof(uint32_t), cudaMemcpyDeviceToDevice, s));
+  }
+}
+
+void gather_points(const double* pts, const double* f, const uint32_t* perm, int64_t n, const double lo[3],
+                   double width, bool unit, double* ux, double* uy, double* uz, double* r, cudaStream_t s) {
+  if (n <= 0) return;
+  unsigned grid = (unsigned)((n + 255) / 256);
+  FMI_LAUNCH(KID_GATHER, s, k_gather, grid, 256, 0, pts, f, perm, n, lo[0], lo[1], lo[2], width, unit, ux, uy, uz,
+             r);
+}
+
+}  // namespace fmi

@@ -1,0 +1,230 @@
+// solve.cu — K5: batched node solve (DESIGN.md §3 K5), one CTA per node.
+//
+// PAPER.md Algorithm 2 computes P_F = R⁻¹ Qᵀ f from the QR of Λ.  In Gram form, with the
+// raw moments M and projection b of K4:
+//   D_α   = sqrt(G_αα) = sqrt(M_{2α}) / α!          (column norms of Λ)
+//   G̃_αβ  = M_{α+β} / sqrt(M_{2α} M_{2β})           (Jacobi-equilibrated Gram; factorials cancel)
+//   b̃_α   = b_α / sqrt(M_{2α})                     (= (Λᵀ r)_α / D_α)
+//   G̃ c̃ = b̃  by Cholesky G̃ = R̃ᵀR̃  (R̃ = the R of the QR of Λ D⁻¹ up to row signs)
+//   monomial coefficients a_α = c̃_α / sqrt(M_{2α}) = P_F,α / α!   (used by Horner in K6/K7)
+// Rank rule (reading G9, identical to the oracle's QR column rejection): at step j the Schur
+// complement diagonal s_jj equals the squared distance of equilibrated column j from the span of the
+// kept columns; the column is dropped (coefficient 0) iff s_jj <= kDelta², or M_{2α} = 0.
+#include <algorithm>
+#include <vector>
+
+#include "fmi_internal.cuh"
+
+namespace fmi {
+
+namespace {
+
+constexpr int K5_THREADS = 256;
+
+struct BasisTab {
+  uint8_t l[286], m[286], n[286];
+};
+
+template <int P>
+BasisTab make_basis() {
+  BasisTab b{};
+  int i = 0;
+  for (int l = 0; l <= P; ++l)
+    for (int m = 0; m <= P - l; ++m)
+      for (int n = 0; n <= P - l - m; ++n) { b.l[i] = (uint8_t)l; b.m[i] = (uint8_t)m; b.n[i] = (uint8_t)n; ++i; }
+  return b;
+}
+
+template <int P>
+struct K5Shape {
+  static constexpr int Q = 2 * P;
+  static constexpr int K = rank3(Q);
+  static constexpr int L = rank3(P);
+  static constexpr int NA = L * (L + 1) / 2;
+  static constexpr size_t VEC = (size_t)K + 5 * L;  // moments, b, dinv, col, piv, scratch
+  static constexpr bool kSmemA = (VEC + NA) * sizeof(double) <= 220 * 1024;
+  static constexpr size_t SMEM = (kSmemA ? VEC + NA : VEC) * sizeof(double);
+};
+
+__device__ __forceinline__ int64_t tri(int i) { return (int64_t)i * (i + 1) / 2; }
+
+template <int P>
+__global__ void __launch_bounds__(K5_THREADS)
+    k_solve(const double* __restrict__ mom, const double* __restrict__ rhs, double* __restrict__ delta,
+            uint8_t* __restrict__ skip, NodeTable nt, int64_t first, int64_t count, double* __restrict__ gscratch,
+            const __grid_constant__ BasisTab bt, double delta2, double conv_tol) {
+  using S = K5Shape<P>;
+  constexpr int Q = S::Q, K = S::K, L = S::L;
+  extern __shared__ double sm[];
+  double* sM = sm;          // [K]
+  double* sb = sM + K;      // [L]  b̃ -> y -> c̃
+  double* dinv = sb + L;    // [L]
+  double* col = dinv + L;   // [L]
+  double* piv = col + L;    // [L]
+  double* red = piv + L;    // [L]
+  double* A = S::kSmemA ? red + L : gscratch + (int64_t)blockIdx.x * S::NA;
+  const int tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5;
+  constexpr int NWARP = K5_THREADS / 32;
+  __shared__ double smin_sh[1];
+  __shared__ double redw[2 * NWARP];
+
+  for (int64_t node = blockIdx.x; node < count; node += gridDim.x) {
+    if (rhs && (nt.flag[first + node] & 3)) {  // QR-path (bit 0) or converged (bit 1): no correction
+      if (tid == 0) skip[node] = 1;
+      continue;
+    }
+    if (tid == 0) smin_sh[0] = INFINITY;
+    const double* mp = mom + node * (int64_t)(K + L);
+    for (int e = tid; e < K; e += K5_THREADS) sm[e] = mp[e];
+    const double* bp = rhs ? rhs + node * (int64_t)L : mp + K;
+    for (int e = tid; e < L; e += K5_THREADS) sb[e] = bp[e];
+    __syncthreads();
+    for (int i = tid; i < L; i += K5_THREADS) {
+      const double m2 = sM[basis_index(Q, 2 * bt.l[i], 2 * bt.m[i], 2 * bt.n[i])];
+      const double di = m2 > 0.0 ? 1.0 / sqrt(m2) : 0.0;
+      dinv[i] = di;
+      sb[i] *= di;
+    }
+    __syncthreads();
+    for (int64_t e = tid; e < S::NA; e += K5_THREADS) {
+      int i = (int)((sqrt(8.0 * (double)e + 1.0) - 1.0) * 0.5);
+      while (tri(i + 1) <= e) ++i;
+      while (tri(i) > e) --i;
+      const int k = (int)(e - tri(i));
+      const double g = sM[basis_index(Q, bt.l[i] + bt.l[k], bt.m[i] + bt.m[k], bt.n[i] + bt.n[k])];
+      A[e] = g * dinv[i] * dinv[k];
+    }
+    __syncthreads();
+
+    // right-looking Cholesky with column rejection
+    for (int j = 0; j < L; ++j) {
+      if (tid == 0) {
+        const double s = A[tri(j) + j];
+        const bool keep = dinv[j] > 0.0 && s > delta2;
+        const double p = keep ? sqrt(s) : 0.0;
+        piv[j] = p;
+        A[tri(j) + j] = p;
+        if (dinv[j] > 0.0 && !(s >= smin_sh[0])) smin_sh[0] = s;  // also catches NaN
+      }
+      __syncthreads();
+      const double p = piv[j];
+      if (p > 0.0) {
+        const double inv = 1.0 / p;
+        for (int i = j + 1 + tid; i < L; i += K5_THREADS) {
+          const double v = A[tri(i) + j] * inv;
+          A[tri(i) + j] = v;
+          col[i] = v;
+        }
+        __syncthreads();
+        for (int i = j + 1 + warp; i < L; i += NWARP) {
+          const double ci = col[i];
+          double* Ai = A + tri(i);
+          for (int k = j + 1 + lane; k <= i; k += 32) Ai[k] -= ci * col[k];
+        }
+      } else {
+        for (int i = j + 1 + tid; i < L; i += K5_THREADS) A[tri(i) + j] = 0.0;
+      }
+      __syncthreads();
+    }
+    // forward substitution R̃ᵀ y = b̃
+    for (int j = 0; j < L; ++j) {
+      const double p = piv[j];
+      const double yj = p > 0.0 ? sb[j] / p : 0.0;
+      __syncthreads();
+      for (int i = j + 1 + tid; i < L; i += K5_THREADS) sb[i] -= A[tri(i) + j] * yj;
+      if (tid == 0) sb[j] = yj;
+      __syncthreads();
+    }
+    // back substitution R̃ c̃ = y
+    for (int j = L - 1; j >= 0; --j) {
+      const double p = piv[j];
+      const double cj = p > 0.0 ? sb[j] / p : 0.0;
+      __syncthreads();
+      const double* Aj = A + tri(j);
+      for (int i = tid; i < j; i += K5_THREADS) sb[i] -= Aj[i] * cj;
+      if (tid == 0) sb[j] = cj;
+      __syncthreads();
+    }
+    double* out = nt.coef + (first + node) * (int64_t)L;
+    if (rhs) {
+      // correction δ = R̃⁻¹R̃⁻ᵀ b̃1 (equilibrated) -> monomial form; converged when |δ̃| <= conv_tol |c̃|
+      double dmax = 0.0, cmax = 0.0;
+      for (int i = tid; i < L; i += K5_THREADS) {
+        const double d = sb[i] * dinv[i];
+        delta[node * (int64_t)L + i] = d;
+        if (dinv[i] > 0.0) {
+          dmax = fmax(dmax, fabs(sb[i]));
+          cmax = fmax(cmax, fabs(out[i] / dinv[i]));
+        }
+        out[i] += d;
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        dmax = fmax(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
+        cmax = fmax(cmax, __shfl_xor_sync(0xffffffffu, cmax, o));
+      }
+      if (lane == 0) { redw[warp] = dmax; redw[NWARP + warp] = cmax; }
+      __syncthreads();
+      if (tid == 0) {
+        double dm = 0.0, cm = 0.0;
+        for (int w = 0; w < NWARP; ++w) { dm = fmax(dm, redw[w]); cm = fmax(cm, redw[NWARP + w]); }
+        skip[node] = 0;
+        if (dm <= conv_tol * cm) nt.flag[first + node] |= 2;
+      }
+      __syncthreads();
+      continue;
+    }
+    for (int i = tid; i < L; i += K5_THREADS) out[i] = sb[i] * dinv[i];
+    if (tid == 0) {
+      int rk = 0;
+      double mn = INFINITY;
+      for (int i = 0; i < L; ++i)
+        if (piv[i] > 0.0) { ++rk; mn = fmin(mn, piv[i]); }
+      nt.rank[first + node] = rk;
+      nt.minpiv[first + node] = rk ? mn : 0.0;
+      // robust-path flag: a pivot of a non-zero column fell where fp64 Gram pivots stop tracking the
+      // QR pivots (or the column was rejected) -> K5q re-fits the node by Householder QR
+      nt.flag[first + node] = (smin_sh[0] < kQrFlagPivot2) ? 1 : 0;
+    }
+    __syncthreads();
+  }
+}
+
+}  // namespace
+
+template <int P>
+void level_solve(const LevelCtx& c, const double* mom, const double* rhs, double* delta, uint8_t* skip,
+                 double* scratch, int64_t scratch_nodes, cudaStream_t s) {
+  using S = K5Shape<P>;
+  static const BasisTab bt = make_basis<P>();
+  static bool attr = false;
+  if (!attr) {
+    FMI_CK(cudaFuncSetAttribute(k_solve<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::SMEM));
+    attr = true;
+  }
+  int64_t grid = c.count;
+  if (!S::kSmemA) grid = std::min<int64_t>(grid, scratch_nodes);
+  grid = std::min<int64_t>(grid, 1 << 20);
+  FMI_LAUNCH(rhs ? KID_REFINE_SOLVE : KID_SOLVE, s, k_solve<P>, (unsigned)grid, K5_THREADS, S::SMEM, mom, rhs, delta,
+             skip, c.nt, c.first, c.count, scratch, bt, kDelta * kDelta, kRefineConv);
+}
+
+// bytes of global scratch the solve needs per concurrently processed node (0 if shared-memory resident)
+size_t solve_scratch_per_node(int p) {
+  switch (p) {
+#define C(P) case P: return K5Shape<P>::kSmemA ? 0 : (size_t)K5Shape<P>::NA * sizeof(double);
+    C(0) C(1) C(2) C(3) C(4) C(5) C(6) C(7) C(8) C(9) C(10)
+#undef C
+  }
+  return 0;
+}
+
+#define FMI_INST(P) \
+  template void level_solve<P>(const LevelCtx&, const double*, const double*, double*, uint8_t*, double*, int64_t,  \
+                               cudaStream_t);
+FMI_INST(0) FMI_INST(1) FMI_INST(2) FMI_INST(3) FMI_INST(4) FMI_INST(5)
+FMI_INST(6) FMI_INST(7) FMI_INST(8) FMI_INST(9) FMI_INST(10)
+#undef FMI_INST
+
+}  // namespace fmi

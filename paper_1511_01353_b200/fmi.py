@@ -1,0 +1,295 @@
+"""Thin ctypes binding of ``libfmi.so`` (include/fmi.h).  Argument marshalling only: every step of the
+fit and the evaluation runs in the library's CUDA kernels.  There is no CPU fallback: importing this
+module without the built library, or calling it without a CUDA device, raises.
+
+Arrays may be numpy arrays (host memory; copied inside the call) or CUDA torch tensors (device
+memory; used in place).  All arrays are float64, C-contiguous; points are (N, 3) row-major.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libfmi.so")
+
+FMI_OK = 0
+FMI_EINPUT = -1
+FMI_EPRECOND = -2
+FMI_EVERSION = -3
+FMI_ENUMERIC = -4
+FMI_ECUDA = -5
+FMI_ENCCL = -6
+FMI_ENOMEM = -7
+MAX_DEGREE = 10
+MAX_DEPTH = 20
+
+# every symbol include/fmi.h declares (tests check the library exports all of them)
+EXPORTED = (
+    "fmi_build", "fmi_eval", "fmi_free", "fmi_last_error", "fmi_set_stream", "fmi_node_count", "fmi_rank",
+    "fmi_export_nodes", "fmi_root_cube", "fmi_residual", "fmi_level_stats", "fmi_profile_enable",
+    "fmi_profile_reset", "fmi_profile_get", "fmi_launch_count",
+)
+
+KERNELS = ("keys", "sort", "gather", "moments", "moments_reduce", "solve", "children", "residual",
+           "residual_reduce", "decide", "chunks", "scan", "eval", "misc", "project", "refine_solve")
+
+
+class FmiNode(ctypes.Structure):
+    _fields_ = [
+        ("depth", ctypes.c_int32), ("cell", ctypes.c_int32 * 3), ("prefix", ctypes.c_uint64),
+        ("n_points", ctypes.c_int64), ("rank", ctypes.c_int32), ("parent", ctypes.c_int32),
+        ("flags", ctypes.c_int32), ("reserved", ctypes.c_int32),
+        ("residual_rms", ctypes.c_double), ("min_pivot", ctypes.c_double),
+        ("child_count", ctypes.c_int64 * 8), ("child_rms", ctypes.c_double * 8), ("child", ctypes.c_int32 * 8),
+    ]
+
+
+class FmiError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"fmi error {code}: {msg}")
+        self.code = code
+
+
+_lib = None
+
+
+def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
+    """Load libfmi.so (raises if it is missing: build it with __graft_entry__.build())."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise ImportError(f"{path} not built; run `python -c 'import __graft_entry__ as g; g.build()'`")
+    lib = ctypes.CDLL(path)
+    P, D, I64, I32, VP = ctypes.POINTER, ctypes.c_double, ctypes.c_int64, ctypes.c_int, ctypes.c_void_p
+    lib.fmi_build.restype = VP
+    lib.fmi_build.argtypes = [VP, VP, I64, I32, D, I32]
+    lib.fmi_eval.restype = I32
+    lib.fmi_eval.argtypes = [VP, VP, I64, VP]
+    lib.fmi_free.restype = None
+    lib.fmi_free.argtypes = [VP]
+    lib.fmi_last_error.restype = I32
+    lib.fmi_last_error.argtypes = [P(ctypes.c_char_p)]
+    lib.fmi_set_stream.restype = I32
+    lib.fmi_set_stream.argtypes = [VP]
+    lib.fmi_node_count.restype = I64
+    lib.fmi_node_count.argtypes = [VP]
+    lib.fmi_rank.restype = I32
+    lib.fmi_rank.argtypes = [VP]
+    lib.fmi_export_nodes.restype = I64
+    lib.fmi_export_nodes.argtypes = [VP, P(FmiNode), VP, I64]
+    lib.fmi_root_cube.restype = I32
+    lib.fmi_root_cube.argtypes = [VP, P(D), P(D)]
+    lib.fmi_residual.restype = I32
+    lib.fmi_residual.argtypes = [VP, VP]
+    lib.fmi_level_stats.restype = I32
+    lib.fmi_level_stats.argtypes = [VP, P(I64), P(I64), I32]
+    lib.fmi_profile_enable.restype = I32
+    lib.fmi_profile_enable.argtypes = [I32]
+    lib.fmi_profile_reset.restype = I32
+    lib.fmi_profile_reset.argtypes = []
+    lib.fmi_profile_get.restype = I32
+    lib.fmi_profile_get.argtypes = [ctypes.c_char_p, P(D), P(I64)]
+    lib.fmi_launch_count.restype = I64
+    lib.fmi_launch_count.argtypes = []
+    _lib = lib
+    return lib
+
+
+def last_error() -> tuple[int, str]:
+    lib = load_library()
+    msg = ctypes.c_char_p()
+    code = lib.fmi_last_error(ctypes.byref(msg))
+    return code, (msg.value.decode() if msg.value else "")
+
+
+def _raise_last(default_code: int = FMI_ECUDA):
+    code, msg = last_error()
+    raise FmiError(code or default_code, msg)
+
+
+def _ptr(a, ncols: int | None, name: str):
+    """(pointer, length, keepalive) of a float64 C-contiguous host array or CUDA tensor."""
+    if hasattr(a, "is_cuda") and hasattr(a, "data_ptr"):  # torch tensor
+        import torch
+        if a.dtype != torch.float64 or not a.is_contiguous():
+            raise TypeError(f"{name}: CUDA tensors must be float64 and contiguous")
+        n = a.shape[0] if a.dim() else 0
+        if ncols is not None and (a.dim() != 2 or a.shape[1] != ncols):
+            raise ValueError(f"{name}: expected shape (n, {ncols})")
+        return ctypes.c_void_p(a.data_ptr()), n, a
+    arr = np.asarray(a)
+    if arr.dtype != np.float64 or not arr.flags.c_contiguous:
+        arr = np.ascontiguousarray(arr, dtype=np.float64)
+    if ncols is not None:
+        if arr.ndim != 2 or arr.shape[1] != ncols:
+            raise ValueError(f"{name}: expected shape (n, {ncols})")
+    n = arr.shape[0] if arr.ndim else 0
+    return ctypes.c_void_p(arr.ctypes.data), n, arr
+
+
+def set_stream(stream) -> None:
+    """Use a CUDA stream (torch.cuda.Stream, raw handle int, or None) for subsequent calls."""
+    lib = load_library()
+    handle = getattr(stream, "cuda_stream", stream)
+    lib.fmi_set_stream(ctypes.c_void_p(handle or 0))
+
+
+class Tree:
+    """Handle of a fitted octree (fmi_tree*).  Freed by ``free()`` or on garbage collection."""
+
+    def __init__(self, handle: int, n: int, degree: int, tol: float, max_depth: int):
+        self._h = handle
+        self.n = n
+        self.degree = degree
+        self.tol = tol
+        self.max_depth = max_depth
+
+    @property
+    def handle(self) -> int:
+        if not self._h:
+            raise FmiError(FMI_EINPUT, "tree already freed")
+        return self._h
+
+    def free(self) -> None:
+        if self._h:
+            load_library().fmi_free(ctypes.c_void_p(self._h))
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.free()
+
+    # -- evaluation ---------------------------------------------------------------------------
+    def eval(self, q, out=None):
+        """Interpolant at the M query points q (M, 3); returns ``out`` (numpy if q is host memory)."""
+        lib = load_library()
+        qp, m, qk = _ptr(q, 3, "q")
+        if out is None:
+            if hasattr(q, "is_cuda"):
+                import torch
+                out = torch.empty(m, dtype=torch.float64, device=q.device)
+            else:
+                out = np.empty(m, dtype=np.float64)
+        if isinstance(out, np.ndarray) and (out.dtype != np.float64 or not out.flags.c_contiguous):
+            raise TypeError("out must be a float64 C-contiguous array")
+        op, mo, ok = _ptr(out, None, "out")
+        if mo != m:
+            raise ValueError("out must have M entries")
+        rc = lib.fmi_eval(ctypes.c_void_p(self.handle), qp, m, op)
+        if rc != 0:
+            _raise_last(rc)
+        return out
+
+    # -- introspection ------------------------------------------------------------------------
+    @property
+    def node_count(self) -> int:
+        return int(load_library().fmi_node_count(ctypes.c_void_p(self.handle)))
+
+    @property
+    def rank(self) -> int:
+        return int(load_library().fmi_rank(ctypes.c_void_p(self.handle)))
+
+    def root_cube(self):
+        lo = (ctypes.c_double * 3)()
+        w = ctypes.c_double()
+        load_library().fmi_root_cube(ctypes.c_void_p(self.handle), lo, ctypes.byref(w))
+        return np.array(lo[:]), float(w.value)
+
+    def export(self) -> dict:
+        """All nodes in canonical (depth, prefix) order as numpy arrays; coeffs = P_F (Λ basis)."""
+        lib = load_library()
+        n = self.node_count
+        L = self.rank
+        nodes = (FmiNode * n)()
+        coeffs = np.zeros((n, L), dtype=np.float64)
+        got = lib.fmi_export_nodes(ctypes.c_void_p(self.handle), nodes, coeffs.ctypes.data_as(ctypes.c_void_p), n)
+        if got < 0:
+            _raise_last(int(got))
+        return {
+            "depth": np.array([nd.depth for nd in nodes], dtype=np.int64),
+            "cell": np.array([list(nd.cell) for nd in nodes], dtype=np.int64).reshape(n, 3),
+            "prefix": np.array([nd.prefix for nd in nodes], dtype=np.uint64),
+            "n_points": np.array([nd.n_points for nd in nodes], dtype=np.int64),
+            "rank": np.array([nd.rank for nd in nodes], dtype=np.int64),
+            "parent": np.array([nd.parent for nd in nodes], dtype=np.int64),
+            "flags": np.array([nd.flags for nd in nodes], dtype=np.int64),
+            "residual_rms": np.array([nd.residual_rms for nd in nodes]),
+            "min_pivot": np.array([nd.min_pivot for nd in nodes]),
+            "child_count": np.array([list(nd.child_count) for nd in nodes], dtype=np.int64).reshape(n, 8),
+            "child_rms": np.array([list(nd.child_rms) for nd in nodes]).reshape(n, 8),
+            "child": np.array([list(nd.child) for nd in nodes], dtype=np.int64).reshape(n, 8),
+            "coeffs": coeffs,
+        }
+
+    def residual(self, out=None):
+        """Final residual at the fit points, in input order."""
+        lib = load_library()
+        if out is None:
+            out = np.empty(self.n, dtype=np.float64)
+        if isinstance(out, np.ndarray) and (out.dtype != np.float64 or not out.flags.c_contiguous):
+            raise TypeError("out must be a float64 C-contiguous array")
+        op, _, _ = _ptr(out, None, "out")
+        rc = lib.fmi_residual(ctypes.c_void_p(self.handle), op)
+        if rc != 0:
+            _raise_last(rc)
+        return out
+
+    def level_stats(self):
+        lib = load_library()
+        nodes = (ctypes.c_int64 * 64)()
+        pts = (ctypes.c_int64 * 64)()
+        k = lib.fmi_level_stats(ctypes.c_void_p(self.handle), nodes, pts, 64)
+        return np.array(nodes[:k], dtype=np.int64), np.array(pts[:k], dtype=np.int64)
+
+
+def build(pts, f, degree: int, tol: float, max_depth: int) -> Tree:
+    """Fit the octree interpolant (fmi_build).  pts (N, 3), f (N,): numpy (host) or CUDA tensors."""
+    lib = load_library()
+    pp, n, pk = _ptr(pts, 3, "pts")
+    fp, nf, fk = _ptr(f, None, "f")
+    if nf != n:
+        raise ValueError("pts and f disagree in length")
+    h = lib.fmi_build(pp, fp, n, int(degree), float(tol), int(max_depth))
+    if not h:
+        _raise_last()
+    return Tree(h, n, degree, tol, max_depth)
+
+
+def profile_enable(on: bool = True) -> None:
+    load_library().fmi_profile_enable(1 if on else 0)
+
+
+def profile_reset() -> None:
+    load_library().fmi_profile_reset()
+
+
+def profile_get() -> dict:
+    lib = load_library()
+    out = {}
+    for k in KERNELS:
+        ms = ctypes.c_double()
+        n = ctypes.c_int64()
+        if lib.fmi_profile_get(k.encode(), ctypes.byref(ms), ctypes.byref(n)) == 0:
+            out[k] = (float(ms.value), int(n.value))
+    return out
+
+
+def launch_count() -> int:
+    return int(load_library().fmi_launch_count())
+
+
+def rank_of(degree: int) -> int:
+    """𝓛 = (p+1)(p+2)(p+3)/6 — host-side argument check helper."""
+    return (degree + 1) * (degree + 2) * (degree + 3) // 6
