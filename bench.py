@@ -1,0 +1,332 @@
+#!/usr/bin/env python
+"""Benchmark of the octree fit + evaluation hot path (BASELINE.json metric).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--impl {fmi,reference}]
+
+One step = fmi_build over the config's N points + fmi_eval at its M queries (+ fmi_free), i.e. every
+§8(a) row of SURVEY.md once.  value = (N + M) points / step time (points/s), inputs resident in HBM
+before the timed region; e2e = the same through the C ABI with pinned HOST buffers (H2D of points,
+values and queries and D2H of the result inside the timed region).  Timing: CUDA events on the stream
+the library launches on, barrier + synchronize on both sides, max over ranks.  Inputs (>= 6 GB at
+the default config) exceed the 126 MB L2, so no explicit flush is needed between steps.
+
+--impl reference times the oracle (oracle/fmt_oracle.py, CPU) on a bounded sample of the same
+workload (there is no reference implementation to install: the paper ships no code).
+
+Multi-GPU (torchrun, N > 1): round 1 runs one independent replica of the workload per rank ("replicas";
+Morton-range sharding with the per-level straddle all-reduce is DESIGN.md §6 future work), and value
+is the aggregate over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import workloads  # noqa: E402
+
+FP64_PEAK_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12  # 37.2: SMs × FP64 FMA/clk/SM × 2 × max SM clock
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=5, choices=[1, 2, 3, 4, 5])
+    ap.add_argument("--impl", default="fmi", choices=["fmi", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--n", type=int, default=None, help="override N (debugging; not a bench line)")
+    ap.add_argument("--m", type=int, default=None, help="override M (debugging; not a bench line)")
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+# ------------------------------------------------------------------------------------------------
+# clocks during the timed region (NVML)
+# ------------------------------------------------------------------------------------------------
+class ClockSampler:
+    REASONS = {
+        0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+        0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+        0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting",
+    }
+
+    def __init__(self, index: int):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                mask = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if mask & bit and name != "gpu_idle":
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.05)
+
+    def __enter__(self):
+        if self.nv:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *exc):
+        if self.nv:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons)}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# ------------------------------------------------------------------------------------------------
+# CPU baseline: the oracle as it stands on a bounded sample of the workload
+# ------------------------------------------------------------------------------------------------
+def oracle_sample_cfg(cfg: workloads.Config, target_points: int) -> workloads.Config:
+    n = min(cfg.n, target_points)
+    m = min(cfg.m, target_points)
+    return cfg.scaled(n=n, m=m)
+
+
+def time_oracle(cfg: workloads.Config, sample_points: int):
+    from oracle import fmt_oracle
+    sc = oracle_sample_cfg(cfg, sample_points)
+    pts, f, q = workloads.make_inputs(sc)
+    t0 = time.perf_counter()
+    tree = fmt_oracle.build(pts, f, sc.degree, sc.tol, sc.max_depth)
+    fmt_oracle.evaluate(tree, q)
+    dt = time.perf_counter() - t0
+    sample = (f"{sc.name} recipe at N={sc.n:,}, M={sc.m:,} (same p={sc.degree}, tol={sc.tol:g}, "
+              f"max_depth={sc.max_depth}, generator) -> {tree.node_count} nodes; oracle = numpy + "
+              f"single-threaded LAPACK QR")
+    return (sc.n + sc.m) / dt, dt, sample
+
+
+# ------------------------------------------------------------------------------------------------
+def flops_per_point_level(p: int) -> int:
+    """Algorithmic flops of K4 per point and level: one FMA (2 flops) per raw moment (|γ| <= 2p) and
+    per projection entry (|α| <= p) — DESIGN.md §5; monomial generation is not counted."""
+    K = (2 * p + 1) * (2 * p + 2) * (2 * p + 3) // 6
+    L = (p + 1) * (p + 2) * (p + 3) // 6
+    return 2 * (K + L)
+
+
+def run_reference(args, cfg, rank, world):
+    if rank != 0:
+        return
+    sample_points = 100_000 if cfg.cfg >= 3 else min(cfg.n, 100_000)
+    times = []
+    for i in range(args.warmup + args.steps):
+        v, dt, sample = time_oracle(cfg, sample_points)
+        if i >= args.warmup:
+            times.append(dt)
+    sc = oracle_sample_cfg(cfg, sample_points)
+    t = statistics.median(times)
+    value = (sc.n + sc.m) / t
+    line = {
+        "impl": "reference", "metric": "fp64 octree fit + eval points/sec", "value": value, "unit": "points/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{cfg.name}: N={cfg.n:,} M={cfg.m:,} p={cfg.degree} max_depth={cfg.max_depth} "
+                               f"tol={cfg.tol:g} ({cfg.points}/{cfg.values})", "sample_n": sc.n, "sample_m": sc.m},
+        "cpu_baseline": {"value": value, "unit": "points/s", "cores": 1, "kind": "oracle", "sample": sample},
+        "e2e": {"value": value, "unit": "points/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    rank, world, local = dist_env()
+    cfg = workloads.CONFIGS[args.config]
+    if args.n or args.m:
+        cfg = cfg.scaled(n=args.n, m=args.m)
+    if args.impl == "reference":
+        run_reference(args, cfg, rank, world)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_1511_01353_b200 as fmi
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.current_stream(dev)
+    fmi.set_stream(stream)
+
+    t_gen = time.perf_counter()
+    pts, f, q = workloads.make_inputs(cfg)
+    gen_s = time.perf_counter() - t_gen
+    N, M = cfg.n, cfg.m
+    d_pts = torch.from_numpy(pts).to(dev)
+    d_f = torch.from_numpy(f).to(dev)
+    d_q = torch.from_numpy(q).to(dev)
+    d_out = torch.empty(M, dtype=torch.float64, device=dev)
+
+    def step_device():
+        tree = fmi.build(d_pts, d_f, cfg.degree, cfg.tol, cfg.max_depth)
+        tree.eval(d_q, out=d_out)
+        return tree
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+
+    # warm-up (also the tree statistics used for the roofline)
+    tree = None
+    for _ in range(args.warmup):
+        if tree is not None:
+            tree.free()
+        tree = step_device()
+    levels_nodes, levels_points = tree.level_stats()
+    node_count = tree.node_count
+    tree.free()
+
+    # ---- timed region: device-resident inputs ------------------------------------------------
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    ev_b = torch.cuda.Event(enable_timing=True)
+    build_ms = []
+    fmi.profile_reset()
+    fmi.profile_enable(True)
+    launches0 = fmi.launch_count()
+    barrier()
+    with ClockSampler(local) as clocks:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            e_s = torch.cuda.Event(enable_timing=True)
+            e_s.record(stream)
+            tree = fmi.build(d_pts, d_f, cfg.degree, cfg.tol, cfg.max_depth)
+            ev_b.record(stream)
+            tree.eval(d_q, out=d_out)
+            tree.free()
+            torch.cuda.synchronize(dev)
+            build_ms.append(e_s.elapsed_time(ev_b))
+        ev1.record(stream)
+        barrier()
+    launches = fmi.launch_count() - launches0
+    fmi.profile_enable(False)
+    prof = fmi.profile_get()
+    total_ms = ev0.elapsed_time(ev1)
+    if world > 1:
+        t = torch.tensor([total_ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    ms_per_step = total_ms / args.steps
+    value = world * (N + M) / (ms_per_step / 1e3)
+    build_pts_s = N / (statistics.median(build_ms) / 1e3)
+    eval_pts_s = M / ((ms_per_step - statistics.median(build_ms)) / 1e3)
+
+    # roofline of the dominant kernel (K4 moments+projection): algorithmic flops per launch / mean
+    # launch time (library events on the launching stream, inside the timed region)
+    mom_ms, mom_n = prof.get("moments", (0.0, 0))
+    pt_levels = int(np.sum(levels_points))
+    flops_step = pt_levels * flops_per_point_level(cfg.degree)
+    launches_per_step = mom_n / max(args.steps, 1)
+    achieved = (flops_step / launches_per_step) / ((mom_ms / max(mom_n, 1)) / 1e3) / 1e12 if mom_n else None
+    step_kernel_ms = sum(v[0] for v in prof.values()) / args.steps
+
+    # ---- e2e through the C ABI with pinned host buffers -----------------------------------------
+    h_pts = torch.from_numpy(pts).pin_memory()
+    h_f = torch.from_numpy(f).pin_memory()
+    h_q = torch.from_numpy(q).pin_memory()
+    h_out = torch.empty(M, dtype=torch.float64).pin_memory()
+    np_pts, np_f, np_q, np_out = h_pts.numpy(), h_f.numpy(), h_q.numpy(), h_out.numpy()
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        tr = fmi.build(np_pts, np_f, cfg.degree, cfg.tol, cfg.max_depth)
+        tr.eval(np_q, out=np_out)
+        tr.free()
+    barrier()
+    e2e_s = (time.perf_counter() - t0) / args.steps
+    if world > 1:
+        t = torch.tensor([e2e_s], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e_value = world * (N + M) / e2e_s
+    gpu_out_max = float(np.max(np.abs(np_out)))
+
+    line = None
+    if rank == 0:
+        cpu = None
+        if not args.no_cpu_baseline and world == 1:
+            v, dt, sample = time_oracle(cfg, 200_000)
+            cpu = {"value": v, "unit": "points/s", "cores": 1, "kind": "oracle", "sample": sample,
+                   "seconds": dt}
+        line = {
+            "metric": "fp64 octree fit + eval points/sec",
+            "value": value, "unit": "points/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {
+                "workload": f"{cfg.name}: N={N:,} M={M:,} p={cfg.degree} max_depth={cfg.max_depth} tol={cfg.tol:g} "
+                            f"({cfg.points} points, {cfg.values} values)",
+                "parallelism": "replicas" if world > 1 else "single-gpu",
+                "l2": "inputs >= 6 GB exceed the 126 MB L2; no flush",
+                "nodes": node_count, "levels": len(levels_nodes), "point_levels": pt_levels,
+                "build_points_per_s": build_pts_s, "eval_points_per_s": eval_pts_s,
+                "input_gen_s": gen_s,
+            },
+            "roofline": {
+                "kernel": "k_moments (K4 moments + projection)",
+                "bound": "alu", "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                "frac": (achieved / FP64_PEAK_TFLOPS) if achieved else None, "traffic": None,
+                "peak_source": "derived fp64: 148 SM x 64 DFMA/clk x 2 x 1.965 GHz (measured DMMA 37.1, DFMA 34.2 "
+                               "TFLOP/s: profiles/round1_fp64_peak.txt)",
+                "flops_per_launch": flops_step / max(launches_per_step, 1e-9),
+                "mean_launch_ms": mom_ms / max(mom_n, 1),
+                "share_of_step": (mom_ms / args.steps) / ms_per_step,
+            },
+            "kernels_ms_per_step": {k: v[0] / args.steps for k, v in sorted(prof.items()) if v[1]},
+            "kernel_time_fraction": step_kernel_ms / ms_per_step,
+            "cpu_baseline": cpu,
+            "e2e": {"value": e2e_value, "unit": "points/s",
+                    "h2d_bytes_per_step": N * 24 + N * 8 + M * 24, "d2h_bytes_per_step": M * 8},
+            "gpu_launches": int(launches),
+            "clocks": clocks.summary(),
+            "check": {"max_abs_out": gpu_out_max},
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -5,15 +5,19 @@
 // and the projection Λᵀr needs  b_α = Σ_i u_i^α r_i, |α| <= p  (the factorials are applied in the
 // solve).  Per point that is C(2p+3,3) + 𝓛 multiply-adds instead of the dense Gram's 𝓛(𝓛+1)/2.
 //
-// The moments are computed as a masked outer-product contraction over the points of a chunk:
-//   rows  (a,b), a+b <= 2p   X_i(a,b) = x_i^a y_i^b            (materialised per batch in smem)
-//   cols  c = 0..2p          W_i(c)   = z_i^c                  moment entries a+b+c <= 2p
-//         c' = 0..p          W_i(c')  = r_i z_i^c'             projection entries a+b+c' <= p
-// Each thread owns a 4 rows × 4 cols register tile (16 fp64 accumulators) of the needed part of
-// the (a,b) × c grid; rows are sorted by a+b so ragged tiles waste little.  Point batches are
-// software-pipelined through shared memory (load/powers -> X -> accumulate, one barrier per batch).
-// Several thread groups split the points of a chunk; their tiles are reduced in a fixed order, and
-// chunk partials are reduced per node in chunk order (deterministic, no atomics).
+// The moments are a masked outer-product contraction over the points of a chunk:
+//   rows  (a,b), a+b <= 2p   X_i(a,b) = x_i^a y_i^b
+//   cols  c = 0..2p          W_i(c)   = z_i^c          -> moment entries a+b+c <= 2p
+//         c' = 0..p          W_i(c')  = r_i z_i^c'     -> projection entries a+b+c' <= p
+// Rows are ordered by s = a+b (then a) and cut into groups of 8; columns into blocks of 4.  Every
+// consumer thread owns one needed 8×4 tile (32 fp64 accumulators).  Per batch of B points:
+//   produce: warp-uniform tasks write whole rows X(a, ·) / W(·) for 32 consecutive points (lanes =
+//            points, so stores are conflict-free); slot layouts are "row-in-tile major" so that the
+//            16-byte loads of a warp whose lanes own different tiles spread over all banks;
+//   consume: each thread walks point PAIRS (j, j+1): 8 + 4 LDS.128 feed 64 DFMA.
+// Production of batch k+1 and consumption of batch k share one barrier interval (double buffer).
+// Thread groups split a chunk's points; their tiles are reduced in a fixed order, and chunk
+// partials per node in chunk order (deterministic, no atomics).
 #include <algorithm>
 #include <vector>
 
@@ -24,81 +28,186 @@ namespace fmi {
 namespace {
 
 constexpr int K4_THREADS = 512;
-constexpr int K4_MAXROWP = 232;   // (2p+1)(2p+2)/2 rounded to 4 at p = 10
-constexpr int K4_MAXTILE = 256;
+constexpr int K4_WARPS = K4_THREADS / 32;
+constexpr int K4_MAXTILE = 96;      // 84 at p = 10
+constexpr int K4_MAXTASK = 64;
+constexpr int K4_TASKS_PER_WARP = 8;
+constexpr size_t K4_SMEM_LIMIT = 220 * 1024;
 
 // PROJ = false: moments (|γ| <= 2p) and projection; PROJ = true: projection only (refinement pass).
 template <int P, bool PROJ = false>
 struct K4Shape {
-  static constexpr int Q = PROJ ? P : 2 * P;     // highest power generated
+  static constexpr int Q = PROJ ? P : 2 * P;     // highest power of x, y in the rows
   static constexpr int NROW = (Q + 1) * (Q + 2) / 2;
-  static constexpr int NROWP = (NROW + 3) / 4 * 4;
+  static constexpr int NRG = (NROW + 7) / 8;      // 8-row groups
+  static constexpr int NROWP = 8 * NRG;
   static constexpr int CM = PROJ ? 0 : (Q + 1 + 3) / 4 * 4;
   static constexpr int CP = (P + 1 + 3) / 4 * 4;
   static constexpr int NW = CM + CP;
-  static constexpr int NPW = 2 * (Q + 1);  // px[0..Q], py[0..Q]
+  static constexpr int NCB = NW / 4;              // 4-column blocks
   static constexpr int K = PROJ ? 0 : rank3(Q);   // moment entries written per chunk
   static constexpr int L = rank3(P);
 };
 
-struct K4Tab {
-  int ntile;
-  int groups;
-  int batch;
-  int pad;
-  uint8_t rowA[K4_MAXROWP];
-  uint8_t rowB[K4_MAXROWP];
-  uint16_t tile[K4_MAXTILE];  // (row group << 8) | col block
+constexpr int row_s(int r) {
+  int s = 0;
+  while ((s + 1) * (s + 2) / 2 <= r) ++s;
+  return s;
+}
+
+// compile-time geometry: tiles, point groups G, batch B, smem row stride SS = B + 2
+template <int P, bool PROJ>
+struct K4Geo {
+  using S = K4Shape<P, PROJ>;
+  static constexpr int ntile() {
+    int nt = 0;
+    for (int g = 0; g < S::NRG; ++g) {
+      const int smin = row_s(8 * g);  // rows are sorted by s: the first row of a group has the least s
+      nt += PROJ ? 0 : (S::Q - smin + 1 + 3) / 4;
+      if (smin <= P) nt += (P - smin + 1 + 3) / 4;
+    }
+    return nt;
+  }
+  static constexpr int NT = ntile();
+  static constexpr int GMAX = (K4_THREADS / NT) < 64 ? (K4_THREADS / NT) : 64;
+  static constexpr long pick() {  // returns G * 1000 + B maximising thread use, then batch size
+    long best = -1, arg = 1004;
+    for (int G = (GMAX > 0 ? GMAX : 1); G >= 1; --G)
+      for (int k = 1; k <= 64; ++k) {
+        const int B = 2 * G * k;
+        if (B % 4) continue;
+        if (B > 128) break;
+        const long pipe = 2L * (S::NROWP + S::NW) * (B + 2) * 8;
+        if (pipe > (long)K4_SMEM_LIMIT) break;
+        const long score = (long)(G * NT) * 1000 / K4_THREADS * 1000 + (B < 64 ? B : 64);
+        if (score > best) { best = score; arg = (long)G * 1000 + B; }
+      }
+    return arg;
+  }
+  static constexpr int G = (int)(pick() / 1000);
+  static constexpr int B = (int)(pick() % 1000);
+  static constexpr int SS = B + 2;
+  static constexpr int NLG = (B + 31) / 32;
+  static constexpr int BUF = (S::NROWP + S::NW) * SS;  // doubles per pipeline buffer
 };
+
+struct K4Tab {
+  int ntile;          // consumer tiles (needed 8×4 blocks)
+  int groups;         // point groups (tile sets working on disjoint point pairs)
+  int batch;          // points per batch B (multiple of 4)
+  int stride;         // smem row stride S = B + 2 (S ≡ 2 mod 4: bank-spread 16-byte loads)
+  int nlane_groups;   // ceil(B / 32)
+  int ntask;
+  uint16_t tile[K4_MAXTILE];                         // (row group << 8) | col block
+  uint8_t task_a[K4_MAXTASK];                        // 255 = W task, else the x power a of an X task
+  uint8_t task_h[K4_MAXTASK];                        // lane group
+  uint8_t warp_task[K4_WARPS][K4_TASKS_PER_WARP];    // tasks of each warp (255 = none)
+};
+
+// exponents (a, b) of row r in the (s = a+b, a) order
+__host__ __device__ __forceinline__ void row_exponents(int r, int& a, int& b) {
+  int s = 0;
+  while ((s + 1) * (s + 2) / 2 <= r) ++s;
+  a = r - s * (s + 1) / 2;
+  b = s - a;
+}
 
 template <int P, bool PROJ = false>
 K4Tab make_tab() {
   using S = K4Shape<P, PROJ>;
   K4Tab t{};
-  int row = 0;
-  for (int s = 0; s <= S::Q; ++s)
-    for (int a = 0; a <= s; ++a) { t.rowA[row] = (uint8_t)a; t.rowB[row] = (uint8_t)(s - a); ++row; }
-  for (; row < S::NROWP; ++row) { t.rowA[row] = 255; t.rowB[row] = 255; }
   int nt = 0;
-  for (int g = 0; g < S::NROWP / 4; ++g) {
+  for (int g = 0; g < S::NRG; ++g) {
     int smin = 1 << 20;
-    for (int i = 0; i < 4; ++i) {
-      int rr = 4 * g + i;
-      if (rr < S::NROW) smin = std::min(smin, t.rowA[rr] + t.rowB[rr]);
+    for (int i = 0; i < 8; ++i) {
+      const int rr = 8 * g + i;
+      if (rr < S::NROW) { int a, b; row_exponents(rr, a, b); smin = std::min(smin, a + b); }
     }
-    int nm = PROJ ? 0 : (S::Q - smin + 1 + 3) / 4;
+    const int nm = PROJ ? 0 : (S::Q - smin + 1 + 3) / 4;
     for (int cb = 0; cb < nm; ++cb) t.tile[nt++] = (uint16_t)((g << 8) | cb);
     if (smin <= P) {
-      int np = (P - smin + 1 + 3) / 4;
+      const int np = (P - smin + 1 + 3) / 4;
       for (int cb = 0; cb < np; ++cb) t.tile[nt++] = (uint16_t)((g << 8) | (S::CM / 4 + cb));
     }
   }
   t.ntile = nt;
-  t.groups = std::max(1, K4_THREADS / nt);
-  // points per batch: a multiple of the group count, ~32-48 points
-  int per = std::max(1, (40 + t.groups - 1) / t.groups);
-  t.batch = per * t.groups;
-  if (t.batch > 64) t.batch = t.groups * std::max(1, 64 / t.groups);
+  using Geo = K4Geo<P, PROJ>;
+  static_assert(Geo::NT <= K4_MAXTILE, "tile table too small");
+  t.groups = Geo::G;
+  t.batch = Geo::B;
+  t.stride = Geo::SS;
+  t.nlane_groups = Geo::NLG;
+  // production tasks: X rows for every power a of x and lane group, one W task per lane group;
+  // longest-processing-time assignment to the 16 warps
+  struct Task { int a, h, len; };
+  std::vector<Task> tasks;
+  for (int h = 0; h < t.nlane_groups; ++h) {
+    for (int a = 0; a <= S::Q; ++a) tasks.push_back({a, h, S::Q - a + 1 + 4});
+    tasks.push_back({255, h, S::NW});
+  }
+  std::sort(tasks.begin(), tasks.end(), [](const Task& x, const Task& y) { return x.len > y.len; });
+  t.ntask = (int)tasks.size();
+  std::vector<int> load(K4_WARPS, 0), cnt(K4_WARPS, 0);
+  for (int w = 0; w < K4_WARPS; ++w)
+    for (int k = 0; k < K4_TASKS_PER_WARP; ++k) t.warp_task[w][k] = 255;
+  for (int i = 0; i < t.ntask; ++i) {
+    int w = 0;
+    for (int v = 1; v < K4_WARPS; ++v)
+      if (cnt[v] < K4_TASKS_PER_WARP && (load[v] < load[w] || cnt[w] >= K4_TASKS_PER_WARP)) w = v;
+    t.task_a[i] = (uint8_t)tasks[i].a;
+    t.task_h[i] = (uint8_t)tasks[i].h;
+    t.warp_task[w][cnt[w]++] = (uint8_t)i;
+    load[w] += tasks[i].len;
+  }
   return t;
 }
 
 template <int P, bool PROJ = false>
 size_t k4_smem_bytes(const K4Tab& t) {
   using S = K4Shape<P, PROJ>;
-  size_t pipe = (size_t)t.batch * (2 * S::NROWP + 3 * S::NW + 2 * S::NPW);
-  size_t red = (size_t)t.groups * t.ntile * 16;
+  const size_t pipe = (size_t)2 * (S::NROWP + S::NW) * K4Geo<P, PROJ>::SS;
+  const size_t red = (size_t)t.groups * t.ntile * 32;
   return std::max(pipe, red) * sizeof(double);
+}
+
+// x^a by binary exponentiation (a <= 20)
+__device__ __forceinline__ double ipow(double x, int a) {
+  double r = 1.0, b = x;
+  while (a) {
+    if (a & 1) r *= b;
+    b *= b;
+    a >>= 1;
+  }
+  return r;
+}
+
+// rows (AA, b), b = 0..Q-AA, of one point: X(AA, b) = x^AA y^b at compile-time slots (row-in-tile major)
+template <typename S, int SS, int AA>
+__device__ __forceinline__ void xrow(double x, double y, double* Xj) {
+  if constexpr (AA <= S::Q) {
+    double v = 1.0;
+#pragma unroll
+    for (int e = 0; e < AA; ++e) v *= x;
+#pragma unroll
+    for (int b = 0; b <= S::Q - AA; ++b) {
+      const int s = AA + b;
+      const int row = s * (s + 1) / 2 + AA;
+      Xj[((row & 7) * S::NRG + (row >> 3)) * SS] = v;
+      v *= y;
+    }
+  }
 }
 
 template <int P, bool PROJ>
 __global__ void __launch_bounds__(K4_THREADS, 1)
     k_moments(const double* __restrict__ ux, const double* __restrict__ uy, const double* __restrict__ uz,
               const double* __restrict__ r, const int4* __restrict__ cell, int64_t first,
-              const Chunk* __restrict__ chunks, const int64_t* __restrict__ nchunks, const __grid_constant__ K4Tab tab,
-              const int32_t* __restrict__ skip_flag, double* __restrict__ partial) {
+              const Chunk* __restrict__ chunks, const int64_t* __restrict__ nchunks,
+              const __grid_constant__ K4Tab tab, const int32_t* __restrict__ skip_flag,
+              double* __restrict__ partial) {
   using S = K4Shape<P, PROJ>;
   constexpr int Q = S::Q;
-  extern __shared__ double smem[];
+  extern __shared__ __align__(16) double smem[];
   const int64_t cidx = blockIdx.x;
   if (cidx >= *nchunks) return;
   const Chunk ck = chunks[cidx];
@@ -108,85 +217,100 @@ __global__ void __launch_bounds__(K4_THREADS, 1)
   const double scale = ldexp(1.0, c.w + 1);
   const double cx = (2.0 * c.x + 1.0) * h, cy = (2.0 * c.y + 1.0) * h, cz = (2.0 * c.z + 1.0) * h;
 
-  const int B = tab.batch, G = tab.groups, NT = tab.ntile;
-  double* sX = smem;                              // [2][B][NROWP]
-  double* sW = sX + 2 * B * S::NROWP;             // [3][B][NW]
-  double* sP = sW + 3 * B * S::NW;                // [2][B][NPW]
-  const int tid = threadIdx.x;
+  using Geo = K4Geo<P, PROJ>;
+  constexpr int B = Geo::B, SS = Geo::SS, G = Geo::G, NT = Geo::NT, bufsz = Geo::BUF;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int grp = tid / NT;
   const int t = tid - grp * NT;
   const bool worker = grp < G;
   int rg = 0, cb = 0;
   if (worker) { rg = tab.tile[t] >> 8; cb = tab.tile[t] & 255; }
 
-  double acc[16];
-#pragma unroll
-  for (int k = 0; k < 16; ++k) acc[k] = 0.0;
-
   const int64_t n = ck.end - ck.start;
   const int nbatch = (int)((n + B - 1) / B);
 
-  for (int it = -2; it < nbatch; ++it) {
-    // stage A (batch it+2): local coordinates, powers, W row
-    const int ia = it + 2;
-    if (ia < nbatch && tid < B) {
-      const int64_t pi = ck.start + (int64_t)ia * B + tid;
-      double* Pp = sP + (ia & 1) * B * S::NPW + tid * S::NPW;
-      double* Wp = sW + (ia % 3) * B * S::NW + tid * S::NW;
-      if (pi < ck.end) {
-        const double x = __dmul_rn(__dsub_rn(ux[pi], cx), scale);
-        const double y = __dmul_rn(__dsub_rn(uy[pi], cy), scale);
-        const double z = __dmul_rn(__dsub_rn(uz[pi], cz), scale);
-        const double rv = r[pi];
-        double px = 1.0, py = 1.0, pz = 1.0;
-#pragma unroll
-        for (int q = 0; q <= Q; ++q) {
-          Pp[q] = px;
-          Pp[Q + 1 + q] = py;
-          Wp[q] = pz;
-          if (q <= P) Wp[S::CM + q] = rv * pz;
-          px *= x; py *= y; pz *= z;
+  // producer: fill buffer `buf` with batch `bi` (every offset below is a compile-time constant)
+  auto produce = [&](int bi, int buf) {
+    double* X = smem + buf * bufsz;
+    double* W = X + S::NROWP * SS;
+    const int64_t base = ck.start + (int64_t)bi * B;
+#pragma unroll 1
+    for (int k = 0; k < K4_TASKS_PER_WARP; ++k) {
+      const int ti = tab.warp_task[warp][k];
+      if (ti == 255) break;
+      const int a = tab.task_a[ti];
+      const int j = 32 * tab.task_h[ti] + lane;
+      const bool inb = j < B;
+      const int64_t pi = base + j;
+      const bool valid = inb && pi < ck.end;
+      if (a != 255) {  // X task: rows (a, b), b = 0..Q-a, one fully unrolled walk per power a
+        const double x = valid ? __dmul_rn(__dsub_rn(ux[pi], cx), scale) : 0.0;
+        const double y = valid ? __dmul_rn(__dsub_rn(uy[pi], cy), scale) : 0.0;
+        if (inb) {
+          double* Xj = X + j;
+          switch (a) {
+#define FMI_XCASE(AA) case AA: xrow<S, SS, AA>(x, y, Xj); break;
+            FMI_XCASE(0) FMI_XCASE(1) FMI_XCASE(2) FMI_XCASE(3) FMI_XCASE(4) FMI_XCASE(5) FMI_XCASE(6)
+            FMI_XCASE(7) FMI_XCASE(8) FMI_XCASE(9) FMI_XCASE(10) FMI_XCASE(11) FMI_XCASE(12) FMI_XCASE(13)
+            FMI_XCASE(14) FMI_XCASE(15) FMI_XCASE(16) FMI_XCASE(17) FMI_XCASE(18) FMI_XCASE(19) FMI_XCASE(20)
+#undef FMI_XCASE
+            default: break;
+          }
         }
+      } else if (inb) {  // W task: z^c (moments) and r z^c (projection); zero for padded points
+        const double z = valid ? __dmul_rn(__dsub_rn(uz[pi], cz), scale) : 0.0;
+        const double rv = valid ? r[pi] : 0.0;
+        double* Wj = W + j;
+        double v = valid ? 1.0 : 0.0;
 #pragma unroll
-        for (int q = Q + 1; q < S::CM; ++q) Wp[q] = 0.0;
+        for (int col = 0; col < S::CM; ++col) {
+          Wj[((col & 3) * S::NCB + (col >> 2)) * SS] = (col <= Q) ? v : 0.0;
+          v *= z;
+        }
+        v = rv;
 #pragma unroll
-        for (int q = S::CM + P + 1; q < S::NW; ++q) Wp[q] = 0.0;
-      } else {
-#pragma unroll
-        for (int q = 0; q < S::NPW; ++q) Pp[q] = 0.0;
-#pragma unroll
-        for (int q = 0; q < S::NW; ++q) Wp[q] = 0.0;
+        for (int col = S::CM; col < S::NW; ++col) {
+          Wj[((col & 3) * S::NCB + (col >> 2)) * SS] = (col - S::CM <= P) ? v : 0.0;
+          v *= z;
+        }
       }
     }
-    // stage B (batch it+1): X(a,b) = x^a y^b
-    const int ib = it + 1;
-    if (ib >= 0 && ib < nbatch) {
-      const double* Pp = sP + (ib & 1) * B * S::NPW;
-      double* Xp = sX + (ib & 1) * B * S::NROWP;
-      for (int e = tid; e < B * S::NROWP; e += K4_THREADS) {
-        const int j = e / S::NROWP;
-        const int row = e - j * S::NROWP;
-        const int a = tab.rowA[row], b = tab.rowB[row];
-        Xp[e] = (a <= Q) ? Pp[j * S::NPW + a] * Pp[j * S::NPW + Q + 1 + b] : 0.0;
+    // padded rows of the last 8-row group stay zero
+    if (S::NROWP > S::NROW) {
+      for (int row = S::NROW + warp; row < S::NROWP; row += K4_WARPS) {
+        const int slot = (row & 7) * S::NRG + (row >> 3);
+        for (int j = lane; j < B; j += 32) X[slot * SS + j] = 0.0;
       }
     }
-    // stage C (batch it): 4×4 register-tile outer products
-    if (it >= 0 && worker) {
-      const double* Xp = sX + (it & 1) * B * S::NROWP + 4 * rg;
-      const double* Wp = sW + (it % 3) * B * S::NW + 4 * cb;
-      const int nb = (int)min((int64_t)B, n - (int64_t)it * B);
-#pragma unroll 2
-      for (int j = grp; j < nb; j += G) {
-        const double2 x01 = *reinterpret_cast<const double2*>(Xp + j * S::NROWP);
-        const double2 x23 = *reinterpret_cast<const double2*>(Xp + j * S::NROWP + 2);
-        const double2 w01 = *reinterpret_cast<const double2*>(Wp + j * S::NW);
-        const double2 w23 = *reinterpret_cast<const double2*>(Wp + j * S::NW + 2);
-        const double xv[4] = {x01.x, x01.y, x23.x, x23.y};
-        const double wv[4] = {w01.x, w01.y, w23.x, w23.y};
+  };
+
+  double acc[32];
 #pragma unroll
-        for (int i = 0; i < 4; ++i)
+  for (int k = 0; k < 32; ++k) acc[k] = 0.0;
+
+  produce(0, 0);
+  __syncthreads();
+  for (int it = 0; it < nbatch; ++it) {
+    if (it + 1 < nbatch) produce(it + 1, (it + 1) & 1);
+    if (worker) {
+      const double* X = smem + (it & 1) * bufsz + rg * SS;            // slot (i, rg) = i*NRG + rg
+      const double* W = smem + (it & 1) * bufsz + S::NROWP * SS + cb * SS;
+      const int npairs = (int)((min((int64_t)B, n - (int64_t)it * B) + 1) >> 1);
+#pragma unroll 1
+      for (int pp = grp; pp < npairs; pp += G) {
+        const int j = 2 * pp;
+        double2 xv[8], wv[4];
 #pragma unroll
-          for (int k = 0; k < 4; ++k) acc[i * 4 + k] = fma(xv[i], wv[k], acc[i * 4 + k]);
+        for (int i = 0; i < 8; ++i) xv[i] = *reinterpret_cast<const double2*>(X + i * (S::NRG * SS) + j);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) wv[k] = *reinterpret_cast<const double2*>(W + k * (S::NCB * SS) + j);
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            acc[i * 4 + k] = fma(xv[i].x, wv[k].x, acc[i * 4 + k]);
+            acc[i * 4 + k] = fma(xv[i].y, wv[k].y, acc[i * 4 + k]);
+          }
       }
     }
     __syncthreads();
@@ -196,20 +320,20 @@ __global__ void __launch_bounds__(K4_THREADS, 1)
   double* red = smem;
   if (worker) {
 #pragma unroll
-    for (int k = 0; k < 16; ++k) red[(grp * NT + t) * 16 + k] = acc[k];
+    for (int k = 0; k < 32; ++k) red[(grp * NT + t) * 32 + k] = acc[k];
   }
   __syncthreads();
   if (grp == 0 && worker) {
     double* out = partial + cidx * (int64_t)(S::K + S::L);
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const int row = 4 * rg + i;
-      const int a = tab.rowA[row], b = tab.rowB[row];
-      if (a > Q) continue;
+    for (int i = 0; i < 8; ++i) {
+      const int row = 8 * rg + i;
+      if (row >= S::NROW) continue;
+      int a, b;
+      row_exponents(row, a, b);
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
         double v = 0.0;
-        for (int g = 0; g < G; ++g) v += red[(g * NT + t) * 16 + i * 4 + k];
+        for (int g = 0; g < G; ++g) v += red[(g * NT + t) * 32 + i * 4 + k];
         const int col = 4 * cb + k;
         if (col < S::CM) {
           if (!PROJ && a + b + col <= Q) out[basis_index(Q, a, b, col)] = v;

@@ -67,6 +67,10 @@ __global__ void __launch_bounds__(K5_THREADS)
   const int lane = tid & 31, warp = tid >> 5;
   constexpr int NWARP = K5_THREADS / 32;
   __shared__ double smin_sh[1];
+  // basis exponents in shared memory (thread-divergent lookups into the parameter bank serialise)
+  __shared__ uint8_t bl[L], bm[L], bn[L];
+  for (int i = tid; i < L; i += K5_THREADS) { bl[i] = bt.l[i]; bm[i] = bt.m[i]; bn[i] = bt.n[i]; }
+  __syncthreads();
   __shared__ double redw[2 * NWARP];
 
   for (int64_t node = blockIdx.x; node < count; node += gridDim.x) {
@@ -81,7 +85,7 @@ __global__ void __launch_bounds__(K5_THREADS)
     for (int e = tid; e < L; e += K5_THREADS) sb[e] = bp[e];
     __syncthreads();
     for (int i = tid; i < L; i += K5_THREADS) {
-      const double m2 = sM[basis_index(Q, 2 * bt.l[i], 2 * bt.m[i], 2 * bt.n[i])];
+      const double m2 = sM[basis_index(Q, 2 * bl[i], 2 * bm[i], 2 * bn[i])];
       const double di = m2 > 0.0 ? 1.0 / sqrt(m2) : 0.0;
       dinv[i] = di;
       sb[i] *= di;
@@ -92,7 +96,7 @@ __global__ void __launch_bounds__(K5_THREADS)
       while (tri(i + 1) <= e) ++i;
       while (tri(i) > e) --i;
       const int k = (int)(e - tri(i));
-      const double g = sM[basis_index(Q, bt.l[i] + bt.l[k], bt.m[i] + bt.m[k], bt.n[i] + bt.n[k])];
+      const double g = sM[basis_index(Q, bl[i] + bl[k], bm[i] + bm[k], bn[i] + bn[k])];
       A[e] = g * dinv[i] * dinv[k];
     }
     __syncthreads();

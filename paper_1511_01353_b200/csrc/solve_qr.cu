@@ -66,13 +66,16 @@ __global__ void __launch_bounds__(KQ_THREADS)
   double* A = scratch + (int64_t)blockIdx.x * LA * LD;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   constexpr int NWARP = KQ_THREADS / 32;
+  __shared__ uint8_t bl[L], bm[L], bn[L];
+  for (int i = tid; i < L; i += KQ_THREADS) { bl[i] = bt.l[i]; bm[i] = bt.m[i]; bn[i] = bt.n[i]; }
+  __syncthreads();
 
   for (int64_t ln = blockIdx.x; ln < count; ln += gridDim.x) {
     const int64_t node = first + ln;
     if (!(nt.flag[node] & 1)) continue;
     const double* mp = mom + ln * (int64_t)(K + L);
     for (int i = tid; i < L; i += KQ_THREADS) {
-      const double m2 = mp[basis_index(Q, 2 * bt.l[i], 2 * bt.m[i], 2 * bt.n[i])];
+      const double m2 = mp[basis_index(Q, 2 * bl[i], 2 * bm[i], 2 * bn[i])];
       dinv[i] = m2 > 0.0 ? 1.0 / sqrt(m2) : 0.0;
     }
     if (tid == 0) dinv[L] = 1.0;  // the residual column is not scaled
@@ -97,9 +100,9 @@ __global__ void __launch_bounds__(KQ_THREADS)
             const double y = __dmul_rn(__dsub_rn(uy[pi], cy), scale);
             const double z = __dmul_rn(__dsub_rn(uz[pi], cz), scale);
             double m = 1.0;
-            for (int k = 0; k < bt.l[col]; ++k) m *= x;
-            for (int k = 0; k < bt.m[col]; ++k) m *= y;
-            for (int k = 0; k < bt.n[col]; ++k) m *= z;
+            for (int k = 0; k < bl[col]; ++k) m *= x;
+            for (int k = 0; k < bm[col]; ++k) m *= y;
+            for (int k = 0; k < bn[col]; ++k) m *= z;
             val = m * dinv[col];
           } else {
             val = r[pi];
