@@ -132,6 +132,12 @@ int fmi_residual(const fmi_tree* tree, double* out);
  * number of points in active nodes (point-levels). Returns the number of levels. */
 int fmi_level_stats(const fmi_tree* tree, int64_t* nodes, int64_t* points, int cap);
 
+/* Build statistics: out[0] = moment-tree nodes (every cell with >= 𝓛 points down to max_depth),
+ * out[1] = fit nodes whose translated moments failed the rounding check and were re-accumulated
+ * directly, out[2] = fit nodes that took semi-normal refinement steps.  Returns the number of
+ * statistics (3) or a negative code; writes min(cap, 3) entries. */
+int fmi_build_stats(const fmi_tree* tree, int64_t* out, int cap);
+
 /* ------------------------------------------------------------------------------------------------
  * Profiling (bench.py).  When enabled, every kernel launch of the library is bracketed by CUDA
  * events on the library stream; fmi_profile_get returns, per kernel name, the summed device time
@@ -140,8 +146,8 @@ int fmi_level_stats(const fmi_tree* tree, int64_t* nodes, int64_t* points, int c
 int fmi_profile_enable(int on);
 int fmi_profile_reset(void);
 /* kernel names: "keys", "sort", "gather", "moments", "moments_reduce", "solve", "children",
- * "residual", "residual_reduce", "decide", "chunks", "scan", "eval", "misc", "project",
- * "refine_solve" */
+ * "residual", "residual_reduce", "decide", "chunks", "scan", "eval", "misc", "project", "m2m",
+ * "level_gather", "refine_solve", "refine" */
 int fmi_profile_get(const char* kernel, double* total_ms, int64_t* launches);
 /* Total kernel launches issued by the library since load (or since fmi_profile_reset). */
 int64_t fmi_launch_count(void);

@@ -1,10 +1,10 @@
 // fmi_api.cu — the C ABI (include/fmi.h) and the host orchestration of the level-synchronous build.
 //
 // fmi_build runs PAPER.md Algorithm 1 breadth-first: all nodes of one depth form a level,
-// and every step of the level runs as a device kernel over all of its nodes at once:
-//   K3 octant block bounds -> K4 moments+projection (Alg. 2 Λ / QR / Qᵀf)
-//   -> K5 node solve -> K6 residual update + block energies
-//   -> decisions + compaction of the next level.
+// and every step of the level runs as a device kernel over all of its nodes at once (run_levels):
+//   moment tree + raw moments once per build (K4 + M2M: the Gram of Alg. 2)
+//   per level: K5 node solve -> fused K6 residual update + block energies + child
+//   projections (Qᵀf of the children) -> decisions + compaction.
 // The only host synchronisation per level is one 16-byte read of the next level's size.
 #include <cuda_runtime.h>
 
@@ -121,7 +121,7 @@ cudaEvent_t get_event() {
 const char* kNames[KID_COUNT] = {"keys",     "sort",     "gather", "moments", "moments_reduce",
                                  "solve",    "children", "residual", "residual_reduce",
                                  "decide",   "chunks",   "scan",   "eval",    "misc",
-                                 "project",  "refine_solve"};
+                                 "project",  "m2m",      "level_gather", "refine_solve", "refine"};
 }  // namespace
 
 const char* kernel_name(int kid) { return (kid >= 0 && kid < KID_COUNT) ? kNames[kid] : "?"; }
@@ -166,7 +166,8 @@ void prof_collect() {
 // ------------------------------------------------------------------------------------------------
 struct fmi_tree {
   int p = 0, L = 0, K = 0, D = 0, Dk = 0, depth_max = 0;
-  int refine = 2;  // max semi-normal refinement steps per level (env FMI_REFINE); adaptive per node
+  int refine_steps = kRefineSteps;   // env FMI_REFINE_STEPS
+  double refine2 = kRefinePivot2;    // env FMI_REFINE_PIVOT2
   double tau = 0;
   double lo[3] = {0, 0, 0};
   double width = 1;
@@ -176,6 +177,9 @@ struct fmi_tree {
   int64_t cap = 0;
   NodeTable nt;
   std::vector<int64_t> lvl_first, lvl_count, lvl_points;
+  int64_t mt_nodes = 0;       // moment-tree size (introspection)
+  int64_t direct_nodes = 0;   // fit nodes whose moments were re-accumulated directly (M2M check)
+  int64_t refined_nodes = 0;  // fit nodes that took semi-normal refinement steps
   double* residual = nullptr;  // Morton order
   uint32_t* perm = nullptr;    // Morton position -> input index
   cudaStream_t stream = 0;
@@ -186,7 +190,7 @@ namespace {
 void free_table(NodeTable& t, cudaStream_t s) {
   dfree(t.start, s); dfree(t.end, s); dfree(t.cell, s); dfree(t.parent, s); dfree(t.child, s);
   dfree(t.child_start, s); dfree(t.child_ss, s); dfree(t.coef, s); dfree(t.rms, s); dfree(t.minpiv, s);
-  dfree(t.rank, s); dfree(t.flag, s);
+  dfree(t.rank, s); dfree(t.flag, s); dfree(t.mtid, s);
   t = NodeTable{};
 }
 
@@ -198,24 +202,41 @@ void grow_array(T*& p, int64_t old_n, int64_t new_n, cudaStream_t s) {
   p = q;
 }
 
-void ensure_capacity(fmi_tree* T, int64_t need, cudaStream_t s) {
-  if (need <= T->cap) return;
-  int64_t nc = std::max<int64_t>(need, std::max<int64_t>(1024, T->cap * 2));
-  const int64_t keep = T->cap;  // copy every existing slot (children of the current level included)
-  NodeTable& t = T->nt;
+// grow a node table to hold `need` nodes; fit = false: geometry fields only (moment tree)
+void ensure_table(NodeTable& t, int64_t& cap, int64_t need, int L, bool fit, cudaStream_t s) {
+  if (need <= cap) return;
+  int64_t nc = std::max<int64_t>(need, std::max<int64_t>(1024, cap * 2));
+  const int64_t keep = cap;  // copy every existing slot (children of the current level included)
   grow_array(t.start, keep, nc, s);
   grow_array(t.end, keep, nc, s);
   grow_array(t.cell, keep, nc, s);
   grow_array(t.parent, keep, nc, s);
   grow_array(t.child, keep * 8, nc * 8, s);
   grow_array(t.child_start, keep * 9, nc * 9, s);
-  grow_array(t.child_ss, keep * 8, nc * 8, s);
-  grow_array(t.coef, keep * T->L, nc * T->L, s);
-  grow_array(t.rms, keep, nc, s);
-  grow_array(t.minpiv, keep, nc, s);
-  grow_array(t.rank, keep, nc, s);
-  grow_array(t.flag, keep, nc, s);
-  T->cap = nc;
+  if (fit) {
+    grow_array(t.child_ss, keep * 8, nc * 8, s);
+    grow_array(t.coef, keep * L, nc * L, s);
+    grow_array(t.rms, keep, nc, s);
+    grow_array(t.minpiv, keep, nc, s);
+    grow_array(t.rank, keep, nc, s);
+    grow_array(t.flag, keep, nc, s);
+    grow_array(t.mtid, keep, nc, s);
+  }
+  cap = nc;
+}
+
+void set_root(NodeTable& t, int64_t N, bool fit, cudaStream_t s) {
+  int64_t st = 0, en = N;
+  int4 c = make_int4(0, 0, 0, 0);
+  int32_t par = -1, mt = 0;
+  std::vector<int32_t> ch(8, -1);
+  FMI_CK(cudaMemcpyAsync(t.start, &st, sizeof st, cudaMemcpyHostToDevice, s));
+  FMI_CK(cudaMemcpyAsync(t.end, &en, sizeof en, cudaMemcpyHostToDevice, s));
+  FMI_CK(cudaMemcpyAsync(t.cell, &c, sizeof c, cudaMemcpyHostToDevice, s));
+  FMI_CK(cudaMemcpyAsync(t.parent, &par, sizeof par, cudaMemcpyHostToDevice, s));
+  FMI_CK(cudaMemcpyAsync(t.child, ch.data(), 8 * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+  if (fit) FMI_CK(cudaMemcpyAsync(t.mtid, &mt, sizeof mt, cudaMemcpyHostToDevice, s));
+  FMI_CK(cudaStreamSynchronize(s));  // host staging values above live on this frame
 }
 
 bool is_device_ptr(const void* p) {
@@ -232,83 +253,161 @@ int64_t choose_chunk(int64_t points, int64_t min_ch, int64_t per_sm_chunks) {
   return std::max(min_ch, target);
 }
 
+// Level-synchronous build:
+//  A. moment tree: every cell with >= 𝓛 points down to max_depth (integer guards of P:306 + G5,
+//     ignoring τ) — the fit tree is a subtree of it;
+//  B. raw moments of every moment-tree node: one pass over all points (owner segments), then the
+//     upward translation (M2M), deepest level first;
+//  C. root projection (one pass), then per fit level: gather [moments | projection] -> K5 solve
+//     (+ K5q QR re-fit of flagged nodes) -> fused K6 (residual, block energies, child projections)
+//     -> decisions + compaction.  One 16-byte D2H per level (the next level's size).
 template <int P>
 void run_levels(fmi_tree* T, const uint64_t* keys, double* ux, double* uy, double* uz, double* r, cudaStream_t s) {
   constexpr int L = rank3(P), K = rank3(2 * P);
-  // root node
-  ensure_capacity(T, 16, s);
-  {
-    int64_t st = 0, en = T->N;
-    int4 c = make_int4(0, 0, 0, 0);
-    int32_t par = -1;
-    std::vector<int32_t> ch(8, -1);
-    FMI_CK(cudaMemcpyAsync(T->nt.start, &st, sizeof st, cudaMemcpyHostToDevice, s));
-    FMI_CK(cudaMemcpyAsync(T->nt.end, &en, sizeof en, cudaMemcpyHostToDevice, s));
-    FMI_CK(cudaMemcpyAsync(T->nt.cell, &c, sizeof c, cudaMemcpyHostToDevice, s));
-    FMI_CK(cudaMemcpyAsync(T->nt.parent, &par, sizeof par, cudaMemcpyHostToDevice, s));
-    FMI_CK(cudaMemcpyAsync(T->nt.child, ch.data(), 8 * sizeof(int32_t), cudaMemcpyHostToDevice, s));
-    FMI_CK(cudaStreamSynchronize(s));  // host staging values above live on this frame
-  }
-  T->nodes = 1;
-  int64_t first = 0, count = 1, points = T->N;
-  DBuf<int64_t> counts, begin4, begin6, flags, scan, dev_small(4, s);
-  DBuf<Chunk> chunks4, chunks6;
-  DBuf<double> partial, mom, segpart, scratch, proj, delta;
-  DBuf<uint8_t> skip;
+  DBuf<int64_t> counts, begin, flags, scan, dev_small(4, s), nflag(2, s);
+  DBuf<Chunk> chunks;
+  DBuf<double> partial, mtmom, mtbnd, segsum, lvlmom, scratch, delta;
+  DBuf<int32_t> srcseg;
   int64_t* host_small = nullptr;
   FMI_CK(cudaMallocHost(&host_small, 4 * sizeof(int64_t)));
-  const size_t scr_per_node = solve_scratch_per_node(P);
-  const int64_t scr_nodes = scr_per_node ? 2048 : 0;
-  if (scr_nodes) scratch.alloc((size_t)scr_nodes * scr_per_node / sizeof(double), s);
-  const int64_t qr_slots = 148;
-  DBuf<double> qr_scratch((size_t)qr_slots * solve_qr_scratch_per_cta(P) / sizeof(double), s);
+  NodeTable mt;
+  int64_t mt_cap = 0;
   try {
+    // ---- A. moment tree --------------------------------------------------------------------------
+    std::vector<int64_t> mfirst, mcount;
+    ensure_table(mt, mt_cap, 16, L, false, s);
+    set_root(mt, T->N, false, s);
+    {
+      int64_t first = 0, count = 1;
+      for (int depth = 0; count > 0; ++depth) {
+        mfirst.push_back(first);
+        mcount.push_back(count);
+        ensure_table(mt, mt_cap, first + count + 8 * count, L, false, s);
+        LevelCtx c{keys, ux, uy, uz, r, mt, first, count, depth, T->D, T->Dk, P, L, K, T->tau};
+        level_children(c, s);
+        flags.ensure(count * 8, s);
+        scan.ensure(count * 8, s);
+        level_decide(c, true, nullptr, nullptr, flags.p, scan.p, dev_small.p + 2, s);
+        FMI_CK(cudaMemcpyAsync(host_small, dev_small.p + 2, 2 * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+        FMI_CK(cudaStreamSynchronize(s));
+        first += count;
+        count = host_small[0];
+      }
+      T->mt_nodes = first;
+    }
+    const int64_t MT = T->mt_nodes;
+    // ---- B. owner-segment moments + M2M (with rounding bounds) ------------------------------------
+    {
+      const int64_t ch = kMomentChunk;
+      const int64_t maxc = T->N / ch + 8 * MT + 1;
+      counts.ensure(MT * 8, s);
+      begin.ensure(MT * 8, s);
+      chunks.ensure(maxc, s);
+      make_chunks(mt.child_start, nullptr, MT * 8, ch, counts.p, begin.p, dev_small.p, chunks.p, maxc, s, mt.child);
+      FMI_CK(cudaMemcpyAsync(host_small, dev_small.p, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+      FMI_CK(cudaStreamSynchronize(s));
+      const int64_t nch = std::min(host_small[0], maxc);
+      partial.ensure((size_t)nch * K, s);
+      mtmom.alloc((size_t)MT * K, s);
+      mtbnd.alloc((size_t)MT * K, s);
+      direct_moments<P>(ux, uy, uz, mt.cell, 3, chunks.p, dev_small.p, nch, partial.p, s);
+      reduce_moments(partial.p, begin.p, dev_small.p, MT, 8, K, nullptr, 0, mtmom.p, K, s);
+      bound_init(mt, MT, K, mtbnd.p, s);
+      for (int d = (int)mfirst.size() - 2; d >= 0; --d)
+        m2m_level<P>(mtmom.p, mtbnd.p, mt.child, mfirst[d], mcount[d], s);
+    }
+    // ---- C. fit levels ---------------------------------------------------------------------------
+    ensure_table(T->nt, T->cap, 16, L, true, s);
+    set_root(T->nt, T->N, true, s);
+    T->nodes = 1;
+    int64_t first = 0, count = 1, points = T->N;
+    {  // root projection b = Λᵀf in the root frame
+      LevelCtx c{keys, ux, uy, uz, r, T->nt, 0, 1, 0, T->D, T->Dk, P, L, K, T->tau};
+      const int64_t ch = choose_chunk(T->N, 1024, 8);
+      const int64_t maxc = T->N / ch + 2;
+      counts.ensure(8, s);
+      begin.ensure(8, s);
+      chunks.ensure(maxc, s);
+      make_chunks(T->nt.start, T->nt.end, 1, ch, counts.p, begin.p, dev_small.p, chunks.p, maxc, s);
+      partial.ensure((size_t)maxc * (L + 1), s);
+      segsum.ensure((size_t)(L + 1), s);
+      level_residual<P>(c, K6_ROOT, 0, nullptr, chunks.p, dev_small.p, maxc, begin.p, 1, partial.p, segsum.p, s);
+      lvlmom.ensure((size_t)(2 * K + L), s);
+      gather_level(mtmom.p, mtbnd.p, T->nt.mtid, segsum.p, nullptr, 0, 1, K, L, lvlmom.p, s);
+    }
+    const size_t scr_per_node = solve_scratch_per_node(P);
+    const int64_t scr_nodes = scr_per_node ? 2048 : 0;
+    if (scr_nodes) scratch.alloc((size_t)scr_nodes * scr_per_node / sizeof(double), s);
+    const int64_t qr_slots = 148;
+    DBuf<double> qr_scratch((size_t)qr_slots * solve_qr_scratch_per_cta(P) / sizeof(double), s);
     for (int depth = 0; count > 0; ++depth) {
       T->lvl_first.push_back(first);
       T->lvl_count.push_back(count);
       T->lvl_points.push_back(points);
       T->depth_max = depth;
-      ensure_capacity(T, first + count + 8 * count, s);
+      ensure_table(T->nt, T->cap, first + count + 8 * count, L, true, s);
       LevelCtx c{keys, ux, uy, uz, r, T->nt, first, count, depth, T->D, T->Dk, P, L, K, T->tau};
       level_children(c, s);
-      // K4 chunk list over the level's nodes
-      const int64_t ch4 = choose_chunk(points, 256, 4);
-      const int64_t max4 = points / ch4 + count + 1;
-      counts.ensure(std::max<int64_t>(count * 8, 1), s);
-      begin4.ensure(count, s);
-      chunks4.ensure(max4, s);
-      make_chunks(T->nt.start + first, T->nt.end + first, count, ch4, counts.p, begin4.p, dev_small.p, chunks4.p,
-                  max4, s);
-      partial.ensure((size_t)max4 * (K + L), s);
-      mom.ensure((size_t)count * (K + L), s);
-      level_moments<P>(c, chunks4.p, dev_small.p, max4, begin4.p, partial.p, mom.p, s);
-      level_solve<P>(c, mom.p, nullptr, nullptr, nullptr, scratch.p, scr_nodes, s);
-      level_solve_qr<P>(c, mom.p, qr_scratch.p, qr_slots, s);
-      // K6 chunk list over the level's octant segments
+      // K5: solve; nodes whose translated moments fail the rounding check are re-accumulated directly
+      FMI_CK(cudaMemsetAsync(nflag.p, 0, 2 * sizeof(int64_t), s));
+      level_solve<P>(c, lvlmom.p, 0, nullptr, nullptr, T->refine2, nflag.p, scratch.p, scr_nodes, s);
+      FMI_CK(cudaMemcpyAsync(&host_small[2], nflag.p, 2 * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+      FMI_CK(cudaStreamSynchronize(s));
+      if (host_small[3] > 0) {
+        const int64_t chd = kMomentChunk;
+        const int64_t maxd = points / chd + count + 1;
+        counts.ensure(count, s);
+        begin.ensure(count, s);
+        chunks.ensure(maxd, s);
+        make_chunks(T->nt.start + first, T->nt.end + first, count, chd, counts.p, begin.p, dev_small.p, chunks.p,
+                    maxd, s, nullptr, T->nt.flag + first, 4);
+        FMI_CK(cudaMemcpyAsync(host_small, dev_small.p, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+        FMI_CK(cudaStreamSynchronize(s));
+        const int64_t nchd = std::min(host_small[0], maxd);
+        partial.ensure((size_t)nchd * K, s);
+        direct_moments<P>(ux, uy, uz, T->nt.cell + first, 0, chunks.p, dev_small.p, nchd, partial.p, s);
+        reduce_moments(partial.p, begin.p, dev_small.p, count, 1, K, T->nt.flag + first, 4, lvlmom.p, 2 * K + L, s);
+        level_solve<P>(c, lvlmom.p, 2, nullptr, nullptr, T->refine2, nflag.p, scratch.p, scr_nodes, s);
+        FMI_CK(cudaMemcpyAsync(&host_small[2], nflag.p, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+        FMI_CK(cudaStreamSynchronize(s));
+        T->direct_nodes += host_small[3];
+      }
+      const int64_t nref = host_small[2];
+      level_solve_qr<P>(c, lvlmom.p, qr_scratch.p, qr_slots, s);
+      // fused K6 over the level's octant segments
       const int64_t ch6 = choose_chunk(points, 1024, 8);
       const int64_t max6 = points / ch6 + 8 * count + 1;
-      begin6.ensure(count * 8, s);
-      chunks6.ensure(max6, s);
-      make_chunks(T->nt.child_start + first * 9, nullptr, count * 8, ch6, counts.p, begin6.p, dev_small.p + 1,
-                  chunks6.p, max6, s);
-      segpart.ensure(max6, s);
-      level_residual<P>(c, T->nt.coef + first * L, nullptr, chunks6.p, dev_small.p + 1, max6, begin6.p, segpart.p, s);
-      // semi-normal iterative refinement (DESIGN.md §3 K5r): b1 = Λᵀ r1, G δ = b1 with the same
-      // factorization, r2 = r1 - Λ δ.  Restores QR-level accuracy where the Gram squares κ.
-      for (int it = 0; it < T->refine; ++it) {
-        proj.ensure((size_t)count * L, s);
+      counts.ensure(count * 8, s);
+      begin.ensure(count * 8, s);
+      chunks.ensure(max6, s);
+      make_chunks(T->nt.child_start + first * 9, nullptr, count * 8, ch6, counts.p, begin.p, dev_small.p + 1,
+                  chunks.p, max6, s);
+      partial.ensure((size_t)max6 * (L + 1), s);
+      segsum.ensure((size_t)count * 8 * (L + 1), s);
+      // semi-normal refinement of small-pivot nodes (DESIGN.md §5 K5r): r1 = r - Λc, b1 = Λᵀr1 (own
+      // frame), δ = G⁻¹b1 with the same Gram, c += δ; the fused pass below then subtracts the last δ.
+      if (nref > 0) {
+        T->refined_nodes += nref;
         delta.ensure((size_t)count * L, s);
-        skip.ensure((size_t)count, s);
-        level_project<P>(c, chunks4.p, dev_small.p, max4, begin4.p, partial.p, proj.p, s);
-        level_solve<P>(c, mom.p, proj.p, delta.p, skip.p, scratch.p, scr_nodes, s);
-        level_residual<P>(c, delta.p, skip.p, chunks6.p, dev_small.p + 1, max6, begin6.p, segpart.p, s);
+        for (int it = 0; it < T->refine_steps; ++it) {
+          level_residual<P>(c, K6_OWN, it, delta.p, chunks.p, dev_small.p + 1, max6, begin.p, count * 8, partial.p,
+                            segsum.p, s);
+          level_solve<P>(c, lvlmom.p, 1, segsum.p, delta.p, T->refine2, nflag.p, scratch.p, scr_nodes, s);
+        }
       }
+      level_residual<P>(c, K6_CHILD, 0, delta.p, chunks.p, dev_small.p + 1, max6, begin.p, count * 8, partial.p,
+                        segsum.p, s);
       flags.ensure(count * 8, s);
       scan.ensure(count * 8, s);
-      level_decide(c, flags.p, scan.p, dev_small.p + 2, s);
+      srcseg.ensure(count * 8, s);
+      level_decide(c, false, mt.child, srcseg.p, flags.p, scan.p, dev_small.p + 2, s);
       FMI_CK(cudaMemcpyAsync(host_small, dev_small.p + 2, 2 * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
       FMI_CK(cudaStreamSynchronize(s));
       const int64_t nnew = host_small[0], npts = host_small[1];
+      if (nnew > 0) {
+        lvlmom.ensure((size_t)nnew * (2 * K + L), s);
+        gather_level(mtmom.p, mtbnd.p, T->nt.mtid, segsum.p, srcseg.p, first + count, nnew, K, L, lvlmom.p, s);
+      }
       first += count;
       T->nodes = first + nnew;
       count = nnew;
@@ -316,9 +415,11 @@ void run_levels(fmi_tree* T, const uint64_t* keys, double* ux, double* uy, doubl
     }
   } catch (...) {
     cudaFreeHost(host_small);
+    free_table(mt, s);
     throw;
   }
   cudaFreeHost(host_small);
+  free_table(mt, s);
 }
 
 template <int P>
@@ -397,7 +498,9 @@ fmi_tree* build_impl(const double* pts, const double* f, int64_t N, int degree, 
     T->tau = tol;
     T->N = N;
     T->stream = s;
-    if (const char* e = std::getenv("FMI_REFINE")) T->refine = std::max(0, std::atoi(e));
+    if (const char* e = std::getenv("FMI_REFINE_STEPS")) T->refine_steps = std::max(0, std::atoi(e));
+    if (const char* e = std::getenv("FMI_REFINE_PIVOT2")) T->refine2 = std::atof(e);
+    if (T->refine_steps == 0) T->refine2 = 0.0;  // no node is flagged for refinement
     bool unit = hb[0] >= 0.0 && hb[1] >= 0.0 && hb[2] >= 0.0 && hb[3] <= 1.0 && hb[4] <= 1.0 && hb[5] <= 1.0;
     if (unit) {
       T->unit = true;
@@ -642,6 +745,14 @@ int fmi_level_stats(const fmi_tree* T, int64_t* nodes, int64_t* points, int cap)
     if (points) points[i] = T->lvl_points[i];
   }
   return n;
+}
+
+int fmi_build_stats(const fmi_tree* T, int64_t* out, int cap) {
+  if (!T || !out) { set_error(FMI_EINPUT, "null argument"); return FMI_EINPUT; }
+  const int64_t v[3] = {T->mt_nodes, T->direct_nodes, T->refined_nodes};
+  const int n = std::min(cap, 3);
+  for (int i = 0; i < n; ++i) out[i] = v[i];
+  return 3;
 }
 
 int fmi_profile_enable(int on) {

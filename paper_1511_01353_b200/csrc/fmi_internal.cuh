@@ -47,7 +47,7 @@ void check_cuda(cudaError_t e, const char* what, const char* file, int line);
 enum KernelId {
   KID_KEYS = 0, KID_SORT, KID_GATHER, KID_MOMENTS, KID_MOMENTS_REDUCE, KID_SOLVE, KID_CHILDREN,
   KID_RESIDUAL, KID_RESIDUAL_REDUCE, KID_DECIDE, KID_CHUNKS, KID_SCAN, KID_EVAL, KID_MISC, KID_PROJECT,
-  KID_REFINE_SOLVE, KID_COUNT
+  KID_M2M, KID_LEVEL_GATHER, KID_REFINE_SOLVE, KID_REFINE, KID_COUNT
 };
 const char* kernel_name(int kid);
 void prof_begin(int kid, cudaStream_t s);
@@ -116,7 +116,8 @@ struct NodeTable {
   double* rms = nullptr;         // [cap]
   double* minpiv = nullptr;      // [cap]
   int32_t* rank = nullptr;       // [cap]
-  int32_t* flag = nullptr;       // [cap] bit0: re-fitted by the QR path (K5q); bit1: refinement converged
+  int32_t* flag = nullptr;       // [cap] bit0: re-fitted by the QR path (K5q)
+  int32_t* mtid = nullptr;       // [cap] node of the moment tree holding this node's moments
 };
 
 // ---------------------------------------------------------------------------------------------
@@ -136,10 +137,15 @@ void gather_points(const double* pts, const double* f, const uint32_t* perm, int
                    double width, bool unit, double* ux, double* uy, double* uz, double* r, cudaStream_t s);
 
 // chunks.cu (level bookkeeping)
-// Build a chunk list over `nr` ranges [rstart[i], rend[i]) with at most `ch` points per chunk.
+// Build a chunk list over `nr` ranges with at most `ch` points per chunk: rend != nullptr: ranges
+// [rstart[i], rend[i]); rend == nullptr: octant segments i = node*8+o of a child_start table (rstart),
+// with seg_mask (a child table): owner runs only — maximal runs of consecutive segments whose child
+// does not exist, each attributed to its first segment (the other segments are empty);
+// node ranges: range i is empty unless (range_flag[i] & flag_bit) when range_flag != nullptr.
 // chunk_begin[i] (exclusive scan of per-range chunk counts) and *nchunks (device) are written.
 void make_chunks(const int64_t* rstart, const int64_t* rend, int64_t nr, int64_t ch, int64_t* counts_tmp,
-                 int64_t* chunk_begin, int64_t* nchunks_dev, Chunk* chunks, int64_t max_chunks, cudaStream_t s);
+                 int64_t* chunk_begin, int64_t* nchunks_dev, Chunk* chunks, int64_t max_chunks, cudaStream_t s,
+                 const int32_t* seg_mask = nullptr, const int32_t* range_flag = nullptr, int flag_bit = 0);
 
 // level ops (level.cu)
 struct LevelCtx {
@@ -156,28 +162,58 @@ struct LevelCtx {
   double tau;
 };
 void level_children(const LevelCtx& c, cudaStream_t s);  // child_start for the level's nodes
-template <int P> void level_moments(const LevelCtx& c, const Chunk* chunks, const int64_t* nchunks_dev,
-                                    int64_t max_chunks, const int64_t* chunk_begin, double* partial,
-                                    double* mom, cudaStream_t s);
-// projection-only pass b_α = Σ u^α r (refinement), proj[node][𝓛]
-template <int P> void level_project(const LevelCtx& c, const Chunk* chunks, const int64_t* nchunks_dev,
-                                    int64_t max_chunks, const int64_t* chunk_begin, double* partial, double* proj,
-                                    cudaStream_t s);
-// rhs == nullptr: initial solve (rhs from mom, writes coef).  rhs != nullptr: refinement solve with the
-// same factorization; writes the correction to delta[node][𝓛] and adds it to coef (QR-path nodes: 0).
-// skip[node] (refinement only) = 1 when the node takes no correction this step.
-template <int P> void level_solve(const LevelCtx& c, const double* mom, const double* rhs, double* delta,
-                                  uint8_t* skip, double* scratch, int64_t scratch_nodes, cudaStream_t s);
-// a node stops refining once its correction is below this fraction of its coefficients (equilibrated)
-constexpr double kRefineConv = 1e-14;
-// coefs: row i = polynomial of the level's local node i (nt.coef + first*𝓛, or a refinement delta)
-// skip (refinement passes): nodes whose correction was not computed keep their residual and sums.
-template <int P> void level_residual(const LevelCtx& c, const double* coefs, const uint8_t* skip,
-                                     const Chunk* chunks, const int64_t* nchunks_dev, int64_t max_chunks,
-                                     const int64_t* chunk_begin, double* seg_part, cudaStream_t s);
+// moments.cu: raw moments (|γ| <= 2p, K per node) of every moment-tree node over its owner segments
+// (chunks over segments node*8+o whose child does not exist), reduced per node in chunk order.
+// (moments.cu) direct accumulation: partial[chunk][K] over each chunk's points in the frame of node
+// cell[chunk.owner >> shift]; reduce_moments sums the chunks of each node's rpn ranges in chunk order
+// into out[node*stride ..], for nodes with (flag[node] & bit) when flag != nullptr.
+template <int P> void direct_moments(const double* ux, const double* uy, const double* uz, const int4* cell,
+                                     int shift, const Chunk* chunks, const int64_t* nchunks_dev, int64_t max_chunks,
+                                     double* partial, cudaStream_t s);
+void reduce_moments(const double* partial, const int64_t* chunk_begin, const int64_t* nchunks_dev, int64_t nodes,
+                    int rpn, int K, const int32_t* flag, int bit, double* out, int64_t stride, cudaStream_t s);
+// (m2m.cu) direct-accumulation rounding bound of every moment-tree node (64·eps·owner points)
+void bound_init(const NodeTable& mt, int64_t n, int K, double* bnd, cudaStream_t s);
+// m2m.cu: mom[node] += Σ_children translate(mom[child]) for the nodes [first, first+count) (one level)
+template <int P> void m2m_level(double* mom, double* bnd, const int32_t* child, int64_t first, int64_t count,
+                                cudaStream_t s);
+// m2m.cu: out[k] = [mtmom[m] (K) | segsum[srcseg[k]][0..𝓛) | mtbnd[m] (K)], m = mtid[first+k]
+// (srcseg null: segment 0)
+void gather_level(const double* mtmom, const double* mtbnd, const int32_t* mtid, const double* segsum,
+                  const int32_t* srcseg, int64_t first, int64_t count, int K, int L, double* out, cudaStream_t s);
+// solve.cu: mom = [moments (K) | projection b (𝓛) | moment rounding bound (K)] per level-local node
+// -> nt.coef (monomial form).  mode 0: flag bit0 -> K5q (pivot < kQrFlagPivot2), bit1 -> semi-normal
+// refinement (pivot < refine2 or n < kRefineFill·𝓛; counted in nflag[0]), bit2 (value 4, exclusive) ->
+// translated moments failed the rounding check (counted in nflag[1]; no solve).  mode 1: refinement
+// step for bit-1 nodes, b1 = Σ_o segrhs[node*8+o][0..𝓛), δ -> delta[node][𝓛], coef += δ.  mode 2:
+// re-solve of bit-2 nodes after direct accumulation (no rounding check).
+template <int P> void level_solve(const LevelCtx& c, const double* mom, int mode, const double* segrhs,
+                                  double* delta, double refine2, int64_t* nflag, double* scratch,
+                                  int64_t scratch_nodes, cudaStream_t s);
+// refinement gate (DESIGN.md §5 K5r)
+constexpr double kRefinePivot2 = 1e-6;
+constexpr double kRefineFill = 8.0;
+constexpr int kRefineSteps = 2;
+// largest accepted equilibrated rounding bound of a translated Gram (DESIGN.md §5 M2M)
+constexpr double kMomentTol = 1e-11;
+// points per K4 work item (one lane accumulates one chunk)
+constexpr int64_t kMomentChunk = 1024;
+// residual.cu (fused K6): over the chunks of the level's octant segments:
+//   K6_CHILD: r -= node polynomial (nt.coef, or delta[node] for refined nodes), Σ r² per segment
+//             (-> nt.child_ss) and the projection onto every potential child's frame;
+//   K6_ROOT:  one segment (the root range), no subtraction, projection in the root frame;
+//   K6_OWN:   refinement step `iter` of bit-1 nodes only: r -= (iter ? delta : coef), projection in
+//             the node's own frame.
+// segsum[seg][0..𝓛) = projection, segsum[seg][𝓛] = Σ r².
+enum K6Mode { K6_CHILD = 0, K6_ROOT = 1, K6_OWN = 2 };
+template <int P> void level_residual(const LevelCtx& c, int mode, int iter, const double* delta, const Chunk* chunks,
+                                     const int64_t* nchunks_dev, int64_t max_chunks, const int64_t* chunk_begin,
+                                     int64_t nseg, double* partial, double* segsum, cudaStream_t s);
 // decisions + compaction: writes the next level's nodes at [first+count, ...), returns via dev_out[0] the
-// number of new nodes and dev_out[1] their total points.
-void level_decide(const LevelCtx& c, int64_t* flags_tmp, int64_t* scan_tmp, int64_t* dev_out, cudaStream_t s);
+// number of new nodes and dev_out[1] their total points.  geo: moment tree (integer guards only).
+// mt_child/srcseg (fit tree): moment-tree ids and source segments of the new nodes.
+void level_decide(const LevelCtx& c, bool geo, const int32_t* mt_child, int32_t* srcseg, int64_t* flags_tmp,
+                  int64_t* scan_tmp, int64_t* dev_out, cudaStream_t s);
 
 // solve_qr.cu (robust path for ill-conditioned nodes)
 size_t solve_qr_scratch_per_cta(int p);

@@ -43,12 +43,30 @@ __global__ void k_children(const uint64_t* __restrict__ keys, NodeTable nt, int6
 
 // range accessor for chunk lists: mode 0 = node ranges, mode 1 = octant segments (node*8 + o)
 struct RangeSrc {
-  const int64_t* a;  // mode 0: start[]; mode 1: child_start[] (9 per node)
-  const int64_t* b;  // mode 0: end[]
+  const int64_t* a;     // mode 0: start[]; mode 1: child_start[] (9 per node)
+  const int64_t* b;     // mode 0: end[]
+  const int32_t* mask;  // mode 1 (optional): child[] — a segment whose child node exists is empty
   int mode;
+  const int32_t* flag;  // mode 0 (optional): a range i with !(flag[i] & bit) is empty
+  int bit;
   __device__ __forceinline__ void get(int64_t i, int64_t& s, int64_t& e) const {
-    if (mode == 0) { s = a[i]; e = b[i]; }
-    else { int64_t nd = i >> 3; int o = (int)(i & 7); s = a[nd * 9 + o]; e = a[nd * 9 + o + 1]; }
+    if (mode == 0) {
+      s = a[i]; e = b[i];
+      if (flag && !(flag[i] & bit)) e = s;
+    } else {
+      int64_t nd = i >> 3; int o = (int)(i & 7); s = a[nd * 9 + o]; e = a[nd * 9 + o + 1];
+      if (mask) {
+        // owner runs: consecutive segments without a child node are one range, attributed to the
+        // first segment of the run (so a leaf's points form a single range)
+        if (mask[i] >= 0 || (o > 0 && mask[i - 1] < 0)) {
+          e = s;
+        } else {
+          int oe = o + 1;
+          while (oe < 8 && mask[nd * 8 + oe] < 0) ++oe;
+          e = a[nd * 9 + oe];
+        }
+      }
+    }
   }
 };
 
@@ -86,14 +104,19 @@ __global__ void k_chunk_fill(RangeSrc src, int64_t nr, const int64_t* __restrict
   chunks[c] = ck;
 }
 
-// decisions: flags[node*8+o] for the level; child_rms/child counts are kept in the node table
-__global__ void k_decide(NodeTable nt, int64_t first, int64_t count, int depth, int D, int L, double tau,
+// decisions: flags[node*8+o] for the level; child_rms/child counts are kept in the node table.
+// geo (moment tree): the integer guards only — every cell that COULD become a node.
+__global__ void k_decide(NodeTable nt, int64_t first, int64_t count, int depth, int D, int L, double tau, bool geo,
                          int64_t* __restrict__ flags) {
   int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= count * 8) return;
   const int64_t node = first + t / 8;
   const int o = (int)(t % 8);
   const int64_t n_o = nt.child_start[node * 9 + o + 1] - nt.child_start[node * 9 + o];
+  if (geo) {
+    flags[t] = (n_o > 0 && n_o >= L && depth + 1 <= D) ? 1 : 0;
+    return;
+  }
   const double ss = nt.child_ss[node * 8 + o];
   const double e = n_o > 0 ? sqrt(ss / (double)n_o) : 0.0;       // E_RMS
   const bool make = n_o > 0 && e > tau && n_o >= L && depth + 1 <= D;  // P:306 (+ G5)
@@ -107,8 +130,11 @@ __global__ void k_decide(NodeTable nt, int64_t first, int64_t count, int depth, 
 }
 
 // compaction: emit the children of the level in (parent, octant) order = canonical (depth, prefix) order
+// mt_child (fit tree only): child table of the moment tree; the new node's moment-tree id is its
+// parent's moment-tree child o.  srcseg[k] = level-local segment of new node k (its projection).
 __global__ void k_emit(NodeTable nt, int64_t first, int64_t count, int depth, const int64_t* __restrict__ flags,
-                       const int64_t* __restrict__ pos, int64_t* __restrict__ out) {
+                       const int64_t* __restrict__ pos, const int32_t* __restrict__ mt_child,
+                       int32_t* __restrict__ srcseg, int64_t* __restrict__ out) {
   int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= count * 8) return;
   const int64_t node = first + t / 8;
@@ -122,6 +148,10 @@ __global__ void k_emit(NodeTable nt, int64_t first, int64_t count, int depth, co
     nt.cell[id] = make_int4(2 * c.x + (o & 1), 2 * c.y + ((o >> 1) & 1), 2 * c.z + ((o >> 2) & 1), depth + 1);
     nt.parent[id] = (int32_t)node;
     nt.child[node * 8 + o] = (int32_t)id;
+    if (mt_child) {
+      nt.mtid[id] = mt_child[(int64_t)nt.mtid[node] * 8 + o];
+      srcseg[pos[t]] = (int32_t)t;
+    }
     for (int k = 0; k < 8; ++k) nt.child[id * 8 + k] = -1;
   } else {
     nt.child[node * 8 + o] = -1;
@@ -165,17 +195,21 @@ void make_chunks_impl(RangeSrc src, int64_t nr, int64_t ch, int64_t* counts_tmp,
 }
 
 void make_chunks(const int64_t* rstart, const int64_t* rend, int64_t nr, int64_t ch, int64_t* counts_tmp,
-                 int64_t* chunk_begin, int64_t* nchunks_dev, Chunk* chunks, int64_t max_chunks, cudaStream_t s) {
-  RangeSrc src{rstart, rend, rend ? 0 : 1};
+                 int64_t* chunk_begin, int64_t* nchunks_dev, Chunk* chunks, int64_t max_chunks, cudaStream_t s,
+                 const int32_t* seg_mask, const int32_t* range_flag, int flag_bit) {
+  RangeSrc src{rstart, rend, seg_mask, rend ? 0 : 1, range_flag, flag_bit};
   make_chunks_impl(src, nr, ch, counts_tmp, chunk_begin, nchunks_dev, chunks, max_chunks, s);
 }
 
-void level_decide(const LevelCtx& c, int64_t* flags_tmp, int64_t* scan_tmp, int64_t* dev_out, cudaStream_t s) {
+void level_decide(const LevelCtx& c, bool geo, const int32_t* mt_child, int32_t* srcseg, int64_t* flags_tmp,
+                  int64_t* scan_tmp, int64_t* dev_out, cudaStream_t s) {
   int64_t work = c.count * 8;
   unsigned grid = (unsigned)((work + 255) / 256);
-  FMI_LAUNCH(KID_DECIDE, s, k_decide, grid, 256, 0, c.nt, c.first, c.count, c.depth, c.D, c.L, c.tau, flags_tmp);
+  FMI_LAUNCH(KID_DECIDE, s, k_decide, grid, 256, 0, c.nt, c.first, c.count, c.depth, c.D, c.L, c.tau, geo,
+             flags_tmp);
   exclusive_scan_i64(flags_tmp, scan_tmp, work, nullptr, s);
-  FMI_LAUNCH(KID_DECIDE, s, k_emit, grid, 256, 0, c.nt, c.first, c.count, c.depth, flags_tmp, scan_tmp, dev_out);
+  FMI_LAUNCH(KID_DECIDE, s, k_emit, grid, 256, 0, c.nt, c.first, c.count, c.depth, flags_tmp, scan_tmp, mt_child,
+             srcseg, dev_out);
   FMI_LAUNCH(KID_DECIDE, s, k_points_of, 1, 256, 0, c.nt, dev_out, c.first + c.count, dev_out + 1);
 }
 

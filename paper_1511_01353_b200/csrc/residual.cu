@@ -1,9 +1,22 @@
-// residual.cu — K6: residual update and per-octant residual energy (DESIGN.md §3 K6).
+// residual.cu — K6: fused residual update, octant-block energies and child projections
+// (DESIGN.md §5 K6).
 //
-// PAPER.md Algorithm 2 last line: f <- f - Λ·P_F over the node's points (here r <- r - Σ a_α u^α,
-// Horner, 𝓛 FMA per point), then Algorithm 1 line 7: E_RMS of each octant block needs Σ r² over
-// the block.  Work items are chunks of one octant block (segment node*8+o), so each CTA reduces one
-// sum; segment sums are reduced in chunk order (deterministic).
+// For every octant block (segment = node*8 + o) of a level's nodes, one pass over its points does
+//   1. r <- r - Σ_α a_α u^α  (Algorithm 2 last line; Horner in the node frame, 𝓛 FMA/point),
+//   2. Σ r² over the block (Algorithm 1 line 7: E_RMS of the block after the parent's fit),
+//   3. if the block may become a child (n_o >= 𝓛 and depth+1 <= max_depth, P:306 + G5), the child's
+//      projection b_α = Σ_i u_i^α r_i in the CHILD frame (the Λᵀf of Algorithm 2 for the child,
+//      P:331, with the factorials applied in the solve) — so the next level needs no pass of its own.
+// Root mode (level -1): no polynomial is subtracted, the single segment is the root and the
+// projection is taken in the root frame.
+//
+// Layout per CTA (one chunk of one segment): a producer phase (one thread per two points: Horner,
+// store of r, child-frame coordinates to shared memory) and a projection phase in which warp w owns
+// a fixed group of outputs (a contiguous range of the Algorithm-2 basis order) and its lanes walk the
+// batch's points: per point, z^0..z^cmax are formed once and every output (a,b,c) of the group costs
+// one FMA  acc += (x^a y^b r) · z^c.  Lane partials are reduced in a fixed order (deterministic).
+#include <utility>
+
 #include "horner.cuh"
 
 namespace fmi {
@@ -11,93 +24,274 @@ namespace fmi {
 namespace {
 
 constexpr int K6_THREADS = 256;
+constexpr int K6_WARPS = K6_THREADS / 32;
+constexpr int K6_BATCH = 2 * K6_THREADS;
 
-template <int P>
-__global__ void __launch_bounds__(K6_THREADS)
-    k_residual(const double* __restrict__ ux, const double* __restrict__ uy, const double* __restrict__ uz,
-               double* __restrict__ r, NodeTable nt, int64_t first, const double* __restrict__ coefs,
-               const Chunk* __restrict__ chunks, const int64_t* __restrict__ nchunks,
-               const uint8_t* __restrict__ skip, double* __restrict__ seg_part) {
-  constexpr int L = rank3(P);
-  __shared__ double sa[L];
-  __shared__ double red[K6_THREADS / 32];
-  const int64_t cidx = blockIdx.x;
-  if (cidx >= *nchunks) return;
-  const Chunk ck = chunks[cidx];
-  const int64_t lnode = ck.owner >> 3;
-  const int64_t node = first + lnode;
-  if (skip && skip[lnode]) return;  // refinement pass: node unchanged, keep its segment sums
-  for (int i = threadIdx.x; i < L; i += K6_THREADS) sa[i] = coefs[lnode * L + i];
-  const Frame fr = node_frame(nt.cell[node]);
-  __syncthreads();
-  const SmemCoef coef(sa);
-  double acc = 0.0;
-  const int64_t n = ck.end - ck.start;
-  const int64_t half = (n + 1) / 2;  // thread t handles points t and t + half (two independent chains)
-  for (int64_t k = threadIdx.x; k < half; k += K6_THREADS) {
-    const int64_t i0 = ck.start + k;
-    const int64_t i1 = i0 + half;
-    const bool has1 = i1 < ck.end;
-    const int64_t j1 = has1 ? i1 : i0;
-    const double x0 = __dmul_rn(__dsub_rn(ux[i0], fr.cx), fr.scale);
-    const double y0 = __dmul_rn(__dsub_rn(uy[i0], fr.cy), fr.scale);
-    const double z0 = __dmul_rn(__dsub_rn(uz[i0], fr.cz), fr.scale);
-    const double x1 = __dmul_rn(__dsub_rn(ux[j1], fr.cx), fr.scale);
-    const double y1 = __dmul_rn(__dsub_rn(uy[j1], fr.cy), fr.scale);
-    const double z1 = __dmul_rn(__dsub_rn(uz[j1], fr.cz), fr.scale);
-    double v0, v1;
-    horner3x2<P>(coef, x0, y0, z0, x1, y1, z1, v0, v1);
-    const double r0 = r[i0] - v0;
-    r[i0] = r0;
-    acc = fma(r0, r0, acc);
-    if (has1) {
-      const double r1 = r[i1] - v1;
-      r[i1] = r1;
-      acc = fma(r1, r1, acc);
-    }
+// ---- compile-time output groups ------------------------------------------------------------------
+// pairs (a,b), a+b <= P, in a-major order (= the (l,m) order of Algorithm 2); pair q owns
+// the outputs c = 0..P-a-b, contiguous in the basis order.
+__host__ __device__ constexpr int npairs(int P) { return (P + 1) * (P + 2) / 2; }
+__host__ __device__ constexpr int pair_a(int P, int q) {
+  int a = 0;
+  while (q >= P - a + 1) { q -= P - a + 1; ++a; }
+  return a;
+}
+__host__ __device__ constexpr int pair_b(int P, int q) {
+  int a = 0;
+  while (q >= P - a + 1) { q -= P - a + 1; ++a; }
+  return q;
+}
+__host__ __device__ constexpr int pair_out(int P, int q) { return P - pair_a(P, q) - pair_b(P, q) + 1; }
+__host__ __device__ constexpr int pair_first(int P, int q) {  // basis index of (a, b, 0)
+  return basis_index(P, pair_a(P, q), pair_b(P, q), 0);
+}
+// number of output groups (a power of two dividing the warp count) with <= 40 outputs each
+__host__ __device__ constexpr int proj_groups(int P) {
+  int g = 1;
+  while (g < K6_WARPS && (rank3(P) + g - 1) / g > 40) g *= 2;
+  return g;
+}
+// first pair of group g: greedy cut at cumulative outputs >= g * ceil(L/G)
+__host__ __device__ constexpr int group_pair_begin(int P, int g) {
+  const int G = proj_groups(P);
+  if (g >= G) return npairs(P);
+  const int target = (rank3(P) + G - 1) / G * g;
+  int q = 0, cum = 0;
+  while (q < npairs(P) && cum < target) { cum += pair_out(P, q); ++q; }
+  return q;
+}
+__host__ __device__ constexpr int group_out_begin(int P, int g) {
+  return group_pair_begin(P, g) >= npairs(P) ? rank3(P) : pair_first(P, group_pair_begin(P, g));
+}
+__host__ __device__ constexpr int group_size(int P, int g) { return group_out_begin(P, g + 1) - group_out_begin(P, g); }
+__host__ __device__ constexpr int max_group(int P) {
+  int m = 0;
+  for (int g = 0; g < proj_groups(P); ++g) m = group_size(P, g) > m ? group_size(P, g) : m;
+  return m;
+}
+__host__ __device__ constexpr int group_cmax(int P, int g) {  // highest z power the group needs
+  int smin = 1 << 20;
+  for (int q = group_pair_begin(P, g); q < group_pair_begin(P, g + 1); ++q) {
+    const int t = pair_a(P, q) + pair_b(P, q);
+    smin = t < smin ? t : smin;
   }
+  return smin > P ? 0 : P - smin;
+}
+
+// pair q of a group: acc[pair_first(q) - o0 + c] += (x^a y^b r) z^c, c = 0..P-a-b; then advance the
+// running x^a r / y^b to pair q+1 (compile-time recursion: every index is a constant)
+template <int P, int q, int q1, int o0>
+__device__ __forceinline__ void proj_pairs(double x, double y, const double* zp, double xr, double yb, double* acc) {
+  if constexpr (q < q1) {
+    constexpr int base = pair_first(P, q) - o0;
+    constexpr int n = pair_out(P, q);
+    const double v = xr * yb;
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double s = 0.0;
-#pragma unroll
-    for (int w = 0; w < K6_THREADS / 32; ++w) s += red[w];
-    seg_part[cidx] = s;
+    for (int c = 0; c < n; ++c) acc[base + c] = fma(v, zp[c], acc[base + c]);
+    if constexpr (q + 1 < q1) {
+      if constexpr (pair_a(P, q + 1) == pair_a(P, q))
+        proj_pairs<P, q + 1, q1, o0>(x, y, zp, xr, yb * y, acc);
+      else
+        proj_pairs<P, q + 1, q1, o0>(x, y, zp, xr * x, 1.0, acc);
+    }
   }
 }
 
-__global__ void k_residual_reduce(const double* __restrict__ seg_part, const int64_t* __restrict__ chunk_begin,
-                                  const int64_t* __restrict__ nchunks, int64_t nseg, NodeTable nt, int64_t first,
-                                  const uint8_t* __restrict__ skip) {
-  const int64_t sgi = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (sgi >= nseg) return;
-  if (skip && skip[sgi >> 3]) return;
+template <int P, int g>
+__device__ __forceinline__ void proj_accum(double x, double y, double z, double r, double* acc) {
+  constexpr int q0 = group_pair_begin(P, g), q1 = group_pair_begin(P, g + 1);
+  constexpr int o0 = group_out_begin(P, g);
+  constexpr int CM = group_cmax(P, g);
+  if constexpr (q0 < q1) {
+    double zp[CM + 1];
+    zp[0] = 1.0;
+#pragma unroll
+    for (int c = 1; c <= CM; ++c) zp[c] = zp[c - 1] * z;
+    double xr = r;
+#pragma unroll
+    for (int e = 0; e < pair_a(P, q0); ++e) xr *= x;
+    double yb = 1.0;
+#pragma unroll
+    for (int e = 0; e < pair_b(P, q0); ++e) yb *= y;
+    proj_pairs<P, q0, q1, o0>(x, y, zp, xr, yb, acc);
+  }
+}
+
+template <int P, int g>
+__device__ __forceinline__ void proj_dispatch_one(int gw, double x, double y, double z, double r, double* acc) {
+  if (gw == g) proj_accum<P, g>(x, y, z, r, acc);
+}
+
+template <int P, int... Gs>
+__device__ __forceinline__ void proj_dispatch(int gw, double x, double y, double z, double r, double* acc,
+                                              std::integer_sequence<int, Gs...>) {
+  (proj_dispatch_one<P, Gs>(gw, x, y, z, r, acc), ...);
+}
+
+template <int P>
+__global__ void __launch_bounds__(K6_THREADS, 2)
+    k_residual(const double* __restrict__ ux, const double* __restrict__ uy, const double* __restrict__ uz,
+               double* __restrict__ r, NodeTable nt, int64_t first, const Chunk* __restrict__ chunks,
+               const int64_t* __restrict__ nchunks, int depth, int D, int mode, int iter,
+               const double* __restrict__ delta, double* __restrict__ partial) {
+  constexpr int L = rank3(P);
+  constexpr int G = proj_groups(P);
+  constexpr int SUB = K6_WARPS / G;  // warps per output group (split the batch's points)
+  constexpr int MG = max_group(P);
+  __shared__ double sa[L];
+  __shared__ double sx[K6_BATCH], sy[K6_BATCH], sz[K6_BATCH], sr[K6_BATCH];
+  __shared__ double red[SUB][L];
+  __shared__ double redw[K6_WARPS];
+  const int64_t cidx = blockIdx.x;
+  if (cidx >= *nchunks) return;
+  const Chunk ck = chunks[cidx];
+  const int o = ck.owner & 7;
+  const int64_t ln = ck.owner >> 3;
+  const int64_t node = first + ln;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  double* out = partial + cidx * (int64_t)(L + 1);
+  const bool horner = mode != K6_ROOT;
+  const bool refined = mode != K6_ROOT && (nt.flag[node] & 2);
+  if (mode == K6_OWN && !refined) {  // refinement pass: this node takes no step
+    for (int e = tid; e <= L; e += K6_THREADS) out[e] = 0.0;
+    return;
+  }
+  bool project;
+  Frame fn{}, fc{};
+  if (mode == K6_ROOT) {
+    project = true;
+    fc = node_frame(nt.cell[node]);
+  } else {
+    const int4 c = nt.cell[node];
+    fn = node_frame(c);
+    if (mode == K6_OWN) {
+      project = true;
+      fc = fn;
+    } else {
+      const int64_t n_o = nt.child_start[node * 9 + o + 1] - nt.child_start[node * 9 + o];
+      project = n_o >= L && depth + 1 <= D;  // potential child (P:306 integer guard + G5)
+      fc = node_frame(make_int4(2 * c.x + (o & 1), 2 * c.y + ((o >> 1) & 1), 2 * c.z + ((o >> 2) & 1), c.w + 1));
+    }
+    // polynomial to subtract: the fit, or (refined nodes) the last refinement correction
+    const bool use_delta = (mode == K6_OWN) ? (iter > 0) : refined;
+    const double* src = use_delta ? delta + ln * L : nt.coef + node * L;
+    for (int i = tid; i < L; i += K6_THREADS) sa[i] = src[i];
+  }
+  __syncthreads();
+  const SmemCoef coef(sa);
+  const int gw = warp % G, sub = warp / G;
+  double acc[MG > 0 ? MG : 1];
+#pragma unroll
+  for (int k = 0; k < MG; ++k) acc[k] = 0.0;
+  double ss = 0.0;
+  for (int64_t base = ck.start; base < ck.end; base += K6_BATCH) {
+    const int64_t i0 = base + tid, i1 = base + tid + K6_THREADS;
+    const bool v0 = i0 < ck.end, v1 = i1 < ck.end;
+    const int64_t j0 = v0 ? i0 : ck.start, j1 = v1 ? i1 : ck.start;
+    const double X0 = ux[j0], Y0 = uy[j0], Z0 = uz[j0], X1 = ux[j1], Y1 = uy[j1], Z1 = uz[j1];
+    double r0 = r[j0], r1 = r[j1];
+    if (horner) {
+      double p0, p1;
+      horner3x2<P>(coef, __dmul_rn(__dsub_rn(X0, fn.cx), fn.scale), __dmul_rn(__dsub_rn(Y0, fn.cy), fn.scale),
+                   __dmul_rn(__dsub_rn(Z0, fn.cz), fn.scale), __dmul_rn(__dsub_rn(X1, fn.cx), fn.scale),
+                   __dmul_rn(__dsub_rn(Y1, fn.cy), fn.scale), __dmul_rn(__dsub_rn(Z1, fn.cz), fn.scale), p0, p1);
+      r0 -= p0;
+      r1 -= p1;
+      if (v0) { r[i0] = r0; ss = fma(r0, r0, ss); }
+      if (v1) { r[i1] = r1; ss = fma(r1, r1, ss); }
+    }
+    if (project) {
+      sx[tid] = __dmul_rn(__dsub_rn(X0, fc.cx), fc.scale);
+      sy[tid] = __dmul_rn(__dsub_rn(Y0, fc.cy), fc.scale);
+      sz[tid] = __dmul_rn(__dsub_rn(Z0, fc.cz), fc.scale);
+      sr[tid] = v0 ? r0 : 0.0;
+      sx[tid + K6_THREADS] = __dmul_rn(__dsub_rn(X1, fc.cx), fc.scale);
+      sy[tid + K6_THREADS] = __dmul_rn(__dsub_rn(Y1, fc.cy), fc.scale);
+      sz[tid + K6_THREADS] = __dmul_rn(__dsub_rn(Z1, fc.cz), fc.scale);
+      sr[tid + K6_THREADS] = v1 ? r1 : 0.0;
+      __syncthreads();
+      const int nb = (int)min((int64_t)K6_BATCH, ck.end - base);
+#pragma unroll 1
+      for (int j = sub * 32 + lane; j < nb; j += 32 * SUB)
+        proj_dispatch<P>(gw, sx[j], sy[j], sz[j], sr[j], acc, std::make_integer_sequence<int, G>{});
+      __syncthreads();
+    }
+  }
+  // Σ r² (fixed-order CTA reduction)
+#pragma unroll
+  for (int s = 16; s > 0; s >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, s);
+  if (lane == 0) redw[warp] = ss;
+  // projection: lane reduction per output, then over the SUB warps of a group in fixed order
+  if (project) {
+    const int ob = [&] {
+      int v = 0;
+#pragma unroll
+      for (int g = 0; g < G; ++g) if (g == gw) v = group_out_begin(P, g);
+      return v;
+    }();
+    const int on = [&] {
+      int v = 0;
+#pragma unroll
+      for (int g = 0; g < G; ++g) if (g == gw) v = group_size(P, g);
+      return v;
+    }();
+#pragma unroll
+    for (int k = 0; k < MG; ++k) {
+      double v = acc[k];
+#pragma unroll
+      for (int s = 16; s > 0; s >>= 1) v += __shfl_xor_sync(0xffffffffu, v, s);
+      if (lane == 0 && k < on) red[sub][ob + k] = v;
+    }
+  }
+  __syncthreads();
+  if (tid == 0) {
+    double t = 0.0;
+#pragma unroll
+    for (int w = 0; w < K6_WARPS; ++w) t += redw[w];
+    out[L] = t;
+  }
+  for (int e = tid; e < L; e += K6_THREADS) {
+    double v = 0.0;
+    if (project)
+      for (int s = 0; s < SUB; ++s) v += red[s][e];
+    out[e] = v;
+  }
+}
+
+// segment sums: partial chunks of segment (node*8+o) in chunk order -> segsum[seg][𝓛+1]; Σr² also to
+// the node table (child_ss) for the decisions.
+__global__ void __launch_bounds__(128)
+    k_residual_reduce(const double* __restrict__ partial, const int64_t* __restrict__ chunk_begin,
+                      const int64_t* __restrict__ nchunks, int64_t nseg, NodeTable nt, int64_t first, int L,
+                      bool write_ss, double* __restrict__ segsum) {
+  const int64_t sgi = blockIdx.x;
   const int64_t c0 = chunk_begin[sgi];
   const int64_t c1 = sgi + 1 < nseg ? chunk_begin[sgi + 1] : *nchunks;
-  double s = 0.0;
-  for (int64_t c = c0; c < c1; ++c) s += seg_part[c];
-  nt.child_ss[first * 8 + sgi] = s;
+  for (int e = threadIdx.x; e <= L; e += blockDim.x) {
+    double s = 0.0;
+    for (int64_t c = c0; c < c1; ++c) s += partial[c * (L + 1) + e];
+    segsum[sgi * (L + 1) + e] = s;
+    if (e == L && write_ss) nt.child_ss[first * 8 + sgi] = s;
+  }
 }
 
 }  // namespace
 
 template <int P>
-void level_residual(const LevelCtx& c, const double* coefs, const uint8_t* skip, const Chunk* chunks,
-                    const int64_t* nchunks_dev, int64_t max_chunks, const int64_t* chunk_begin, double* seg_part,
-                    cudaStream_t s) {
+void level_residual(const LevelCtx& c, int mode, int iter, const double* delta, const Chunk* chunks,
+                    const int64_t* nchunks_dev, int64_t max_chunks, const int64_t* chunk_begin, int64_t nseg,
+                    double* partial, double* segsum, cudaStream_t s) {
+  const int kid = mode == K6_ROOT ? KID_PROJECT : (mode == K6_OWN ? KID_REFINE : KID_RESIDUAL);
   if (max_chunks > 0)
-    FMI_LAUNCH(KID_RESIDUAL, s, k_residual<P>, (unsigned)max_chunks, K6_THREADS, 0, c.ux, c.uy, c.uz, c.r, c.nt,
-               c.first, coefs, chunks, nchunks_dev, skip, seg_part);
-  const int64_t nseg = c.count * 8;
-  FMI_LAUNCH(KID_RESIDUAL_REDUCE, s, k_residual_reduce, (unsigned)((nseg + 255) / 256), 256, 0, seg_part, chunk_begin,
-             nchunks_dev, nseg, c.nt, c.first, skip);
+    FMI_LAUNCH(kid, s, k_residual<P>, (unsigned)max_chunks, K6_THREADS, 0, c.ux, c.uy, c.uz, c.r, c.nt, c.first,
+               chunks, nchunks_dev, c.depth, c.D, mode, iter, delta, partial);
+  FMI_LAUNCH(KID_RESIDUAL_REDUCE, s, k_residual_reduce, (unsigned)nseg, 128, 0, partial, chunk_begin, nchunks_dev, nseg,
+             c.nt, c.first, rank3(P), mode == K6_CHILD, segsum);
 }
 
-#define FMI_INST(P)                                                                                         \
-  template void level_residual<P>(const LevelCtx&, const double*, const uint8_t*, const Chunk*, const int64_t*,  \
-                                  int64_t, const int64_t*, double*, cudaStream_t);
+#define FMI_INST(P)                                                                                            \
+  template void level_residual<P>(const LevelCtx&, int, int, const double*, const Chunk*, const int64_t*, int64_t, \
+                                  const int64_t*, int64_t, double*, double*, cudaStream_t);
 FMI_INST(0) FMI_INST(1) FMI_INST(2) FMI_INST(3) FMI_INST(4) FMI_INST(5)
 FMI_INST(6) FMI_INST(7) FMI_INST(8) FMI_INST(9) FMI_INST(10)
 #undef FMI_INST

@@ -50,9 +50,10 @@ __device__ __forceinline__ int64_t tri(int i) { return (int64_t)i * (i + 1) / 2;
 
 template <int P>
 __global__ void __launch_bounds__(K5_THREADS)
-    k_solve(const double* __restrict__ mom, const double* __restrict__ rhs, double* __restrict__ delta,
-            uint8_t* __restrict__ skip, NodeTable nt, int64_t first, int64_t count, double* __restrict__ gscratch,
-            const __grid_constant__ BasisTab bt, double delta2, double conv_tol) {
+    k_solve(const double* __restrict__ mom, int mode, const double* __restrict__ segrhs, double* __restrict__ delta,
+            NodeTable nt, int64_t first, int64_t count, double* __restrict__ gscratch,
+            const __grid_constant__ BasisTab bt, double delta2, double refine2, double refine_fill,
+            double mom_tol, int64_t* __restrict__ nflag) {
   using S = K5Shape<P>;
   constexpr int Q = S::Q, K = S::K, L = S::L;
   extern __shared__ double sm[];
@@ -67,22 +68,30 @@ __global__ void __launch_bounds__(K5_THREADS)
   const int lane = tid & 31, warp = tid >> 5;
   constexpr int NWARP = K5_THREADS / 32;
   __shared__ double smin_sh[1];
+  __shared__ double errw[NWARP];
   // basis exponents in shared memory (thread-divergent lookups into the parameter bank serialise)
   __shared__ uint8_t bl[L], bm[L], bn[L];
   for (int i = tid; i < L; i += K5_THREADS) { bl[i] = bt.l[i]; bm[i] = bt.m[i]; bn[i] = bt.n[i]; }
   __syncthreads();
-  __shared__ double redw[2 * NWARP];
 
   for (int64_t node = blockIdx.x; node < count; node += gridDim.x) {
-    if (rhs && (nt.flag[first + node] & 3)) {  // QR-path (bit 0) or converged (bit 1): no correction
-      if (tid == 0) skip[node] = 1;
-      continue;
-    }
+    // mode 1 (refinement): bit-1 nodes only; mode 2 (direct-moment re-solve): bit-2 nodes only
+    if (mode == 1 && !(nt.flag[first + node] & 2)) continue;
+    if (mode == 2 && !(nt.flag[first + node] & 4)) continue;
     if (tid == 0) smin_sh[0] = INFINITY;
-    const double* mp = mom + node * (int64_t)(K + L);
+    const double* mp = mom + node * (int64_t)(2 * K + L);
+    const double* bnd = mp + K + L;
     for (int e = tid; e < K; e += K5_THREADS) sm[e] = mp[e];
-    const double* bp = rhs ? rhs + node * (int64_t)L : mp + K;
-    for (int e = tid; e < L; e += K5_THREADS) sb[e] = bp[e];
+    if (mode == 1) {  // b1 = Λᵀ r1 over the node's 8 octant segments, fixed order
+      for (int e = tid; e < L; e += K5_THREADS) {
+        double v = 0.0;
+        for (int o = 0; o < 8; ++o) v += segrhs[(node * 8 + o) * (L + 1) + e];
+        sb[e] = v;
+      }
+    } else {
+      const double* bp = mp + K;
+      for (int e = tid; e < L; e += K5_THREADS) sb[e] = bp[e];
+    }
     __syncthreads();
     for (int i = tid; i < L; i += K5_THREADS) {
       const double m2 = sM[basis_index(Q, 2 * bl[i], 2 * bm[i], 2 * bn[i])];
@@ -91,15 +100,35 @@ __global__ void __launch_bounds__(K5_THREADS)
       sb[i] *= di;
     }
     __syncthreads();
+    double errl = 0.0;  // equilibrated rounding bound of the Gram (translated moments)
     for (int64_t e = tid; e < S::NA; e += K5_THREADS) {
       int i = (int)((sqrt(8.0 * (double)e + 1.0) - 1.0) * 0.5);
       while (tri(i + 1) <= e) ++i;
       while (tri(i) > e) --i;
       const int k = (int)(e - tri(i));
-      const double g = sM[basis_index(Q, bl[i] + bl[k], bm[i] + bm[k], bn[i] + bn[k])];
-      A[e] = g * dinv[i] * dinv[k];
+      const int gi = basis_index(Q, bl[i] + bl[k], bm[i] + bm[k], bn[i] + bn[k]);
+      const double dd = dinv[i] * dinv[k];
+      A[e] = sM[gi] * dd;
+      errl = fmax(errl, bnd[gi] * dd);
+    }
+    if (mode == 0) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) errl = fmax(errl, __shfl_xor_sync(0xffffffffu, errl, o));
+      if (lane == 0) errw[warp] = errl;
     }
     __syncthreads();
+    if (mode == 0) {
+      double em = 0.0;
+      for (int w = 0; w < NWARP; ++w) em = fmax(em, errw[w]);
+      if (!(em <= mom_tol)) {  // translated moments lost their precision: re-accumulate directly
+        if (tid == 0) {
+          nt.flag[first + node] = 4;
+          atomicAdd(reinterpret_cast<unsigned long long*>(nflag + 1), 1ull);
+        }
+        __syncthreads();
+        continue;
+      }
+    }
 
     // right-looking Cholesky with column rejection
     for (int j = 0; j < L; ++j) {
@@ -151,30 +180,11 @@ __global__ void __launch_bounds__(K5_THREADS)
       __syncthreads();
     }
     double* out = nt.coef + (first + node) * (int64_t)L;
-    if (rhs) {
-      // correction δ = R̃⁻¹R̃⁻ᵀ b̃1 (equilibrated) -> monomial form; converged when |δ̃| <= conv_tol |c̃|
-      double dmax = 0.0, cmax = 0.0;
+    if (mode == 1) {  // refinement correction δ (monomial form): delta[node] = δ, coef += δ
       for (int i = tid; i < L; i += K5_THREADS) {
         const double d = sb[i] * dinv[i];
         delta[node * (int64_t)L + i] = d;
-        if (dinv[i] > 0.0) {
-          dmax = fmax(dmax, fabs(sb[i]));
-          cmax = fmax(cmax, fabs(out[i] / dinv[i]));
-        }
         out[i] += d;
-      }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        dmax = fmax(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
-        cmax = fmax(cmax, __shfl_xor_sync(0xffffffffu, cmax, o));
-      }
-      if (lane == 0) { redw[warp] = dmax; redw[NWARP + warp] = cmax; }
-      __syncthreads();
-      if (tid == 0) {
-        double dm = 0.0, cm = 0.0;
-        for (int w = 0; w < NWARP; ++w) { dm = fmax(dm, redw[w]); cm = fmax(cm, redw[NWARP + w]); }
-        skip[node] = 0;
-        if (dm <= conv_tol * cm) nt.flag[first + node] |= 2;
       }
       __syncthreads();
       continue;
@@ -189,7 +199,13 @@ __global__ void __launch_bounds__(K5_THREADS)
       nt.minpiv[first + node] = rk ? mn : 0.0;
       // robust-path flag: a pivot of a non-zero column fell where fp64 Gram pivots stop tracking the
       // QR pivots (or the column was rejected) -> K5q re-fits the node by Householder QR
-      nt.flag[first + node] = (smin_sh[0] < kQrFlagPivot2) ? 1 : 0;
+      // semi-normal refinement flag (bit 1): small pivots, or few points per unknown, where the normal
+      // equations lose digits (DESIGN.md §5 K5r)
+      const double npts = (double)(nt.end[first + node] - nt.start[first + node]);
+      const bool refine = refine2 > 0.0 && (smin_sh[0] < refine2 || npts < refine_fill * L);
+      const int fl = (smin_sh[0] < kQrFlagPivot2) ? 1 : (refine ? 2 : 0);
+      nt.flag[first + node] = fl;
+      if (fl == 2) atomicAdd(reinterpret_cast<unsigned long long*>(nflag), 1ull);
     }
     __syncthreads();
   }
@@ -198,8 +214,8 @@ __global__ void __launch_bounds__(K5_THREADS)
 }  // namespace
 
 template <int P>
-void level_solve(const LevelCtx& c, const double* mom, const double* rhs, double* delta, uint8_t* skip,
-                 double* scratch, int64_t scratch_nodes, cudaStream_t s) {
+void level_solve(const LevelCtx& c, const double* mom, int mode, const double* segrhs, double* delta, double refine2,
+                 int64_t* nflag, double* scratch, int64_t scratch_nodes, cudaStream_t s) {
   using S = K5Shape<P>;
   static const BasisTab bt = make_basis<P>();
   static bool attr = false;
@@ -210,8 +226,9 @@ void level_solve(const LevelCtx& c, const double* mom, const double* rhs, double
   int64_t grid = c.count;
   if (!S::kSmemA) grid = std::min<int64_t>(grid, scratch_nodes);
   grid = std::min<int64_t>(grid, 1 << 20);
-  FMI_LAUNCH(rhs ? KID_REFINE_SOLVE : KID_SOLVE, s, k_solve<P>, (unsigned)grid, K5_THREADS, S::SMEM, mom, rhs, delta,
-             skip, c.nt, c.first, c.count, scratch, bt, kDelta * kDelta, kRefineConv);
+  FMI_LAUNCH(mode == 1 ? KID_REFINE_SOLVE : KID_SOLVE, s, k_solve<P>, (unsigned)grid, K5_THREADS, S::SMEM, mom, mode,
+             segrhs, delta, c.nt, c.first, c.count, scratch, bt, kDelta * kDelta, refine2, kRefineFill, kMomentTol,
+             nflag);
 }
 
 // bytes of global scratch the solve needs per concurrently processed node (0 if shared-memory resident)
@@ -225,8 +242,8 @@ size_t solve_scratch_per_node(int p) {
 }
 
 #define FMI_INST(P) \
-  template void level_solve<P>(const LevelCtx&, const double*, const double*, double*, uint8_t*, double*, int64_t,  \
-                               cudaStream_t);
+  template void level_solve<P>(const LevelCtx&, const double*, int, const double*, double*, double, int64_t*, \
+                               double*, int64_t, cudaStream_t);
 FMI_INST(0) FMI_INST(1) FMI_INST(2) FMI_INST(3) FMI_INST(4) FMI_INST(5)
 FMI_INST(6) FMI_INST(7) FMI_INST(8) FMI_INST(9) FMI_INST(10)
 #undef FMI_INST

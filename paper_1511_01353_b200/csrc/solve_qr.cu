@@ -73,7 +73,7 @@ __global__ void __launch_bounds__(KQ_THREADS)
   for (int64_t ln = blockIdx.x; ln < count; ln += gridDim.x) {
     const int64_t node = first + ln;
     if (!(nt.flag[node] & 1)) continue;
-    const double* mp = mom + ln * (int64_t)(K + L);
+    const double* mp = mom + ln * (int64_t)(2 * K + L);
     for (int i = tid; i < L; i += KQ_THREADS) {
       const double m2 = mp[basis_index(Q, 2 * bl[i], 2 * bm[i], 2 * bn[i])];
       dinv[i] = m2 > 0.0 ? 1.0 / sqrt(m2) : 0.0;

@@ -30,11 +30,12 @@ MAX_DEPTH = 20
 EXPORTED = (
     "fmi_build", "fmi_eval", "fmi_free", "fmi_last_error", "fmi_set_stream", "fmi_node_count", "fmi_rank",
     "fmi_export_nodes", "fmi_root_cube", "fmi_residual", "fmi_level_stats", "fmi_profile_enable",
-    "fmi_profile_reset", "fmi_profile_get", "fmi_launch_count",
+    "fmi_profile_reset", "fmi_profile_get", "fmi_launch_count", "fmi_build_stats",
 )
 
 KERNELS = ("keys", "sort", "gather", "moments", "moments_reduce", "solve", "children", "residual",
-           "residual_reduce", "decide", "chunks", "scan", "eval", "misc", "project", "refine_solve")
+           "residual_reduce", "decide", "chunks", "scan", "eval", "misc", "project", "m2m", "level_gather",
+           "refine_solve", "refine")
 
 
 class FmiNode(ctypes.Structure):
@@ -93,6 +94,8 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.fmi_profile_reset.argtypes = []
     lib.fmi_profile_get.restype = I32
     lib.fmi_profile_get.argtypes = [ctypes.c_char_p, P(D), P(I64)]
+    lib.fmi_build_stats.restype = I32
+    lib.fmi_build_stats.argtypes = [VP, P(I64), I32]
     lib.fmi_launch_count.restype = I64
     lib.fmi_launch_count.argtypes = []
     _lib = lib
@@ -252,6 +255,13 @@ class Tree:
         pts = (ctypes.c_int64 * 64)()
         k = lib.fmi_level_stats(ctypes.c_void_p(self.handle), nodes, pts, 64)
         return np.array(nodes[:k], dtype=np.int64), np.array(pts[:k], dtype=np.int64)
+
+    def build_stats(self) -> dict:
+        """Moment-tree size, fit nodes re-accumulated directly (M2M rounding check), refined nodes."""
+        lib = load_library()
+        out = (ctypes.c_int64 * 3)()
+        lib.fmi_build_stats(ctypes.c_void_p(self.handle), out, 3)
+        return {"moment_tree_nodes": int(out[0]), "direct_moment_nodes": int(out[1]), "refined_nodes": int(out[2])}
 
 
 def build(pts, f, degree: int, tol: float, max_depth: int) -> Tree:

@@ -1,0 +1,5 @@
+mkdir -p gpurun_out
+set -x
+timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu_v1.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu_v1.log
+for c in 3 4; do timeout 300 python tools/run_build.py --config $c --reps 3 > gpurun_out/run_cfg${c}_v1.log 2>&1; done
+timeout 900 python bench.py --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/bench_cfg5_v1.log 2>&1; echo "bench rc=$?" >> gpurun_out/bench_cfg5_v1.log

@@ -28,5 +28,5 @@ for _ in range(a.reps):
     out = tr.eval(dq)
     torch.cuda.synchronize()
     print(f"{cfg.name} N={cfg.n} M={cfg.m}: nodes {tr.node_count} levels {tr.level_stats()} "
-          f"step {1e3 * (time.perf_counter() - t):.1f} ms", flush=True)
+          f"step {1e3 * (time.perf_counter() - t):.1f} ms {tr.build_stats()}", flush=True)
     tr.free()
