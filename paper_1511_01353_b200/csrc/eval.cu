@@ -1,10 +1,15 @@
-// eval.cu — K7: interpolant evaluation over Morton-sorted queries (DESIGN.md §3 K7).
+// eval.cu — K7: interpolant evaluation over Morton-sorted queries (DESIGN.md §5 K7) and the
+// pre-summed node polynomials it uses.
 //
 // f(r) = Λ(r)·F_p (§2), accumulated over the nodes on the query's root-to-deepest-existing-node
 // path ("only downward recursion to accumulate local polynomial representation of the residual",
-// P:367-368 §4; reading G11).  Queries are processed in Morton order so that neighbouring threads walk
-// the same nodes (coefficient loads are warp-broadcast, L1-resident); results are scattered back to the
-// caller's order.  A query outside the root cube gets the root polynomial only.
+// P:367-368 §4; reading G11).  After the build, every node's polynomial is pre-summed with all of its
+// ancestors' — each ancestor polynomial translated into the node's frame, u_parent = (u_child + s)/2
+// per axis (FMT_New_Octant), an exact change of variables — so a query evaluates ONE polynomial
+// (the deepest node's) instead of one per level; the value equals the path sum up to rounding.
+// Queries are processed in Morton order so that neighbouring threads use the same node (coefficient
+// loads are warp-broadcast, L1-resident); results are scattered back to the caller's order.  A query
+// outside the root cube gets the root polynomial only.
 #include "horner.cuh"
 
 namespace fmi {
@@ -13,6 +18,76 @@ namespace {
 
 __device__ __forceinline__ double to_unit_e(double x, double lo, double w, bool unit) {
   return unit ? x : __ddiv_rn(__dsub_rn(x, lo), w);
+}
+
+// ---- pre-summed polynomials ----------------------------------------------------------------------
+constexpr int PS_THREADS = 128;
+
+// dst[..j..] = Σ_{g>=j} src[..g..] C(g,j) s^(g-j) 2^-g along one axis (Taylor shift of a polynomial
+// from the parent frame to the child frame); entries in Algorithm-2 order of degree P.
+template <int P>
+__device__ __forceinline__ void poly_shift(const double* __restrict__ src, double* __restrict__ dst, int axis,
+                                           double s, const double* coef, const uint8_t* ea, const uint8_t* eb,
+                                           const uint8_t* ec) {
+  constexpr int L = rank3(P);
+  for (int e = threadIdx.x; e < L; e += PS_THREADS) {
+    const int a = ea[e], b = eb[e], c = ec[e];
+    double v = 0.0;
+    if (axis == 2) {
+      const double* sp = src + (e - c);
+      double sg = 1.0;
+      for (int g = c; g <= P - a - b; ++g) { v = fma(coef[g * (P + 1) + c] * sg, sp[g], v); sg *= s; }
+    } else if (axis == 1) {
+      double sg = 1.0;
+      for (int g = b; g <= P - a - c; ++g) { v = fma(coef[g * (P + 1) + b] * sg, src[basis_index(P, a, g, c)], v); sg *= s; }
+    } else {
+      double sg = 1.0;
+      for (int g = a; g <= P - b - c; ++g) { v = fma(coef[g * (P + 1) + a] * sg, src[basis_index(P, g, b, c)], v); sg *= s; }
+    }
+    dst[e] = v;
+  }
+  __syncthreads();
+}
+
+// pcoef[node] = coef[node] + shift(pcoef[parent]) for the nodes [first, first+count) of one level
+template <int P>
+__global__ void __launch_bounds__(PS_THREADS) k_presum(NodeTable nt, int64_t first, int64_t count) {
+  constexpr int L = rank3(P);
+  __shared__ double b0[L], b1[L];
+  __shared__ double coef[(P + 1) * (P + 1)];
+  __shared__ uint8_t ea[L], eb[L], ec[L];
+  const int64_t node = first + blockIdx.x;
+  const int tid = threadIdx.x;
+  const int32_t par = nt.parent[node];
+  if (par < 0) {
+    for (int e = tid; e < L; e += PS_THREADS) nt.pcoef[node * L + e] = nt.coef[node * L + e];
+    return;
+  }
+  for (int e = tid; e < (P + 1) * (P + 1); e += PS_THREADS) {
+    const int g = e / (P + 1), j = e % (P + 1);
+    double c = 0.0;
+    if (j <= g) {
+      double bin = 1.0;
+      for (int t = 1; t <= j; ++t) bin = bin * (double)(g - j + t) / (double)t;
+      c = ldexp(bin, -g);
+    }
+    coef[e] = c;
+  }
+  for (int e = tid; e < L; e += PS_THREADS) {
+    int l = 0;
+    while (rank3(P) - rank3(P - l - 1) <= e) ++l;
+    int rem = e - (rank3(P) - rank3(P - l));
+    int m = 0;
+    while (rem >= P - l - m + 1) { rem -= P - l - m + 1; ++m; }
+    ea[e] = (uint8_t)l; eb[e] = (uint8_t)m; ec[e] = (uint8_t)rem;
+    b0[e] = nt.pcoef[(int64_t)par * L + e];
+  }
+  __syncthreads();
+  const int4 c = nt.cell[node];  // octant bits = low bits of the cell (FMT_New_Octant)
+  poly_shift<P>(b0, b1, 2, (c.z & 1) ? 1.0 : -1.0, coef, ea, eb, ec);
+  poly_shift<P>(b1, b0, 1, (c.y & 1) ? 1.0 : -1.0, coef, ea, eb, ec);
+  poly_shift<P>(b0, b1, 0, (c.x & 1) ? 1.0 : -1.0, coef, ea, eb, ec);
+  for (int e = tid; e < L; e += PS_THREADS) nt.pcoef[node * L + e] = b1[e] + nt.coef[node * L + e];
 }
 
 template <int P>
@@ -28,29 +103,33 @@ __global__ void __launch_bounds__(256) k_eval(const double* __restrict__ q, cons
   const double uy = to_unit_e(q[3 * qi + 1], lo1, w, unit);
   const double uz = to_unit_e(q[3 * qi + 2], lo2, w, unit);
   const bool inside = ux >= 0.0 && ux <= 1.0 && uy >= 0.0 && uy <= 1.0 && uz >= 0.0 && uz <= 1.0;
+  // descend to the deepest existing node containing the query
   int64_t node = 0;
-  int4 cell = make_int4(0, 0, 0, 0);
-  double acc = 0.0;
-  const uint64_t key = keys ? keys[i] : 0;
-  for (int level = 0;; ++level) {
-    const Frame fr = node_frame(cell);
-    const double x = __dmul_rn(__dsub_rn(ux, fr.cx), fr.scale);
-    const double y = __dmul_rn(__dsub_rn(uy, fr.cy), fr.scale);
-    const double z = __dmul_rn(__dsub_rn(uz, fr.cz), fr.scale);
-    const double* a = nt.coef + node * L;
-    auto coef = [&](int k) { return __ldg(a + k); };
-    acc += horner3<P>(coef, x, y, z);
-    if (!inside || level >= Dk) break;
-    const int o = (int)((key >> (3 * (Dk - level - 1))) & 7ull);
-    const int32_t ch = __ldg(nt.child + node * 8 + o);
-    if (ch < 0) break;
-    node = ch;
-    cell = nt.cell[node];
+  if (inside && keys) {
+    const uint64_t key = keys[i];
+    for (int level = 0; level < Dk; ++level) {
+      const int o = (int)((key >> (3 * (Dk - level - 1))) & 7ull);
+      const int32_t ch = __ldg(nt.child + node * 8 + o);
+      if (ch < 0) break;
+      node = ch;
+    }
   }
-  out[qi] = acc;
+  const Frame fr = node_frame(nt.cell[node]);
+  const double x = __dmul_rn(__dsub_rn(ux, fr.cx), fr.scale);
+  const double y = __dmul_rn(__dsub_rn(uy, fr.cy), fr.scale);
+  const double z = __dmul_rn(__dsub_rn(uz, fr.cz), fr.scale);
+  const double* a = nt.pcoef + node * L;
+  auto coef = [&](int k) { return __ldg(a + k); };
+  out[qi] = horner3<P>(coef, x, y, z);
 }
 
 }  // namespace
+
+template <int P>
+void presum_level(const NodeTable& nt, int64_t first, int64_t count, cudaStream_t s) {
+  if (count <= 0) return;
+  FMI_LAUNCH(KID_PRESUM, s, k_presum<P>, (unsigned)count, PS_THREADS, 0, nt, first, count);
+}
 
 template <int P>
 void eval_sorted(const double* q, const uint64_t* keys, const uint32_t* idx, int64_t M, const double lo[3],
@@ -62,7 +141,8 @@ void eval_sorted(const double* q, const uint64_t* keys, const uint32_t* idx, int
 
 #define FMI_INST(P)                                                                                            \
   template void eval_sorted<P>(const double*, const uint64_t*, const uint32_t*, int64_t, const double*, double, \
-                               bool, int, const NodeTable&, double*, cudaStream_t);
+                               bool, int, const NodeTable&, double*, cudaStream_t);                             \
+  template void presum_level<P>(const NodeTable&, int64_t, int64_t, cudaStream_t);
 FMI_INST(0) FMI_INST(1) FMI_INST(2) FMI_INST(3) FMI_INST(4) FMI_INST(5)
 FMI_INST(6) FMI_INST(7) FMI_INST(8) FMI_INST(9) FMI_INST(10)
 #undef FMI_INST

@@ -121,7 +121,7 @@ cudaEvent_t get_event() {
 const char* kNames[KID_COUNT] = {"keys",     "sort",     "gather", "moments", "moments_reduce",
                                  "solve",    "children", "residual", "residual_reduce",
                                  "decide",   "chunks",   "scan",   "eval",    "misc",
-                                 "project",  "m2m",      "level_gather", "refine_solve", "refine"};
+                                 "project",  "m2m",      "level_gather", "refine_solve", "refine", "presum"};
 }  // namespace
 
 const char* kernel_name(int kid) { return (kid >= 0 && kid < KID_COUNT) ? kNames[kid] : "?"; }
@@ -190,7 +190,7 @@ namespace {
 void free_table(NodeTable& t, cudaStream_t s) {
   dfree(t.start, s); dfree(t.end, s); dfree(t.cell, s); dfree(t.parent, s); dfree(t.child, s);
   dfree(t.child_start, s); dfree(t.child_ss, s); dfree(t.coef, s); dfree(t.rms, s); dfree(t.minpiv, s);
-  dfree(t.rank, s); dfree(t.flag, s); dfree(t.mtid, s);
+  dfree(t.rank, s); dfree(t.flag, s); dfree(t.mtid, s); dfree(t.pcoef, s);
   t = NodeTable{};
 }
 
@@ -221,6 +221,7 @@ void ensure_table(NodeTable& t, int64_t& cap, int64_t need, int L, bool fit, cud
     grow_array(t.rank, keep, nc, s);
     grow_array(t.flag, keep, nc, s);
     grow_array(t.mtid, keep, nc, s);
+    grow_array(t.pcoef, keep * L, nc * L, s);
   }
   cap = nc;
 }
@@ -266,7 +267,9 @@ void run_levels(fmi_tree* T, const uint64_t* keys, double* ux, double* uy, doubl
   constexpr int L = rank3(P), K = rank3(2 * P);
   DBuf<int64_t> counts, begin, flags, scan, dev_small(4, s), nflag(2, s);
   DBuf<Chunk> chunks;
-  DBuf<double> partial, mtmom, mtbnd, segsum, lvlmom, scratch, delta;
+  DBuf<double> partial, mtmom, segsum, lvlmom, scratch, delta;
+  DBuf<float> mtbnd;
+  constexpr int KS = (K + 3) & ~3;  // padded moment-tree stride (16-byte rows for TMA)
   DBuf<int32_t> srcseg;
   int64_t* host_small = nullptr;
   FMI_CK(cudaMallocHost(&host_small, 4 * sizeof(int64_t)));
@@ -308,11 +311,11 @@ void run_levels(fmi_tree* T, const uint64_t* keys, double* ux, double* uy, doubl
       FMI_CK(cudaStreamSynchronize(s));
       const int64_t nch = std::min(host_small[0], maxc);
       partial.ensure((size_t)nch * K, s);
-      mtmom.alloc((size_t)MT * K, s);
-      mtbnd.alloc((size_t)MT * K, s);
+      mtmom.alloc((size_t)MT * KS, s);
+      mtbnd.alloc((size_t)MT * KS, s);
       direct_moments<P>(ux, uy, uz, mt.cell, 3, chunks.p, dev_small.p, nch, partial.p, s);
-      reduce_moments(partial.p, begin.p, dev_small.p, MT, 8, K, nullptr, 0, mtmom.p, K, s);
-      bound_init(mt, MT, K, mtbnd.p, s);
+      reduce_moments(partial.p, begin.p, dev_small.p, MT, 8, K, nullptr, 0, mtmom.p, KS, s);
+      bound_init(mt, MT, K, KS, mtbnd.p, s);
       for (int d = (int)mfirst.size() - 2; d >= 0; --d)
         m2m_level<P>(mtmom.p, mtbnd.p, mt.child, mfirst[d], mcount[d], s);
     }
@@ -333,7 +336,7 @@ void run_levels(fmi_tree* T, const uint64_t* keys, double* ux, double* uy, doubl
       segsum.ensure((size_t)(L + 1), s);
       level_residual<P>(c, K6_ROOT, 0, nullptr, chunks.p, dev_small.p, maxc, begin.p, 1, partial.p, segsum.p, s);
       lvlmom.ensure((size_t)(2 * K + L), s);
-      gather_level(mtmom.p, mtbnd.p, T->nt.mtid, segsum.p, nullptr, 0, 1, K, L, lvlmom.p, s);
+      gather_level(mtmom.p, mtbnd.p, T->nt.mtid, segsum.p, nullptr, 0, 1, K, KS, L, lvlmom.p, s);
     }
     const size_t scr_per_node = solve_scratch_per_node(P);
     const int64_t scr_nodes = scr_per_node ? 2048 : 0;
@@ -406,13 +409,15 @@ void run_levels(fmi_tree* T, const uint64_t* keys, double* ux, double* uy, doubl
       const int64_t nnew = host_small[0], npts = host_small[1];
       if (nnew > 0) {
         lvlmom.ensure((size_t)nnew * (2 * K + L), s);
-        gather_level(mtmom.p, mtbnd.p, T->nt.mtid, segsum.p, srcseg.p, first + count, nnew, K, L, lvlmom.p, s);
+        gather_level(mtmom.p, mtbnd.p, T->nt.mtid, segsum.p, srcseg.p, first + count, nnew, K, KS, L, lvlmom.p, s);
       }
       first += count;
       T->nodes = first + nnew;
       count = nnew;
       points = npts;
     }
+    // pre-summed polynomials for the evaluation (f1), level by level from the root
+    for (size_t d = 0; d < T->lvl_first.size(); ++d) presum_level<P>(T->nt, T->lvl_first[d], T->lvl_count[d], s);
   } catch (...) {
     cudaFreeHost(host_small);
     free_table(mt, s);

@@ -47,7 +47,7 @@ void check_cuda(cudaError_t e, const char* what, const char* file, int line);
 enum KernelId {
   KID_KEYS = 0, KID_SORT, KID_GATHER, KID_MOMENTS, KID_MOMENTS_REDUCE, KID_SOLVE, KID_CHILDREN,
   KID_RESIDUAL, KID_RESIDUAL_REDUCE, KID_DECIDE, KID_CHUNKS, KID_SCAN, KID_EVAL, KID_MISC, KID_PROJECT,
-  KID_M2M, KID_LEVEL_GATHER, KID_REFINE_SOLVE, KID_REFINE, KID_COUNT
+  KID_M2M, KID_LEVEL_GATHER, KID_REFINE_SOLVE, KID_REFINE, KID_PRESUM, KID_COUNT
 };
 const char* kernel_name(int kid);
 void prof_begin(int kid, cudaStream_t s);
@@ -118,6 +118,7 @@ struct NodeTable {
   int32_t* rank = nullptr;       // [cap]
   int32_t* flag = nullptr;       // [cap] bit0: re-fitted by the QR path (K5q)
   int32_t* mtid = nullptr;       // [cap] node of the moment tree holding this node's moments
+  double* pcoef = nullptr;       // [cap*L] pre-summed polynomial: own + ancestors' in this node's frame
 };
 
 // ---------------------------------------------------------------------------------------------
@@ -172,15 +173,17 @@ template <int P> void direct_moments(const double* ux, const double* uy, const d
                                      double* partial, cudaStream_t s);
 void reduce_moments(const double* partial, const int64_t* chunk_begin, const int64_t* nchunks_dev, int64_t nodes,
                     int rpn, int K, const int32_t* flag, int bit, double* out, int64_t stride, cudaStream_t s);
-// (m2m.cu) direct-accumulation rounding bound of every moment-tree node (64·eps·owner points)
-void bound_init(const NodeTable& mt, int64_t n, int K, double* bnd, cudaStream_t s);
+// (m2m.cu) direct-accumulation rounding bound of every moment-tree node (64·eps·owner points);
+// moment-tree tensors use the padded stride KS = K rounded up to a multiple of 4 (16-byte rows for TMA, fp64 and fp32)
+void bound_init(const NodeTable& mt, int64_t n, int K, int KS, float* bnd, cudaStream_t s);
 // m2m.cu: mom[node] += Σ_children translate(mom[child]) for the nodes [first, first+count) (one level)
-template <int P> void m2m_level(double* mom, double* bnd, const int32_t* child, int64_t first, int64_t count,
+template <int P> void m2m_level(double* mom, float* bnd, const int32_t* child, int64_t first, int64_t count,
                                 cudaStream_t s);
 // m2m.cu: out[k] = [mtmom[m] (K) | segsum[srcseg[k]][0..𝓛) | mtbnd[m] (K)], m = mtid[first+k]
 // (srcseg null: segment 0)
-void gather_level(const double* mtmom, const double* mtbnd, const int32_t* mtid, const double* segsum,
-                  const int32_t* srcseg, int64_t first, int64_t count, int K, int L, double* out, cudaStream_t s);
+void gather_level(const double* mtmom, const float* mtbnd, const int32_t* mtid, const double* segsum,
+                  const int32_t* srcseg, int64_t first, int64_t count, int K, int KS, int L, double* out,
+                  cudaStream_t s);
 // solve.cu: mom = [moments (K) | projection b (𝓛) | moment rounding bound (K)] per level-local node
 // -> nt.coef (monomial form).  mode 0: flag bit0 -> K5q (pivot < kQrFlagPivot2), bit1 -> semi-normal
 // refinement (pivot < refine2 or n < kRefineFill·𝓛; counted in nflag[0]), bit2 (value 4, exclusive) ->
@@ -223,6 +226,8 @@ template <int P> void level_solve_qr(const LevelCtx& c, const double* mom, doubl
 constexpr double kQrFlagPivot2 = 1e-9;
 
 // eval.cu
+// eval.cu: pcoef of the nodes [first, first+count) of one level (parents' pcoef must be final)
+template <int P> void presum_level(const NodeTable& nt, int64_t first, int64_t count, cudaStream_t s);
 template <int P> void eval_sorted(const double* q, const uint64_t* keys, const uint32_t* idx, int64_t M,
                                   const double lo[3], double width, bool unit, int Dk, const NodeTable& nt,
                                   double* out, cudaStream_t s);

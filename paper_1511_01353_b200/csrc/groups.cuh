@@ -105,8 +105,10 @@ __device__ __forceinline__ void accum(double x, double y, double z, double w, do
   if constexpr (q0 < q1) {
     double zp[CM + 1];
     zp[0] = 1.0;
+    if constexpr (CM >= 1) zp[1] = z;
+    // log-depth power tree: z^c = z^(c/2) z^(c - c/2) (critical path ~log2(c) multiplies, not c)
 #pragma unroll
-    for (int c = 1; c <= CM; ++c) zp[c] = zp[c - 1] * z;
+    for (int c = 2; c <= CM; ++c) zp[c] = zp[c / 2] * zp[c - c / 2];
     const double xw = cpow<pair_a(Q, q0)>(x) * w;
     const double yb = cpow<pair_b(Q, q0)>(y);
     pairs<Q, q0, q1, o0>(x, y, zp, xw, yb, acc);

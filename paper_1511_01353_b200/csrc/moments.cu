@@ -24,6 +24,12 @@ namespace {
 constexpr int K4_THREADS = 256;
 constexpr int K4_WARPS = K4_THREADS / 32;
 constexpr int K4_LIM = 64;  // outputs per group (128 accumulator registers)
+constexpr int K4_RING = 8;  // per-lane point ring (cp.async prefetch distance K4_RING - 1)
+
+__device__ __forceinline__ void cp_async8(double* dst, const double* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)), "l"(src)
+               : "memory");
+}
 
 template <int P>
 struct K4Plan {
@@ -67,6 +73,7 @@ __global__ void __launch_bounds__(K4_THREADS, 1)
               const int64_t* __restrict__ nchunks, double* __restrict__ partial) {
   using PL = K4Plan<P>;
   constexpr int K = PL::K;
+  __shared__ __align__(16) double ring[K4_WARPS * K4_RING * 3 * 32];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int gw = blockIdx.y * K4_WARPS + warp;
   const int64_t cidx = (int64_t)blockIdx.x * 32 + lane;
@@ -76,15 +83,30 @@ __global__ void __launch_bounds__(K4_THREADS, 1)
   double acc[PL::MG];
 #pragma unroll
   for (int k = 0; k < PL::MG; ++k) acc[k] = 0.0;
-  int64_t i = ck.start;
-  double X = 0.0, Y = 0.0, Z = 0.0;
-  if (i < ck.end) { X = ux[i]; Y = uy[i]; Z = uz[i]; }
+  // point stream through a per-warp shared-memory ring filled by cp.async (8-byte LDGSTS): the load of
+  // point i+PD is in flight while points i..i+PD-1 are processed, without tying up registers
+  constexpr int R = K4_RING, PD = K4_RING - 1;
+  double* rg = ring + (size_t)warp * R * 3 * 32;
+  auto issue = [&](int64_t j, int slot) {
+    if (j < ck.end) {
+      double* d = rg + slot * 96 + lane;
+      cp_async8(d, ux + j);
+      cp_async8(d + 32, uy + j);
+      cp_async8(d + 64, uz + j);
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+#pragma unroll
+  for (int k = 0; k < PD; ++k) issue(ck.start + k, k);
+  int t = 0;
 #pragma unroll 1
-  for (; i < ck.end; ++i) {
-    const double x = __dmul_rn(__dsub_rn(X, fr.cx), fr.scale);
-    const double y = __dmul_rn(__dsub_rn(Y, fr.cy), fr.scale);
-    const double z = __dmul_rn(__dsub_rn(Z, fr.cz), fr.scale);
-    if (i + 1 < ck.end) { X = ux[i + 1]; Y = uy[i + 1]; Z = uz[i + 1]; }  // prefetch
+  for (int64_t i = ck.start; i < ck.end; ++i, t = (t + 1 == R) ? 0 : t + 1) {
+    asm volatile("cp.async.wait_group %0;" ::"n"(PD - 1) : "memory");
+    const double* sp = rg + t * 96 + lane;
+    const double x = __dmul_rn(__dsub_rn(sp[0], fr.cx), fr.scale);
+    const double y = __dmul_rn(__dsub_rn(sp[32], fr.cy), fr.scale);
+    const double z = __dmul_rn(__dsub_rn(sp[64], fr.cz), fr.scale);
+    issue(i + PD, (t + PD) % R);
     k4_dispatch<P>(gw, x, y, z, acc, std::make_integer_sequence<int, PL::NG>{});
   }
   int o0 = 0, n = 0;

@@ -43,7 +43,10 @@ struct K5Shape {
   static constexpr int NA = L * (L + 1) / 2;
   static constexpr size_t VEC = (size_t)K + 5 * L;  // moments, b, dinv, col, piv, scratch
   static constexpr bool kSmemA = (VEC + NA) * sizeof(double) <= 220 * 1024;
-  static constexpr size_t SMEM = (kSmemA ? VEC + NA : VEC) * sizeof(double);
+  // global-matrix path: blocked right-looking Cholesky with a column panel of KB columns in smem
+  static constexpr int KB = 32, PLD = KB + 1;
+  static constexpr size_t PANEL = (size_t)L * PLD;
+  static constexpr size_t SMEM = (kSmemA ? VEC + NA : VEC + PANEL) * sizeof(double);
 };
 
 __device__ __forceinline__ int64_t tri(int i) { return (int64_t)i * (i + 1) / 2; }
@@ -130,35 +133,119 @@ __global__ void __launch_bounds__(K5_THREADS)
       }
     }
 
-    // right-looking Cholesky with column rejection
-    for (int j = 0; j < L; ++j) {
-      if (tid == 0) {
-        const double s = A[tri(j) + j];
-        const bool keep = dinv[j] > 0.0 && s > delta2;
-        const double p = keep ? sqrt(s) : 0.0;
-        piv[j] = p;
-        A[tri(j) + j] = p;
-        if (dinv[j] > 0.0 && !(s >= smin_sh[0])) smin_sh[0] = s;  // also catches NaN
-      }
-      __syncthreads();
-      const double p = piv[j];
-      if (p > 0.0) {
-        const double inv = 1.0 / p;
-        for (int i = j + 1 + tid; i < L; i += K5_THREADS) {
-          const double v = A[tri(i) + j] * inv;
-          A[tri(i) + j] = v;
-          col[i] = v;
+    if constexpr (S::kSmemA) {
+      // right-looking Cholesky with column rejection (matrix in shared memory)
+      for (int j = 0; j < L; ++j) {
+        if (tid == 0) {
+          const double s = A[tri(j) + j];
+          const bool keep = dinv[j] > 0.0 && s > delta2;
+          const double p = keep ? sqrt(s) : 0.0;
+          piv[j] = p;
+          A[tri(j) + j] = p;
+          if (dinv[j] > 0.0 && !(s >= smin_sh[0])) smin_sh[0] = s;  // also catches NaN
         }
         __syncthreads();
-        for (int i = j + 1 + warp; i < L; i += NWARP) {
-          const double ci = col[i];
-          double* Ai = A + tri(i);
-          for (int k = j + 1 + lane; k <= i; k += 32) Ai[k] -= ci * col[k];
+        const double p = piv[j];
+        if (p > 0.0) {
+          const double inv = 1.0 / p;
+          for (int i = j + 1 + tid; i < L; i += K5_THREADS) {
+            const double v = A[tri(i) + j] * inv;
+            A[tri(i) + j] = v;
+            col[i] = v;
+          }
+          __syncthreads();
+          for (int i = j + 1 + warp; i < L; i += NWARP) {
+            const double ci = col[i];
+            double* Ai = A + tri(i);
+            for (int k = j + 1 + lane; k <= i; k += 32) Ai[k] -= ci * col[k];
+          }
+        } else {
+          for (int i = j + 1 + tid; i < L; i += K5_THREADS) A[tri(i) + j] = 0.0;
         }
-      } else {
-        for (int i = j + 1 + tid; i < L; i += K5_THREADS) A[tri(i) + j] = 0.0;
+        __syncthreads();
       }
-      __syncthreads();
+    } else {
+      // Blocked right-looking Cholesky with column rejection, matrix in global scratch (L2-resident):
+      // per block of KB columns, the column panel (rows j0..L-1) is factored in shared memory column by
+      // column (the same pivots, rejections and updates as the unblocked algorithm), written back, and
+      // the trailing triangle is updated once with 4x4 register tiles (SYRK against the panel).
+      constexpr int KB = S::KB, PLD = S::PLD;
+      double* Pn = red + L;  // panel [L - j0][PLD]
+      for (int j0 = 0; j0 < L; j0 += KB) {
+        const int bw = min(KB, L - j0), R = L - j0;
+        for (int e = tid; e < R * bw; e += K5_THREADS) {
+          const int r = e / bw, c = e % bw;
+          Pn[r * PLD + c] = (c <= r) ? A[tri(j0 + r) + j0 + c] : 0.0;
+        }
+        __syncthreads();
+        for (int c = 0; c < bw; ++c) {
+          const int j = j0 + c;
+          if (tid == 0) {
+            const double sjj = Pn[c * PLD + c];
+            const bool keep = dinv[j] > 0.0 && sjj > delta2;
+            const double p = keep ? sqrt(sjj) : 0.0;
+            piv[j] = p;
+            Pn[c * PLD + c] = p;
+            if (dinv[j] > 0.0 && !(sjj >= smin_sh[0])) smin_sh[0] = sjj;  // also catches NaN
+          }
+          __syncthreads();
+          const double p = piv[j];
+          const double inv = p > 0.0 ? 1.0 / p : 0.0;
+          for (int r = c + 1 + tid; r < R; r += K5_THREADS) Pn[r * PLD + c] *= inv;
+          __syncthreads();
+          const int nc = bw - c - 1;
+          if (p > 0.0 && nc > 0) {
+            for (int e = tid; e < (R - c - 1) * nc; e += K5_THREADS) {
+              const int r = c + 1 + e / nc, c2 = c + 1 + e % nc;
+              if (c2 <= r) Pn[r * PLD + c2] -= Pn[r * PLD + c] * Pn[c2 * PLD + c];
+            }
+          }
+          __syncthreads();
+        }
+        for (int e = tid; e < R * bw; e += K5_THREADS) {
+          const int r = e / bw, c = e % bw;
+          if (c <= r) A[tri(j0 + r) + j0 + c] = Pn[r * PLD + c];
+        }
+        // trailing update A[i][k] -= Σ_c Pn[i-j0][c] Pn[k-j0][c], j0+bw <= k <= i < L, 4x4 tiles
+        const int j1 = j0 + bw, R2 = L - j1;
+        if (R2 > 0) {
+          const int nt = (R2 + 3) / 4;
+          const int ntile = nt * (nt + 1) / 2;
+          for (int t = tid; t < ntile; t += K5_THREADS) {
+            int ti = (int)((sqrt(8.0 * (double)t + 1.0) - 1.0) * 0.5);
+            while ((ti + 1) * (ti + 2) / 2 <= t) ++ti;
+            while (ti * (ti + 1) / 2 > t) --ti;
+            const int tk = t - ti * (ti + 1) / 2;
+            const int i0 = j1 + 4 * ti, k0 = j1 + 4 * tk;
+            double acc[4][4];
+#pragma unroll
+            for (int a = 0; a < 4; ++a)
+#pragma unroll
+              for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
+            const double* pi = Pn + (i0 - j0) * PLD;
+            const double* pk = Pn + (k0 - j0) * PLD;
+            for (int c = 0; c < bw; ++c) {
+              double av[4], bv[4];
+#pragma unroll
+              for (int a = 0; a < 4; ++a) av[a] = (i0 + a < L) ? pi[a * PLD + c] : 0.0;
+#pragma unroll
+              for (int b = 0; b < 4; ++b) bv[b] = (k0 + b < L) ? pk[b * PLD + c] : 0.0;
+#pragma unroll
+              for (int a = 0; a < 4; ++a)
+#pragma unroll
+                for (int b = 0; b < 4; ++b) acc[a][b] = fma(av[a], bv[b], acc[a][b]);
+            }
+#pragma unroll
+            for (int a = 0; a < 4; ++a)
+#pragma unroll
+              for (int b = 0; b < 4; ++b) {
+                const int i = i0 + a, k = k0 + b;
+                if (i < L && k <= i) A[tri(i) + k] -= acc[a][b];
+              }
+          }
+        }
+        __syncthreads();
+      }
     }
     // forward substitution R̃ᵀ y = b̃
     for (int j = 0; j < L; ++j) {

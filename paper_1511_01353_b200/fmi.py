@@ -35,7 +35,7 @@ EXPORTED = (
 
 KERNELS = ("keys", "sort", "gather", "moments", "moments_reduce", "solve", "children", "residual",
            "residual_reduce", "decide", "chunks", "scan", "eval", "misc", "project", "m2m", "level_gather",
-           "refine_solve", "refine")
+           "refine_solve", "refine", "presum")
 
 
 class FmiNode(ctypes.Structure):
