@@ -36,6 +36,16 @@ sys.path.insert(0, ROOT)
 import workloads  # noqa: E402
 
 FP64_PEAK_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12  # 37.2: SMs × FP64 FMA/clk/SM × 2 × max SM clock
+PEAK_SOURCE = ("alu: fp64 derived 148 SM x 64 FMA/clk x 2 x 1.965 GHz = 37.2 TFLOP/s (measured on this pool: DMMA "
+               "37.0, DFMA 34.2 TFLOP/s, profiles/round1_fp64_peak.txt); hbm: MEASURED_PEAKS.json hbm_gbs")
+
+
+def measured_hbm_peak() -> float:
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return float(json.load(fh)["hbm_gbs"])
+    except Exception:
+        return 6456.8  # the pool's measured copy bandwidth at the time of writing
 
 
 def parse():
@@ -134,18 +144,58 @@ def time_oracle(cfg: workloads.Config, sample_points: int):
 
 
 # ------------------------------------------------------------------------------------------------
-def flops_per_point_level(p: int) -> int:
-    """Algorithmic flops of K4 per point and level: one FMA (2 flops) per raw moment (|γ| <= 2p) and
-    per projection entry (|α| <= p) — DESIGN.md §5; monomial generation is not counted."""
-    K = (2 * p + 1) * (2 * p + 2) * (2 * p + 3) // 6
-    L = (p + 1) * (p + 2) * (p + 3) // 6
-    return 2 * (K + L)
+# algorithmic work per kernel: counted from the method's definition, never from the
+# instructions the kernels issue (monomial generation, padding and masking are not useful work)
+def ranks(p: int):
+    K = (2 * p + 1) * (2 * p + 2) * (2 * p + 3) // 6  # raw moments |γ| <= 2p
+    L = (p + 1) * (p + 2) * (p + 3) // 6              # basis size 𝓛
+    return K, L
+
+
+def kernel_work(cfg, levels_points, depth_max: int):
+    """Per-step algorithmic work of the main kernels: (unit, amount) — flops or bytes."""
+    K, L = ranks(cfg.degree)
+    N, M = cfg.n, cfg.m
+    pts = [int(x) for x in levels_points]
+    return {
+        # K4: one FMA per raw moment per point, once per build (owner pass)
+        "moments": ("flop", 2 * K * N),
+        # K6 per level: Horner (𝓛 FMA) + child projection (𝓛 FMA) + Σr² (1 FMA) per point
+        "residual": ("flop", sum(n * (4 * L + 2) for n in pts)),
+        # K6 root mode: projection of f onto the root frame (𝓛 FMA per point)
+        "project": ("flop", 2 * L * N),
+        # K7: one Horner of the pre-summed polynomial per query
+        "eval": ("flop", 2 * L * M),
+        # K2: per 8-bit pass read key+index (12 B), write them (12 B), histogram read (8 B)
+        "sort": ("byte", 32 * (N * -(-3 * (cfg.max_depth + 1) // 8) + M * -(-3 * depth_max // 8))),
+        # gather: perm (4 B) + point (24 B) + value (8 B) read, 4 SoA doubles (32 B) written
+        "gather": ("byte", 68 * N),
+    }
+
+
+def rooflines(cfg, levels_points, depth_max, prof, steps, ms_per_step, hbm_peak):
+    out = {}
+    for name, (unit, work) in kernel_work(cfg, levels_points, depth_max).items():
+        ms, n = prof.get(name, (0.0, 0))
+        if not n or ms <= 0:
+            continue
+        launches = n / steps
+        per_launch = work / launches
+        mean_s = (ms / n) / 1e3
+        if unit == "flop":
+            achieved, peak, u, bound = per_launch / mean_s / 1e12, FP64_PEAK_TFLOPS, "TFLOP/s", "alu"
+        else:
+            achieved, peak, u, bound = per_launch / mean_s / 1e9, hbm_peak, "GB/s", "hbm"
+        out[name] = {"bound": bound, "achieved": achieved, "peak": peak, "unit": u, "frac": achieved / peak,
+                     "traffic": None, "work_per_launch": per_launch, "launches_per_step": launches,
+                     "mean_launch_ms": ms / n, "share_of_step": (ms / steps) / ms_per_step}
+    return out
 
 
 def run_reference(args, cfg, rank, world):
     if rank != 0:
         return
-    sample_points = 100_000 if cfg.cfg >= 3 else min(cfg.n, 100_000)
+    sample_points = 50_000 if cfg.cfg >= 3 else min(cfg.n, 50_000)
     times = []
     for i in range(args.warmup + args.steps):
         v, dt, sample = time_oracle(cfg, sample_points)
@@ -252,13 +302,12 @@ def main():
     build_pts_s = N / (statistics.median(build_ms) / 1e3)
     eval_pts_s = M / ((ms_per_step - statistics.median(build_ms)) / 1e3)
 
-    # roofline of the dominant kernel (K4 moments+projection): algorithmic flops per launch / mean
-    # launch time (library events on the launching stream, inside the timed region)
-    mom_ms, mom_n = prof.get("moments", (0.0, 0))
+    # rooflines: algorithmic work per launch / mean launch time (library events on the launching
+    # stream, inside the timed region); the dominant kernel is the bench line's "roofline"
     pt_levels = int(np.sum(levels_points))
-    flops_step = pt_levels * flops_per_point_level(cfg.degree)
-    launches_per_step = mom_n / max(args.steps, 1)
-    achieved = (flops_step / launches_per_step) / ((mom_ms / max(mom_n, 1)) / 1e3) / 1e12 if mom_n else None
+    hbm_peak = measured_hbm_peak()
+    roofs = rooflines(cfg, levels_points, len(levels_points) - 1, prof, args.steps, ms_per_step, hbm_peak)
+    dominant = max(roofs, key=lambda k: roofs[k]["share_of_step"]) if roofs else None
     step_kernel_ms = sum(v[0] for v in prof.values()) / args.steps
 
     # ---- e2e through the C ABI with pinned host buffers -----------------------------------------
@@ -286,7 +335,7 @@ def main():
     if rank == 0:
         cpu = None
         if not args.no_cpu_baseline and world == 1:
-            v, dt, sample = time_oracle(cfg, 200_000)
+            v, dt, sample = time_oracle(cfg, 100_000)
             cpu = {"value": v, "unit": "points/s", "cores": 1, "kind": "oracle", "sample": sample,
                    "seconds": dt}
         line = {
@@ -301,18 +350,11 @@ def main():
                 "l2": "inputs >= 6 GB exceed the 126 MB L2; no flush",
                 "nodes": node_count, "levels": len(levels_nodes), "point_levels": pt_levels,
                 "build_points_per_s": build_pts_s, "eval_points_per_s": eval_pts_s,
+                "build_ms_per_step": [round(x, 3) for x in build_ms],
                 "input_gen_s": gen_s,
             },
-            "roofline": {
-                "kernel": "k_moments (K4 moments + projection)",
-                "bound": "alu", "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
-                "frac": (achieved / FP64_PEAK_TFLOPS) if achieved else None, "traffic": None,
-                "peak_source": "derived fp64: 148 SM x 64 DFMA/clk x 2 x 1.965 GHz (measured DMMA 37.1, DFMA 34.2 "
-                               "TFLOP/s: profiles/round1_fp64_peak.txt)",
-                "flops_per_launch": flops_step / max(launches_per_step, 1e-9),
-                "mean_launch_ms": mom_ms / max(mom_n, 1),
-                "share_of_step": (mom_ms / args.steps) / ms_per_step,
-            },
+            "roofline": dict(kernel=dominant, **roofs[dominant], peak_source=PEAK_SOURCE) if dominant else None,
+            "rooflines": roofs,
             "kernels_ms_per_step": {k: v[0] / args.steps for k, v in sorted(prof.items()) if v[1]},
             "kernel_time_fraction": step_kernel_ms / ms_per_step,
             "cpu_baseline": cpu,

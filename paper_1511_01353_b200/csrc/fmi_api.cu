@@ -10,6 +10,8 @@
 
 #include <algorithm>
 #include <atomic>
+#include <chrono>
+#include <cstdio>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -21,7 +23,6 @@
 #include "fmi_internal.cuh"
 
 namespace fmi {
-size_t solve_scratch_per_node(int p);
 
 __global__ void k_scatter_residual(const double* __restrict__ r, const uint32_t* __restrict__ perm, int64_t n,
                                    double* __restrict__ out) {
@@ -187,6 +188,44 @@ struct fmi_tree {
 
 namespace {
 
+// FMI_TRACE=1: host wall time of the build phases to stderr; FMI_TRACE=2: the stream is synchronised
+// at every mark (device + host time per phase).  Diagnostics only.
+struct Trace {
+  int level = 0;
+  std::chrono::steady_clock::time_point t0, last;
+  std::string out;
+  explicit Trace() {
+    if (const char* e = std::getenv("FMI_TRACE")) level = std::atoi(e);
+    t0 = last = std::chrono::steady_clock::now();
+  }
+  void mark(const char* what, cudaStream_t s) {
+    if (!level) return;
+    if (level >= 2) cudaStreamSynchronize(s);
+    const auto now = std::chrono::steady_clock::now();
+    char buf[96];
+    snprintf(buf, sizeof buf, " %s=%.2f", what, std::chrono::duration<double, std::milli>(now - last).count());
+    out += buf;
+    last = now;
+  }
+  void flush(const char* tag) {
+    if (!level) return;
+    const double tot = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    fprintf(stderr, "[fmi trace] %s total=%.2f ms:%s\n", tag, tot, out.c_str());
+  }
+};
+
+thread_local Trace* tl_trace = nullptr;
+inline void tmark(const char* what, cudaStream_t s) {
+  if (tl_trace) tl_trace->mark(what, s);
+}
+
+// pinned 64-byte staging area for the small per-level device->host reads (allocated once per thread)
+int64_t* host_staging() {
+  thread_local int64_t* p = nullptr;
+  if (!p) FMI_CK(cudaMallocHost(&p, 8 * sizeof(int64_t)));
+  return p;
+}
+
 void free_table(NodeTable& t, cudaStream_t s) {
   dfree(t.start, s); dfree(t.end, s); dfree(t.cell, s); dfree(t.parent, s); dfree(t.child, s);
   dfree(t.child_start, s); dfree(t.child_ss, s); dfree(t.coef, s); dfree(t.rms, s); dfree(t.minpiv, s);
@@ -271,8 +310,7 @@ void run_levels(fmi_tree* T, const uint64_t* keys, double* ux, double* uy, doubl
   DBuf<float> mtbnd;
   constexpr int KS = (K + 3) & ~3;  // padded moment-tree stride (16-byte rows for TMA)
   DBuf<int32_t> srcseg;
-  int64_t* host_small = nullptr;
-  FMI_CK(cudaMallocHost(&host_small, 4 * sizeof(int64_t)));
+  int64_t* host_small = host_staging();
   NodeTable mt;
   int64_t mt_cap = 0;
   try {
@@ -298,6 +336,7 @@ void run_levels(fmi_tree* T, const uint64_t* keys, double* ux, double* uy, doubl
       }
       T->mt_nodes = first;
     }
+    tmark("mtree", s);
     const int64_t MT = T->mt_nodes;
     // ---- B. owner-segment moments + M2M (with rounding bounds) ------------------------------------
     {
@@ -313,11 +352,14 @@ void run_levels(fmi_tree* T, const uint64_t* keys, double* ux, double* uy, doubl
       partial.ensure((size_t)nch * K, s);
       mtmom.alloc((size_t)MT * KS, s);
       mtbnd.alloc((size_t)MT * KS, s);
+      tmark("chunks", s);
       direct_moments<P>(ux, uy, uz, mt.cell, 3, chunks.p, dev_small.p, nch, partial.p, s);
       reduce_moments(partial.p, begin.p, dev_small.p, MT, 8, K, nullptr, 0, mtmom.p, KS, s);
       bound_init(mt, MT, K, KS, mtbnd.p, s);
+      tmark("moments", s);
       for (int d = (int)mfirst.size() - 2; d >= 0; --d)
         m2m_level<P>(mtmom.p, mtbnd.p, mt.child, mfirst[d], mcount[d], s);
+      tmark("m2m", s);
     }
     // ---- C. fit levels ---------------------------------------------------------------------------
     ensure_table(T->nt, T->cap, 16, L, true, s);
@@ -338,9 +380,8 @@ void run_levels(fmi_tree* T, const uint64_t* keys, double* ux, double* uy, doubl
       lvlmom.ensure((size_t)(2 * K + L), s);
       gather_level(mtmom.p, mtbnd.p, T->nt.mtid, segsum.p, nullptr, 0, 1, K, KS, L, lvlmom.p, s);
     }
-    const size_t scr_per_node = solve_scratch_per_node(P);
-    const int64_t scr_nodes = scr_per_node ? 2048 : 0;
-    if (scr_nodes) scratch.alloc((size_t)scr_nodes * scr_per_node / sizeof(double), s);
+    tmark("rootproj", s);
+    const size_t fac_per_node = solve_factor_per_node(P);
     const int64_t qr_slots = 148;
     DBuf<double> qr_scratch((size_t)qr_slots * solve_qr_scratch_per_cta(P) / sizeof(double), s);
     for (int depth = 0; count > 0; ++depth) {
@@ -353,7 +394,8 @@ void run_levels(fmi_tree* T, const uint64_t* keys, double* ux, double* uy, doubl
       level_children(c, s);
       // K5: solve; nodes whose translated moments fail the rounding check are re-accumulated directly
       FMI_CK(cudaMemsetAsync(nflag.p, 0, 2 * sizeof(int64_t), s));
-      level_solve<P>(c, lvlmom.p, 0, nullptr, nullptr, T->refine2, nflag.p, scratch.p, scr_nodes, s);
+      scratch.ensure((size_t)count * fac_per_node, s);
+      level_solve<P>(c, lvlmom.p, 0, nullptr, nullptr, T->refine2, nflag.p, scratch.p, s);
       FMI_CK(cudaMemcpyAsync(&host_small[2], nflag.p, 2 * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
       FMI_CK(cudaStreamSynchronize(s));
       if (host_small[3] > 0) {
@@ -370,12 +412,13 @@ void run_levels(fmi_tree* T, const uint64_t* keys, double* ux, double* uy, doubl
         partial.ensure((size_t)nchd * K, s);
         direct_moments<P>(ux, uy, uz, T->nt.cell + first, 0, chunks.p, dev_small.p, nchd, partial.p, s);
         reduce_moments(partial.p, begin.p, dev_small.p, count, 1, K, T->nt.flag + first, 4, lvlmom.p, 2 * K + L, s);
-        level_solve<P>(c, lvlmom.p, 2, nullptr, nullptr, T->refine2, nflag.p, scratch.p, scr_nodes, s);
+        level_solve<P>(c, lvlmom.p, 2, nullptr, nullptr, T->refine2, nflag.p, scratch.p, s);
         FMI_CK(cudaMemcpyAsync(&host_small[2], nflag.p, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
         FMI_CK(cudaStreamSynchronize(s));
         T->direct_nodes += host_small[3];
       }
       const int64_t nref = host_small[2];
+      tmark("solve", s);
       level_solve_qr<P>(c, lvlmom.p, qr_scratch.p, qr_slots, s);
       // fused K6 over the level's octant segments
       const int64_t ch6 = choose_chunk(points, 1024, 8);
@@ -395,11 +438,13 @@ void run_levels(fmi_tree* T, const uint64_t* keys, double* ux, double* uy, doubl
         for (int it = 0; it < T->refine_steps; ++it) {
           level_residual<P>(c, K6_OWN, it, delta.p, chunks.p, dev_small.p + 1, max6, begin.p, count * 8, partial.p,
                             segsum.p, s);
-          level_solve<P>(c, lvlmom.p, 1, segsum.p, delta.p, T->refine2, nflag.p, scratch.p, scr_nodes, s);
+          level_solve<P>(c, lvlmom.p, 1, segsum.p, delta.p, T->refine2, nflag.p, scratch.p, s);
         }
       }
+      tmark("qr+refine", s);
       level_residual<P>(c, K6_CHILD, 0, delta.p, chunks.p, dev_small.p + 1, max6, begin.p, count * 8, partial.p,
                         segsum.p, s);
+      tmark("residual", s);
       flags.ensure(count * 8, s);
       scan.ensure(count * 8, s);
       srcseg.ensure(count * 8, s);
@@ -407,6 +452,7 @@ void run_levels(fmi_tree* T, const uint64_t* keys, double* ux, double* uy, doubl
       FMI_CK(cudaMemcpyAsync(host_small, dev_small.p + 2, 2 * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
       FMI_CK(cudaStreamSynchronize(s));
       const int64_t nnew = host_small[0], npts = host_small[1];
+      tmark("decide", s);
       if (nnew > 0) {
         lvlmom.ensure((size_t)nnew * (2 * K + L), s);
         gather_level(mtmom.p, mtbnd.p, T->nt.mtid, segsum.p, srcseg.p, first + count, nnew, K, KS, L, lvlmom.p, s);
@@ -418,12 +464,11 @@ void run_levels(fmi_tree* T, const uint64_t* keys, double* ux, double* uy, doubl
     }
     // pre-summed polynomials for the evaluation (f1), level by level from the root
     for (size_t d = 0; d < T->lvl_first.size(); ++d) presum_level<P>(T->nt, T->lvl_first[d], T->lvl_count[d], s);
+    tmark("presum", s);
   } catch (...) {
-    cudaFreeHost(host_small);
     free_table(mt, s);
     throw;
   }
-  cudaFreeHost(host_small);
   free_table(mt, s);
 }
 
@@ -469,6 +514,8 @@ fmi_tree* build_impl(const double* pts, const double* f, int64_t N, int degree, 
   if (N > (int64_t)UINT32_MAX) fail(FMI_EPRECOND, "N exceeds 2^32 - 1");
   require_device();
   cudaStream_t s = tl_stream;
+  Trace trace;
+  tl_trace = trace.level ? &trace : nullptr;
 
   // inputs on the device
   DBuf<double> dpts_own, df_own;
@@ -491,6 +538,7 @@ fmi_tree* build_impl(const double* pts, const double* f, int64_t N, int degree, 
   double hb[8];
   FMI_CK(cudaMemcpyAsync(hb, bb.p, sizeof hb, cudaMemcpyDeviceToHost, s));
   FMI_CK(cudaStreamSynchronize(s));
+  tmark("inputs+bbox", s);
   if (hb[6] != 0.0) fail(FMI_EINPUT, "non-finite coordinate or value");
 
   fmi_tree* T = new fmi_tree();
@@ -521,13 +569,16 @@ fmi_tree* build_impl(const double* pts, const double* f, int64_t N, int degree, 
     DBuf<uint64_t> keys(N, s), ktmp(N, s);
     DBuf<uint32_t> perm(N, s), ptmp(N, s);
     morton_keys(dpts, N, T->lo, T->width, T->unit, T->Dk, keys.p, perm.p, s);
+    tmark("keys", s);
     radix_sort_pairs(keys.p, perm.p, ktmp.p, ptmp.p, N, 3 * T->Dk, s);
     ktmp.release();
     ptmp.release();
+    tmark("sort", s);
     DBuf<double> ux(N, s), uy(N, s), uz(N, s), r(N, s);
     gather_points(dpts, df, perm.p, N, T->lo, T->width, T->unit, ux.p, uy.p, uz.p, r.p, s);
     dpts_own.release();
     df_own.release();
+    tmark("gather", s);
     FMI_DISPATCH(degree, run_levels, T, keys.p, ux.p, uy.p, uz.p, r.p, s);
     T->residual = r.p;
     r.p = nullptr;
@@ -542,6 +593,9 @@ fmi_tree* build_impl(const double* pts, const double* f, int64_t N, int degree, 
     throw;
   }
   prof_collect();
+  tmark("end", s);
+  trace.flush("build");
+  tl_trace = nullptr;
   return T;
 }
 
@@ -597,9 +651,11 @@ int guard(F&& fn) {
     tl_err = 0;
     return fn();
   } catch (const Error& e) {
+    tl_trace = nullptr;
     set_error(e.code, e.msg);
     return e.code;
   } catch (const std::exception& e) {
+    tl_trace = nullptr;
     set_error(FMI_ECUDA, e.what());
     return FMI_ECUDA;
   }

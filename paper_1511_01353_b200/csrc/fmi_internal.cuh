@@ -132,7 +132,9 @@ void bbox_and_check(const double* pts, int64_t n, double* out8 /*device: min3,ma
                     const double* f, cudaStream_t s);
 void morton_keys(const double* pts, int64_t n, const double lo[3], double width, bool unit, int D,
                  uint64_t* keys, uint32_t* idx, cudaStream_t s);
-void radix_sort_pairs(uint64_t* keys, uint32_t* vals, uint64_t* keys_tmp, uint32_t* vals_tmp, int64_t n,
+// LSD radix sort of (keys, vals) by the low nbits key bits, stable.  On return keys/vals point at the
+// sorted data and keys_tmp/vals_tmp at the scratch (the pointers may have been swapped).
+void radix_sort_pairs(uint64_t*& keys, uint32_t*& vals, uint64_t*& keys_tmp, uint32_t*& vals_tmp, int64_t n,
                       int nbits, cudaStream_t s);
 void gather_points(const double* pts, const double* f, const uint32_t* perm, int64_t n, const double lo[3],
                    double width, bool unit, double* ux, double* uy, double* uz, double* r, cudaStream_t s);
@@ -191,8 +193,10 @@ void gather_level(const double* mtmom, const float* mtbnd, const int32_t* mtid, 
 // step for bit-1 nodes, b1 = Σ_o segrhs[node*8+o][0..𝓛), δ -> delta[node][𝓛], coef += δ.  mode 2:
 // re-solve of bit-2 nodes after direct accumulation (no rounding check).
 template <int P> void level_solve(const LevelCtx& c, const double* mom, int mode, const double* segrhs,
-                                  double* delta, double refine2, int64_t* nflag, double* scratch,
-                                  int64_t scratch_nodes, cudaStream_t s);
+                                  double* delta, double refine2, int64_t* nflag, double* fac, cudaStream_t s);
+// fac: per level-local node solve_factor_per_node(p) doubles (bordered packed lower factor, kept for
+// the refinement solves)
+size_t solve_factor_per_node(int p);
 // refinement gate (DESIGN.md §5 K5r)
 constexpr double kRefinePivot2 = 1e-6;
 constexpr double kRefineFill = 8.0;

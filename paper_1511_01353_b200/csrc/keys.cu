@@ -117,6 +117,7 @@ constexpr int RS_WARPS = RS_THREADS / 32;
 constexpr int RS_ITEMS = 16;
 constexpr int RS_TILE = RS_THREADS * RS_ITEMS;  // 4096
 constexpr int RS_WARP_ITEMS = RS_TILE / RS_WARPS; // 512
+constexpr size_t kScatterSmem = (size_t)RS_TILE * (sizeof(uint64_t) + sizeof(uint32_t));
 
 __global__ void __launch_bounds__(RS_THREADS) k_rs_hist(const uint64_t* __restrict__ keys, int64_t n, int shift,
                                                         int64_t nblk, int64_t* __restrict__ counts) {
@@ -133,17 +134,25 @@ __global__ void __launch_bounds__(RS_THREADS) k_rs_hist(const uint64_t* __restri
   counts[(int64_t)threadIdx.x * nblk + blockIdx.x] = hist[threadIdx.x];
 }
 
+// Downsweep: stable rank of every item of the tile (per-warp match.any ranking + prefix over warps and
+// digits), the tile is rearranged in shared memory in digit order, then written out so that
+// consecutive threads store consecutive positions of each digit's global run (coalesced).
 __global__ void __launch_bounds__(RS_THREADS) k_rs_scatter(const uint64_t* __restrict__ kin,
                                                            const uint32_t* __restrict__ vin, int64_t n, int shift,
                                                            int64_t nblk, const int64_t* __restrict__ offs,
                                                            uint64_t* __restrict__ kout, uint32_t* __restrict__ vout) {
   __shared__ int whist[RS_WARPS][257];
+  __shared__ int tstart[257];           // exclusive prefix of the tile's digit counts
   __shared__ int64_t boff[256];
+  extern __shared__ __align__(16) uint64_t rs_dyn[];
+  uint64_t* sk = rs_dyn;                                       // [RS_TILE]
+  uint32_t* sv = reinterpret_cast<uint32_t*>(rs_dyn + RS_TILE);  // [RS_TILE]
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   for (int t = threadIdx.x; t < RS_WARPS * 257; t += RS_THREADS) (&whist[0][0])[t] = 0;
   boff[threadIdx.x] = offs[(int64_t)threadIdx.x * nblk + blockIdx.x];
   __syncthreads();
-  const int64_t base = (int64_t)blockIdx.x * RS_TILE + (int64_t)warp * RS_WARP_ITEMS;
+  const int64_t tbase = (int64_t)blockIdx.x * RS_TILE;
+  const int64_t base = tbase + (int64_t)warp * RS_WARP_ITEMS;
   const unsigned lt_mask = (1u << lane) - 1u;
   uint64_t k[RS_ITEMS];
   uint32_t v[RS_ITEMS];
@@ -168,7 +177,7 @@ __global__ void __launch_bounds__(RS_THREADS) k_rs_scatter(const uint64_t* __res
     rank[it] = before + __popc(peers & lt_mask);
   }
   __syncthreads();
-  {  // exclusive prefix over warps for each digit
+  {  // exclusive prefix over warps for each digit; digit totals of the tile
     int d = threadIdx.x, run = 0;
 #pragma unroll
     for (int w = 0; w < RS_WARPS; ++w) {
@@ -176,15 +185,41 @@ __global__ void __launch_bounds__(RS_THREADS) k_rs_scatter(const uint64_t* __res
       whist[w][d] = run;
       run += t;
     }
+    tstart[d] = run;  // count for now
+  }
+  __syncthreads();
+  if (warp == 0) {  // exclusive scan of the 256 digit counts (8 per lane)
+    int c[8], sum = 0;
+#pragma unroll
+    for (int t = 0; t < 8; ++t) { c[t] = tstart[lane * 8 + t]; sum += c[t]; }
+    int inc = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int y = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += y;
+    }
+    int run = inc - sum;
+#pragma unroll
+    for (int t = 0; t < 8; ++t) { tstart[lane * 8 + t] = run; run += c[t]; }
+    if (lane == 31) tstart[256] = run;
   }
   __syncthreads();
 #pragma unroll
   for (int it = 0; it < RS_ITEMS; ++it) {
     if (dig[it] < 256) {
-      int64_t pos = boff[dig[it]] + whist[warp][dig[it]] + rank[it];
-      kout[pos] = k[it];
-      vout[pos] = v[it];
+      const int pos = tstart[dig[it]] + whist[warp][dig[it]] + rank[it];
+      sk[pos] = k[it];
+      sv[pos] = v[it];
     }
+  }
+  __syncthreads();
+  const int cnt = tstart[256];
+  for (int pos = threadIdx.x; pos < cnt; pos += RS_THREADS) {
+    const uint64_t kk = sk[pos];
+    const int d = (int)((kk >> shift) & 255);
+    const int64_t g = boff[d] + (pos - tstart[d]);
+    kout[g] = kk;
+    vout[g] = sv[pos];
   }
 }
 
@@ -222,9 +257,14 @@ void morton_keys(const double* pts, int64_t n, const double lo[3], double width,
   FMI_LAUNCH(KID_KEYS, s, k_keys, grid, 256, 0, pts, n, lo[0], lo[1], lo[2], width, unit, D, keys, idx);
 }
 
-void radix_sort_pairs(uint64_t* keys, uint32_t* vals, uint64_t* keys_tmp, uint32_t* vals_tmp, int64_t n, int nbits,
-                      cudaStream_t s) {
+void radix_sort_pairs(uint64_t*& keys, uint32_t*& vals, uint64_t*& keys_tmp, uint32_t*& vals_tmp, int64_t n,
+                      int nbits, cudaStream_t s) {
   if (n <= 1 || nbits <= 0) return;
+  static bool attr = false;
+  if (!attr) {
+    FMI_CK(cudaFuncSetAttribute(k_rs_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kScatterSmem));
+    attr = true;
+  }
   const int64_t nblk = (n + RS_TILE - 1) / RS_TILE;
   DBuf<int64_t> counts((size_t)nblk * 256, s);
   uint64_t* ka = keys; uint32_t* va = vals; uint64_t* kb = keys_tmp; uint32_t* vb = vals_tmp;
@@ -232,14 +272,13 @@ void radix_sort_pairs(uint64_t* keys, uint32_t* vals, uint64_t* keys_tmp, uint32
   for (int shift = 0; shift < nbits; shift += 8, ++passes) {
     FMI_LAUNCH(KID_SORT, s, k_rs_hist, (unsigned)nblk, RS_THREADS, 0, ka, n, shift, nblk, counts.p);
     exclusive_scan_i64(counts.p, counts.p, nblk * 256, nullptr, s);
-    FMI_LAUNCH(KID_SORT, s, k_rs_scatter, (unsigned)nblk, RS_THREADS, 0, ka, va, n, shift, nblk, counts.p, kb, vb);
+    FMI_LAUNCH(KID_SORT, s, k_rs_scatter, (unsigned)nblk, RS_THREADS, kScatterSmem, ka, va, n, shift, nblk, counts.p,
+               kb, vb);
     std::swap(ka, kb);
     std::swap(va, vb);
   }
-  if (passes & 1) {  // result is in the tmp buffers: copy back
-    FMI_CK(cudaMemcpyAsync(keys, ka, n * sizeof(uint64_t), cudaMemcpyDeviceToDevice, s));
-    FMI_CK(cudaMemcpyAsync(vals, va, n * sizeof(uint32_t), cudaMemcpyDeviceToDevice, s));
-  }
+  // the sorted result is in (ka, va): hand the buffers back swapped instead of copying
+  keys = ka; vals = va; keys_tmp = kb; vals_tmp = vb;
 }
 
 void gather_points(const double* pts, const double* f, const uint32_t* perm, int64_t n, const double lo[3],
