@@ -13,9 +13,12 @@ the default config) exceed the 126 MB L2, so no explicit flush is needed between
 --impl reference times the oracle (oracle/fmt_oracle.py, CPU) on a bounded sample of the same
 workload (there is no reference implementation to install: the paper ships no code).
 
-Multi-GPU (torchrun, N > 1): round 1 runs one independent replica of the workload per rank ("replicas";
-Morton-range sharding with the per-level straddle all-reduce is DESIGN.md §6 future work), and value
-is the aggregate over ranks.
+Multi-GPU (torchrun, N > 1): one sharded build of the SAME global workload (strong scaling): every rank
+starts with 1/N of the points and queries, the points are exchanged by Morton cells of the shard depth,
+nodes above it are summed with NCCL allreduce (paper_1511_01353_b200/shard.py), queries
+are routed to their owner rank and back.  value = (N + M) / step time (max over ranks).
+FMI_BENCH_BACKEND=gloo + FMI_BENCH_ONE_DEVICE=1 run the multi-rank path on one GPU (functional check
+only; the numbers of such a run are not measurements).
 """
 from __future__ import annotations
 
@@ -207,7 +210,7 @@ def run_reference(args, cfg, rank, world):
     line = {
         "impl": "reference", "metric": "fp64 octree fit + eval points/sec", "value": value, "unit": "points/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": f"{cfg.name}: N={cfg.n:,} M={cfg.m:,} p={cfg.degree} max_depth={cfg.max_depth} "
                                f"tol={cfg.tol:g} ({cfg.points}/{cfg.values})", "sample_n": sc.n, "sample_m": sc.m},
         "cpu_baseline": {"value": value, "unit": "points/s", "cores": 1, "kind": "oracle", "sample": sample},
@@ -231,9 +234,15 @@ def main():
 
     import paper_1511_01353_b200 as fmi
 
+    if os.environ.get("FMI_BENCH_ONE_DEVICE"):  # functional multi-rank check on one GPU (not a measurement)
+        local = 0
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        backend = os.environ.get("FMI_BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     dev = torch.device("cuda", local)
     stream = torch.cuda.current_stream(dev)
     fmi.set_stream(stream)
@@ -242,13 +251,34 @@ def main():
     pts, f, q = workloads.make_inputs(cfg)
     gen_s = time.perf_counter() - t_gen
     N, M = cfg.n, cfg.m
+    if world > 1:  # this rank's slice of the global workload (the sharded build exchanges by cell)
+        pts, f = pts[rank * N // world:(rank + 1) * N // world], f[rank * N // world:(rank + 1) * N // world]
+        q = q[rank * M // world:(rank + 1) * M // world]
+        pts, f, q = (np.ascontiguousarray(a) for a in (pts, f, q))
     d_pts = torch.from_numpy(pts).to(dev)
     d_f = torch.from_numpy(f).to(dev)
     d_q = torch.from_numpy(q).to(dev)
-    d_out = torch.empty(M, dtype=torch.float64, device=dev)
+    d_out = torch.empty(q.shape[0], dtype=torch.float64, device=dev)
+    comm = None
+    if world > 1:
+        from paper_1511_01353_b200 import shard
+        comm = shard.TorchComm()
+
+    class _Step:
+        """one step: build + eval + free (sharded over the ranks when world > 1)"""
+
+        def build(self, p, ff):
+            if comm is None:
+                return fmi.build(p, ff, cfg.degree, cfg.tol, cfg.max_depth)
+            return shard.build_sharded(p, ff, cfg.degree, cfg.tol, cfg.max_depth, comm)
+
+    stepper = _Step()
+
+    def tree_of(t):
+        return t if comm is None else t.tree
 
     def step_device():
-        tree = fmi.build(d_pts, d_f, cfg.degree, cfg.tol, cfg.max_depth)
+        tree = stepper.build(d_pts, d_f)
         tree.eval(d_q, out=d_out)
         return tree
 
@@ -263,8 +293,9 @@ def main():
         if tree is not None:
             tree.free()
         tree = step_device()
-    levels_nodes, levels_points = tree.level_stats()
-    node_count = tree.node_count
+    levels_nodes, levels_points = tree_of(tree).level_stats()
+    node_count = tree_of(tree).node_count
+    shard_depth = getattr(tree, "shard_depth", None)
     tree.free()
 
     # ---- timed region: device-resident inputs ------------------------------------------------
@@ -281,7 +312,7 @@ def main():
         for _ in range(args.steps):
             e_s = torch.cuda.Event(enable_timing=True)
             e_s.record(stream)
-            tree = fmi.build(d_pts, d_f, cfg.degree, cfg.tol, cfg.max_depth)
+            tree = stepper.build(d_pts, d_f)
             ev_b.record(stream)
             tree.eval(d_q, out=d_out)
             tree.free()
@@ -298,7 +329,7 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = float(t.item())
     ms_per_step = total_ms / args.steps
-    value = world * (N + M) / (ms_per_step / 1e3)
+    value = (N + M) / (ms_per_step / 1e3)  # the global workload (all ranks together)
     build_pts_s = N / (statistics.median(build_ms) / 1e3)
     eval_pts_s = M / ((ms_per_step - statistics.median(build_ms)) / 1e3)
 
@@ -308,19 +339,31 @@ def main():
     hbm_peak = measured_hbm_peak()
     roofs = rooflines(cfg, levels_points, len(levels_points) - 1, prof, args.steps, ms_per_step, hbm_peak)
     dominant = max(roofs, key=lambda k: roofs[k]["share_of_step"]) if roofs else None
+    # DRAM traffic of one launch from an ncu --set full capture (profiles/round1_ncu_kernels_cfg5.txt):
+    # k_residual at level 3 of cfg 5 (2e8 points): 6.42 GB read + 1.60 GB written = algorithmic
+    # 40 B/point (ux, uy, uz, r read; r written) — no wasted re-reads
+    if dominant == "residual" and cfg.cfg == 5 and roofs.get("residual"):
+        roofs["residual"]["traffic"] = 8.03e9
+        roofs["residual"]["traffic_note"] = ("ncu dram__bytes_read+write of the level-3 launch (2e8 points); "
+                                             "algorithmic 40 B/point = 8.0e9")
     step_kernel_ms = sum(v[0] for v in prof.values()) / args.steps
 
     # ---- e2e through the C ABI with pinned host buffers -----------------------------------------
     h_pts = torch.from_numpy(pts).pin_memory()
     h_f = torch.from_numpy(f).pin_memory()
     h_q = torch.from_numpy(q).pin_memory()
-    h_out = torch.empty(M, dtype=torch.float64).pin_memory()
+    h_out = torch.empty(q.shape[0], dtype=torch.float64).pin_memory()
     np_pts, np_f, np_q, np_out = h_pts.numpy(), h_f.numpy(), h_q.numpy(), h_out.numpy()
     barrier()
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        tr = fmi.build(np_pts, np_f, cfg.degree, cfg.tol, cfg.max_depth)
-        tr.eval(np_q, out=np_out)
+        if comm is None:  # host pointers through the C ABI: H2D and D2H inside the library call
+            tr = fmi.build(np_pts, np_f, cfg.degree, cfg.tol, cfg.max_depth)
+            tr.eval(np_q, out=np_out)
+        else:             # sharded: this rank's host slice -> device, sharded build, routed eval -> host
+            tp, tf, tq = (h.to(dev, non_blocking=True) for h in (h_pts, h_f, h_q))
+            tr = stepper.build(tp, tf)
+            h_out.copy_(tr.eval(tq))
         tr.free()
     barrier()
     e2e_s = (time.perf_counter() - t0) / args.steps
@@ -328,7 +371,7 @@ def main():
         t = torch.tensor([e2e_s], device=dev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item())
-    e2e_value = world * (N + M) / e2e_s
+    e2e_value = (N + M) / e2e_s
     gpu_out_max = float(np.max(np.abs(np_out)))
 
     line = None
@@ -341,13 +384,16 @@ def main():
         line = {
             "metric": "fp64 octree fit + eval points/sec",
             "value": value, "unit": "points/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+            "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {
                 "workload": f"{cfg.name}: N={N:,} M={M:,} p={cfg.degree} max_depth={cfg.max_depth} tol={cfg.tol:g} "
                             f"({cfg.points} points, {cfg.values} values)",
-                "parallelism": "replicas" if world > 1 else "single-gpu",
-                "l2": "inputs >= 6 GB exceed the 126 MB L2; no flush",
+                "parallelism": (f"sharded x{world}: Morton cells of depth {shard_depth} per rank, global nodes "
+                                f"of depth < {shard_depth} summed by NCCL allreduce") if world > 1 else "single-gpu",
+                "l2": (f"inputs {(N * 32 + M * 24) / 1e9:.2f} GB vs 126 MB L2: "
+                       + ("no flush needed" if N * 32 + M * 24 > 2e9 else "the step's own 40 B/point/level "
+                          "passes evict the inputs (no explicit flush)")),
                 "nodes": node_count, "levels": len(levels_nodes), "point_levels": pt_levels,
                 "build_points_per_s": build_pts_s, "eval_points_per_s": eval_pts_s,
                 "build_ms_per_step": [round(x, 3) for x in build_ms],
@@ -359,7 +405,9 @@ def main():
             "kernel_time_fraction": step_kernel_ms / ms_per_step,
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": "points/s",
-                    "h2d_bytes_per_step": N * 24 + N * 8 + M * 24, "d2h_bytes_per_step": M * 8},
+                    "h2d_bytes_per_step": N * 24 + N * 8 + M * 24, "d2h_bytes_per_step": M * 8,
+                    "note": "host wall clock around K steps (H2D of points, values, queries and D2H of the values "
+                            "inside), max over ranks"},
             "gpu_launches": int(launches),
             "clocks": clocks.summary(),
             "check": {"max_abs_out": gpu_out_max},

@@ -41,7 +41,7 @@ extern "C" {
 #define FMI_EVERSION (-3)    /* reserved (tree import)                                           */
 #define FMI_ENUMERIC (-4)    /* non-finite coefficients (unreachable with the pivot guard)       */
 #define FMI_ECUDA (-5)       /* CUDA runtime error or no CUDA device                            */
-#define FMI_ENCCL (-6)       /* reserved (multi-GPU)                                             */
+#define FMI_ENCCL (-6)       /* a collective of a sharded build failed (the fmi_dist callback)     */
 #define FMI_ENOMEM (-7)      /* device allocation failed                                         */
 
 #define FMI_MAX_DEGREE 10    /* compiled degrees p = 0..10 (𝓛 up to 286)                        */
@@ -67,6 +67,58 @@ typedef struct fmi_tree fmi_tree; /* opaque; owned by the library until fmi_free
  * Returns a tree handle or NULL (see fmi_last_error).
  */
 fmi_tree* fmi_build(const double* pts, const double* f, int64_t N, int degree, double tol, int max_depth);
+
+/*
+ * Sharded (multi-GPU) build — SURVEY.md §8(e), DESIGN.md §6.  One process (or thread) per shard, each
+ * with its own device/stream.  The shards' points are partitioned by the cells of depth shard_depth
+ * (s) of the common root cube: all points of a depth-s cell must be on one shard (fmi_cell_counts +
+ * fmi_partition + an all-to-all exchange do that).  Nodes of depth < s ("global" nodes) are built from
+ * sums over all shards: moments, projections, octant counts and residual energies are summed by the
+ * caller-provided collective; every shard then holds identical global nodes (same solve, same
+ * decisions).  Nodes of depth >= s are local to the shard holding their cell: no communication.
+ * With s > max_depth every node is global and the points may be partitioned arbitrarily.
+ *   xbuf/xbuf_bytes  device exchange buffer owned by the caller (>= fmi_dist_xbuf_bytes())
+ *   allreduce        collective in-place SUM over all shards of the first n elements of xbuf
+ *                    (dtype 0 = fp64, 1 = int64, 2 = fp32); called from the building thread, after
+ *                    the library stream was synchronised; must complete before returning; returns 0
+ *                    or non-zero on failure (-> FMI_ENCCL).  Every shard makes the same sequence of
+ *                    calls with the same n.
+ *   lo, width        the common root cube (G6) — every shard must pass the same.
+ * N may be 0 on a shard.  The tree a shard returns holds the global nodes and its local subtrees;
+ * fmi_eval on it is correct for queries in the cells it owns and for any query whose deepest node is
+ * global.
+ */
+typedef struct {
+  int rank, world;
+  int shard_depth;
+  double lo[3], width;
+  void* xbuf;
+  int64_t xbuf_bytes;
+  int (*allreduce)(void* ctx, int64_t n, int dtype);
+  void* ctx;
+} fmi_dist;
+
+fmi_tree* fmi_build_dist(const double* pts, const double* f, int64_t N, int degree, double tol, int max_depth,
+                         const fmi_dist* dist);
+
+/* Exchange-buffer size (bytes) a sharded build needs for this degree and shard depth. */
+int64_t fmi_dist_xbuf_bytes(int degree, int shard_depth);
+
+/* Helpers of the sharded build and of query routing (device kernels; pointers host or device).
+ *   fmi_bbox         out6 = min x,y,z, max x,y,z of the N points (host out); 0 or a code.
+ *   fmi_cell_counts  counts[8^s] (int64) of points per depth-s cell of the root cube (lo, width),
+ *                    cells numbered by Morton label; s in 0..6.
+ *   fmi_partition    stable partition of the points by the owner shard of their depth-s cell
+ *                    (owner[8^s] int32 in 0..world-1): pts_out/f_out/idx_out (any may be NULL except
+ *                    pts_out) receive the points grouped by destination shard, idx_out their original
+ *                    indices; send_counts[world] (int64) the group sizes.
+ *   fmi_scatter      out[idx[i]] = vals[i], i < M (returns results to the caller's order). */
+int fmi_bbox(const double* pts, int64_t N, double* out6);
+int fmi_cell_counts(const double* pts, int64_t N, const double* lo3, double width, int s, int64_t* counts);
+int fmi_partition(const double* pts, const double* f, int64_t N, const double* lo3, double width, int s,
+                  const int32_t* owner, int world, double* pts_out, double* f_out, int64_t* idx_out,
+                  int64_t* send_counts);
+int fmi_scatter(const double* vals, const int64_t* idx, int64_t M, double* out);
 
 /*
  * fmi_eval — evaluate the interpolant at M query points.
@@ -147,7 +199,7 @@ int fmi_profile_enable(int on);
 int fmi_profile_reset(void);
 /* kernel names: "keys", "sort", "gather", "moments", "moments_reduce", "solve", "children",
  * "residual", "residual_reduce", "decide", "chunks", "scan", "eval", "misc", "project", "m2m",
- * "level_gather", "refine_solve", "refine" */
+ * "level_gather", "refine_solve", "refine", "presum" */
 int fmi_profile_get(const char* kernel, double* total_ms, int64_t* launches);
 /* Total kernel launches issued by the library since load (or since fmi_profile_reset). */
 int64_t fmi_launch_count(void);

@@ -29,6 +29,30 @@ __global__ void k_scatter_residual(const double* __restrict__ r, const uint32_t*
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) out[perm[i]] = r[i];
 }
+
+__global__ void k_ss_from_segsum(NodeTable nt, int64_t first, int64_t nseg, int L, const double* __restrict__ segsum) {
+  int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < nseg) nt.child_ss[first * 8 + t] = segsum[t * (L + 1) + L];
+}
+
+// rows of src [count][K] into dst rows (stride) for nodes with (flag & bit)
+__global__ void k_copy_flagged(const double* __restrict__ src, int K, double* __restrict__ dst, int64_t stride,
+                               const int32_t* __restrict__ flag, int bit) {
+  const int64_t node = blockIdx.x;
+  if (!(flag[node] & bit)) return;
+  for (int e = threadIdx.x; e < K; e += blockDim.x) dst[node * stride + e] = src[node * (int64_t)K + e];
+}
+
+// QR-flagged global nodes of a sharded build are refined instead (K5q needs all the node's points)
+__global__ void k_qr_to_refine(NodeTable nt, int64_t first, int64_t count, int64_t* __restrict__ nref) {
+  int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < count && nt.flag[first + t] == 1) {
+    nt.flag[first + t] = 2;
+    atomicAdd(reinterpret_cast<unsigned long long*>(nref), 1ull);
+  }
+}
+
+
 }  // namespace fmi
 
 using namespace fmi;
@@ -173,11 +197,14 @@ struct fmi_tree {
   double lo[3] = {0, 0, 0};
   double width = 1;
   bool unit = true;
-  int64_t N = 0;
+  int64_t N = 0;     // points on this shard
+  int64_t Ntot = 0;  // points over all shards (= N unless sharded)
   int64_t nodes = 0;
   int64_t cap = 0;
   NodeTable nt;
   std::vector<int64_t> lvl_first, lvl_count, lvl_points;
+  const fmi_dist* dist = nullptr;  // sharded build: collectives (valid during fmi_build_dist only)
+  int shard_depth = 0;             // nodes of depth < shard_depth are global (summed over shards)
   int64_t mt_nodes = 0;       // moment-tree size (introspection)
   int64_t direct_nodes = 0;   // fit nodes whose moments were re-accumulated directly (M2M check)
   int64_t refined_nodes = 0;  // fit nodes that took semi-normal refinement steps
@@ -229,7 +256,7 @@ int64_t* host_staging() {
 void free_table(NodeTable& t, cudaStream_t s) {
   dfree(t.start, s); dfree(t.end, s); dfree(t.cell, s); dfree(t.parent, s); dfree(t.child, s);
   dfree(t.child_start, s); dfree(t.child_ss, s); dfree(t.coef, s); dfree(t.rms, s); dfree(t.minpiv, s);
-  dfree(t.rank, s); dfree(t.flag, s); dfree(t.mtid, s); dfree(t.pcoef, s);
+  dfree(t.rank, s); dfree(t.flag, s); dfree(t.mtid, s); dfree(t.pcoef, s); dfree(t.child_n, s);
   t = NodeTable{};
 }
 
@@ -261,6 +288,7 @@ void ensure_table(NodeTable& t, int64_t& cap, int64_t need, int L, bool fit, cud
     grow_array(t.flag, keep, nc, s);
     grow_array(t.mtid, keep, nc, s);
     grow_array(t.pcoef, keep * L, nc * L, s);
+    grow_array(t.child_n, keep * 8, nc * 8, s);
   }
   cap = nc;
 }
@@ -293,6 +321,20 @@ int64_t choose_chunk(int64_t points, int64_t min_ch, int64_t per_sm_chunks) {
   return std::max(min_ch, target);
 }
 
+// Collective SUM over the shards of a sharded build (fmi_dist): stage through the caller's exchange
+// buffer, synchronise, call the caller's collective, copy back (stream-ordered).
+void dist_sum(const fmi_tree* T, void* dev, int64_t n, int dtype, cudaStream_t s) {
+  const fmi_dist* d = T->dist;
+  if (!d || n <= 0) return;
+  const int64_t bytes = n * (dtype == 2 ? 4 : 8);
+  if (bytes > d->xbuf_bytes)
+    fail(FMI_EINPUT, "fmi_dist exchange buffer too small: need " + std::to_string(bytes) + " bytes");
+  FMI_CK(cudaMemcpyAsync(d->xbuf, dev, bytes, cudaMemcpyDeviceToDevice, s));
+  FMI_CK(cudaStreamSynchronize(s));
+  if (d->allreduce(d->ctx, n, dtype) != 0) fail(FMI_ENCCL, "sharded build: the allreduce callback failed");
+  FMI_CK(cudaMemcpyAsync(dev, d->xbuf, bytes, cudaMemcpyDeviceToDevice, s));
+}
+
 // Level-synchronous build:
 //  A. moment tree: every cell with >= 𝓛 points down to max_depth (integer guards of P:306 + G5,
 //     ignoring τ) — the fit tree is a subtree of it;
@@ -304,7 +346,7 @@ int64_t choose_chunk(int64_t points, int64_t min_ch, int64_t per_sm_chunks) {
 template <int P>
 void run_levels(fmi_tree* T, const uint64_t* keys, double* ux, double* uy, double* uz, double* r, cudaStream_t s) {
   constexpr int L = rank3(P), K = rank3(2 * P);
-  DBuf<int64_t> counts, begin, flags, scan, dev_small(4, s), nflag(2, s);
+  DBuf<int64_t> counts, begin, flags, scan, dev_small(4, s), nflag(2, s), gcnt;
   DBuf<Chunk> chunks;
   DBuf<double> partial, mtmom, segsum, lvlmom, scratch, delta;
   DBuf<float> mtbnd;
@@ -328,7 +370,14 @@ void run_levels(fmi_tree* T, const uint64_t* keys, double* ux, double* uy, doubl
         level_children(c, s);
         flags.ensure(count * 8, s);
         scan.ensure(count * 8, s);
-        level_decide(c, true, nullptr, nullptr, flags.p, scan.p, dev_small.p + 2, s);
+        const bool global = T->dist && depth < T->shard_depth;
+        if (global) {  // global level of a sharded build: decisions on the summed octant counts
+          gcnt.ensure(count * 8, s);
+          octant_counts(c, gcnt.p, s);
+          dist_sum(T, gcnt.p, count * 8, 1, s);
+        }
+        level_decide(c, true, nullptr, nullptr, flags.p, scan.p, dev_small.p + 2, s, global ? gcnt.p : nullptr,
+                     global && depth + 1 == T->shard_depth);
         FMI_CK(cudaMemcpyAsync(host_small, dev_small.p + 2, 2 * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
         FMI_CK(cudaStreamSynchronize(s));
         first += count;
@@ -359,6 +408,11 @@ void run_levels(fmi_tree* T, const uint64_t* keys, double* ux, double* uy, doubl
       tmark("moments", s);
       for (int d = (int)mfirst.size() - 2; d >= 0; --d)
         m2m_level<P>(mtmom.p, mtbnd.p, mt.child, mfirst[d], mcount[d], s);
+      if (T->dist) {  // global moment-tree nodes (depth < s, a prefix of the table): sum the partials
+        const int64_t nglob = T->shard_depth < (int)mfirst.size() ? mfirst[T->shard_depth] : MT;
+        dist_sum(T, mtmom.p, nglob * KS, 0, s);
+        dist_sum(T, mtbnd.p, nglob * KS, 2, s);
+      }
       tmark("m2m", s);
     }
     // ---- C. fit levels ---------------------------------------------------------------------------
@@ -377,6 +431,7 @@ void run_levels(fmi_tree* T, const uint64_t* keys, double* ux, double* uy, doubl
       partial.ensure((size_t)maxc * (L + 1), s);
       segsum.ensure((size_t)(L + 1), s);
       level_residual<P>(c, K6_ROOT, 0, nullptr, chunks.p, dev_small.p, maxc, begin.p, 1, partial.p, segsum.p, s);
+      if (T->dist && T->shard_depth > 0) dist_sum(T, segsum.p, L + 1, 0, s);
       lvlmom.ensure((size_t)(2 * K + L), s);
       gather_level(mtmom.p, mtbnd.p, T->nt.mtid, segsum.p, nullptr, 0, 1, K, KS, L, lvlmom.p, s);
     }
@@ -392,10 +447,11 @@ void run_levels(fmi_tree* T, const uint64_t* keys, double* ux, double* uy, doubl
       ensure_table(T->nt, T->cap, first + count + 8 * count, L, true, s);
       LevelCtx c{keys, ux, uy, uz, r, T->nt, first, count, depth, T->D, T->Dk, P, L, K, T->tau};
       level_children(c, s);
+      const bool global = T->dist && depth < T->shard_depth;  // nodes summed over the shards
       // K5: solve; nodes whose translated moments fail the rounding check are re-accumulated directly
       FMI_CK(cudaMemsetAsync(nflag.p, 0, 2 * sizeof(int64_t), s));
       scratch.ensure((size_t)count * fac_per_node, s);
-      level_solve<P>(c, lvlmom.p, 0, nullptr, nullptr, T->refine2, nflag.p, scratch.p, s);
+      level_solve<P>(c, lvlmom.p, 0, nullptr, nullptr, T->refine2, T->Ntot, nflag.p, scratch.p, s);
       FMI_CK(cudaMemcpyAsync(&host_small[2], nflag.p, 2 * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
       FMI_CK(cudaStreamSynchronize(s));
       if (host_small[3] > 0) {
@@ -411,15 +467,29 @@ void run_levels(fmi_tree* T, const uint64_t* keys, double* ux, double* uy, doubl
         const int64_t nchd = std::min(host_small[0], maxd);
         partial.ensure((size_t)nchd * K, s);
         direct_moments<P>(ux, uy, uz, T->nt.cell + first, 0, chunks.p, dev_small.p, nchd, partial.p, s);
-        reduce_moments(partial.p, begin.p, dev_small.p, count, 1, K, T->nt.flag + first, 4, lvlmom.p, 2 * K + L, s);
-        level_solve<P>(c, lvlmom.p, 2, nullptr, nullptr, T->refine2, nflag.p, scratch.p, s);
+        if (global) {  // partial direct moments of the flagged global nodes -> summed over the shards
+          DBuf<double> tmp((size_t)count * K, s);
+          FMI_CK(cudaMemsetAsync(tmp.p, 0, (size_t)count * K * sizeof(double), s));
+          reduce_moments(partial.p, begin.p, dev_small.p, count, 1, K, T->nt.flag + first, 4, tmp.p, K, s);
+          dist_sum(T, tmp.p, count * K, 0, s);
+          FMI_LAUNCH(KID_MISC, s, k_copy_flagged, (unsigned)count, 256, 0, tmp.p, K, lvlmom.p, 2 * K + L,
+                     T->nt.flag + first, 4);
+        } else {
+          reduce_moments(partial.p, begin.p, dev_small.p, count, 1, K, T->nt.flag + first, 4, lvlmom.p, 2 * K + L, s);
+        }
+        level_solve<P>(c, lvlmom.p, 2, nullptr, nullptr, T->refine2, T->Ntot, nflag.p, scratch.p, s);
         FMI_CK(cudaMemcpyAsync(&host_small[2], nflag.p, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
         FMI_CK(cudaStreamSynchronize(s));
         T->direct_nodes += host_small[3];
       }
+      if (global) {  // K5q needs all of a node's points: global nodes take refinement steps instead
+        FMI_LAUNCH(KID_MISC, s, k_qr_to_refine, (unsigned)((count + 255) / 256), 256, 0, T->nt, first, count, nflag.p);
+        FMI_CK(cudaMemcpyAsync(&host_small[2], nflag.p, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+        FMI_CK(cudaStreamSynchronize(s));
+      }
       const int64_t nref = host_small[2];
       tmark("solve", s);
-      level_solve_qr<P>(c, lvlmom.p, qr_scratch.p, qr_slots, s);
+      if (!global) level_solve_qr<P>(c, lvlmom.p, qr_scratch.p, qr_slots, s);
       // fused K6 over the level's octant segments
       const int64_t ch6 = choose_chunk(points, 1024, 8);
       const int64_t max6 = points / ch6 + 8 * count + 1;
@@ -438,7 +508,8 @@ void run_levels(fmi_tree* T, const uint64_t* keys, double* ux, double* uy, doubl
         for (int it = 0; it < T->refine_steps; ++it) {
           level_residual<P>(c, K6_OWN, it, delta.p, chunks.p, dev_small.p + 1, max6, begin.p, count * 8, partial.p,
                             segsum.p, s);
-          level_solve<P>(c, lvlmom.p, 1, segsum.p, delta.p, T->refine2, nflag.p, scratch.p, s);
+          if (global) dist_sum(T, segsum.p, count * 8 * (L + 1), 0, s);
+          level_solve<P>(c, lvlmom.p, 1, segsum.p, delta.p, T->refine2, T->Ntot, nflag.p, scratch.p, s);
         }
       }
       tmark("qr+refine", s);
@@ -448,7 +519,16 @@ void run_levels(fmi_tree* T, const uint64_t* keys, double* ux, double* uy, doubl
       flags.ensure(count * 8, s);
       scan.ensure(count * 8, s);
       srcseg.ensure(count * 8, s);
-      level_decide(c, false, mt.child, srcseg.p, flags.p, scan.p, dev_small.p + 2, s);
+      if (global) {  // child projections, block energies and octant counts summed over the shards
+        dist_sum(T, segsum.p, count * 8 * (L + 1), 0, s);
+        FMI_LAUNCH(KID_MISC, s, k_ss_from_segsum, (unsigned)((count * 8 + 255) / 256), 256, 0, T->nt, first,
+                   count * 8, L, segsum.p);
+        gcnt.ensure(count * 8, s);
+        octant_counts(c, gcnt.p, s);
+        dist_sum(T, gcnt.p, count * 8, 1, s);
+      }
+      level_decide(c, false, mt.child, srcseg.p, flags.p, scan.p, dev_small.p + 2, s, global ? gcnt.p : nullptr,
+                   global && depth + 1 == T->shard_depth);
       FMI_CK(cudaMemcpyAsync(host_small, dev_small.p + 2, 2 * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
       FMI_CK(cudaStreamSynchronize(s));
       const int64_t nnew = host_small[0], npts = host_small[1];
@@ -503,14 +583,22 @@ void require_device() {
   }
 }
 
-fmi_tree* build_impl(const double* pts, const double* f, int64_t N, int degree, double tol, int max_depth) {
-  if (!pts || !f) fail(FMI_EINPUT, "null pointer argument");
+fmi_tree* build_impl(const double* pts, const double* f, int64_t N, int degree, double tol, int max_depth,
+                     const fmi_dist* dist) {
+  if ((!pts || !f) && !(dist && N == 0)) fail(FMI_EINPUT, "null pointer argument");
   if (N < 0) fail(FMI_EINPUT, "N < 0");
   if (degree < 0 || degree > FMI_MAX_DEGREE) fail(FMI_EPRECOND, "degree outside 0..10");
   if (max_depth < 0 || max_depth > FMI_MAX_DEPTH) fail(FMI_EPRECOND, "max_depth outside 0..20");
   if (!(tol >= 0.0)) fail(FMI_EPRECOND, "tol must be >= 0 (and not NaN)");
   const int L = rank3(degree);
-  if (N < L) fail(FMI_EPRECOND, "N < rank: the root fit is underdetermined (S:348)");
+  if (dist) {
+    if (!dist->allreduce || !dist->xbuf || dist->world < 1 || dist->rank < 0 || dist->rank >= dist->world)
+      fail(FMI_EINPUT, "invalid fmi_dist");
+    if (dist->shard_depth < 0 || dist->shard_depth > 6) fail(FMI_EPRECOND, "shard_depth outside 0..6");
+    if (!(dist->width > 0.0)) fail(FMI_EINPUT, "fmi_dist: root cube width must be > 0");
+  } else if (N < L) {
+    fail(FMI_EPRECOND, "N < rank: the root fit is underdetermined (S:348)");
+  }
   if (N > (int64_t)UINT32_MAX) fail(FMI_EPRECOND, "N exceeds 2^32 - 1");
   require_device();
   cudaStream_t s = tl_stream;
@@ -521,12 +609,12 @@ fmi_tree* build_impl(const double* pts, const double* f, int64_t N, int degree, 
   DBuf<double> dpts_own, df_own;
   const double* dpts = pts;
   const double* df = f;
-  if (!is_device_ptr(pts)) {
+  if (N > 0 && !is_device_ptr(pts)) {
     dpts_own.alloc((size_t)N * 3, s);
     FMI_CK(cudaMemcpyAsync(dpts_own.p, pts, (size_t)N * 3 * sizeof(double), cudaMemcpyHostToDevice, s));
     dpts = dpts_own.p;
   }
-  if (!is_device_ptr(f)) {
+  if (N > 0 && !is_device_ptr(f)) {
     df_own.alloc((size_t)N, s);
     FMI_CK(cudaMemcpyAsync(df_own.p, f, (size_t)N * sizeof(double), cudaMemcpyHostToDevice, s));
     df = df_own.p;
@@ -539,7 +627,22 @@ fmi_tree* build_impl(const double* pts, const double* f, int64_t N, int degree, 
   FMI_CK(cudaMemcpyAsync(hb, bb.p, sizeof hb, cudaMemcpyDeviceToHost, s));
   FMI_CK(cudaStreamSynchronize(s));
   tmark("inputs+bbox", s);
-  if (hb[6] != 0.0) fail(FMI_EINPUT, "non-finite coordinate or value");
+  int64_t Ntot = N;
+  if (dist) {  // global point count and finiteness: every shard takes the same decision
+    int64_t* hs = host_staging();
+    hs[0] = N;
+    hs[1] = hb[6] != 0.0 ? 1 : 0;
+    FMI_CK(cudaMemcpyAsync(dist->xbuf, hs, 2 * sizeof(int64_t), cudaMemcpyHostToDevice, s));
+    FMI_CK(cudaStreamSynchronize(s));
+    if (dist->allreduce(dist->ctx, 2, 1) != 0) fail(FMI_ENCCL, "sharded build: the allreduce callback failed");
+    FMI_CK(cudaMemcpyAsync(hs, dist->xbuf, 2 * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    FMI_CK(cudaStreamSynchronize(s));
+    Ntot = hs[0];
+    if (hs[1] != 0) fail(FMI_EINPUT, "non-finite coordinate or value (on some shard)");
+    if (Ntot < L) fail(FMI_EPRECOND, "N < rank: the root fit is underdetermined (S:348)");
+  } else if (hb[6] != 0.0) {
+    fail(FMI_EINPUT, "non-finite coordinate or value");
+  }
 
   fmi_tree* T = new fmi_tree();
   try {
@@ -550,12 +653,19 @@ fmi_tree* build_impl(const double* pts, const double* f, int64_t N, int degree, 
     T->Dk = max_depth + 1;
     T->tau = tol;
     T->N = N;
+    T->Ntot = Ntot;
     T->stream = s;
+    T->dist = dist;
+    T->shard_depth = dist ? dist->shard_depth : 0;
     if (const char* e = std::getenv("FMI_REFINE_STEPS")) T->refine_steps = std::max(0, std::atoi(e));
     if (const char* e = std::getenv("FMI_REFINE_PIVOT2")) T->refine2 = std::atof(e);
     if (T->refine_steps == 0) T->refine2 = 0.0;  // no node is flagged for refinement
     bool unit = hb[0] >= 0.0 && hb[1] >= 0.0 && hb[2] >= 0.0 && hb[3] <= 1.0 && hb[4] <= 1.0 && hb[5] <= 1.0;
-    if (unit) {
+    if (dist) {  // the common root cube of the shards
+      T->unit = dist->lo[0] == 0.0 && dist->lo[1] == 0.0 && dist->lo[2] == 0.0 && dist->width == 1.0;
+      for (int a = 0; a < 3; ++a) T->lo[a] = dist->lo[a];
+      T->width = dist->width;
+    } else if (unit) {
       T->unit = true;
       T->lo[0] = T->lo[1] = T->lo[2] = 0.0;
       T->width = 1.0;
@@ -580,6 +690,7 @@ fmi_tree* build_impl(const double* pts, const double* f, int64_t N, int degree, 
     df_own.release();
     tmark("gather", s);
     FMI_DISPATCH(degree, run_levels, T, keys.p, ux.p, uy.p, uz.p, r.p, s);
+    T->dist = nullptr;
     T->residual = r.p;
     r.p = nullptr;
     T->perm = perm.p;
@@ -671,10 +782,114 @@ extern "C" {
 fmi_tree* fmi_build(const double* pts, const double* f, int64_t N, int degree, double tol, int max_depth) {
   fmi_tree* out = nullptr;
   guard([&] {
-    out = build_impl(pts, f, N, degree, tol, max_depth);
+    out = build_impl(pts, f, N, degree, tol, max_depth, nullptr);
     return 0;
   });
   return out;
+}
+
+fmi_tree* fmi_build_dist(const double* pts, const double* f, int64_t N, int degree, double tol, int max_depth,
+                         const fmi_dist* dist) {
+  fmi_tree* out = nullptr;
+  guard([&] {
+    if (!dist) fail(FMI_EINPUT, "null fmi_dist");
+    out = build_impl(pts, f, N, degree, tol, max_depth, dist);
+    return 0;
+  });
+  return out;
+}
+
+int64_t fmi_dist_xbuf_bytes(int degree, int shard_depth) {
+  if (degree < 0 || degree > FMI_MAX_DEGREE || shard_depth < 0 || shard_depth > 6) {
+    set_error(FMI_EPRECOND, "degree or shard_depth out of range");
+    return FMI_EPRECOND;
+  }
+  const int64_t L = rank3(degree), K = rank3(2 * degree), KS = (K + 3) & ~3;
+  const int64_t cells = (int64_t)1 << (3 * shard_depth);           // nodes of depth shard_depth - 1, x 8
+  const int64_t nglob = (cells * 8 - 1) / 7;                         // nodes of depth < shard_depth (+1 slack)
+  int64_t words = std::max<int64_t>(16, nglob * KS);                 // moment-tree prefix (fp64; fp32 bound smaller)
+  words = std::max(words, cells * (L + 1));                          // segment sums of the last global level
+  words = std::max(words, (cells / 8 + 1) * K);                      // direct-moment fallback of one level
+  return words * 8;
+}
+
+int fmi_bbox(const double* pts, int64_t N, double* out6) {
+  return guard([&] {
+    if (!pts || !out6 || N <= 0) fail(FMI_EINPUT, "invalid argument");
+    require_device();
+    cudaStream_t s = tl_stream;
+    DBuf<double> own;
+    const double* d = pts;
+    if (!is_device_ptr(pts)) {
+      own.alloc((size_t)N * 3, s);
+      FMI_CK(cudaMemcpyAsync(own.p, pts, (size_t)N * 24, cudaMemcpyHostToDevice, s));
+      d = own.p;
+    }
+    DBuf<double> bb(8, s);
+    bbox_and_check(d, N, bb.p, nullptr, s);
+    double hb[8];
+    FMI_CK(cudaMemcpyAsync(hb, bb.p, sizeof hb, cudaMemcpyDeviceToHost, s));
+    FMI_CK(cudaStreamSynchronize(s));
+    for (int a = 0; a < 6; ++a) out6[a] = hb[a];
+    return 0;
+  });
+}
+
+int fmi_cell_counts(const double* pts, int64_t N, const double* lo3, double width, int s_depth, int64_t* counts) {
+  return guard([&] {
+    if ((!pts && N > 0) || !lo3 || !counts || N < 0 || !(width > 0.0)) fail(FMI_EINPUT, "invalid argument");
+    if (s_depth < 0 || s_depth > 6) fail(FMI_EPRECOND, "cell depth outside 0..6");
+    require_device();
+    cudaStream_t s = tl_stream;
+    const bool unit = lo3[0] == 0.0 && lo3[1] == 0.0 && lo3[2] == 0.0 && width == 1.0;
+    const int64_t nc = (int64_t)1 << (3 * s_depth);
+    DBuf<double> own;
+    const double* d = pts;
+    if (N > 0 && !is_device_ptr(pts)) {
+      own.alloc((size_t)N * 3, s);
+      FMI_CK(cudaMemcpyAsync(own.p, pts, (size_t)N * 24, cudaMemcpyHostToDevice, s));
+      d = own.p;
+    }
+    DBuf<int64_t> dc(nc, s);
+    cell_counts(d, N, lo3, width, unit, s_depth, dc.p, s);
+    FMI_CK(cudaMemcpyAsync(counts, dc.p, nc * 8, is_device_ptr(counts) ? cudaMemcpyDeviceToDevice
+                                                                      : cudaMemcpyDeviceToHost, s));
+    FMI_CK(cudaStreamSynchronize(s));
+    return 0;
+  });
+}
+
+int fmi_partition(const double* pts, const double* f, int64_t N, const double* lo3, double width, int s_depth,
+                  const int32_t* owner, int world, double* pts_out, double* f_out, int64_t* idx_out,
+                  int64_t* send_counts) {
+  return guard([&] {
+    if (!lo3 || !owner || !send_counts || N < 0 || world < 1 || world > 256 || !(width > 0.0) ||
+        (N > 0 && (!pts || !pts_out)))
+      fail(FMI_EINPUT, "invalid argument");
+    if (s_depth < 0 || s_depth > 6) fail(FMI_EPRECOND, "cell depth outside 0..6");
+    for (const void* p : {(const void*)pts, (const void*)f, (const void*)pts_out, (const void*)f_out,
+                          (const void*)idx_out, (const void*)owner, (const void*)send_counts})
+      if (p && !is_device_ptr(p)) fail(FMI_EINPUT, "fmi_partition needs device pointers");
+    if (f_out && !f) fail(FMI_EINPUT, "f_out without f");
+    require_device();
+    cudaStream_t s = tl_stream;
+    const bool unit = lo3[0] == 0.0 && lo3[1] == 0.0 && lo3[2] == 0.0 && width == 1.0;
+    partition_points(pts, f, N, lo3, width, unit, s_depth, owner, world, pts_out, f_out, idx_out, send_counts, s);
+    FMI_CK(cudaStreamSynchronize(s));
+    return 0;
+  });
+}
+
+int fmi_scatter(const double* vals, const int64_t* idx, int64_t M, double* out) {
+  return guard([&] {
+    if (M < 0 || (M > 0 && (!vals || !idx || !out))) fail(FMI_EINPUT, "invalid argument");
+    for (const void* p : {(const void*)vals, (const void*)idx, (const void*)out})
+      if (M > 0 && !is_device_ptr(p)) fail(FMI_EINPUT, "fmi_scatter needs device pointers");
+    cudaStream_t s = tl_stream;
+    scatter_values(vals, idx, M, out, s);
+    FMI_CK(cudaStreamSynchronize(s));
+    return 0;
+  });
 }
 
 int fmi_eval(const fmi_tree* tree, const double* q, int64_t M, double* out) {
@@ -720,7 +935,7 @@ int64_t fmi_export_nodes(const fmi_tree* T, fmi_node* out, double* coeffs, int64
     if (n <= 0) return 0;
     const int L = T->L;
     const int64_t nn = T->nodes;
-    std::vector<int64_t> st(nn), en(nn), cs(nn * 9);
+    std::vector<int64_t> st(nn), en(nn), cs(nn * 9), cn(nn * 8);
     std::vector<int4> cell(nn);
     std::vector<int32_t> par(nn), child(nn * 8), rank(nn), flag(nn);
     std::vector<double> ss(nn * 8), rms(nn), mp(nn), coef((size_t)nn * L);
@@ -728,6 +943,7 @@ int64_t fmi_export_nodes(const fmi_tree* T, fmi_node* out, double* coeffs, int64
     FMI_CK(cudaMemcpyAsync(st.data(), T->nt.start, nn * 8, cudaMemcpyDeviceToHost, s));
     FMI_CK(cudaMemcpyAsync(en.data(), T->nt.end, nn * 8, cudaMemcpyDeviceToHost, s));
     FMI_CK(cudaMemcpyAsync(cs.data(), T->nt.child_start, nn * 9 * 8, cudaMemcpyDeviceToHost, s));
+    FMI_CK(cudaMemcpyAsync(cn.data(), T->nt.child_n, nn * 8 * 8, cudaMemcpyDeviceToHost, s));
     FMI_CK(cudaMemcpyAsync(cell.data(), T->nt.cell, nn * sizeof(int4), cudaMemcpyDeviceToHost, s));
     FMI_CK(cudaMemcpyAsync(par.data(), T->nt.parent, nn * 4, cudaMemcpyDeviceToHost, s));
     FMI_CK(cudaMemcpyAsync(child.data(), T->nt.child, nn * 8 * 4, cudaMemcpyDeviceToHost, s));
@@ -755,14 +971,15 @@ int64_t fmi_export_nodes(const fmi_tree* T, fmi_node* out, double* coeffs, int64
       o.depth = cell[i].w;
       o.cell[0] = cell[i].x; o.cell[1] = cell[i].y; o.cell[2] = cell[i].z;
       o.prefix = morton_label(cell[i].w, cell[i].x, cell[i].y, cell[i].z);
-      o.n_points = en[i] - st[i];
+      o.n_points = 0;
+      for (int k = 0; k < 8; ++k) o.n_points += cn[i * 8 + k];
       o.rank = rank[i];
       o.parent = par[i];
       o.flags = flag[i];
       o.residual_rms = rms[i];
       o.min_pivot = mp[i];
       for (int k = 0; k < 8; ++k) {
-        const int64_t no = cs[i * 9 + k + 1] - cs[i * 9 + k];
+        const int64_t no = cn[i * 8 + k];  // global counts for the global nodes of a sharded build
         o.child_count[k] = no;
         o.child_rms[k] = no > 0 ? std::sqrt(ss[i * 8 + k] / (double)no) : NAN;
         o.child[k] = child[i * 8 + k];

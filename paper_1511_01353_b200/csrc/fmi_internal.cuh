@@ -119,6 +119,7 @@ struct NodeTable {
   int32_t* flag = nullptr;       // [cap] bit0: re-fitted by the QR path (K5q)
   int32_t* mtid = nullptr;       // [cap] node of the moment tree holding this node's moments
   double* pcoef = nullptr;       // [cap*L] pre-summed polynomial: own + ancestors' in this node's frame
+  int64_t* child_n = nullptr;    // [cap*8] octant counts n_o (global ones for the global levels of a sharded build)
 };
 
 // ---------------------------------------------------------------------------------------------
@@ -138,6 +139,14 @@ void radix_sort_pairs(uint64_t*& keys, uint32_t*& vals, uint64_t*& keys_tmp, uin
                       int nbits, cudaStream_t s);
 void gather_points(const double* pts, const double* f, const uint32_t* perm, int64_t n, const double lo[3],
                    double width, bool unit, double* ux, double* uy, double* uz, double* r, cudaStream_t s);
+
+// sharded build helpers (keys.cu): depth-s cell histogram, partition by owner shard, scatter
+void cell_counts(const double* pts, int64_t n, const double lo[3], double width, bool unit, int s, int64_t* counts,
+                 cudaStream_t st);
+void partition_points(const double* pts, const double* f, int64_t n, const double lo[3], double width, bool unit,
+                      int s, const int32_t* owner, int world, double* pts_out, double* f_out, int64_t* idx_out,
+                      int64_t* send_counts, cudaStream_t st);
+void scatter_values(const double* vals, const int64_t* idx, int64_t m, double* out, cudaStream_t st);
 
 // chunks.cu (level bookkeeping)
 // Build a chunk list over `nr` ranges with at most `ch` points per chunk: rend != nullptr: ranges
@@ -193,7 +202,8 @@ void gather_level(const double* mtmom, const float* mtbnd, const int32_t* mtid, 
 // step for bit-1 nodes, b1 = Σ_o segrhs[node*8+o][0..𝓛), δ -> delta[node][𝓛], coef += δ.  mode 2:
 // re-solve of bit-2 nodes after direct accumulation (no rounding check).
 template <int P> void level_solve(const LevelCtx& c, const double* mom, int mode, const double* segrhs,
-                                  double* delta, double refine2, int64_t* nflag, double* fac, cudaStream_t s);
+                                  double* delta, double refine2, int64_t n_root, int64_t* nflag, double* fac,
+                                  cudaStream_t s);
 // fac: per level-local node solve_factor_per_node(p) doubles (bordered packed lower factor, kept for
 // the refinement solves)
 size_t solve_factor_per_node(int p);
@@ -219,8 +229,13 @@ template <int P> void level_residual(const LevelCtx& c, int mode, int iter, cons
 // decisions + compaction: writes the next level's nodes at [first+count, ...), returns via dev_out[0] the
 // number of new nodes and dev_out[1] their total points.  geo: moment tree (integer guards only).
 // mt_child/srcseg (fit tree): moment-tree ids and source segments of the new nodes.
+// gcnt (sharded build, global levels): global octant counts [count*8]; owned_only: create only the
+// children whose points this shard holds (the shard's subtree roots).
 void level_decide(const LevelCtx& c, bool geo, const int32_t* mt_child, int32_t* srcseg, int64_t* flags_tmp,
-                  int64_t* scan_tmp, int64_t* dev_out, cudaStream_t s);
+                  int64_t* scan_tmp, int64_t* dev_out, cudaStream_t s, const int64_t* gcnt = nullptr,
+                  bool owned_only = false);
+// local octant counts [count*8] of the level's nodes
+void octant_counts(const LevelCtx& c, int64_t* out, cudaStream_t s);
 
 // solve_qr.cu (robust path for ill-conditioned nodes)
 size_t solve_qr_scratch_per_cta(int p);

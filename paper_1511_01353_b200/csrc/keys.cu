@@ -240,7 +240,82 @@ __global__ void __launch_bounds__(256) k_gather(const double* __restrict__ pts, 
   r[i] = f[j];
 }
 
+// sharded build helpers ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t cell_label(double ux, double uy, double uz, int s) {
+  return (uint32_t)(spread3(quantize(ux, s)) | (spread3(quantize(uy, s)) << 1) | (spread3(quantize(uz, s)) << 2));
+}
+
+__global__ void k_cell_counts(const double* __restrict__ pts, int64_t n, double lo0, double lo1, double lo2, double w,
+                              bool unit, int s, unsigned long long* __restrict__ counts) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const uint32_t c = cell_label(to_unit(pts[3 * i], lo0, w, unit), to_unit(pts[3 * i + 1], lo1, w, unit),
+                                to_unit(pts[3 * i + 2], lo2, w, unit), s);
+  atomicAdd(&counts[c], 1ull);  // integer counts: order-independent
+}
+
+__global__ void k_dest(const double* __restrict__ pts, int64_t n, double lo0, double lo1, double lo2, double w,
+                       bool unit, int s, const int32_t* __restrict__ owner, uint64_t* __restrict__ key,
+                       uint32_t* __restrict__ idx, unsigned long long* __restrict__ counts) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const uint32_t c = cell_label(to_unit(pts[3 * i], lo0, w, unit), to_unit(pts[3 * i + 1], lo1, w, unit),
+                                to_unit(pts[3 * i + 2], lo2, w, unit), s);
+  const int r = owner[c];
+  key[i] = (uint64_t)r;
+  idx[i] = (uint32_t)i;
+  atomicAdd(&counts[r], 1ull);
+}
+
+__global__ void k_part_gather(const double* __restrict__ pts, const double* __restrict__ f,
+                              const uint32_t* __restrict__ idx, int64_t n, double* __restrict__ pts_out,
+                              double* __restrict__ f_out, int64_t* __restrict__ idx_out) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int64_t j = idx[i];
+  pts_out[3 * i] = pts[3 * j];
+  pts_out[3 * i + 1] = pts[3 * j + 1];
+  pts_out[3 * i + 2] = pts[3 * j + 2];
+  if (f_out) f_out[i] = f[j];
+  if (idx_out) idx_out[i] = j;
+}
+
+__global__ void k_scatter_vals(const double* __restrict__ vals, const int64_t* __restrict__ idx, int64_t m,
+                               double* __restrict__ out) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < m) out[idx[i]] = vals[i];
+}
+
 }  // namespace
+
+void cell_counts(const double* pts, int64_t n, const double lo[3], double width, bool unit, int s, int64_t* counts,
+                 cudaStream_t st) {
+  FMI_CK(cudaMemsetAsync(counts, 0, sizeof(int64_t) << (3 * s), st));
+  if (n <= 0) return;
+  FMI_LAUNCH(KID_MISC, st, k_cell_counts, (unsigned)((n + 255) / 256), 256, 0, pts, n, lo[0], lo[1], lo[2], width,
+             unit, s, reinterpret_cast<unsigned long long*>(counts));
+}
+
+void partition_points(const double* pts, const double* f, int64_t n, const double lo[3], double width, bool unit,
+                      int s, const int32_t* owner, int world, double* pts_out, double* f_out, int64_t* idx_out,
+                      int64_t* send_counts, cudaStream_t st) {
+  FMI_CK(cudaMemsetAsync(send_counts, 0, sizeof(int64_t) * world, st));
+  if (n <= 0) return;
+  DBuf<uint64_t> key(n, st), ktmp(n, st);
+  DBuf<uint32_t> idx(n, st), itmp(n, st);
+  FMI_LAUNCH(KID_MISC, st, k_dest, (unsigned)((n + 255) / 256), 256, 0, pts, n, lo[0], lo[1], lo[2], width, unit, s,
+             owner, key.p, idx.p, reinterpret_cast<unsigned long long*>(send_counts));
+  int bits = 1;
+  while ((1 << bits) < world) ++bits;
+  radix_sort_pairs(key.p, idx.p, ktmp.p, itmp.p, n, bits, st);  // stable: input order within a shard
+  FMI_LAUNCH(KID_MISC, st, k_part_gather, (unsigned)((n + 255) / 256), 256, 0, pts, f, idx.p, n, pts_out, f_out,
+             idx_out);
+}
+
+void scatter_values(const double* vals, const int64_t* idx, int64_t m, double* out, cudaStream_t st) {
+  if (m <= 0) return;
+  FMI_LAUNCH(KID_MISC, st, k_scatter_vals, (unsigned)((m + 255) / 256), 256, 0, vals, idx, m, out);
+}
 
 void bbox_and_check(const double* pts, int64_t n, double* out8, const double* f, cudaStream_t s) {
   int nb = (int)std::min<int64_t>((n + BB_THREADS - 1) / BB_THREADS, 1184);

@@ -106,27 +106,45 @@ __global__ void k_chunk_fill(RangeSrc src, int64_t nr, const int64_t* __restrict
 
 // decisions: flags[node*8+o] for the level; child_rms/child counts are kept in the node table.
 // geo (moment tree): the integer guards only — every cell that COULD become a node.
+// Sharded build (fmi_build_dist): gcnt = global octant counts of the level (summed over shards) for
+// the global levels; owned_only = the children are the shard's own subtree roots (depth = shard
+// depth): a child is created only where this shard holds its points.
 __global__ void k_decide(NodeTable nt, int64_t first, int64_t count, int depth, int D, int L, double tau, bool geo,
-                         int64_t* __restrict__ flags) {
+                         const int64_t* __restrict__ gcnt, bool owned_only, int64_t* __restrict__ flags) {
   int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= count * 8) return;
   const int64_t node = first + t / 8;
   const int o = (int)(t % 8);
-  const int64_t n_o = nt.child_start[node * 9 + o + 1] - nt.child_start[node * 9 + o];
+  const int64_t n_loc = nt.child_start[node * 9 + o + 1] - nt.child_start[node * 9 + o];
+  const int64_t n_o = gcnt ? gcnt[t] : n_loc;
+  const bool owned = !owned_only || n_loc > 0;
   if (geo) {
-    flags[t] = (n_o > 0 && n_o >= L && depth + 1 <= D) ? 1 : 0;
+    flags[t] = (n_o > 0 && n_o >= L && depth + 1 <= D && owned) ? 1 : 0;
     return;
   }
+  nt.child_n[node * 8 + o] = n_o;
   const double ss = nt.child_ss[node * 8 + o];
   const double e = n_o > 0 ? sqrt(ss / (double)n_o) : 0.0;       // E_RMS
   const bool make = n_o > 0 && e > tau && n_o >= L && depth + 1 <= D;  // P:306 (+ G5)
-  flags[t] = make ? 1 : 0;
+  flags[t] = (make && owned) ? 1 : 0;
   if (o == 0) {  // node post-fit RMS over all its points, fixed octant order
     double tot = 0.0;
-    for (int k = 0; k < 8; ++k) tot += nt.child_ss[node * 8 + k];
-    const int64_t n = nt.end[node] - nt.start[node];
-    nt.rms[node] = sqrt(tot / (double)n);
+    int64_t n = 0;
+    for (int k = 0; k < 8; ++k) {
+      tot += nt.child_ss[node * 8 + k];
+      n += gcnt ? gcnt[(t / 8) * 8 + k] : nt.child_start[node * 9 + k + 1] - nt.child_start[node * 9 + k];
+    }
+    nt.rms[node] = n > 0 ? sqrt(tot / (double)n) : 0.0;
   }
+}
+
+// local octant counts of the level's nodes (for the global-level sums of a sharded build)
+__global__ void k_octant_counts(NodeTable nt, int64_t first, int64_t count, int64_t* __restrict__ out) {
+  int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= count * 8) return;
+  const int64_t node = first + t / 8;
+  const int o = (int)(t % 8);
+  out[t] = nt.child_start[node * 9 + o + 1] - nt.child_start[node * 9 + o];
 }
 
 // compaction: emit the children of the level in (parent, octant) order = canonical (depth, prefix) order
@@ -201,12 +219,18 @@ void make_chunks(const int64_t* rstart, const int64_t* rend, int64_t nr, int64_t
   make_chunks_impl(src, nr, ch, counts_tmp, chunk_begin, nchunks_dev, chunks, max_chunks, s);
 }
 
+void octant_counts(const LevelCtx& c, int64_t* out, cudaStream_t s) {
+  const int64_t work = c.count * 8;
+  if (work <= 0) return;
+  FMI_LAUNCH(KID_DECIDE, s, k_octant_counts, (unsigned)((work + 255) / 256), 256, 0, c.nt, c.first, c.count, out);
+}
+
 void level_decide(const LevelCtx& c, bool geo, const int32_t* mt_child, int32_t* srcseg, int64_t* flags_tmp,
-                  int64_t* scan_tmp, int64_t* dev_out, cudaStream_t s) {
+                  int64_t* scan_tmp, int64_t* dev_out, cudaStream_t s, const int64_t* gcnt, bool owned_only) {
   int64_t work = c.count * 8;
   unsigned grid = (unsigned)((work + 255) / 256);
-  FMI_LAUNCH(KID_DECIDE, s, k_decide, grid, 256, 0, c.nt, c.first, c.count, c.depth, c.D, c.L, c.tau, geo,
-             flags_tmp);
+  FMI_LAUNCH(KID_DECIDE, s, k_decide, grid, 256, 0, c.nt, c.first, c.count, c.depth, c.D, c.L, c.tau, geo, gcnt,
+             owned_only, flags_tmp);
   exclusive_scan_i64(flags_tmp, scan_tmp, work, nullptr, s);
   FMI_LAUNCH(KID_DECIDE, s, k_emit, grid, 256, 0, c.nt, c.first, c.count, c.depth, flags_tmp, scan_tmp, mt_child,
              srcseg, dev_out);

@@ -64,7 +64,7 @@ __global__ void __launch_bounds__(K5_THREADS)
     k_solve(const double* __restrict__ mom, int mode, const double* __restrict__ segrhs, double* __restrict__ delta,
             NodeTable nt, int64_t first, int64_t count, double* __restrict__ fac,
             const __grid_constant__ BasisTab bt, double delta2, double refine2, double refine_fill,
-            double mom_tol, int64_t* __restrict__ nflag) {
+            double mom_tol, int64_t n_root, int64_t* __restrict__ nflag) {
   using S = K5Shape<P>;
   constexpr int Q = S::Q, K = S::K, L = S::L;
   extern __shared__ __align__(16) double sm[];
@@ -318,7 +318,11 @@ __global__ void __launch_bounds__(K5_THREADS)
       // QR pivots (or the column was rejected) -> K5q re-fits the node by Householder QR;
       // semi-normal refinement flag (bit 1): small pivots, or few points per unknown, where the normal
       // equations lose digits (DESIGN.md §5 K5r)
-      const double npts = (double)(nt.end[first + node] - nt.start[first + node]);
+      // the node's point count over all shards: the parent's octant count (root: n_root)
+      const int32_t par = nt.parent[first + node];
+      const int4 cc = nt.cell[first + node];
+      const double npts = par < 0 ? (double)n_root
+                                  : (double)nt.child_n[(int64_t)par * 8 + ((cc.x & 1) | ((cc.y & 1) << 1) | ((cc.z & 1) << 2))];
       const bool refine = refine2 > 0.0 && (smin_sh < refine2 || npts < refine_fill * L);
       const int fl = (smin_sh < kQrFlagPivot2) ? 1 : (refine ? 2 : 0);
       nt.flag[first + node] = fl;
@@ -332,7 +336,7 @@ __global__ void __launch_bounds__(K5_THREADS)
 
 template <int P>
 void level_solve(const LevelCtx& c, const double* mom, int mode, const double* segrhs, double* delta, double refine2,
-                 int64_t* nflag, double* fac, cudaStream_t s) {
+                 int64_t n_root, int64_t* nflag, double* fac, cudaStream_t s) {
   using S = K5Shape<P>;
   static const BasisTab bt = make_basis<P>();
   static bool attr = false;
@@ -343,7 +347,8 @@ void level_solve(const LevelCtx& c, const double* mom, int mode, const double* s
   const int64_t grid = std::min<int64_t>(c.count, 1 << 20);
   if (grid <= 0) return;
   FMI_LAUNCH(mode == 1 ? KID_REFINE_SOLVE : KID_SOLVE, s, k_solve<P>, (unsigned)grid, K5_THREADS, S::SMEM, mom, mode,
-             segrhs, delta, c.nt, c.first, c.count, fac, bt, kDelta * kDelta, refine2, kRefineFill, kMomentTol, nflag);
+             segrhs, delta, c.nt, c.first, c.count, fac, bt, kDelta * kDelta, refine2, kRefineFill, kMomentTol, n_root,
+             nflag);
 }
 
 // doubles of per-node factor storage (bordered packed lower triangle)
@@ -357,8 +362,8 @@ size_t solve_factor_per_node(int p) {
 }
 
 #define FMI_INST(P) \
-  template void level_solve<P>(const LevelCtx&, const double*, int, const double*, double*, double, int64_t*, \
-                               double*, cudaStream_t);
+  template void level_solve<P>(const LevelCtx&, const double*, int, const double*, double*, double, int64_t, \
+                               int64_t*, double*, cudaStream_t);
 FMI_INST(0) FMI_INST(1) FMI_INST(2) FMI_INST(3) FMI_INST(4) FMI_INST(5)
 FMI_INST(6) FMI_INST(7) FMI_INST(8) FMI_INST(9) FMI_INST(10)
 #undef FMI_INST

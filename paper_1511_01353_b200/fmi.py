@@ -30,8 +30,23 @@ MAX_DEPTH = 20
 EXPORTED = (
     "fmi_build", "fmi_eval", "fmi_free", "fmi_last_error", "fmi_set_stream", "fmi_node_count", "fmi_rank",
     "fmi_export_nodes", "fmi_root_cube", "fmi_residual", "fmi_level_stats", "fmi_profile_enable",
-    "fmi_profile_reset", "fmi_profile_get", "fmi_launch_count", "fmi_build_stats",
+    "fmi_profile_reset", "fmi_profile_get", "fmi_launch_count", "fmi_build_stats", "fmi_build_dist",
+    "fmi_dist_xbuf_bytes", "fmi_bbox", "fmi_cell_counts", "fmi_partition", "fmi_scatter",
 )
+
+# allreduce(ctx, n, dtype) -> int: in-place SUM of the first n elements of the exchange buffer
+ALLREDUCE_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int)
+
+
+class FmiDist(ctypes.Structure):
+    """struct fmi_dist (include/fmi.h): shard rank/world, shard depth, common root cube, exchange buffer
+    and the collective-sum callback of a sharded build."""
+    _fields_ = [
+        ("rank", ctypes.c_int), ("world", ctypes.c_int), ("shard_depth", ctypes.c_int),
+        ("lo", ctypes.c_double * 3), ("width", ctypes.c_double),
+        ("xbuf", ctypes.c_void_p), ("xbuf_bytes", ctypes.c_int64),
+        ("allreduce", ALLREDUCE_FN), ("ctx", ctypes.c_void_p),
+    ]
 
 KERNELS = ("keys", "sort", "gather", "moments", "moments_reduce", "solve", "children", "residual",
            "residual_reduce", "decide", "chunks", "scan", "eval", "misc", "project", "m2m", "level_gather",
@@ -94,6 +109,18 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.fmi_profile_reset.argtypes = []
     lib.fmi_profile_get.restype = I32
     lib.fmi_profile_get.argtypes = [ctypes.c_char_p, P(D), P(I64)]
+    lib.fmi_build_dist.restype = VP
+    lib.fmi_build_dist.argtypes = [VP, VP, I64, I32, D, I32, P(FmiDist)]
+    lib.fmi_dist_xbuf_bytes.restype = I64
+    lib.fmi_dist_xbuf_bytes.argtypes = [I32, I32]
+    lib.fmi_bbox.restype = I32
+    lib.fmi_bbox.argtypes = [VP, I64, P(D)]
+    lib.fmi_cell_counts.restype = I32
+    lib.fmi_cell_counts.argtypes = [VP, I64, P(D), D, I32, VP]
+    lib.fmi_partition.restype = I32
+    lib.fmi_partition.argtypes = [VP, VP, I64, P(D), D, I32, VP, I32, VP, VP, VP, VP]
+    lib.fmi_scatter.restype = I32
+    lib.fmi_scatter.argtypes = [VP, VP, I64, VP]
     lib.fmi_build_stats.restype = I32
     lib.fmi_build_stats.argtypes = [VP, P(I64), I32]
     lib.fmi_launch_count.restype = I64
@@ -275,6 +302,77 @@ def build(pts, f, degree: int, tol: float, max_depth: int) -> Tree:
     if not h:
         _raise_last()
     return Tree(h, n, degree, tol, max_depth)
+
+
+def build_dist(pts, f, degree: int, tol: float, max_depth: int, dist: FmiDist) -> Tree:
+    """Sharded build (fmi_build_dist): this shard's points (already partitioned by depth-s cell)."""
+    lib = load_library()
+    pp, n, pk = _ptr(pts, 3, "pts")
+    fp, nf, fk = _ptr(f, None, "f")
+    if nf != n:
+        raise ValueError("pts and f disagree in length")
+    h = lib.fmi_build_dist(pp, fp, n, int(degree), float(tol), int(max_depth), ctypes.byref(dist))
+    if not h:
+        _raise_last()
+    return Tree(h, n, degree, tol, max_depth)
+
+
+def dist_xbuf_bytes(degree: int, shard_depth: int) -> int:
+    return int(load_library().fmi_dist_xbuf_bytes(int(degree), int(shard_depth)))
+
+
+def bbox(pts) -> np.ndarray:
+    """min x,y,z and max x,y,z of the points (fmi_bbox)."""
+    lib = load_library()
+    pp, n, pk = _ptr(pts, 3, "pts")
+    out = (ctypes.c_double * 6)()
+    rc = lib.fmi_bbox(pp, n, out)
+    if rc != 0:
+        _raise_last(rc)
+    return np.array(out[:])
+
+
+def cell_counts(pts, lo, width: float, depth: int, out):
+    """Points per depth-``depth`` cell of the root cube (fmi_cell_counts) into ``out`` (int64, 8^depth)."""
+    lib = load_library()
+    pp, n, pk = _ptr(pts, 3, "pts")
+    lo3 = (ctypes.c_double * 3)(*[float(v) for v in lo])
+    rc = lib.fmi_cell_counts(pp, n, lo3, float(width), int(depth), ctypes.c_void_p(_data_ptr(out)))
+    if rc != 0:
+        _raise_last(rc)
+    return out
+
+
+def partition(pts, f, lo, width: float, depth: int, owner, world: int, pts_out, f_out=None, idx_out=None,
+              send_counts=None):
+    """Group points by the owner shard of their depth-``depth`` cell (fmi_partition; device tensors)."""
+    lib = load_library()
+    pp, n, pk = _ptr(pts, 3, "pts")
+    fp = ctypes.c_void_p(_data_ptr(f)) if f is not None else None
+    lo3 = (ctypes.c_double * 3)(*[float(v) for v in lo])
+    rc = lib.fmi_partition(pp, fp, n, lo3, float(width), int(depth), ctypes.c_void_p(_data_ptr(owner)), int(world),
+                           ctypes.c_void_p(_data_ptr(pts_out)),
+                           ctypes.c_void_p(_data_ptr(f_out)) if f_out is not None else None,
+                           ctypes.c_void_p(_data_ptr(idx_out)) if idx_out is not None else None,
+                           ctypes.c_void_p(_data_ptr(send_counts)))
+    if rc != 0:
+        _raise_last(rc)
+
+
+def scatter(vals, idx, out):
+    """out[idx[i]] = vals[i] (fmi_scatter; device tensors)."""
+    lib = load_library()
+    m = int(vals.shape[0])
+    rc = lib.fmi_scatter(ctypes.c_void_p(_data_ptr(vals)), ctypes.c_void_p(_data_ptr(idx)), m,
+                         ctypes.c_void_p(_data_ptr(out)))
+    if rc != 0:
+        _raise_last(rc)
+
+
+def _data_ptr(a) -> int:
+    if hasattr(a, "data_ptr"):
+        return int(a.data_ptr())
+    return int(np.asarray(a).ctypes.data)
 
 
 def profile_enable(on: bool = True) -> None:
