@@ -53,6 +53,33 @@ __device__ __forceinline__ void horner3x2(const Coef& coef, double x0, double y0
   v1 = px1;
 }
 
+// Four points per call: every coefficient load feeds four FMAs, four independent chains.
+template <int P, typename Coef>
+__device__ __forceinline__ void horner3x4(const Coef& coef, const double* x, const double* y, const double* z,
+                                          double* v) {
+  double px[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+  for (int l = P; l >= 0; --l) {
+    double py[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+    for (int m = P - l; m >= 0; --m) {
+      double pz[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+      for (int n = P - l - m; n >= 0; --n) {
+        const double a = coef(basis_index(P, l, m, n));
+#pragma unroll
+        for (int k = 0; k < 4; ++k) pz[k] = fma(pz[k], z[k], a);
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k) py[k] = fma(py[k], y[k], pz[k]);
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) px[k] = fma(px[k], x[k], py[k]);
+  }
+#pragma unroll
+  for (int k = 0; k < 4; ++k) v[k] = px[k];
+}
+
 // Shared-memory coefficient reader that the compiler cannot hoist out of a point loop (a hoisted
 // copy of 𝓛 = 286 coefficients would not fit in registers).
 struct SmemCoef {

@@ -25,7 +25,8 @@ namespace {
 
 constexpr int K6_THREADS = 256;
 constexpr int K6_WARPS = K6_THREADS / 32;
-constexpr int K6_BATCH = 2 * K6_THREADS;
+constexpr int K6_PPT = 2;                       // points per thread in the Horner phase
+constexpr int K6_BATCH = K6_PPT * K6_THREADS;
 
 // ---- compile-time output groups ------------------------------------------------------------------
 // pairs (a,b), a+b <= P, in a-major order (= the (l,m) order of Algorithm 2); pair q owns
@@ -105,8 +106,9 @@ __device__ __forceinline__ void proj_accum(double x, double y, double z, double 
   if constexpr (q0 < q1) {
     double zp[CM + 1];
     zp[0] = 1.0;
+    if constexpr (CM >= 1) zp[1] = z;
 #pragma unroll
-    for (int c = 1; c <= CM; ++c) zp[c] = zp[c - 1] * z;
+    for (int c = 2; c <= CM; ++c) zp[c] = zp[c / 2] * zp[c - c / 2];  // log-depth power tree
     double xr = r;
 #pragma unroll
     for (int e = 0; e < pair_a(P, q0); ++e) xr *= x;
@@ -139,8 +141,13 @@ __global__ void __launch_bounds__(K6_THREADS, 2)
   constexpr int SUB = K6_WARPS / G;  // warps per output group (split the batch's points)
   constexpr int MG = max_group(P);
   __shared__ double sa[L];
-  __shared__ double sx[K6_BATCH], sy[K6_BATCH], sz[K6_BATCH], sr[K6_BATCH];
-  __shared__ double red[SUB][L];
+  __shared__ double sbuf[4 * K6_BATCH];  // batch coordinates in the child frame + residuals
+  double* sx = sbuf;
+  double* sy = sbuf + K6_BATCH;
+  double* sz = sbuf + 2 * K6_BATCH;
+  double* sr = sbuf + 3 * K6_BATCH;
+  static_assert(SUB * L <= 4 * K6_BATCH, "reduction buffer");
+  double (*red)[L] = reinterpret_cast<double (*)[L]>(sbuf);  // after the point loop
   __shared__ double redw[K6_WARPS];
   const int64_t cidx = blockIdx.x;
   if (cidx >= *nchunks) return;
@@ -185,30 +192,44 @@ __global__ void __launch_bounds__(K6_THREADS, 2)
   for (int k = 0; k < MG; ++k) acc[k] = 0.0;
   double ss = 0.0;
   for (int64_t base = ck.start; base < ck.end; base += K6_BATCH) {
-    const int64_t i0 = base + tid, i1 = base + tid + K6_THREADS;
-    const bool v0 = i0 < ck.end, v1 = i1 < ck.end;
-    const int64_t j0 = v0 ? i0 : ck.start, j1 = v1 ? i1 : ck.start;
-    const double X0 = ux[j0], Y0 = uy[j0], Z0 = uz[j0], X1 = ux[j1], Y1 = uy[j1], Z1 = uz[j1];
-    double r0 = r[j0], r1 = r[j1];
+    double X[K6_PPT], Y[K6_PPT], Z[K6_PPT], R[K6_PPT];
+    bool V[K6_PPT];
+#pragma unroll
+    for (int k = 0; k < K6_PPT; ++k) {
+      const int64_t i = base + tid + k * K6_THREADS;
+      V[k] = i < ck.end;
+      const int64_t j = V[k] ? i : ck.start;
+      X[k] = ux[j]; Y[k] = uy[j]; Z[k] = uz[j]; R[k] = r[j];
+    }
     if (horner) {
-      double p0, p1;
-      horner3x2<P>(coef, __dmul_rn(__dsub_rn(X0, fn.cx), fn.scale), __dmul_rn(__dsub_rn(Y0, fn.cy), fn.scale),
-                   __dmul_rn(__dsub_rn(Z0, fn.cz), fn.scale), __dmul_rn(__dsub_rn(X1, fn.cx), fn.scale),
-                   __dmul_rn(__dsub_rn(Y1, fn.cy), fn.scale), __dmul_rn(__dsub_rn(Z1, fn.cz), fn.scale), p0, p1);
-      r0 -= p0;
-      r1 -= p1;
-      if (v0) { r[i0] = r0; ss = fma(r0, r0, ss); }
-      if (v1) { r[i1] = r1; ss = fma(r1, r1, ss); }
+      double hx[K6_PPT], hy[K6_PPT], hz[K6_PPT], pv[K6_PPT];
+#pragma unroll
+      for (int k = 0; k < K6_PPT; ++k) {
+        hx[k] = __dmul_rn(__dsub_rn(X[k], fn.cx), fn.scale);
+        hy[k] = __dmul_rn(__dsub_rn(Y[k], fn.cy), fn.scale);
+        hz[k] = __dmul_rn(__dsub_rn(Z[k], fn.cz), fn.scale);
+      }
+      if constexpr (K6_PPT == 4) {
+        horner3x4<P>(coef, hx, hy, hz, pv);
+      } else {
+        static_assert(K6_PPT == 2, "K6_PPT");
+        horner3x2<P>(coef, hx[0], hy[0], hz[0], hx[1], hy[1], hz[1], pv[0], pv[1]);
+      }
+#pragma unroll
+      for (int k = 0; k < K6_PPT; ++k) {
+        R[k] -= pv[k];
+        if (V[k]) { r[base + tid + k * K6_THREADS] = R[k]; ss = fma(R[k], R[k], ss); }
+      }
     }
     if (project) {
-      sx[tid] = __dmul_rn(__dsub_rn(X0, fc.cx), fc.scale);
-      sy[tid] = __dmul_rn(__dsub_rn(Y0, fc.cy), fc.scale);
-      sz[tid] = __dmul_rn(__dsub_rn(Z0, fc.cz), fc.scale);
-      sr[tid] = v0 ? r0 : 0.0;
-      sx[tid + K6_THREADS] = __dmul_rn(__dsub_rn(X1, fc.cx), fc.scale);
-      sy[tid + K6_THREADS] = __dmul_rn(__dsub_rn(Y1, fc.cy), fc.scale);
-      sz[tid + K6_THREADS] = __dmul_rn(__dsub_rn(Z1, fc.cz), fc.scale);
-      sr[tid + K6_THREADS] = v1 ? r1 : 0.0;
+#pragma unroll
+      for (int k = 0; k < K6_PPT; ++k) {
+        const int j = tid + k * K6_THREADS;
+        sx[j] = __dmul_rn(__dsub_rn(X[k], fc.cx), fc.scale);
+        sy[j] = __dmul_rn(__dsub_rn(Y[k], fc.cy), fc.scale);
+        sz[j] = __dmul_rn(__dsub_rn(Z[k], fc.cz), fc.scale);
+        sr[j] = V[k] ? R[k] : 0.0;
+      }
       __syncthreads();
       const int nb = (int)min((int64_t)K6_BATCH, ck.end - base);
 #pragma unroll 1

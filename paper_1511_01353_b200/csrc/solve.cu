@@ -28,7 +28,7 @@ namespace fmi {
 
 namespace {
 
-constexpr int K5_THREADS = 128;
+constexpr int K5_THREADS = 256;
 constexpr int K5_WARPS = K5_THREADS / 32;
 constexpr int KB = 32;
 
@@ -232,6 +232,15 @@ __global__ void __launch_bounds__(K5_THREADS)
             while (ti * (ti + 1) / 2 > t) --ti;
             const int tk = t - ti * (ti + 1) / 2;
             const int i0 = j1 + 4 * ti, k0 = j1 + 4 * tk;
+            // the old values first: their L2 latency overlaps the register-tile FMAs below
+            double old[4][4];
+#pragma unroll
+            for (int a = 0; a < 4; ++a)
+#pragma unroll
+              for (int b = 0; b < 4; ++b) {
+                const int i = i0 + a, k = k0 + b;
+                old[a][b] = (i <= L && k < L && (k <= i || i == L)) ? A[tri(i) + k] : 0.0;
+              }
             double acc[4][4];
 #pragma unroll
             for (int a = 0; a < 4; ++a)
@@ -256,7 +265,7 @@ __global__ void __launch_bounds__(K5_THREADS)
 #pragma unroll
               for (int b = 0; b < 4; ++b) {
                 const int i = i0 + a, k = k0 + b;
-                if (i <= L && k < L && (k <= i || i == L)) A[tri(i) + k] -= acc[a][b];
+                if (i <= L && k < L && (k <= i || i == L)) A[tri(i) + k] = old[a][b] - acc[a][b];
               }
           }
         }
