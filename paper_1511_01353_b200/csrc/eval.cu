@@ -90,37 +90,57 @@ __global__ void __launch_bounds__(PS_THREADS) k_presum(NodeTable nt, int64_t fir
   for (int e = tid; e < L; e += PS_THREADS) nt.pcoef[node * L + e] = b1[e] + nt.coef[node * L + e];
 }
 
+// One query per thread.  Sorted queries make the deepest node warp-uniform almost everywhere: the warp
+// then stages that node's pre-summed coefficients in shared memory once (coalesced) and every lane
+// reads them as broadcasts; otherwise each lane reads its node's coefficients through L1.
 template <int P>
 __global__ void __launch_bounds__(256) k_eval(const double* __restrict__ q, const uint64_t* __restrict__ keys,
                                               const uint32_t* __restrict__ idx, int64_t M, double lo0, double lo1,
                                               double lo2, double w, bool unit, int Dk, NodeTable nt,
                                               double* __restrict__ out) {
   constexpr int L = rank3(P);
+  __shared__ double cs[256 / 32][L];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= M) return;
-  const int64_t qi = idx ? (int64_t)idx[i] : i;
-  const double ux = to_unit_e(q[3 * qi + 0], lo0, w, unit);
-  const double uy = to_unit_e(q[3 * qi + 1], lo1, w, unit);
-  const double uz = to_unit_e(q[3 * qi + 2], lo2, w, unit);
-  const bool inside = ux >= 0.0 && ux <= 1.0 && uy >= 0.0 && uy <= 1.0 && uz >= 0.0 && uz <= 1.0;
-  // descend to the deepest existing node containing the query
+  const bool active = i < M;
+  const int64_t qi = !active ? 0 : (idx ? (int64_t)idx[i] : i);
+  double ux = 0.0, uy = 0.0, uz = 0.0;
   int64_t node = 0;
-  if (inside && keys) {
-    const uint64_t key = keys[i];
-    for (int level = 0; level < Dk; ++level) {
-      const int o = (int)((key >> (3 * (Dk - level - 1))) & 7ull);
-      const int32_t ch = __ldg(nt.child + node * 8 + o);
-      if (ch < 0) break;
-      node = ch;
+  if (active) {
+    ux = to_unit_e(q[3 * qi + 0], lo0, w, unit);
+    uy = to_unit_e(q[3 * qi + 1], lo1, w, unit);
+    uz = to_unit_e(q[3 * qi + 2], lo2, w, unit);
+    const bool inside = ux >= 0.0 && ux <= 1.0 && uy >= 0.0 && uy <= 1.0 && uz >= 0.0 && uz <= 1.0;
+    // descend to the deepest existing node containing the query
+    if (inside && keys) {
+      const uint64_t key = keys[i];
+      for (int level = 0; level < Dk; ++level) {
+        const int o = (int)((key >> (3 * (Dk - level - 1))) & 7ull);
+        const int32_t ch = __ldg(nt.child + node * 8 + o);
+        if (ch < 0) break;
+        node = ch;
+      }
     }
   }
+  const int64_t node0 = __shfl_sync(0xffffffffu, node, 0);
+  const bool uniform = __all_sync(0xffffffffu, !active || node == node0);
+  double v;
   const Frame fr = node_frame(nt.cell[node]);
   const double x = __dmul_rn(__dsub_rn(ux, fr.cx), fr.scale);
   const double y = __dmul_rn(__dsub_rn(uy, fr.cy), fr.scale);
   const double z = __dmul_rn(__dsub_rn(uz, fr.cz), fr.scale);
-  const double* a = nt.pcoef + node * L;
-  auto coef = [&](int k) { return __ldg(a + k); };
-  out[qi] = horner3<P>(coef, x, y, z);
+  if (uniform) {
+    const double* a = nt.pcoef + node0 * L;
+    for (int k = lane; k < L; k += 32) cs[warp][k] = __ldg(a + k);
+    __syncwarp();
+    const SmemCoef coef(cs[warp]);
+    v = horner3<P>(coef, x, y, z);
+  } else {
+    const double* a = nt.pcoef + node * L;
+    auto coef = [&](int k) { return __ldg(a + k); };
+    v = horner3<P>(coef, x, y, z);
+  }
+  if (active) out[qi] = v;
 }
 
 }  // namespace

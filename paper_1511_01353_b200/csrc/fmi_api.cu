@@ -191,8 +191,10 @@ void prof_collect() {
 // ------------------------------------------------------------------------------------------------
 struct fmi_tree {
   int p = 0, L = 0, K = 0, D = 0, Dk = 0, depth_max = 0;
+  int Dsorted = 0;  // key levels sorted (octant digits valid down to this depth)
   int refine_steps = kRefineSteps;   // env FMI_REFINE_STEPS
   double refine2 = kRefinePivot2;    // env FMI_REFINE_PIVOT2
+  double refine_fill = kRefineFill;  // env FMI_REFINE_FILL
   double tau = 0;
   double lo[3] = {0, 0, 0};
   double width = 1;
@@ -321,6 +323,21 @@ int64_t choose_chunk(int64_t points, int64_t min_ch, int64_t per_sm_chunks) {
   return std::max(min_ch, target);
 }
 
+// thrown by run_levels when the moment tree needs key digits below the sorted depth
+struct KeysShort {};
+
+// back to an empty tree (before a rebuild)
+void reset_tree(fmi_tree* T, cudaStream_t s) {
+  free_table(T->nt, s);
+  T->cap = 0;
+  T->nodes = 0;
+  T->mt_nodes = T->direct_nodes = T->refined_nodes = 0;
+  T->lvl_first.clear();
+  T->lvl_count.clear();
+  T->lvl_points.clear();
+  T->depth_max = 0;
+}
+
 // Collective SUM over the shards of a sharded build (fmi_dist): stage through the caller's exchange
 // buffer, synchronise, call the caller's collective, copy back (stream-ordered).
 void dist_sum(const fmi_tree* T, void* dev, int64_t n, int dtype, cudaStream_t s) {
@@ -363,6 +380,7 @@ void run_levels(fmi_tree* T, const uint64_t* keys, double* ux, double* uy, doubl
     {
       int64_t first = 0, count = 1;
       for (int depth = 0; count > 0; ++depth) {
+        if (depth >= T->Dsorted) throw KeysShort{};  // octant digits below this depth are not sorted
         mfirst.push_back(first);
         mcount.push_back(count);
         ensure_table(mt, mt_cap, first + count + 8 * count, L, false, s);
@@ -451,11 +469,13 @@ void run_levels(fmi_tree* T, const uint64_t* keys, double* ux, double* uy, doubl
       // K5: solve; nodes whose translated moments fail the rounding check are re-accumulated directly
       FMI_CK(cudaMemsetAsync(nflag.p, 0, 2 * sizeof(int64_t), s));
       scratch.ensure((size_t)count * fac_per_node, s);
-      level_solve<P>(c, lvlmom.p, 0, nullptr, nullptr, T->refine2, T->Ntot, nflag.p, scratch.p, s);
+      level_solve<P>(c, lvlmom.p, 0, nullptr, nullptr, T->refine2, T->refine_fill, T->Ntot, nflag.p, scratch.p, s);
       FMI_CK(cudaMemcpyAsync(&host_small[2], nflag.p, 2 * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
       FMI_CK(cudaStreamSynchronize(s));
       if (host_small[3] > 0) {
-        const int64_t chd = kMomentChunk;
+        // few flagged nodes, possibly huge (a root): longer chunks keep the chunk count (and the
+        // per-node partial sums) bounded
+        const int64_t chd = std::max<int64_t>(kMomentChunk, points / (148 * 64));
         const int64_t maxd = points / chd + count + 1;
         counts.ensure(count, s);
         begin.ensure(count, s);
@@ -477,7 +497,7 @@ void run_levels(fmi_tree* T, const uint64_t* keys, double* ux, double* uy, doubl
         } else {
           reduce_moments(partial.p, begin.p, dev_small.p, count, 1, K, T->nt.flag + first, 4, lvlmom.p, 2 * K + L, s);
         }
-        level_solve<P>(c, lvlmom.p, 2, nullptr, nullptr, T->refine2, T->Ntot, nflag.p, scratch.p, s);
+        level_solve<P>(c, lvlmom.p, 2, nullptr, nullptr, T->refine2, T->refine_fill, T->Ntot, nflag.p, scratch.p, s);
         FMI_CK(cudaMemcpyAsync(&host_small[2], nflag.p, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
         FMI_CK(cudaStreamSynchronize(s));
         T->direct_nodes += host_small[3];
@@ -509,7 +529,7 @@ void run_levels(fmi_tree* T, const uint64_t* keys, double* ux, double* uy, doubl
           level_residual<P>(c, K6_OWN, it, delta.p, chunks.p, dev_small.p + 1, max6, begin.p, count * 8, partial.p,
                             segsum.p, s);
           if (global) dist_sum(T, segsum.p, count * 8 * (L + 1), 0, s);
-          level_solve<P>(c, lvlmom.p, 1, segsum.p, delta.p, T->refine2, T->Ntot, nflag.p, scratch.p, s);
+          level_solve<P>(c, lvlmom.p, 1, segsum.p, delta.p, T->refine2, T->refine_fill, T->Ntot, nflag.p, scratch.p, s);
         }
       }
       tmark("qr+refine", s);
@@ -659,6 +679,7 @@ fmi_tree* build_impl(const double* pts, const double* f, int64_t N, int degree, 
     T->shard_depth = dist ? dist->shard_depth : 0;
     if (const char* e = std::getenv("FMI_REFINE_STEPS")) T->refine_steps = std::max(0, std::atoi(e));
     if (const char* e = std::getenv("FMI_REFINE_PIVOT2")) T->refine2 = std::atof(e);
+    if (const char* e = std::getenv("FMI_REFINE_FILL")) T->refine_fill = std::atof(e);
     if (T->refine_steps == 0) T->refine2 = 0.0;  // no node is flagged for refinement
     bool unit = hb[0] >= 0.0 && hb[1] >= 0.0 && hb[2] >= 0.0 && hb[3] <= 1.0 && hb[4] <= 1.0 && hb[5] <= 1.0;
     if (dist) {  // the common root cube of the shards
@@ -675,21 +696,40 @@ fmi_tree* build_impl(const double* pts, const double* f, int64_t N, int degree, 
       double w = std::max(hb[3] - hb[0], std::max(hb[4] - hb[1], hb[5] - hb[2]));
       T->width = w > 0.0 ? w : 1.0;
     }
-    // K1 keys + K2 sort + gather
+    // K1 keys + K2 sort + gather.  Only the top Dsort levels of the keys are sorted: no node is deeper
+    // than the moment tree, whose depth is ~log8(N/𝓛) for space-filling data.  If the moment tree does
+    // reach depth Dsort (clustered data), run_levels throws KeysShort and the sort is redone over all
+    // levels.  Sharded builds sort all levels (every shard must take the same path).
     DBuf<uint64_t> keys(N, s), ktmp(N, s);
     DBuf<uint32_t> perm(N, s), ptmp(N, s);
-    morton_keys(dpts, N, T->lo, T->width, T->unit, T->Dk, keys.p, perm.p, s);
-    tmark("keys", s);
-    radix_sort_pairs(keys.p, perm.p, ktmp.p, ptmp.p, N, 3 * T->Dk, s);
+    DBuf<double4> packed(N, s);
+    DBuf<double> ux(N, s), uy(N, s), uz(N, s), r(N, s);
+    int Dsort = T->Dk;
+    if (!dist && !std::getenv("FMI_FULL_SORT")) {
+      const double fill = std::max(1.0, (double)std::max<int64_t>(Ntot, 1) / (double)L);
+      Dsort = std::min(T->Dk, (int)std::ceil(std::log(fill) / std::log(8.0)) + 1);
+    }
+    for (;;) {
+      morton_keys(dpts, N, T->lo, T->width, T->unit, T->Dk, keys.p, perm.p, s, df, packed.p);
+      tmark("keys", s);
+      radix_sort_pairs(keys.p, perm.p, ktmp.p, ptmp.p, N, 3 * T->Dk, s, 3 * (T->Dk - Dsort));
+      T->Dsorted = Dsort;
+      tmark("sort", s);
+      gather_points(packed.p, perm.p, N, ux.p, uy.p, uz.p, r.p, s);
+      tmark("gather", s);
+      try {
+        FMI_DISPATCH(degree, run_levels, T, keys.p, ux.p, uy.p, uz.p, r.p, s);
+        break;
+      } catch (const KeysShort&) {
+        reset_tree(T, s);
+        Dsort = T->Dk;
+      }
+    }
     ktmp.release();
     ptmp.release();
-    tmark("sort", s);
-    DBuf<double> ux(N, s), uy(N, s), uz(N, s), r(N, s);
-    gather_points(dpts, df, perm.p, N, T->lo, T->width, T->unit, ux.p, uy.p, uz.p, r.p, s);
+    packed.release();
     dpts_own.release();
     df_own.release();
-    tmark("gather", s);
-    FMI_DISPATCH(degree, run_levels, T, keys.p, ux.p, uy.p, uz.p, r.p, s);
     T->dist = nullptr;
     T->residual = r.p;
     r.p = nullptr;

@@ -131,14 +131,15 @@ void exclusive_scan_i64(const int64_t* in, int64_t* out, int64_t n, int64_t* tot
 // keys.cu
 void bbox_and_check(const double* pts, int64_t n, double* out8 /*device: min3,max3,nonfinite,unused*/,
                     const double* f, cudaStream_t s);
-void morton_keys(const double* pts, int64_t n, const double lo[3], double width, bool unit, int D,
-                 uint64_t* keys, uint32_t* idx, cudaStream_t s);
-// LSD radix sort of (keys, vals) by the low nbits key bits, stable.  On return keys/vals point at the
+// f/packed (fit points): also write the 32-byte records (u_x, u_y, u_z, f) read by gather_points
+void morton_keys(const double* pts, int64_t n, const double lo[3], double width, bool unit, int D, uint64_t* keys,
+                 uint32_t* idx, cudaStream_t s, const double* f = nullptr, double4* packed = nullptr);
+// LSD radix sort of (keys, vals) by key bits [bit_lo, nbits), stable.  On return keys/vals point at the
 // sorted data and keys_tmp/vals_tmp at the scratch (the pointers may have been swapped).
 void radix_sort_pairs(uint64_t*& keys, uint32_t*& vals, uint64_t*& keys_tmp, uint32_t*& vals_tmp, int64_t n,
-                      int nbits, cudaStream_t s);
-void gather_points(const double* pts, const double* f, const uint32_t* perm, int64_t n, const double lo[3],
-                   double width, bool unit, double* ux, double* uy, double* uz, double* r, cudaStream_t s);
+                      int nbits, cudaStream_t s, int bit_lo = 0);
+void gather_points(const double4* packed, const uint32_t* perm, int64_t n, double* ux, double* uy, double* uz,
+                   double* r, cudaStream_t s);
 
 // sharded build helpers (keys.cu): depth-s cell histogram, partition by owner shard, scatter
 void cell_counts(const double* pts, int64_t n, const double lo[3], double width, bool unit, int s, int64_t* counts,
@@ -202,14 +203,14 @@ void gather_level(const double* mtmom, const float* mtbnd, const int32_t* mtid, 
 // step for bit-1 nodes, b1 = Σ_o segrhs[node*8+o][0..𝓛), δ -> delta[node][𝓛], coef += δ.  mode 2:
 // re-solve of bit-2 nodes after direct accumulation (no rounding check).
 template <int P> void level_solve(const LevelCtx& c, const double* mom, int mode, const double* segrhs,
-                                  double* delta, double refine2, int64_t n_root, int64_t* nflag, double* fac,
-                                  cudaStream_t s);
+                                  double* delta, double refine2, double refine_fill, int64_t n_root,
+                                  int64_t* nflag, double* fac, cudaStream_t s);
 // fac: per level-local node solve_factor_per_node(p) doubles (bordered packed lower factor, kept for
 // the refinement solves)
 size_t solve_factor_per_node(int p);
 // refinement gate (DESIGN.md §5 K5r)
 constexpr double kRefinePivot2 = 1e-6;
-constexpr double kRefineFill = 8.0;
+constexpr double kRefineFill = 2.0;
 constexpr int kRefineSteps = 2;
 // largest accepted equilibrated rounding bound of a translated Gram (DESIGN.md §5 M2M)
 constexpr double kMomentTol = 1e-11;

@@ -95,9 +95,12 @@ __device__ __forceinline__ uint64_t quantize(double u, int D) {
   return (uint64_t)t;
 }
 
+// packed != nullptr (fit points): also write (u_x, u_y, u_z, f) as one 32-byte record, so that the
+// Morton-order gather reads ONE aligned sector per point instead of scattered pieces of pts and f.
 __global__ void __launch_bounds__(256) k_keys(const double* __restrict__ pts, int64_t n, double lo0, double lo1,
                                               double lo2, double w, bool unit, int D, uint64_t* __restrict__ keys,
-                                              uint32_t* __restrict__ idx) {
+                                              uint32_t* __restrict__ idx, const double* __restrict__ f,
+                                              double4* __restrict__ packed) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   double ux = to_unit(pts[3 * i + 0], lo0, w, unit);
@@ -106,6 +109,7 @@ __global__ void __launch_bounds__(256) k_keys(const double* __restrict__ pts, in
   uint64_t k = spread3(quantize(ux, D)) | (spread3(quantize(uy, D)) << 1) | (spread3(quantize(uz, D)) << 2);
   keys[i] = k;
   idx[i] = (uint32_t)i;
+  if (packed) packed[i] = make_double4(ux, uy, uz, f[i]);
 }
 
 // ------------------------------------------------------------------------------------------------
@@ -226,18 +230,17 @@ __global__ void __launch_bounds__(RS_THREADS) k_rs_scatter(const uint64_t* __res
 // ------------------------------------------------------------------------------------------------
 // SoA gather in Morton order
 // ------------------------------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) k_gather(const double* __restrict__ pts, const double* __restrict__ f,
-                                                const uint32_t* __restrict__ perm, int64_t n, double lo0, double lo1,
-                                                double lo2, double w, bool unit, double* __restrict__ ux,
-                                                double* __restrict__ uy, double* __restrict__ uz,
-                                                double* __restrict__ r) {
+__global__ void __launch_bounds__(256) k_gather(const double4* __restrict__ packed, const uint32_t* __restrict__ perm,
+                                                int64_t n, double* __restrict__ ux, double* __restrict__ uy,
+                                                double* __restrict__ uz, double* __restrict__ r) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
-  int64_t j = perm[i];
-  ux[i] = to_unit(pts[3 * j + 0], lo0, w, unit);
-  uy[i] = to_unit(pts[3 * j + 1], lo1, w, unit);
-  uz[i] = to_unit(pts[3 * j + 2], lo2, w, unit);
-  r[i] = f[j];
+  const double2* p = reinterpret_cast<const double2*>(packed + perm[i]);  // one 32-byte sector
+  const double2 a = __ldg(p), b = __ldg(p + 1);
+  ux[i] = a.x;
+  uy[i] = a.y;
+  uz[i] = b.x;
+  r[i] = b.y;
 }
 
 // sharded build helpers ---------------------------------------------------------------------------
@@ -326,14 +329,14 @@ void bbox_and_check(const double* pts, int64_t n, double* out8, const double* f,
 }
 
 void morton_keys(const double* pts, int64_t n, const double lo[3], double width, bool unit, int D, uint64_t* keys,
-                 uint32_t* idx, cudaStream_t s) {
+                 uint32_t* idx, cudaStream_t s, const double* f, double4* packed) {
   if (n <= 0) return;
   unsigned grid = (unsigned)((n + 255) / 256);
-  FMI_LAUNCH(KID_KEYS, s, k_keys, grid, 256, 0, pts, n, lo[0], lo[1], lo[2], width, unit, D, keys, idx);
+  FMI_LAUNCH(KID_KEYS, s, k_keys, grid, 256, 0, pts, n, lo[0], lo[1], lo[2], width, unit, D, keys, idx, f, packed);
 }
 
 void radix_sort_pairs(uint64_t*& keys, uint32_t*& vals, uint64_t*& keys_tmp, uint32_t*& vals_tmp, int64_t n,
-                      int nbits, cudaStream_t s) {
+                      int nbits, cudaStream_t s, int bit_lo) {
   if (n <= 1 || nbits <= 0) return;
   static bool attr = false;
   if (!attr) {
@@ -344,7 +347,7 @@ void radix_sort_pairs(uint64_t*& keys, uint32_t*& vals, uint64_t*& keys_tmp, uin
   DBuf<int64_t> counts((size_t)nblk * 256, s);
   uint64_t* ka = keys; uint32_t* va = vals; uint64_t* kb = keys_tmp; uint32_t* vb = vals_tmp;
   int passes = 0;
-  for (int shift = 0; shift < nbits; shift += 8, ++passes) {
+  for (int shift = bit_lo; shift < nbits; shift += 8, ++passes) {
     FMI_LAUNCH(KID_SORT, s, k_rs_hist, (unsigned)nblk, RS_THREADS, 0, ka, n, shift, nblk, counts.p);
     exclusive_scan_i64(counts.p, counts.p, nblk * 256, nullptr, s);
     FMI_LAUNCH(KID_SORT, s, k_rs_scatter, (unsigned)nblk, RS_THREADS, kScatterSmem, ka, va, n, shift, nblk, counts.p,
@@ -356,12 +359,11 @@ void radix_sort_pairs(uint64_t*& keys, uint32_t*& vals, uint64_t*& keys_tmp, uin
   keys = ka; vals = va; keys_tmp = kb; vals_tmp = vb;
 }
 
-void gather_points(const double* pts, const double* f, const uint32_t* perm, int64_t n, const double lo[3],
-                   double width, bool unit, double* ux, double* uy, double* uz, double* r, cudaStream_t s) {
+void gather_points(const double4* packed, const uint32_t* perm, int64_t n, double* ux, double* uy, double* uz,
+                   double* r, cudaStream_t s) {
   if (n <= 0) return;
   unsigned grid = (unsigned)((n + 255) / 256);
-  FMI_LAUNCH(KID_GATHER, s, k_gather, grid, 256, 0, pts, f, perm, n, lo[0], lo[1], lo[2], width, unit, ux, uy, uz,
-             r);
+  FMI_LAUNCH(KID_GATHER, s, k_gather, grid, 256, 0, packed, perm, n, ux, uy, uz, r);
 }
 
 }  // namespace fmi

@@ -118,7 +118,9 @@ __global__ void __launch_bounds__(K4_THREADS, 1)
 }
 
 // out[node·stride + e] = Σ of the chunk partials of the node's ranges (rpn ranges per node: 8 owner
-// segments, or 1 node range) in chunk order, for nodes with (flag[node] & bit) when flag != nullptr.
+// segments, or 1 node range) in a fixed order, for nodes with (flag[node] & bit) when flag != nullptr.
+// CTA = node, thread = entries; the chunk loop keeps 8 independent partial sums (chunks c ≡ k mod 8,
+// combined k = 0..7) so nodes with many chunks have 8 loads in flight per thread; deterministic.
 __global__ void __launch_bounds__(256) k_moments_reduce(const double* __restrict__ partial,
                                                         const int64_t* __restrict__ chunk_begin,
                                                         const int64_t* __restrict__ nchunks, int64_t nodes, int rpn,
@@ -129,9 +131,17 @@ __global__ void __launch_bounds__(256) k_moments_reduce(const double* __restrict
   const int64_t c0 = chunk_begin[node * rpn];
   const int64_t c1 = node + 1 < nodes ? chunk_begin[(node + 1) * rpn] : *nchunks;
   for (int e = threadIdx.x; e < K; e += blockDim.x) {
-    double s = 0.0;
-    for (int64_t ci = c0; ci < c1; ++ci) s += partial[ci * K + e];
-    out[node * stride + e] = s;
+    double s[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    int64_t ci = c0;
+    for (; ci + 8 <= c1; ci += 8) {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) s[k] += partial[(ci + k) * K + e];
+    }
+    for (; ci < c1; ++ci) s[0] += partial[ci * K + e];
+    double t = 0.0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) t += s[k];
+    out[node * stride + e] = t;
   }
 }
 

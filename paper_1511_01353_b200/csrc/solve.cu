@@ -28,8 +28,9 @@ namespace fmi {
 
 namespace {
 
-constexpr int K5_THREADS = 256;
-constexpr int K5_WARPS = K5_THREADS / 32;
+// threads per node: 128 for the small systems (more nodes per SM), 256 for 𝓛 >= 220 (p >= 9)
+template <int P>
+constexpr int k5_threads() { return rank3(P) >= 220 ? 256 : 128; }
 constexpr int KB = 32;
 
 struct BasisTab {
@@ -60,13 +61,14 @@ struct K5Shape {
 };
 
 template <int P>
-__global__ void __launch_bounds__(K5_THREADS)
+__global__ void __launch_bounds__(k5_threads<P>())
     k_solve(const double* __restrict__ mom, int mode, const double* __restrict__ segrhs, double* __restrict__ delta,
             NodeTable nt, int64_t first, int64_t count, double* __restrict__ fac,
             const __grid_constant__ BasisTab bt, double delta2, double refine2, double refine_fill,
             double mom_tol, int64_t n_root, int64_t* __restrict__ nflag) {
   using S = K5Shape<P>;
   constexpr int Q = S::Q, K = S::K, L = S::L;
+  constexpr int K5_THREADS = k5_threads<P>(), K5_WARPS = K5_THREADS / 32;
   extern __shared__ __align__(16) double sm[];
   double* sM = sm;          // [K]
   double* dinv = sM + K;    // [L]
@@ -345,7 +347,7 @@ __global__ void __launch_bounds__(K5_THREADS)
 
 template <int P>
 void level_solve(const LevelCtx& c, const double* mom, int mode, const double* segrhs, double* delta, double refine2,
-                 int64_t n_root, int64_t* nflag, double* fac, cudaStream_t s) {
+                 double refine_fill, int64_t n_root, int64_t* nflag, double* fac, cudaStream_t s) {
   using S = K5Shape<P>;
   static const BasisTab bt = make_basis<P>();
   static bool attr = false;
@@ -355,8 +357,8 @@ void level_solve(const LevelCtx& c, const double* mom, int mode, const double* s
   }
   const int64_t grid = std::min<int64_t>(c.count, 1 << 20);
   if (grid <= 0) return;
-  FMI_LAUNCH(mode == 1 ? KID_REFINE_SOLVE : KID_SOLVE, s, k_solve<P>, (unsigned)grid, K5_THREADS, S::SMEM, mom, mode,
-             segrhs, delta, c.nt, c.first, c.count, fac, bt, kDelta * kDelta, refine2, kRefineFill, kMomentTol, n_root,
+  FMI_LAUNCH(mode == 1 ? KID_REFINE_SOLVE : KID_SOLVE, s, k_solve<P>, (unsigned)grid, k5_threads<P>(), S::SMEM, mom, mode,
+             segrhs, delta, c.nt, c.first, c.count, fac, bt, kDelta * kDelta, refine2, refine_fill, kMomentTol, n_root,
              nflag);
 }
 
@@ -371,7 +373,7 @@ size_t solve_factor_per_node(int p) {
 }
 
 #define FMI_INST(P) \
-  template void level_solve<P>(const LevelCtx&, const double*, int, const double*, double*, double, int64_t, \
+  template void level_solve<P>(const LevelCtx&, const double*, int, const double*, double*, double, double, int64_t, \
                                int64_t*, double*, cudaStream_t);
 FMI_INST(0) FMI_INST(1) FMI_INST(2) FMI_INST(3) FMI_INST(4) FMI_INST(5)
 FMI_INST(6) FMI_INST(7) FMI_INST(8) FMI_INST(9) FMI_INST(10)
