@@ -195,6 +195,7 @@ struct fmi_tree {
   int refine_steps = kRefineSteps;   // env FMI_REFINE_STEPS
   double refine2 = kRefinePivot2;    // env FMI_REFINE_PIVOT2
   double refine_fill = kRefineFill;  // env FMI_REFINE_FILL
+  int64_t mt_min = 0;                // moment-tree cell minimum (points); env FMI_MT_FILL (multiple of 𝓛)
   double tau = 0;
   double lo[3] = {0, 0, 0};
   double width = 1;
@@ -395,7 +396,7 @@ void run_levels(fmi_tree* T, const uint64_t* keys, double* ux, double* uy, doubl
           dist_sum(T, gcnt.p, count * 8, 1, s);
         }
         level_decide(c, true, nullptr, nullptr, flags.p, scan.p, dev_small.p + 2, s, global ? gcnt.p : nullptr,
-                     global && depth + 1 == T->shard_depth);
+                     global && depth + 1 == T->shard_depth, T->mt_min);
         FMI_CK(cudaMemcpyAsync(host_small, dev_small.p + 2, 2 * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
         FMI_CK(cudaStreamSynchronize(s));
         first += count;
@@ -458,6 +459,7 @@ void run_levels(fmi_tree* T, const uint64_t* keys, double* ux, double* uy, doubl
     const int64_t qr_slots = 148;
     DBuf<double> qr_scratch((size_t)qr_slots * solve_qr_scratch_per_cta(P) / sizeof(double), s);
     for (int depth = 0; count > 0; ++depth) {
+      if (depth >= T->Dsorted) throw KeysShort{};  // octant digits below this depth are not sorted
       T->lvl_first.push_back(first);
       T->lvl_count.push_back(count);
       T->lvl_points.push_back(points);
@@ -680,6 +682,11 @@ fmi_tree* build_impl(const double* pts, const double* f, int64_t N, int degree, 
     if (const char* e = std::getenv("FMI_REFINE_STEPS")) T->refine_steps = std::max(0, std::atoi(e));
     if (const char* e = std::getenv("FMI_REFINE_PIVOT2")) T->refine2 = std::atof(e);
     if (const char* e = std::getenv("FMI_REFINE_FILL")) T->refine_fill = std::atof(e);
+    {
+      double mf = kMomentTreeFill;
+      if (const char* e = std::getenv("FMI_MT_FILL")) mf = std::atof(e);
+      T->mt_min = (int64_t)std::ceil(mf * L);
+    }
     if (T->refine_steps == 0) T->refine2 = 0.0;  // no node is flagged for refinement
     bool unit = hb[0] >= 0.0 && hb[1] >= 0.0 && hb[2] >= 0.0 && hb[3] <= 1.0 && hb[4] <= 1.0 && hb[5] <= 1.0;
     if (dist) {  // the common root cube of the shards

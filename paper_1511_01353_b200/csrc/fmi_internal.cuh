@@ -214,6 +214,9 @@ constexpr double kRefineFill = 2.0;
 constexpr int kRefineSteps = 2;
 // largest accepted equilibrated rounding bound of a translated Gram (DESIGN.md §5 M2M)
 constexpr double kMomentTol = 1e-11;
+// moment-tree cells need >= kMomentTreeFill·𝓛 points: smaller (deeper) fit nodes, which are few, get
+// their moments accumulated on demand (the fallback path), and the costly last M2M level disappears
+constexpr double kMomentTreeFill = 8.0;
 // points per K4 work item (one lane accumulates one chunk)
 constexpr int64_t kMomentChunk = 1024;
 // residual.cu (fused K6): over the chunks of the level's octant segments:
@@ -232,9 +235,10 @@ template <int P> void level_residual(const LevelCtx& c, int mode, int iter, cons
 // mt_child/srcseg (fit tree): moment-tree ids and source segments of the new nodes.
 // gcnt (sharded build, global levels): global octant counts [count*8]; owned_only: create only the
 // children whose points this shard holds (the shard's subtree roots).
+// geo_min (moment tree): a cell needs at least this many points to get a moment-tree node.
 void level_decide(const LevelCtx& c, bool geo, const int32_t* mt_child, int32_t* srcseg, int64_t* flags_tmp,
                   int64_t* scan_tmp, int64_t* dev_out, cudaStream_t s, const int64_t* gcnt = nullptr,
-                  bool owned_only = false);
+                  bool owned_only = false, int64_t geo_min = 0);
 // local octant counts [count*8] of the level's nodes
 void octant_counts(const LevelCtx& c, int64_t* out, cudaStream_t s);
 

@@ -110,7 +110,8 @@ __global__ void k_chunk_fill(RangeSrc src, int64_t nr, const int64_t* __restrict
 // the global levels; owned_only = the children are the shard's own subtree roots (depth = shard
 // depth): a child is created only where this shard holds its points.
 __global__ void k_decide(NodeTable nt, int64_t first, int64_t count, int depth, int D, int L, double tau, bool geo,
-                         const int64_t* __restrict__ gcnt, bool owned_only, int64_t* __restrict__ flags) {
+                         const int64_t* __restrict__ gcnt, bool owned_only, int64_t geo_min,
+                         int64_t* __restrict__ flags) {
   int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= count * 8) return;
   const int64_t node = first + t / 8;
@@ -119,7 +120,7 @@ __global__ void k_decide(NodeTable nt, int64_t first, int64_t count, int depth, 
   const int64_t n_o = gcnt ? gcnt[t] : n_loc;
   const bool owned = !owned_only || n_loc > 0;
   if (geo) {
-    flags[t] = (n_o > 0 && n_o >= L && depth + 1 <= D && owned) ? 1 : 0;
+    flags[t] = (n_o > 0 && n_o >= L && n_o >= geo_min && depth + 1 <= D && owned) ? 1 : 0;
     return;
   }
   nt.child_n[node * 8 + o] = n_o;
@@ -167,7 +168,8 @@ __global__ void k_emit(NodeTable nt, int64_t first, int64_t count, int depth, co
     nt.parent[id] = (int32_t)node;
     nt.child[node * 8 + o] = (int32_t)id;
     if (mt_child) {
-      nt.mtid[id] = mt_child[(int64_t)nt.mtid[node] * 8 + o];
+      const int32_t pm = nt.mtid[node];  // -1: deeper than the moment tree (moments accumulated on demand)
+      nt.mtid[id] = pm < 0 ? -1 : mt_child[(int64_t)pm * 8 + o];
       srcseg[pos[t]] = (int32_t)t;
     }
     for (int k = 0; k < 8; ++k) nt.child[id * 8 + k] = -1;
@@ -226,11 +228,12 @@ void octant_counts(const LevelCtx& c, int64_t* out, cudaStream_t s) {
 }
 
 void level_decide(const LevelCtx& c, bool geo, const int32_t* mt_child, int32_t* srcseg, int64_t* flags_tmp,
-                  int64_t* scan_tmp, int64_t* dev_out, cudaStream_t s, const int64_t* gcnt, bool owned_only) {
+                  int64_t* scan_tmp, int64_t* dev_out, cudaStream_t s, const int64_t* gcnt, bool owned_only,
+                  int64_t geo_min) {
   int64_t work = c.count * 8;
   unsigned grid = (unsigned)((work + 255) / 256);
   FMI_LAUNCH(KID_DECIDE, s, k_decide, grid, 256, 0, c.nt, c.first, c.count, c.depth, c.D, c.L, c.tau, geo, gcnt,
-             owned_only, flags_tmp);
+             owned_only, geo_min, flags_tmp);
   exclusive_scan_i64(flags_tmp, scan_tmp, work, nullptr, s);
   FMI_LAUNCH(KID_DECIDE, s, k_emit, grid, 256, 0, c.nt, c.first, c.count, c.depth, flags_tmp, scan_tmp, mt_child,
              srcseg, dev_out);

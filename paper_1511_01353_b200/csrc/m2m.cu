@@ -223,9 +223,9 @@ __global__ void __launch_bounds__(256)
   const int64_t m = mtid[first + ln];
   const int64_t sg = srcseg ? srcseg[ln] : 0;
   const int64_t st = 2 * K + L;
-  for (int e = threadIdx.x; e < K; e += blockDim.x) {
-    out[ln * st + e] = mtmom[m * KS + e];
-    out[ln * st + K + L + e] = (double)mtbnd[m * KS + e];
+  for (int e = threadIdx.x; e < K; e += blockDim.x) {  // m < 0: no moments yet -> the solve's check fails
+    out[ln * st + e] = m < 0 ? 0.0 : mtmom[m * KS + e];
+    out[ln * st + K + L + e] = m < 0 ? INFINITY : (double)mtbnd[m * KS + e];
   }
   for (int e = threadIdx.x; e < L; e += blockDim.x) out[ln * st + K + e] = segsum[sg * (L + 1) + e];
 }

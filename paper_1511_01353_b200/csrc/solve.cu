@@ -97,6 +97,14 @@ __global__ void __launch_bounds__(k5_threads<P>())
     if (tid == 0) smin_sh = INFINITY;
     for (int e = tid; e < K; e += K5_THREADS) sM[e] = mp[e];
     __syncthreads();
+    if (mode == 0 && !(sM[0] > 0.0)) {  // below the moment tree (M_000 = 0): accumulate directly
+      if (tid == 0) {
+        nt.flag[first + node] = 4;
+        atomicAdd(reinterpret_cast<unsigned long long*>(nflag + 1), 1ull);
+      }
+      __syncthreads();
+      continue;
+    }
     for (int i = tid; i < L; i += K5_THREADS) {
       const double m2 = sM[basis_index(Q, 2 * bl[i], 2 * bm[i], 2 * bn[i])];
       const double di = m2 > 0.0 ? 1.0 / sqrt(m2) : 0.0;
@@ -167,7 +175,9 @@ __global__ void __launch_bounds__(k5_threads<P>())
       if (mode == 0) {
         double em = 0.0;
         for (int w = 0; w < K5_WARPS; ++w) em = fmax(em, errw[w]);
-        if (!(em <= mom_tol)) {  // translated moments lost their precision: re-accumulate directly
+        // translated moments lost their precision, or the node is below the moment tree (M_000 = 0:
+        // no moments yet): accumulate them directly from the node's points
+        if (!(em <= mom_tol) || !(sM[0] > 0.0)) {
           if (tid == 0) {
             nt.flag[first + node] = 4;
             atomicAdd(reinterpret_cast<unsigned long long*>(nflag + 1), 1ull);
