@@ -1,0 +1,2 @@
+mkdir -p gpurun_out
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"^k_solve$" -s 4 -c 1 -o gpurun_out/k5_v27 -f python tools/run_build.py --config 5 > gpurun_out/ncu_k5_v27.log 2>&1
