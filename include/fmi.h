@@ -184,10 +184,11 @@ int fmi_residual(const fmi_tree* tree, double* out);
  * number of points in active nodes (point-levels). Returns the number of levels. */
 int fmi_level_stats(const fmi_tree* tree, int64_t* nodes, int64_t* points, int cap);
 
-/* Build statistics: out[0] = moment-tree nodes (every cell with >= 𝓛 points down to max_depth),
- * out[1] = fit nodes whose translated moments failed the rounding check and were re-accumulated
- * directly, out[2] = fit nodes that took semi-normal refinement steps.  Returns the number of
- * statistics (3) or a negative code; writes min(cap, 3) entries. */
+/* Build statistics: out[0] = moment-tree nodes (cells with >= 8𝓛 points down to max_depth),
+ * out[1] = fit nodes whose moments were accumulated directly (below the moment tree, or the translated
+ * moments failed the rounding check), out[2] = fit nodes that took semi-normal refinement steps,
+ * out[3] = children whose projections ran in a deferred pass.  Returns the number of statistics (4)
+ * or a negative code; writes min(cap, 4) entries. */
 int fmi_build_stats(const fmi_tree* tree, int64_t* out, int cap);
 
 /* ------------------------------------------------------------------------------------------------

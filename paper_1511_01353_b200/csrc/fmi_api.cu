@@ -46,8 +46,8 @@ __global__ void k_copy_flagged(const double* __restrict__ src, int K, double* __
 // QR-flagged global nodes of a sharded build are refined instead (K5q needs all the node's points)
 __global__ void k_qr_to_refine(NodeTable nt, int64_t first, int64_t count, int64_t* __restrict__ nref) {
   int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t < count && nt.flag[first + t] == 1) {
-    nt.flag[first + t] = 2;
+  if (t < count && (nt.flag[first + t] & 3) == 1) {
+    nt.flag[first + t] = (nt.flag[first + t] & ~3) | 2;
     atomicAdd(reinterpret_cast<unsigned long long*>(nref), 1ull);
   }
 }
@@ -196,6 +196,8 @@ struct fmi_tree {
   double refine2 = kRefinePivot2;    // env FMI_REFINE_PIVOT2
   double refine_fill = kRefineFill;  // env FMI_REFINE_FILL
   int64_t mt_min = 0;                // moment-tree cell minimum (points); env FMI_MT_FILL (multiple of 𝓛)
+  double defer_theta = kDeferTheta;  // env FMI_DEFER_THETA (0: never defer)
+  int64_t deferred_children = 0;     // children whose projections ran in a K6_PROJ pass
   double tau = 0;
   double lo[3] = {0, 0, 0};
   double width = 1;
@@ -332,7 +334,7 @@ void reset_tree(fmi_tree* T, cudaStream_t s) {
   free_table(T->nt, s);
   T->cap = 0;
   T->nodes = 0;
-  T->mt_nodes = T->direct_nodes = T->refined_nodes = 0;
+  T->mt_nodes = T->direct_nodes = T->refined_nodes = T->deferred_children = 0;
   T->lvl_first.clear();
   T->lvl_count.clear();
   T->lvl_points.clear();
@@ -364,7 +366,8 @@ void dist_sum(const fmi_tree* T, void* dev, int64_t n, int dtype, cudaStream_t s
 template <int P>
 void run_levels(fmi_tree* T, const uint64_t* keys, double* ux, double* uy, double* uz, double* r, cudaStream_t s) {
   constexpr int L = rank3(P), K = rank3(2 * P);
-  DBuf<int64_t> counts, begin, flags, scan, dev_small(4, s), nflag(2, s), gcnt;
+  DBuf<int64_t> counts, begin, flags, scan, dev_small(8, s), nflag(2, s), gcnt;
+  DBuf<int32_t> dsel;
   DBuf<Chunk> chunks;
   DBuf<double> partial, mtmom, segsum, lvlmom, scratch, delta;
   DBuf<float> mtbnd;
@@ -471,7 +474,9 @@ void run_levels(fmi_tree* T, const uint64_t* keys, double* ux, double* uy, doubl
       // K5: solve; nodes whose translated moments fail the rounding check are re-accumulated directly
       FMI_CK(cudaMemsetAsync(nflag.p, 0, 2 * sizeof(int64_t), s));
       scratch.ensure((size_t)count * fac_per_node, s);
-      level_solve<P>(c, lvlmom.p, 0, nullptr, nullptr, T->refine2, T->refine_fill, T->Ntot, nflag.p, scratch.p, s);
+      const double defer_tau = global ? 0.0 : T->defer_theta * T->tau;  // deferral: single shard only
+      level_solve<P>(c, lvlmom.p, 0, nullptr, nullptr, T->refine2, T->refine_fill, T->Ntot, nflag.p, scratch.p, s,
+                     defer_tau);
       FMI_CK(cudaMemcpyAsync(&host_small[2], nflag.p, 2 * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
       FMI_CK(cudaStreamSynchronize(s));
       if (host_small[3] > 0) {
@@ -499,7 +504,8 @@ void run_levels(fmi_tree* T, const uint64_t* keys, double* ux, double* uy, doubl
         } else {
           reduce_moments(partial.p, begin.p, dev_small.p, count, 1, K, T->nt.flag + first, 4, lvlmom.p, 2 * K + L, s);
         }
-        level_solve<P>(c, lvlmom.p, 2, nullptr, nullptr, T->refine2, T->refine_fill, T->Ntot, nflag.p, scratch.p, s);
+        level_solve<P>(c, lvlmom.p, 2, nullptr, nullptr, T->refine2, T->refine_fill, T->Ntot, nflag.p, scratch.p, s,
+                       defer_tau);
         FMI_CK(cudaMemcpyAsync(&host_small[2], nflag.p, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
         FMI_CK(cudaStreamSynchronize(s));
         T->direct_nodes += host_small[3];
@@ -549,12 +555,22 @@ void run_levels(fmi_tree* T, const uint64_t* keys, double* ux, double* uy, doubl
         octant_counts(c, gcnt.p, s);
         dist_sum(T, gcnt.p, count * 8, 1, s);
       }
+      FMI_CK(cudaMemsetAsync(dev_small.p + 4, 0, sizeof(int64_t), s));
       level_decide(c, false, mt.child, srcseg.p, flags.p, scan.p, dev_small.p + 2, s, global ? gcnt.p : nullptr,
                    global && depth + 1 == T->shard_depth);
-      FMI_CK(cudaMemcpyAsync(host_small, dev_small.p + 2, 2 * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+      FMI_CK(cudaMemcpyAsync(host_small, dev_small.p + 2, 3 * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
       FMI_CK(cudaStreamSynchronize(s));
-      const int64_t nnew = host_small[0], npts = host_small[1];
+      const int64_t nnew = host_small[0], npts = host_small[1], ndefer = host_small[2];
       tmark("decide", s);
+      if (ndefer > 0) {  // children created under deferred parents: their projections now (K6_PROJ)
+        dsel.ensure(count * 8, s);
+        defer_select(c, dsel.p, s);
+        make_chunks(T->nt.child_start + first * 9, nullptr, count * 8, ch6, counts.p, begin.p, dev_small.p + 1,
+                    chunks.p, max6, s, nullptr, nullptr, 0, dsel.p);
+        level_residual<P>(c, K6_PROJ, 0, nullptr, chunks.p, dev_small.p + 1, max6, begin.p, count * 8, partial.p,
+                          segsum.p, s, dsel.p);
+        T->deferred_children += ndefer;
+      }
       if (nnew > 0) {
         lvlmom.ensure((size_t)nnew * (2 * K + L), s);
         gather_level(mtmom.p, mtbnd.p, T->nt.mtid, segsum.p, srcseg.p, first + count, nnew, K, KS, L, lvlmom.p, s);
@@ -682,6 +698,7 @@ fmi_tree* build_impl(const double* pts, const double* f, int64_t N, int degree, 
     if (const char* e = std::getenv("FMI_REFINE_STEPS")) T->refine_steps = std::max(0, std::atoi(e));
     if (const char* e = std::getenv("FMI_REFINE_PIVOT2")) T->refine2 = std::atof(e);
     if (const char* e = std::getenv("FMI_REFINE_FILL")) T->refine_fill = std::atof(e);
+    if (const char* e = std::getenv("FMI_DEFER_THETA")) T->defer_theta = std::atof(e);
     {
       double mf = kMomentTreeFill;
       if (const char* e = std::getenv("FMI_MT_FILL")) mf = std::atof(e);
@@ -1074,10 +1091,10 @@ int fmi_level_stats(const fmi_tree* T, int64_t* nodes, int64_t* points, int cap)
 
 int fmi_build_stats(const fmi_tree* T, int64_t* out, int cap) {
   if (!T || !out) { set_error(FMI_EINPUT, "null argument"); return FMI_EINPUT; }
-  const int64_t v[3] = {T->mt_nodes, T->direct_nodes, T->refined_nodes};
-  const int n = std::min(cap, 3);
+  const int64_t v[4] = {T->mt_nodes, T->direct_nodes, T->refined_nodes, T->deferred_children};
+  const int n = std::min(cap, 4);
   for (int i = 0; i < n; ++i) out[i] = v[i];
-  return 3;
+  return 4;
 }
 
 int fmi_profile_enable(int on) {

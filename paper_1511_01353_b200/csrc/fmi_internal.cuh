@@ -158,7 +158,8 @@ void scatter_values(const double* vals, const int64_t* idx, int64_t m, double* o
 // chunk_begin[i] (exclusive scan of per-range chunk counts) and *nchunks (device) are written.
 void make_chunks(const int64_t* rstart, const int64_t* rend, int64_t nr, int64_t ch, int64_t* counts_tmp,
                  int64_t* chunk_begin, int64_t* nchunks_dev, Chunk* chunks, int64_t max_chunks, cudaStream_t s,
-                 const int32_t* seg_mask = nullptr, const int32_t* range_flag = nullptr, int flag_bit = 0);
+                 const int32_t* seg_mask = nullptr, const int32_t* range_flag = nullptr, int flag_bit = 0,
+                 const int32_t* seg_sel = nullptr);
 
 // level ops (level.cu)
 struct LevelCtx {
@@ -204,7 +205,7 @@ void gather_level(const double* mtmom, const float* mtbnd, const int32_t* mtid, 
 // re-solve of bit-2 nodes after direct accumulation (no rounding check).
 template <int P> void level_solve(const LevelCtx& c, const double* mom, int mode, const double* segrhs,
                                   double* delta, double refine2, double refine_fill, int64_t n_root,
-                                  int64_t* nflag, double* fac, cudaStream_t s);
+                                  int64_t* nflag, double* fac, cudaStream_t s, double defer_tau = 0.0);
 // fac: per level-local node solve_factor_per_node(p) doubles (bordered packed lower factor, kept for
 // the refinement solves)
 size_t solve_factor_per_node(int p);
@@ -226,10 +227,16 @@ constexpr int64_t kMomentChunk = 1024;
 //   K6_OWN:   refinement step `iter` of bit-1 nodes only: r -= (iter ? delta : coef), projection in
 //             the node's own frame.
 // segsum[seg][0..𝓛) = projection, segsum[seg][𝓛] = Σ r².
-enum K6Mode { K6_CHILD = 0, K6_ROOT = 1, K6_OWN = 2 };
+//   K6_PROJ:  child-frame projections only (residual already updated) for the segments selected by
+//             sel (children created under a parent whose projections were deferred, flag bit 3).
+enum K6Mode { K6_CHILD = 0, K6_ROOT = 1, K6_OWN = 2, K6_PROJ = 3 };
 template <int P> void level_residual(const LevelCtx& c, int mode, int iter, const double* delta, const Chunk* chunks,
                                      const int64_t* nchunks_dev, int64_t max_chunks, const int64_t* chunk_begin,
-                                     int64_t nseg, double* partial, double* segsum, cudaStream_t s);
+                                     int64_t nseg, double* partial, double* segsum, cudaStream_t s,
+                                     const int32_t* sel = nullptr);
+// child projections of a node are deferred (flag bit 3) when its pre-fit RMS is below kDeferTheta·τ:
+// its children are then unlikely to be created, and the projection pass runs only for those that are
+constexpr double kDeferTheta = 100.0;
 // decisions + compaction: writes the next level's nodes at [first+count, ...), returns via dev_out[0] the
 // number of new nodes and dev_out[1] their total points.  geo: moment tree (integer guards only).
 // mt_child/srcseg (fit tree): moment-tree ids and source segments of the new nodes.
@@ -241,6 +248,8 @@ void level_decide(const LevelCtx& c, bool geo, const int32_t* mt_child, int32_t*
                   bool owned_only = false, int64_t geo_min = 0);
 // local octant counts [count*8] of the level's nodes
 void octant_counts(const LevelCtx& c, int64_t* out, cudaStream_t s);
+// sel[node*8+o] = 1 for children created under a parent with deferred projections (flag bit 3), else -1
+void defer_select(const LevelCtx& c, int32_t* sel, cudaStream_t s);
 
 // solve_qr.cu (robust path for ill-conditioned nodes)
 size_t solve_qr_scratch_per_cta(int p);

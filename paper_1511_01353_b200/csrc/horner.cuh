@@ -16,9 +16,13 @@ __device__ __forceinline__ double horner3(const Coef& coef, double x, double y, 
     double py = 0.0;
 #pragma unroll
     for (int m = P - l; m >= 0; --m) {
+      // the row's coefficients are loaded back to back first (one latency per row, not per FMA)
+      double cr[P + 1];
+#pragma unroll
+      for (int n = 0; n <= P - l - m; ++n) cr[n] = coef(basis_index(P, l, m, n));
       double pz = 0.0;
 #pragma unroll
-      for (int n = P - l - m; n >= 0; --n) pz = fma(pz, z, coef(basis_index(P, l, m, n)));
+      for (int n = P - l - m; n >= 0; --n) pz = fma(pz, z, cr[n]);
       py = fma(py, y, pz);
     }
     px = fma(px, x, py);
@@ -26,7 +30,7 @@ __device__ __forceinline__ double horner3(const Coef& coef, double x, double y, 
   return px;
 }
 
-// Two points per call: every coefficient load feeds two FMAs.
+// Two points per call: every coefficient load feeds two FMAs; each row's loads are issued back to back.
 template <int P, typename Coef>
 __device__ __forceinline__ void horner3x2(const Coef& coef, double x0, double y0, double z0, double x1, double y1,
                                           double z1, double& v0, double& v1) {
@@ -36,12 +40,14 @@ __device__ __forceinline__ void horner3x2(const Coef& coef, double x0, double y0
     double py0 = 0.0, py1 = 0.0;
 #pragma unroll
     for (int m = P - l; m >= 0; --m) {
+      double cr[P + 1];
+#pragma unroll
+      for (int n = 0; n <= P - l - m; ++n) cr[n] = coef(basis_index(P, l, m, n));
       double pz0 = 0.0, pz1 = 0.0;
 #pragma unroll
       for (int n = P - l - m; n >= 0; --n) {
-        const double a = coef(basis_index(P, l, m, n));
-        pz0 = fma(pz0, z0, a);
-        pz1 = fma(pz1, z1, a);
+        pz0 = fma(pz0, z0, cr[n]);
+        pz1 = fma(pz1, z1, cr[n]);
       }
       py0 = fma(py0, y0, pz0);
       py1 = fma(py1, y1, pz1);

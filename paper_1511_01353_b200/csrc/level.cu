@@ -49,12 +49,14 @@ struct RangeSrc {
   int mode;
   const int32_t* flag;  // mode 0 (optional): a range i with !(flag[i] & bit) is empty
   int bit;
+  const int32_t* sel;   // mode 1 (optional): a segment i with sel[i] < 0 is empty
   __device__ __forceinline__ void get(int64_t i, int64_t& s, int64_t& e) const {
     if (mode == 0) {
       s = a[i]; e = b[i];
       if (flag && !(flag[i] & bit)) e = s;
     } else {
       int64_t nd = i >> 3; int o = (int)(i & 7); s = a[nd * 9 + o]; e = a[nd * 9 + o + 1];
+      if (sel && sel[i] < 0) e = s;
       if (mask) {
         // owner runs: consecutive segments without a child node are one range, attributed to the
         // first segment of the run (so a leaf's points form a single range)
@@ -139,6 +141,14 @@ __global__ void k_decide(NodeTable nt, int64_t first, int64_t count, int depth, 
   }
 }
 
+// segments of children created under a deferred parent (the deferred projection pass)
+__global__ void k_defer_sel(NodeTable nt, int64_t first, int64_t count, int32_t* __restrict__ sel) {
+  int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= count * 8) return;
+  const int64_t node = first + t / 8;
+  sel[t] = ((nt.flag[node] & 8) && nt.child[node * 8 + (t % 8)] >= 0) ? 1 : -1;
+}
+
 // local octant counts of the level's nodes (for the global-level sums of a sharded build)
 __global__ void k_octant_counts(NodeTable nt, int64_t first, int64_t count, int64_t* __restrict__ out) {
   int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -179,6 +189,8 @@ __global__ void k_emit(NodeTable nt, int64_t first, int64_t count, int depth, co
   if (t == count * 8 - 1) {
     out[0] = pos[t] + flags[t];
   }
+  // children of parents whose child projections were deferred (flag bit 3): their projection pass
+  if (mt_child && flags[t] && (nt.flag[node] & 8)) atomicAdd(reinterpret_cast<unsigned long long*>(out + 2), 1ull);
 }
 
 // total points of the emitted nodes (single CTA, fixed order)
@@ -216,9 +228,15 @@ void make_chunks_impl(RangeSrc src, int64_t nr, int64_t ch, int64_t* counts_tmp,
 
 void make_chunks(const int64_t* rstart, const int64_t* rend, int64_t nr, int64_t ch, int64_t* counts_tmp,
                  int64_t* chunk_begin, int64_t* nchunks_dev, Chunk* chunks, int64_t max_chunks, cudaStream_t s,
-                 const int32_t* seg_mask, const int32_t* range_flag, int flag_bit) {
-  RangeSrc src{rstart, rend, seg_mask, rend ? 0 : 1, range_flag, flag_bit};
+                 const int32_t* seg_mask, const int32_t* range_flag, int flag_bit, const int32_t* seg_sel) {
+  RangeSrc src{rstart, rend, seg_mask, rend ? 0 : 1, range_flag, flag_bit, seg_sel};
   make_chunks_impl(src, nr, ch, counts_tmp, chunk_begin, nchunks_dev, chunks, max_chunks, s);
+}
+
+void defer_select(const LevelCtx& c, int32_t* sel, cudaStream_t s) {
+  const int64_t work = c.count * 8;
+  if (work <= 0) return;
+  FMI_LAUNCH(KID_DECIDE, s, k_defer_sel, (unsigned)((work + 255) / 256), 256, 0, c.nt, c.first, c.count, sel);
 }
 
 void octant_counts(const LevelCtx& c, int64_t* out, cudaStream_t s) {

@@ -157,8 +157,8 @@ __global__ void __launch_bounds__(K6_THREADS, 2)
   const int64_t node = first + ln;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   double* out = partial + cidx * (int64_t)(L + 1);
-  const bool horner = mode != K6_ROOT;
-  const bool refined = mode != K6_ROOT && (nt.flag[node] & 2);
+  const bool horner = mode != K6_ROOT && mode != K6_PROJ;
+  const bool refined = horner && (nt.flag[node] & 2);
   if (mode == K6_OWN && !refined) {  // refinement pass: this node takes no step
     for (int e = tid; e <= L; e += K6_THREADS) out[e] = 0.0;
     return;
@@ -176,7 +176,8 @@ __global__ void __launch_bounds__(K6_THREADS, 2)
       fc = fn;
     } else {
       const int64_t n_o = nt.child_start[node * 9 + o + 1] - nt.child_start[node * 9 + o];
-      project = n_o >= L && depth + 1 <= D;  // potential child (P:306 integer guard + G5)
+      // potential child (P:306 integer guard + G5), unless deferred (flag bit 3: see K6_PROJ)
+      project = mode == K6_PROJ || (n_o >= L && depth + 1 <= D && !(nt.flag[node] & 8));
       fc = node_frame(make_int4(2 * c.x + (o & 1), 2 * c.y + ((o >> 1) & 1), 2 * c.z + ((o >> 2) & 1), c.w + 1));
     }
     // polynomial to subtract: the fit, or (refined nodes) the last refinement correction
@@ -284,8 +285,9 @@ __global__ void __launch_bounds__(K6_THREADS, 2)
 __global__ void __launch_bounds__(128)
     k_residual_reduce(const double* __restrict__ partial, const int64_t* __restrict__ chunk_begin,
                       const int64_t* __restrict__ nchunks, int64_t nseg, NodeTable nt, int64_t first, int L,
-                      bool write_ss, double* __restrict__ segsum) {
+                      bool write_ss, const int32_t* __restrict__ sel, double* __restrict__ segsum) {
   const int64_t sgi = blockIdx.x;
+  if (sel && sel[sgi] < 0) return;  // K6_PROJ: only the selected segments are (re)written
   const int64_t c0 = chunk_begin[sgi];
   const int64_t c1 = sgi + 1 < nseg ? chunk_begin[sgi + 1] : *nchunks;
   for (int e = threadIdx.x; e <= L; e += blockDim.x) {
@@ -301,18 +303,18 @@ __global__ void __launch_bounds__(128)
 template <int P>
 void level_residual(const LevelCtx& c, int mode, int iter, const double* delta, const Chunk* chunks,
                     const int64_t* nchunks_dev, int64_t max_chunks, const int64_t* chunk_begin, int64_t nseg,
-                    double* partial, double* segsum, cudaStream_t s) {
+                    double* partial, double* segsum, cudaStream_t s, const int32_t* sel) {
   const int kid = mode == K6_ROOT ? KID_PROJECT : (mode == K6_OWN ? KID_REFINE : KID_RESIDUAL);
   if (max_chunks > 0)
     FMI_LAUNCH(kid, s, k_residual<P>, (unsigned)max_chunks, K6_THREADS, 0, c.ux, c.uy, c.uz, c.r, c.nt, c.first,
                chunks, nchunks_dev, c.depth, c.D, mode, iter, delta, partial);
   FMI_LAUNCH(KID_RESIDUAL_REDUCE, s, k_residual_reduce, (unsigned)nseg, 128, 0, partial, chunk_begin, nchunks_dev, nseg,
-             c.nt, c.first, rank3(P), mode == K6_CHILD, segsum);
+             c.nt, c.first, rank3(P), mode == K6_CHILD, sel, segsum);
 }
 
 #define FMI_INST(P)                                                                                            \
   template void level_residual<P>(const LevelCtx&, int, int, const double*, const Chunk*, const int64_t*, int64_t, \
-                                  const int64_t*, int64_t, double*, double*, cudaStream_t);
+                                  const int64_t*, int64_t, double*, double*, cudaStream_t, const int32_t*);
 FMI_INST(0) FMI_INST(1) FMI_INST(2) FMI_INST(3) FMI_INST(4) FMI_INST(5)
 FMI_INST(6) FMI_INST(7) FMI_INST(8) FMI_INST(9) FMI_INST(10)
 #undef FMI_INST

@@ -65,7 +65,7 @@ __global__ void __launch_bounds__(k5_threads<P>())
     k_solve(const double* __restrict__ mom, int mode, const double* __restrict__ segrhs, double* __restrict__ delta,
             NodeTable nt, int64_t first, int64_t count, double* __restrict__ fac,
             const __grid_constant__ BasisTab bt, double delta2, double refine2, double refine_fill,
-            double mom_tol, int64_t n_root, int64_t* __restrict__ nflag) {
+            double mom_tol, int64_t n_root, double defer_tau, int64_t* __restrict__ nflag) {
   using S = K5Shape<P>;
   constexpr int Q = S::Q, K = S::K, L = S::L;
   constexpr int K5_THREADS = k5_threads<P>(), K5_WARPS = K5_THREADS / 32;
@@ -346,7 +346,15 @@ __global__ void __launch_bounds__(k5_threads<P>())
                                   : (double)nt.child_n[(int64_t)par * 8 + ((cc.x & 1) | ((cc.y & 1) << 1) | ((cc.z & 1) << 2))];
       const bool refine = refine2 > 0.0 && (smin_sh < refine2 || npts < refine_fill * L);
       const int fl = (smin_sh < kQrFlagPivot2) ? 1 : (refine ? 2 : 0);
-      nt.flag[first + node] = fl;
+      // defer this node's child projections when its pre-fit RMS (the parent's octant E_RMS) is below
+      // defer_tau: its children are then unlikely to be created (K6_PROJ runs for those that are)
+      int defer = 0;
+      if (par >= 0 && defer_tau > 0.0) {
+        const int oc = (cc.x & 1) | ((cc.y & 1) << 1) | ((cc.z & 1) << 2);
+        const double e_pre = sqrt(nt.child_ss[(int64_t)par * 8 + oc] / fmax(npts, 1.0));
+        defer = e_pre < defer_tau ? 8 : 0;
+      }
+      nt.flag[first + node] = fl | defer;
       if (fl == 2) atomicAdd(reinterpret_cast<unsigned long long*>(nflag), 1ull);
     }
     __syncthreads();
@@ -357,7 +365,7 @@ __global__ void __launch_bounds__(k5_threads<P>())
 
 template <int P>
 void level_solve(const LevelCtx& c, const double* mom, int mode, const double* segrhs, double* delta, double refine2,
-                 double refine_fill, int64_t n_root, int64_t* nflag, double* fac, cudaStream_t s) {
+                 double refine_fill, int64_t n_root, int64_t* nflag, double* fac, cudaStream_t s, double defer_tau) {
   using S = K5Shape<P>;
   static const BasisTab bt = make_basis<P>();
   static bool attr = false;
@@ -369,7 +377,7 @@ void level_solve(const LevelCtx& c, const double* mom, int mode, const double* s
   if (grid <= 0) return;
   FMI_LAUNCH(mode == 1 ? KID_REFINE_SOLVE : KID_SOLVE, s, k_solve<P>, (unsigned)grid, k5_threads<P>(), S::SMEM, mom, mode,
              segrhs, delta, c.nt, c.first, c.count, fac, bt, kDelta * kDelta, refine2, refine_fill, kMomentTol, n_root,
-             nflag);
+             defer_tau, nflag);
 }
 
 // doubles of per-node factor storage (bordered packed lower triangle)
@@ -384,7 +392,7 @@ size_t solve_factor_per_node(int p) {
 
 #define FMI_INST(P) \
   template void level_solve<P>(const LevelCtx&, const double*, int, const double*, double*, double, double, int64_t, \
-                               int64_t*, double*, cudaStream_t);
+                               int64_t*, double*, cudaStream_t, double);
 FMI_INST(0) FMI_INST(1) FMI_INST(2) FMI_INST(3) FMI_INST(4) FMI_INST(5)
 FMI_INST(6) FMI_INST(7) FMI_INST(8) FMI_INST(9) FMI_INST(10)
 #undef FMI_INST

@@ -286,9 +286,10 @@ class Tree:
     def build_stats(self) -> dict:
         """Moment-tree size, fit nodes re-accumulated directly (M2M rounding check), refined nodes."""
         lib = load_library()
-        out = (ctypes.c_int64 * 3)()
-        lib.fmi_build_stats(ctypes.c_void_p(self.handle), out, 3)
-        return {"moment_tree_nodes": int(out[0]), "direct_moment_nodes": int(out[1]), "refined_nodes": int(out[2])}
+        out = (ctypes.c_int64 * 4)()
+        lib.fmi_build_stats(ctypes.c_void_p(self.handle), out, 4)
+        return {"moment_tree_nodes": int(out[0]), "direct_moment_nodes": int(out[1]), "refined_nodes": int(out[2]),
+                "deferred_children": int(out[3])}
 
 
 def build(pts, f, degree: int, tol: float, max_depth: int) -> Tree:
