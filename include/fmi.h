@@ -129,6 +129,24 @@ int fmi_scatter(const double* vals, const int64_t* idx, int64_t M, double* out);
  */
 int fmi_eval(const fmi_tree* tree, const double* q, int64_t M, double* out);
 
+/*
+ * fmi_transfer — the paper's mesh-to-mesh transfer f_p -> f_q (§2: f'_q = Λ'·F_p):
+ * fmi_build over (pts, f, N) + fmi_eval at (q, M) into out + fmi_free, in one call.  Arguments and
+ * errors as fmi_build / fmi_eval.  Returns 0 or a negative FMI_E* code.
+ */
+int fmi_transfer(const double* pts, const double* f, int64_t N, const double* q, int64_t M, double* out, int degree,
+                 double tol, int max_depth);
+
+/*
+ * Tree files (layout after SPEC's FMT1 node records): header (magic "FMITREE1", version,
+ * degree, depth, root cube, τ, point count) + per-node cell, parent, children, octant counts and
+ * energies, coefficients P_F (monomial form) and the pre-summed polynomials, rms, pivots, ranks, flags.
+ * fmi_save returns 0 or a code; fmi_load returns a tree (NULL on error: FMI_EVERSION for a foreign or
+ * corrupt file).  A loaded tree evaluates and exports like a built one; fmi_residual is unavailable.
+ */
+int fmi_save(const fmi_tree* tree, const char* path);
+fmi_tree* fmi_load(const char* path);
+
 /* fmi_free — release the tree and its device memory.  NULL-safe. */
 void fmi_free(fmi_tree* tree);
 

@@ -94,10 +94,10 @@ __global__ void __launch_bounds__(PS_THREADS) k_presum(NodeTable nt, int64_t fir
 // then stages that node's pre-summed coefficients in shared memory once (coalesced) and every lane
 // reads them as broadcasts; otherwise each lane reads its node's coefficients through L1.
 template <int P>
-__global__ void __launch_bounds__(256) k_eval(const double* __restrict__ q, const uint64_t* __restrict__ keys,
-                                              const uint32_t* __restrict__ idx, int64_t M, double lo0, double lo1,
-                                              double lo2, double w, bool unit, int Dk, NodeTable nt,
-                                              double* __restrict__ out) {
+__global__ void __launch_bounds__(256) k_eval(const double* __restrict__ q, const double4* __restrict__ qpk,
+                                              const uint64_t* __restrict__ keys, const uint32_t* __restrict__ idx,
+                                              int64_t M, double lo0, double lo1, double lo2, double w, bool unit,
+                                              int Dk, NodeTable nt, double* __restrict__ out) {
   constexpr int L = rank3(P);
   __shared__ double cs[256 / 32][L];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -107,9 +107,15 @@ __global__ void __launch_bounds__(256) k_eval(const double* __restrict__ q, cons
   double ux = 0.0, uy = 0.0, uz = 0.0;
   int64_t node = 0;
   if (active) {
-    ux = to_unit_e(q[3 * qi + 0], lo0, w, unit);
-    uy = to_unit_e(q[3 * qi + 1], lo1, w, unit);
-    uz = to_unit_e(q[3 * qi + 2], lo2, w, unit);
+    if (qpk) {  // root-cube coordinates written by the key kernel: one 32-byte record per query
+      const double2* p = reinterpret_cast<const double2*>(qpk + qi);
+      const double2 a = __ldg(p), b = __ldg(p + 1);
+      ux = a.x; uy = a.y; uz = b.x;
+    } else {
+      ux = to_unit_e(q[3 * qi + 0], lo0, w, unit);
+      uy = to_unit_e(q[3 * qi + 1], lo1, w, unit);
+      uz = to_unit_e(q[3 * qi + 2], lo2, w, unit);
+    }
     const bool inside = ux >= 0.0 && ux <= 1.0 && uy >= 0.0 && uy <= 1.0 && uz >= 0.0 && uz <= 1.0;
     // descend to the deepest existing node containing the query
     if (inside && keys) {
@@ -152,16 +158,17 @@ void presum_level(const NodeTable& nt, int64_t first, int64_t count, cudaStream_
 }
 
 template <int P>
-void eval_sorted(const double* q, const uint64_t* keys, const uint32_t* idx, int64_t M, const double lo[3],
-                 double width, bool unit, int Dk, const NodeTable& nt, double* out, cudaStream_t s) {
+void eval_sorted(const double* q, const double4* qpk, const uint64_t* keys, const uint32_t* idx, int64_t M,
+                 const double lo[3], double width, bool unit, int Dk, const NodeTable& nt, double* out,
+                 cudaStream_t s) {
   if (M <= 0) return;
-  FMI_LAUNCH(KID_EVAL, s, k_eval<P>, (unsigned)((M + 255) / 256), 256, 0, q, keys, idx, M, lo[0], lo[1], lo[2],
+  FMI_LAUNCH(KID_EVAL, s, k_eval<P>, (unsigned)((M + 255) / 256), 256, 0, q, qpk, keys, idx, M, lo[0], lo[1], lo[2],
              width, unit, Dk, nt, out);
 }
 
 #define FMI_INST(P)                                                                                            \
-  template void eval_sorted<P>(const double*, const uint64_t*, const uint32_t*, int64_t, const double*, double, \
-                               bool, int, const NodeTable&, double*, cudaStream_t);                             \
+  template void eval_sorted<P>(const double*, const double4*, const uint64_t*, const uint32_t*, int64_t,          \
+                               const double*, double, bool, int, const NodeTable&, double*, cudaStream_t);       \
   template void presum_level<P>(const NodeTable&, int64_t, int64_t, cudaStream_t);
 FMI_INST(0) FMI_INST(1) FMI_INST(2) FMI_INST(3) FMI_INST(4) FMI_INST(5)
 FMI_INST(6) FMI_INST(7) FMI_INST(8) FMI_INST(9) FMI_INST(10)

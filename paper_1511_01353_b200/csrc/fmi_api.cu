@@ -591,9 +591,9 @@ void run_levels(fmi_tree* T, const uint64_t* keys, double* ux, double* uy, doubl
 }
 
 template <int P>
-void run_eval(const fmi_tree* T, const double* q, const uint64_t* keys, const uint32_t* idx, int64_t M, int Dk,
-              double* out, cudaStream_t s) {
-  eval_sorted<P>(q, keys, idx, M, T->lo, T->width, T->unit, Dk, T->nt, out, s);
+void run_eval(const fmi_tree* T, const double* q, const double4* qpk, const uint64_t* keys, const uint32_t* idx,
+              int64_t M, int Dk, double* out, cudaStream_t s) {
+  eval_sorted<P>(q, qpk, keys, idx, M, T->lo, T->width, T->unit, Dk, T->nt, out, s);
 }
 
 #define FMI_DISPATCH(p, FN, ...)                      \
@@ -796,13 +796,14 @@ int eval_impl(const fmi_tree* T, const double* q, int64_t M, double* out) {
   }
   const int Dk = T->depth_max;
   if (Dk == 0) {
-    FMI_DISPATCH(T->p, run_eval, T, dq, nullptr, nullptr, M, 0, dout, s);
+    FMI_DISPATCH(T->p, run_eval, T, dq, nullptr, nullptr, nullptr, M, 0, dout, s);
   } else {
     DBuf<uint64_t> keys(M, s), ktmp(M, s);
     DBuf<uint32_t> idx(M, s), itmp(M, s);
-    morton_keys(dq, M, T->lo, T->width, T->unit, Dk, keys.p, idx.p, s);
+    DBuf<double4> qpk(M, s);
+    morton_keys(dq, M, T->lo, T->width, T->unit, Dk, keys.p, idx.p, s, nullptr, qpk.p);
     radix_sort_pairs(keys.p, idx.p, ktmp.p, itmp.p, M, 3 * Dk, s);
-    FMI_DISPATCH(T->p, run_eval, T, dq, keys.p, idx.p, M, Dk, dout, s);
+    FMI_DISPATCH(T->p, run_eval, T, dq, qpk.p, keys.p, idx.p, M, Dk, dout, s);
   }
   if (host_out) FMI_CK(cudaMemcpyAsync(out, dout, (size_t)M * sizeof(double), cudaMemcpyDeviceToHost, s));
   FMI_CK(cudaStreamSynchronize(s));
@@ -841,6 +842,33 @@ int guard(F&& fn) {
 // ------------------------------------------------------------------------------------------------
 // C ABI
 // ------------------------------------------------------------------------------------------------
+// ---- tree files (SPEC FMT1-like record layout) ------------------------------------------
+namespace {
+constexpr char kMagic[8] = {'F', 'M', 'I', 'T', 'R', 'E', 'E', '1'};
+constexpr int32_t kFileVersion = 1;
+struct FileHeader {
+  char magic[8];
+  int32_t version, p, depth_max, unit;
+  int64_t nodes, N;
+  double lo[3], width, tau;
+  int32_t D, pad;
+};
+template <typename T>
+void dump(FILE* fp, const T* dev, int64_t n, cudaStream_t s) {
+  std::vector<T> h((size_t)n);
+  if (n) FMI_CK(cudaMemcpyAsync(h.data(), dev, (size_t)n * sizeof(T), cudaMemcpyDeviceToHost, s));
+  FMI_CK(cudaStreamSynchronize(s));
+  if (n && fwrite(h.data(), sizeof(T), (size_t)n, fp) != (size_t)n) fail(FMI_EINPUT, "short write");
+}
+template <typename T>
+void undump(FILE* fp, T* dev, int64_t n, cudaStream_t s) {
+  std::vector<T> h((size_t)n);
+  if (n && fread(h.data(), sizeof(T), (size_t)n, fp) != (size_t)n) fail(FMI_EVERSION, "truncated tree file");
+  if (n) FMI_CK(cudaMemcpyAsync(dev, h.data(), (size_t)n * sizeof(T), cudaMemcpyHostToDevice, s));
+  FMI_CK(cudaStreamSynchronize(s));
+}
+}  // namespace
+
 extern "C" {
 
 fmi_tree* fmi_build(const double* pts, const double* f, int64_t N, int degree, double tol, int max_depth) {
@@ -960,6 +988,140 @@ int fmi_eval(const fmi_tree* tree, const double* q, int64_t M, double* out) {
   return guard([&] { return eval_impl(tree, q, M, out); });
 }
 
+int fmi_transfer(const double* pts, const double* f, int64_t N, const double* q, int64_t M, double* out, int degree,
+                 double tol, int max_depth) {
+  return guard([&] {
+    fmi_tree* T = build_impl(pts, f, N, degree, tol, max_depth, nullptr);
+    int rc = 0;
+    try {
+      rc = eval_impl(T, q, M, out);
+    } catch (...) {
+      fmi_free(T);
+      throw;
+    }
+    fmi_free(T);
+    return rc;
+  });
+}
+
+
+int fmi_save(const fmi_tree* T, const char* path) {
+  return guard([&] {
+    if (!T || !path) fail(FMI_EINPUT, "null argument");
+    FILE* fp = fopen(path, "wb");
+    if (!fp) fail(FMI_EINPUT, std::string("cannot open ") + path);
+    try {
+      FileHeader h{};
+      std::memcpy(h.magic, kMagic, 8);
+      h.version = kFileVersion;
+      h.p = T->p;
+      h.depth_max = T->depth_max;
+      h.unit = T->unit;
+      h.nodes = T->nodes;
+      h.N = T->Ntot;
+      for (int a = 0; a < 3; ++a) h.lo[a] = T->lo[a];
+      h.width = T->width;
+      h.tau = T->tau;
+      h.D = T->D;
+      if (fwrite(&h, sizeof h, 1, fp) != 1) fail(FMI_EINPUT, "short write");
+      const int64_t n = T->nodes, L = T->L;
+      cudaStream_t s = tl_stream;
+      dump(fp, T->nt.cell, n, s);
+      dump(fp, T->nt.parent, n, s);
+      dump(fp, T->nt.child, n * 8, s);
+      dump(fp, T->nt.child_n, n * 8, s);
+      dump(fp, T->nt.child_ss, n * 8, s);
+      dump(fp, T->nt.coef, n * L, s);
+      dump(fp, T->nt.pcoef, n * L, s);
+      dump(fp, T->nt.rms, n, s);
+      dump(fp, T->nt.minpiv, n, s);
+      dump(fp, T->nt.rank, n, s);
+      dump(fp, T->nt.flag, n, s);
+    } catch (...) {
+      fclose(fp);
+      throw;
+    }
+    fclose(fp);
+    return 0;
+  });
+}
+
+fmi_tree* fmi_load(const char* path) {
+  fmi_tree* out = nullptr;
+  guard([&] {
+    if (!path) fail(FMI_EINPUT, "null path");
+    require_device();
+    FILE* fp = fopen(path, "rb");
+    if (!fp) fail(FMI_EINPUT, std::string("cannot open ") + path);
+    fmi_tree* T = nullptr;
+    cudaStream_t s = tl_stream;
+    try {
+      FileHeader h{};
+      if (fread(&h, sizeof h, 1, fp) != 1 || std::memcmp(h.magic, kMagic, 8) != 0)
+        fail(FMI_EVERSION, "not an fmi tree file");
+      if (h.version != kFileVersion) fail(FMI_EVERSION, "unsupported tree file version");
+      if (h.p < 0 || h.p > FMI_MAX_DEGREE || h.nodes < 1 || h.depth_max < 0 || h.depth_max > FMI_MAX_DEPTH)
+        fail(FMI_EVERSION, "corrupt tree file header");
+      T = new fmi_tree();
+      T->p = h.p;
+      T->L = rank3(h.p);
+      T->K = rank3(2 * h.p);
+      T->D = h.D;
+      T->Dk = h.D + 1;
+      T->depth_max = h.depth_max;
+      T->unit = h.unit != 0;
+      T->N = 0;  // no fit points: fmi_residual is unavailable
+      T->Ntot = h.N;
+      for (int a = 0; a < 3; ++a) T->lo[a] = h.lo[a];
+      T->width = h.width;
+      T->tau = h.tau;
+      T->stream = s;
+      ensure_table(T->nt, T->cap, h.nodes, T->L, true, s);
+      T->nodes = h.nodes;
+      const int64_t n = h.nodes, L = T->L;
+      undump(fp, T->nt.cell, n, s);
+      undump(fp, T->nt.parent, n, s);
+      undump(fp, T->nt.child, n * 8, s);
+      undump(fp, T->nt.child_n, n * 8, s);
+      undump(fp, T->nt.child_ss, n * 8, s);
+      undump(fp, T->nt.coef, n * L, s);
+      undump(fp, T->nt.pcoef, n * L, s);
+      undump(fp, T->nt.rms, n, s);
+      undump(fp, T->nt.minpiv, n, s);
+      undump(fp, T->nt.rank, n, s);
+      undump(fp, T->nt.flag, n, s);
+      // level bookkeeping from the (canonical, level-contiguous) depths
+      std::vector<int4> cell((size_t)n);
+      FMI_CK(cudaMemcpy(cell.data(), T->nt.cell, (size_t)n * sizeof(int4), cudaMemcpyDeviceToHost));
+      for (int64_t i = 0; i < n; ++i) {
+        const int d = cell[i].w;
+        if (d >= (int)T->lvl_first.size()) {
+          T->lvl_first.push_back(i);
+          T->lvl_count.push_back(0);
+          T->lvl_points.push_back(0);
+        }
+        T->lvl_count[d]++;
+      }
+      // start/end are not stored (no fit points); zero them for the export
+      FMI_CK(cudaMemsetAsync(T->nt.start, 0, (size_t)n * 8, s));
+      FMI_CK(cudaMemsetAsync(T->nt.end, 0, (size_t)n * 8, s));
+      FMI_CK(cudaMemsetAsync(T->nt.child_start, 0, (size_t)n * 9 * 8, s));
+      FMI_CK(cudaStreamSynchronize(s));
+    } catch (...) {
+      fclose(fp);
+      if (T) {
+        free_table(T->nt, s);
+        delete T;
+      }
+      throw;
+    }
+    fclose(fp);
+    out = T;
+    return 0;
+  });
+  return out;
+}
+
 void fmi_free(fmi_tree* T) {
   if (!T) return;
   cudaStream_t s = tl_stream;
@@ -1067,6 +1229,7 @@ int fmi_root_cube(const fmi_tree* T, double* lo3, double* width) {
 int fmi_residual(const fmi_tree* T, double* out) {
   return guard([&] {
     if (!T || !out) fail(FMI_EINPUT, "null argument");
+    if (!T->residual) fail(FMI_EINPUT, "the tree has no fit points (loaded from a file)");
     cudaStream_t s = tl_stream;
     DBuf<double> tmp;
     double* d = out;

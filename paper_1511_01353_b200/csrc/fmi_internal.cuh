@@ -261,8 +261,9 @@ constexpr double kQrFlagPivot2 = 1e-9;
 // eval.cu
 // eval.cu: pcoef of the nodes [first, first+count) of one level (parents' pcoef must be final)
 template <int P> void presum_level(const NodeTable& nt, int64_t first, int64_t count, cudaStream_t s);
-template <int P> void eval_sorted(const double* q, const uint64_t* keys, const uint32_t* idx, int64_t M,
-                                  const double lo[3], double width, bool unit, int Dk, const NodeTable& nt,
+// qpk (optional): the queries' root-cube coordinates as 32-byte records (from morton_keys)
+template <int P> void eval_sorted(const double* q, const double4* qpk, const uint64_t* keys, const uint32_t* idx,
+                                  int64_t M, const double lo[3], double width, bool unit, int Dk, const NodeTable& nt,
                                   double* out, cudaStream_t s);
 
 }  // namespace fmi

@@ -109,7 +109,7 @@ __global__ void __launch_bounds__(256) k_keys(const double* __restrict__ pts, in
   uint64_t k = spread3(quantize(ux, D)) | (spread3(quantize(uy, D)) << 1) | (spread3(quantize(uz, D)) << 2);
   keys[i] = k;
   idx[i] = (uint32_t)i;
-  if (packed) packed[i] = make_double4(ux, uy, uz, f[i]);
+  if (packed) packed[i] = make_double4(ux, uy, uz, f ? f[i] : 0.0);
 }
 
 // ------------------------------------------------------------------------------------------------

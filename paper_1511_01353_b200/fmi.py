@@ -31,7 +31,8 @@ EXPORTED = (
     "fmi_build", "fmi_eval", "fmi_free", "fmi_last_error", "fmi_set_stream", "fmi_node_count", "fmi_rank",
     "fmi_export_nodes", "fmi_root_cube", "fmi_residual", "fmi_level_stats", "fmi_profile_enable",
     "fmi_profile_reset", "fmi_profile_get", "fmi_launch_count", "fmi_build_stats", "fmi_build_dist",
-    "fmi_dist_xbuf_bytes", "fmi_bbox", "fmi_cell_counts", "fmi_partition", "fmi_scatter",
+    "fmi_dist_xbuf_bytes", "fmi_bbox", "fmi_cell_counts", "fmi_partition", "fmi_scatter", "fmi_transfer",
+    "fmi_save", "fmi_load",
 )
 
 # allreduce(ctx, n, dtype) -> int: in-place SUM of the first n elements of the exchange buffer
@@ -121,6 +122,12 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.fmi_partition.argtypes = [VP, VP, I64, P(D), D, I32, VP, I32, VP, VP, VP, VP]
     lib.fmi_scatter.restype = I32
     lib.fmi_scatter.argtypes = [VP, VP, I64, VP]
+    lib.fmi_transfer.restype = I32
+    lib.fmi_transfer.argtypes = [VP, VP, I64, VP, I64, VP, I32, D, I32]
+    lib.fmi_save.restype = I32
+    lib.fmi_save.argtypes = [VP, ctypes.c_char_p]
+    lib.fmi_load.restype = VP
+    lib.fmi_load.argtypes = [ctypes.c_char_p]
     lib.fmi_build_stats.restype = I32
     lib.fmi_build_stats.argtypes = [VP, P(I64), I32]
     lib.fmi_launch_count.restype = I64
@@ -276,6 +283,12 @@ class Tree:
             _raise_last(rc)
         return out
 
+    def save(self, path: str) -> None:
+        """Write the tree to a file (fmi_save)."""
+        rc = load_library().fmi_save(ctypes.c_void_p(self.handle), str(path).encode())
+        if rc != 0:
+            _raise_last(rc)
+
     def level_stats(self):
         lib = load_library()
         nodes = (ctypes.c_int64 * 64)()
@@ -303,6 +316,37 @@ def build(pts, f, degree: int, tol: float, max_depth: int) -> Tree:
     if not h:
         _raise_last()
     return Tree(h, n, degree, tol, max_depth)
+
+
+def transfer(pts, f, q, degree: int, tol: float, max_depth: int, out=None):
+    """Mesh-to-mesh transfer f_p -> f_q (fmi_transfer): build over (pts, f), evaluate at q, free."""
+    lib = load_library()
+    pp, n, pk = _ptr(pts, 3, "pts")
+    fp, nf, fk = _ptr(f, None, "f")
+    qp, m, qk = _ptr(q, 3, "q")
+    if nf != n:
+        raise ValueError("pts and f disagree in length")
+    if out is None:
+        if hasattr(q, "is_cuda"):
+            import torch
+            out = torch.empty(m, dtype=torch.float64, device=q.device)
+        else:
+            out = np.empty(m, dtype=np.float64)
+    op, mo, ok = _ptr(out, None, "out")
+    rc = lib.fmi_transfer(pp, fp, n, qp, m, op, int(degree), float(tol), int(max_depth))
+    if rc != 0:
+        _raise_last(rc)
+    return out
+
+
+def load(path: str) -> Tree:
+    """A tree saved with Tree.save (fmi_load)."""
+    lib = load_library()
+    h = lib.fmi_load(str(path).encode())
+    if not h:
+        _raise_last()
+    t = Tree(h, 0, None, None, None)
+    return t
 
 
 def build_dist(pts, f, degree: int, tol: float, max_depth: int, dist: FmiDist) -> Tree:

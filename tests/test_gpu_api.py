@@ -1,0 +1,52 @@
+"""The remaining public calls on a GPU: mesh-to-mesh transfer (fmi_transfer) and tree
+files (fmi_save / fmi_load): a loaded tree evaluates bit-identically and exports the same nodes."""
+import numpy as np
+import pytest
+
+import workloads
+from oracle import fmt_oracle as fo
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+def test_transfer_matches_build_eval_and_oracle():
+    import paper_1511_01353_b200 as fmi
+    from paper_1511_01353_b200 import fmi as f_
+    cfg = workloads.CONFIGS[1]
+    pts, f, q = workloads.make_inputs(cfg)
+    got = f_.transfer(pts, f, q, cfg.degree, cfg.tol, cfg.max_depth)
+    with fmi.build(pts, f, cfg.degree, cfg.tol, cfg.max_depth) as t:
+        ref = t.eval(q)
+    assert np.array_equal(got, ref)
+    ora = fo.evaluate(fo.build(pts, f, cfg.degree, cfg.tol, cfg.max_depth), q)
+    assert np.max(np.abs(got - ora)) <= 1e-9 * np.max(np.abs(f))
+
+
+def test_save_load_roundtrip(tmp_path):
+    import paper_1511_01353_b200 as fmi
+    from paper_1511_01353_b200 import fmi as f_
+    cfg = workloads.CONFIGS[2]
+    pts, f, q = workloads.make_inputs(cfg)
+    q = q[:50_000]
+    path = tmp_path / "tree.fmi"
+    with fmi.build(pts, f, cfg.degree, cfg.tol, cfg.max_depth) as t:
+        v1 = t.eval(q)
+        e1 = t.export()
+        t.save(str(path))
+    t2 = f_.load(str(path))
+    try:
+        v2 = t2.eval(q)
+        e2 = t2.export()
+        assert np.array_equal(v1, v2)
+        for k in ("depth", "cell", "n_points", "child_count", "child", "coeffs", "residual_rms", "rank"):
+            assert np.array_equal(e1[k], e2[k]), k
+        with pytest.raises(f_.FmiError):
+            t2.residual()
+    finally:
+        t2.free()
+    bad = tmp_path / "bad.fmi"
+    bad.write_bytes(b"not a tree file at all")
+    with pytest.raises(f_.FmiError) as ei:
+        f_.load(str(bad))
+    assert ei.value.code == f_.FMI_EVERSION
