@@ -90,23 +90,22 @@ __global__ void __launch_bounds__(PS_THREADS) k_presum(NodeTable nt, int64_t fir
   for (int e = tid; e < L; e += PS_THREADS) nt.pcoef[node * L + e] = b1[e] + nt.coef[node * L + e];
 }
 
-// One query per thread.  Sorted queries make the deepest node warp-uniform almost everywhere: the warp
-// then stages that node's pre-summed coefficients in shared memory once (coalesced) and every lane
-// reads them as broadcasts; otherwise each lane reads its node's coefficients through L1.
+// Two sorted queries per thread: warp w of a CTA takes 64 consecutive queries (lane l: base + l and
+// base + 32 + l).  Sorted queries make the deepest node warp-uniform almost everywhere: the warp then
+// stages that node's pre-summed coefficients in shared memory once (coalesced) and every lane
+// evaluates its two queries with one coefficient read per two FMAs (horner3x2); otherwise each query
+// reads its own node's coefficients through L1.
 template <int P>
-__global__ void __launch_bounds__(256) k_eval(const double* __restrict__ q, const double4* __restrict__ qpk,
-                                              const uint64_t* __restrict__ keys, const uint32_t* __restrict__ idx,
-                                              int64_t M, double lo0, double lo1, double lo2, double w, bool unit,
-                                              int Dk, NodeTable nt, double* __restrict__ out) {
-  constexpr int L = rank3(P);
-  __shared__ double cs[256 / 32][L];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const bool active = i < M;
-  const int64_t qi = !active ? 0 : (idx ? (int64_t)idx[i] : i);
+__device__ __forceinline__ void eval_locate(const double* __restrict__ q, const double4* __restrict__ qpk,
+                                            const uint64_t* __restrict__ keys, const uint32_t* __restrict__ idx,
+                                            int64_t i, int64_t M, double lo0, double lo1, double lo2, double w,
+                                            bool unit, int Dk, const NodeTable& nt, int64_t& qi, int64_t& node,
+                                            double& x, double& y, double& z) {
+  qi = 0;
+  node = 0;
   double ux = 0.0, uy = 0.0, uz = 0.0;
-  int64_t node = 0;
-  if (active) {
+  if (i < M) {
+    qi = idx ? (int64_t)idx[i] : i;
     if (qpk) {  // root-cube coordinates written by the key kernel: one 32-byte record per query
       const double2* p = reinterpret_cast<const double2*>(qpk + qi);
       const double2 a = __ldg(p), b = __ldg(p + 1);
@@ -128,25 +127,45 @@ __global__ void __launch_bounds__(256) k_eval(const double* __restrict__ q, cons
       }
     }
   }
-  const int64_t node0 = __shfl_sync(0xffffffffu, node, 0);
-  const bool uniform = __all_sync(0xffffffffu, !active || node == node0);
-  double v;
   const Frame fr = node_frame(nt.cell[node]);
-  const double x = __dmul_rn(__dsub_rn(ux, fr.cx), fr.scale);
-  const double y = __dmul_rn(__dsub_rn(uy, fr.cy), fr.scale);
-  const double z = __dmul_rn(__dsub_rn(uz, fr.cz), fr.scale);
+  x = __dmul_rn(__dsub_rn(ux, fr.cx), fr.scale);
+  y = __dmul_rn(__dsub_rn(uy, fr.cy), fr.scale);
+  z = __dmul_rn(__dsub_rn(uz, fr.cz), fr.scale);
+}
+
+template <int P>
+__global__ void __launch_bounds__(256) k_eval(const double* __restrict__ q, const double4* __restrict__ qpk,
+                                              const uint64_t* __restrict__ keys, const uint32_t* __restrict__ idx,
+                                              int64_t M, double lo0, double lo1, double lo2, double w, bool unit,
+                                              int Dk, NodeTable nt, double* __restrict__ out) {
+  constexpr int L = rank3(P);
+  __shared__ double cs[256 / 32][L];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t base = ((int64_t)blockIdx.x * 8 + warp) * 64;
+  const int64_t i0 = base + lane, i1 = base + 32 + lane;
+  int64_t qi0, qi1, n0, n1;
+  double x0, y0, z0, x1, y1, z1;
+  eval_locate<P>(q, qpk, keys, idx, i0, M, lo0, lo1, lo2, w, unit, Dk, nt, qi0, n0, x0, y0, z0);
+  eval_locate<P>(q, qpk, keys, idx, i1, M, lo0, lo1, lo2, w, unit, Dk, nt, qi1, n1, x1, y1, z1);
+  const int64_t node0 = __shfl_sync(0xffffffffu, n0, 0);
+  const bool uniform = __all_sync(0xffffffffu, (i0 >= M || n0 == node0) && (i1 >= M || n1 == node0));
+  double v0, v1;
   if (uniform) {
     const double* a = nt.pcoef + node0 * L;
     for (int k = lane; k < L; k += 32) cs[warp][k] = __ldg(a + k);
     __syncwarp();
     const SmemCoef coef(cs[warp]);
-    v = horner3<P>(coef, x, y, z);
+    horner3x2<P>(coef, x0, y0, z0, x1, y1, z1, v0, v1);
   } else {
-    const double* a = nt.pcoef + node * L;
-    auto coef = [&](int k) { return __ldg(a + k); };
-    v = horner3<P>(coef, x, y, z);
+    const double* a0 = nt.pcoef + n0 * L;
+    const double* a1 = nt.pcoef + n1 * L;
+    auto c0 = [&](int k) { return __ldg(a0 + k); };
+    auto c1 = [&](int k) { return __ldg(a1 + k); };
+    v0 = horner3<P>(c0, x0, y0, z0);
+    v1 = horner3<P>(c1, x1, y1, z1);
   }
-  if (active) out[qi] = v;
+  if (i0 < M) out[qi0] = v0;
+  if (i1 < M) out[qi1] = v1;
 }
 
 }  // namespace
@@ -162,7 +181,7 @@ void eval_sorted(const double* q, const double4* qpk, const uint64_t* keys, cons
                  const double lo[3], double width, bool unit, int Dk, const NodeTable& nt, double* out,
                  cudaStream_t s) {
   if (M <= 0) return;
-  FMI_LAUNCH(KID_EVAL, s, k_eval<P>, (unsigned)((M + 255) / 256), 256, 0, q, qpk, keys, idx, M, lo[0], lo[1], lo[2],
+  FMI_LAUNCH(KID_EVAL, s, k_eval<P>, (unsigned)((M + 511) / 512), 256, 0, q, qpk, keys, idx, M, lo[0], lo[1], lo[2],
              width, unit, Dk, nt, out);
 }
 
