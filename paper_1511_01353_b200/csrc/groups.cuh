@@ -78,20 +78,22 @@ __device__ __forceinline__ double cpow(double x) {
   else return x * cpow<E - 1>(x);
 }
 
-// pairs q..q1-1 of a group: acc[pair_first(q) - o0 + c] += v z^c, v = x^a y^b w (running)
+// pairs q..q1-1 of a group: acc[pair_first(q) - o0 + c] += v z^c with v = x^a y^b w, advanced by ONE
+// multiply per pair (v·y within a row of equal a; xw·x, the row start, at a new a)
 template <int Q, int q, int q1, int o0>
-__device__ __forceinline__ void pairs(double x, double y, const double* zp, double xw, double yb, double* acc) {
+__device__ __forceinline__ void pairs(double x, double y, const double* zp, double xw, double v, double* acc) {
   if constexpr (q < q1) {
     constexpr int base = pair_first(Q, q) - o0;
     constexpr int n = pair_out(Q, q);
-    const double v = xw * yb;
 #pragma unroll
     for (int c = 0; c < n; ++c) acc[base + c] = fma(v, zp[c], acc[base + c]);
     if constexpr (q + 1 < q1) {
-      if constexpr (pair_a(Q, q + 1) == pair_a(Q, q))
-        pairs<Q, q + 1, q1, o0>(x, y, zp, xw, yb * y, acc);
-      else
-        pairs<Q, q + 1, q1, o0>(x, y, zp, xw * x, 1.0, acc);
+      if constexpr (pair_a(Q, q + 1) == pair_a(Q, q)) {
+        pairs<Q, q + 1, q1, o0>(x, y, zp, xw, v * y, acc);
+      } else {
+        const double xn = xw * x;
+        pairs<Q, q + 1, q1, o0>(x, y, zp, xn, xn, acc);
+      }
     }
   }
 }
@@ -110,8 +112,7 @@ __device__ __forceinline__ void accum(double x, double y, double z, double w, do
 #pragma unroll
     for (int c = 2; c <= CM; ++c) zp[c] = zp[c / 2] * zp[c - c / 2];
     const double xw = cpow<pair_a(Q, q0)>(x) * w;
-    const double yb = cpow<pair_b(Q, q0)>(y);
-    pairs<Q, q0, q1, o0>(x, y, zp, xw, yb, acc);
+    pairs<Q, q0, q1, o0>(x, y, zp, xw, xw * cpow<pair_b(Q, q0)>(y), acc);
   }
 }
 
@@ -132,7 +133,7 @@ struct Prep {
 #pragma unroll
     for (int c = 2; c <= CM; ++c) zp[c] = zp[c / 2] * zp[c - c / 2];
     xw = cpow<pair_a(Q, q0)>(x) * w;
-    yb = cpow<pair_b(Q, q0)>(y);
+    yb = xw * cpow<pair_b(Q, q0)>(y);  // first pair's x^a y^b w
   }
   __device__ __forceinline__ void apply(double* acc) const {
     if constexpr (q0 < q1) pairs<Q, q0, q1, o0>(x, y, zp, xw, yb, acc);

@@ -79,21 +79,23 @@ __host__ __device__ constexpr int group_cmax(int P, int g) {  // highest z power
   return smin > P ? 0 : P - smin;
 }
 
-// pair q of a group: acc[pair_first(q) - o0 + c] += (x^a y^b r) z^c, c = 0..P-a-b; then advance the
-// running x^a r / y^b to pair q+1 (compile-time recursion: every index is a constant)
+// pair q of a group: acc[pair_first(q) - o0 + c] += v z^c, c = 0..P-a-b, v = x^a y^b r; then advance
+// v to pair q+1 with one multiply (v·y in a row of equal a, the row start x^(a+1) r at a new a)
+// (compile-time recursion: every index is a constant)
 template <int P, int q, int q1, int o0>
-__device__ __forceinline__ void proj_pairs(double x, double y, const double* zp, double xr, double yb, double* acc) {
+__device__ __forceinline__ void proj_pairs(double x, double y, const double* zp, double xr, double v, double* acc) {
   if constexpr (q < q1) {
     constexpr int base = pair_first(P, q) - o0;
     constexpr int n = pair_out(P, q);
-    const double v = xr * yb;
 #pragma unroll
     for (int c = 0; c < n; ++c) acc[base + c] = fma(v, zp[c], acc[base + c]);
     if constexpr (q + 1 < q1) {
-      if constexpr (pair_a(P, q + 1) == pair_a(P, q))
-        proj_pairs<P, q + 1, q1, o0>(x, y, zp, xr, yb * y, acc);
-      else
-        proj_pairs<P, q + 1, q1, o0>(x, y, zp, xr * x, 1.0, acc);
+      if constexpr (pair_a(P, q + 1) == pair_a(P, q)) {
+        proj_pairs<P, q + 1, q1, o0>(x, y, zp, xr, v * y, acc);
+      } else {
+        const double xn = xr * x;
+        proj_pairs<P, q + 1, q1, o0>(x, y, zp, xn, xn, acc);
+      }
     }
   }
 }
@@ -112,10 +114,10 @@ __device__ __forceinline__ void proj_accum(double x, double y, double z, double 
     double xr = r;
 #pragma unroll
     for (int e = 0; e < pair_a(P, q0); ++e) xr *= x;
-    double yb = 1.0;
+    double v = xr;
 #pragma unroll
-    for (int e = 0; e < pair_b(P, q0); ++e) yb *= y;
-    proj_pairs<P, q0, q1, o0>(x, y, zp, xr, yb, acc);
+    for (int e = 0; e < pair_b(P, q0); ++e) v *= y;
+    proj_pairs<P, q0, q1, o0>(x, y, zp, xr, v, acc);
   }
 }
 
