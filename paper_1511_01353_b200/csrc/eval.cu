@@ -139,7 +139,8 @@ __global__ void __launch_bounds__(256) k_eval(const double* __restrict__ q, cons
                                               int64_t M, double lo0, double lo1, double lo2, double w, bool unit,
                                               int Dk, NodeTable nt, double* __restrict__ out) {
   constexpr int L = rank3(P);
-  __shared__ double cs[256 / 32][L];
+  constexpr int LA = (L + 1) & ~1;  // 16-byte aligned rows for pair loads
+  __shared__ __align__(16) double cs[256 / 32][LA];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t base = ((int64_t)blockIdx.x * 8 + warp) * 64;
   const int64_t i0 = base + lane, i1 = base + 32 + lane;

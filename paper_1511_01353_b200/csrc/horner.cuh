@@ -30,6 +30,26 @@ __device__ __forceinline__ double horner3(const Coef& coef, double x, double y, 
   return px;
 }
 
+// Loads coefficients i0 .. i0+n-1 into cr[]: 16-byte pair loads at even indices (one shared-memory
+// wavefront per two coefficients when every lane reads the same address), if the reader offers them.
+template <int P, typename Coef>
+__device__ __forceinline__ void load_row(const Coef& coef, int i0, int n, double* cr) {
+  if constexpr (Coef::kPairs) {
+    int k = 0;
+    if (i0 & 1) { cr[0] = coef(i0); k = 1; }
+#pragma unroll
+    for (; k + 1 < n; k += 2) {
+      const double2 v = coef.pair(i0 + k);
+      cr[k] = v.x;
+      cr[k + 1] = v.y;
+    }
+    if (k < n) cr[k] = coef(i0 + k);
+  } else {
+#pragma unroll
+    for (int k = 0; k < n; ++k) cr[k] = coef(i0 + k);
+  }
+}
+
 // Two points per call: every coefficient load feeds two FMAs; each row's loads are issued back to back.
 template <int P, typename Coef>
 __device__ __forceinline__ void horner3x2(const Coef& coef, double x0, double y0, double z0, double x1, double y1,
@@ -41,8 +61,7 @@ __device__ __forceinline__ void horner3x2(const Coef& coef, double x0, double y0
 #pragma unroll
     for (int m = P - l; m >= 0; --m) {
       double cr[P + 1];
-#pragma unroll
-      for (int n = 0; n <= P - l - m; ++n) cr[n] = coef(basis_index(P, l, m, n));
+      load_row<P>(coef, basis_index(P, l, m, 0), P - l - m + 1, cr);
       double pz0 = 0.0, pz1 = 0.0;
 #pragma unroll
       for (int n = P - l - m; n >= 0; --n) {
@@ -89,12 +108,18 @@ __device__ __forceinline__ void horner3x4(const Coef& coef, const double* x, con
 // Shared-memory coefficient reader that the compiler cannot hoist out of a point loop (a hoisted
 // copy of 𝓛 = 286 coefficients would not fit in registers).
 struct SmemCoef {
+  static constexpr bool kPairs = true;  // coefficient 0 must be 16-byte aligned
   uint32_t base;  // shared-window address of coefficient 0
   __device__ __forceinline__ explicit SmemCoef(const double* p)
       : base((uint32_t)__cvta_generic_to_shared(p)) {}
   __device__ __forceinline__ double operator()(int i) const {
     double v;
     asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(base + 8u * (uint32_t)i));
+    return v;
+  }
+  __device__ __forceinline__ double2 pair(int i) const {  // i even
+    double2 v;
+    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(base + 8u * (uint32_t)i));
     return v;
   }
 };

@@ -142,7 +142,7 @@ __global__ void __launch_bounds__(K6_THREADS, 2)
   constexpr int G = proj_groups(P);
   constexpr int SUB = K6_WARPS / G;  // warps per output group (split the batch's points)
   constexpr int MG = max_group(P);
-  __shared__ double sa[L];
+  __shared__ __align__(16) double sa[L];
   __shared__ double sbuf[4 * K6_BATCH];  // batch coordinates in the child frame + residuals
   double* sx = sbuf;
   double* sy = sbuf + K6_BATCH;

@@ -55,13 +55,15 @@ struct K5Shape {
   static constexpr int K = rank3(Q);
   static constexpr int L = rank3(P);
   static constexpr int64_t NAB = tri(L) + L;  // packed lower factor + RHS row
-  static constexpr int LDP = (L + 1 + 3) & ~3;  // panel column stride (rows padded to 4: 16-byte vectors)
-  // shared: moments [K], dinv, piv, y/c [L], column-major panel [KB x LDP], exponents
-  static constexpr size_t SMEM = ((size_t)K + 3 * L + (size_t)KB * LDP + 8) * sizeof(double) + 3 * L + 16;
+  // panel column stride: rows padded to 4 (16-byte vectors of 4 rows), and not a multiple of 16 so that
+  // consecutive columns of one row fall in different banks
+  static constexpr int LDP = ((L + 1 + 3) & ~3) % 16 == 0 ? ((L + 1 + 3) & ~3) + 2 : ((L + 1 + 3) & ~3);
+  // shared: moments [K], dinv, piv, 1/piv, y/c [L], column-major panel [KB x LDP], exponents
+  static constexpr size_t SMEM = ((size_t)K + 4 * L + (size_t)KB * LDP + 8) * sizeof(double) + 3 * L + 16;
 };
 
 template <int P>
-__global__ void __launch_bounds__(k5_threads<P>())
+__global__ void __launch_bounds__(k5_threads<P>(), k5_threads<P>() == 256 ? 2 : 3)
     k_solve(const double* __restrict__ mom, int mode, const double* __restrict__ segrhs, double* __restrict__ delta,
             NodeTable nt, int64_t first, int64_t count, double* __restrict__ fac,
             const __grid_constant__ BasisTab bt, double delta2, double refine2, double refine_fill,
@@ -73,7 +75,8 @@ __global__ void __launch_bounds__(k5_threads<P>())
   double* sM = sm;          // [K]
   double* dinv = sM + K;    // [L]
   double* piv = dinv + L;   // [L]
-  double* sy = piv + L;     // [L]  b̃ -> y -> c̃
+  double* pinv = piv + L;   // [L]  1/piv (0 for rejected columns)
+  double* sy = pinv + L;    // [L]  b̃ -> y -> c̃
   constexpr int LDP = S::LDP;
   // column-major panel, 16-byte aligned: Pn[c * LDP + r] = row j0 + r, column j0 + c
   double* Pn = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(sy + L) + 15) & ~uintptr_t(15));
@@ -82,7 +85,7 @@ __global__ void __launch_bounds__(k5_threads<P>())
   uint8_t* bn = bm + L;
   __shared__ double smin_sh;
   __shared__ double errw[K5_WARPS];
-  __shared__ double sc[KB];  // scaled column entries of the panel's diagonal-block rows
+  __shared__ double sinv[KB];  // inverse pivots of the current panel
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   for (int i = tid; i < L; i += K5_THREADS) { bl[i] = bt.l[i]; bm[i] = bt.m[i]; bn[i] = bt.n[i]; }
   __syncthreads();
@@ -122,7 +125,10 @@ __global__ void __launch_bounds__(k5_threads<P>())
 
     if (mode == 1) {
       // ---- refinement: forward substitution with the stored factor (blocked, rows contiguous) -----
-      for (int i = tid; i < L; i += K5_THREADS) piv[i] = A[tri(i) + i];
+      for (int i = tid; i < L; i += K5_THREADS) {
+        piv[i] = A[tri(i) + i];
+        pinv[i] = piv[i] > 0.0 ? 1.0 / piv[i] : 0.0;
+      }
       __syncthreads();
       for (int j0 = 0; j0 < L; j0 += KB) {
         const int j1 = min(j0 + KB, L);
@@ -152,19 +158,20 @@ __global__ void __launch_bounds__(k5_threads<P>())
     } else {
       // ---- assemble the equilibrated Gram + RHS row and check the moments' rounding bound -------
       double errl = 0.0;
-      for (int64_t e = tid; e < S::NAB; e += K5_THREADS) {
-        if (e >= tri(L)) {  // RHS row
-          A[e] = sy[e - tri(L)];
+      for (int i = warp; i <= L; i += K5_WARPS) {  // warp per packed row; row L = RHS
+        double* Ai = A + tri(i);
+        if (i == L) {
+          for (int k = lane; k < L; k += 32) Ai[k] = sy[k];
           continue;
         }
-        int i = (int)((sqrt(8.0 * (double)e + 1.0) - 1.0) * 0.5);
-        while (tri(i + 1) <= e) ++i;
-        while (tri(i) > e) --i;
-        const int k = (int)(e - tri(i));
-        const int gi = basis_index(Q, bl[i] + bl[k], bm[i] + bm[k], bn[i] + bn[k]);
-        const double dd = dinv[i] * dinv[k];
-        A[e] = sM[gi] * dd;
-        if (mode == 0) errl = fmax(errl, bnd[gi] * dd);
+        const int li = bl[i], mi = bm[i], ni = bn[i];
+        const double di = dinv[i];
+        for (int k = lane; k <= i; k += 32) {
+          const int gi = basis_index(Q, li + bl[k], mi + bm[k], ni + bn[k]);
+          const double dd = di * dinv[k];
+          Ai[k] = sM[gi] * dd;
+          if (mode == 0) errl = fmax(errl, bnd[gi] * dd);
+        }
       }
       if (mode == 0) {
 #pragma unroll
@@ -195,38 +202,67 @@ __global__ void __launch_bounds__(k5_threads<P>())
           Pn[c * LDP + r] = (i == L || c <= r) ? A[tri(i) + j0 + c] : 0.0;
         }
         __syncthreads();
-        for (int c = 0; c < bw; ++c) {
-          const int j = j0 + c;
-          double* Pc = Pn + c * LDP;
-          if (warp == 0) {  // pivot (lane 0) and the scaled column entries of the block rows
-            double p = 0.0;
-            if (lane == 0) {
-              const double sjj = Pc[c];
+        // (1) diagonal block: unblocked Cholesky with column rejection by warp 0, lane = row, the row
+        // in registers; column entries travel by shuffles (no shared-memory round trips)
+        if (warp == 0) {
+          double row[KB];
+#pragma unroll
+          for (int c = 0; c < KB; ++c) row[c] = (c <= lane && lane < bw) ? Pn[c * LDP + lane] : 0.0;
+#pragma unroll
+          for (int c = 0; c < KB; ++c) {
+            if (c < bw) {
+              const int j = j0 + c;
+              const double sjj = __shfl_sync(0xffffffffu, row[c], c);
               const bool keep = dinv[j] > 0.0 && sjj > delta2;
-              p = keep ? sqrt(sjj) : 0.0;
-              piv[j] = p;
-              Pc[c] = p;
-              if (dinv[j] > 0.0 && !(sjj >= smin_sh)) smin_sh = sjj;  // also catches NaN
-            }
-            p = __shfl_sync(0xffffffffu, p, 0);
-            const double inv = p > 0.0 ? 1.0 / p : 0.0;
-            const int c2 = c + 1 + lane;
-            if (c2 < bw) sc[c2] = Pc[c2] * inv;
-          }
-          __syncthreads();
-          const double p = piv[j];
-          const double inv = p > 0.0 ? 1.0 / p : 0.0;
-          // thread per row r > c: scale L[r][c] and update the row's remaining panel columns
-          for (int r = c + 1 + tid; r < R; r += K5_THREADS) {
-            const double lrc = Pc[r] * inv;
-            Pc[r] = lrc;
-            if (p > 0.0) {
-              const int cend = (r == R - 1) ? bw : min(bw, r + 1);
-              for (int c2 = c + 1; c2 < cend; ++c2) Pn[c2 * LDP + r] -= lrc * sc[c2];
+              const double p = keep ? sqrt(sjj) : 0.0;
+              const double inv = p > 0.0 ? 1.0 / p : 0.0;
+              if (lane == 0) {
+                piv[j] = p;
+                sinv[c] = inv;
+                pinv[j] = inv;
+                if (dinv[j] > 0.0 && !(sjj >= smin_sh)) smin_sh = sjj;  // also catches NaN
+              }
+              row[c] = lane == c ? p : row[c] * inv;
+              if (p > 0.0) {
+#pragma unroll
+                for (int c2 = c + 1; c2 < KB; ++c2) {
+                  const double l2 = __shfl_sync(0xffffffffu, row[c], c2);  // L[c2][c]
+                  if (lane >= c2) row[c2] -= row[c] * l2;
+                }
+              }
             }
           }
-          __syncthreads();
+          if (lane < bw) {
+#pragma unroll
+            for (int c = 0; c < KB; ++c)
+              if (c <= lane) Pn[c * LDP + lane] = row[c];
+          }
         }
+        __syncthreads();
+        // (2) rows below the diagonal block (RHS row included): L_r = A_r L_diag⁻ᵀ, thread per row,
+        // the row in registers, the same updates in the same order as the unblocked algorithm
+        for (int r = bw + tid; r < R; r += K5_THREADS) {
+          double x[KB];
+#pragma unroll
+          for (int c = 0; c < KB; ++c) x[c] = c < bw ? Pn[c * LDP + r] : 0.0;
+#pragma unroll
+          for (int c = 0; c < KB; ++c) {
+            if (c < bw) {
+              const double inv = sinv[c];
+              const double lc = x[c] * inv;
+              x[c] = lc;
+              if (inv > 0.0) {
+#pragma unroll
+                for (int c2 = c + 1; c2 < KB; ++c2)
+                  if (c2 < bw) x[c2] -= lc * Pn[c * LDP + c2];
+              }
+            }
+          }
+#pragma unroll
+          for (int c = 0; c < KB; ++c)
+            if (c < bw) Pn[c * LDP + r] = x[c];
+        }
+        __syncthreads();
         for (int e = tid; e < R * bw; e += K5_THREADS) {
           const int r = e / bw, c = e % bw;
           const int i = j0 + r;
@@ -297,21 +333,27 @@ __global__ void __launch_bounds__(k5_threads<P>())
         Pn[r * KB + c] = (c <= r) ? A[tri(j0 + r) + j0 + c] : 0.0;
       }
       __syncthreads();
-      if (warp == 0) {  // c_j = (y_j - Σ_{j<i<j1} L[i][j] c_i) / L[j][j]
-        for (int j = j1 - 1; j >= j0; --j) {
-          double v = 0.0;
-          for (int i = j + 1 + lane; i < j1; i += 32) v = fma(Pn[(i - j0) * KB + (j - j0)], sy[i], v);
-#pragma unroll
-          for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-          if (lane == 0) sy[j] = piv[j] > 0.0 ? (sy[j] - v) / piv[j] : 0.0;
-          __syncwarp();
+      if (warp == 0) {  // c_j = (y_j - Σ_{j<i<j1} L[i][j] c_i) / L[j][j]; lane t holds y_t, right-looking
+        double yv = lane < bw ? sy[j0 + lane] : 0.0;
+        const double pl = lane < bw ? pinv[j0 + lane] : 0.0;
+        for (int j = bw - 1; j >= 0; --j) {
+          const double cj = __shfl_sync(0xffffffffu, pl > 0.0 ? yv * pl : 0.0, j);
+          if (lane < j) yv -= Pn[j * KB + lane] * cj;
+          if (lane == j) yv = cj;
         }
+        if (lane < bw) sy[j0 + lane] = yv;
       }
       __syncthreads();
-      // rows above: y_k -= Σ_{i in [j0,j1)} L[i][k] c_i, k < j0 (rows i are contiguous in k)
+      // rows above: y_k -= Σ_{i in [j0,j1)} L[i][k] c_i, k < j0 (rows i are contiguous in k); the
+      // block's loads are issued together (one L2 latency, not bw)
       for (int k = tid; k < j0; k += K5_THREADS) {
+        double a[KB];
+#pragma unroll
+        for (int t = 0; t < KB; ++t) a[t] = t < bw ? A[tri(j0 + t) + k] : 0.0;
         double v = 0.0;
-        for (int i = j0; i < j1; ++i) v = fma(A[tri(i) + k], sy[i], v);
+#pragma unroll
+        for (int t = 0; t < KB; ++t)
+          if (t < bw) v = fma(a[t], sy[j0 + t], v);
         sy[k] -= v;
       }
       __syncthreads();
