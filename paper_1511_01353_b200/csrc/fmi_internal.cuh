@@ -234,9 +234,10 @@ template <int P> void level_residual(const LevelCtx& c, int mode, int iter, cons
                                      const int64_t* nchunks_dev, int64_t max_chunks, const int64_t* chunk_begin,
                                      int64_t nseg, double* partial, double* segsum, cudaStream_t s,
                                      const int32_t* sel = nullptr);
-// child projections of a node are deferred (flag bit 3) when its pre-fit RMS is below kDeferTheta·τ:
-// its children are then unlikely to be created, and the projection pass runs only for those that are
-constexpr double kDeferTheta = 100.0;
+// child projections of a node are deferred (flag bit 3) when its predicted post-fit RMS (pre-fit energy
+// minus the energy the fit removes) is below kDeferTheta·τ: its children are then unlikely to be
+// created, and the projection pass runs only for those that are
+constexpr double kDeferTheta = 1.0;
 // decisions + compaction: writes the next level's nodes at [first+count, ...), returns via dev_out[0] the
 // number of new nodes and dev_out[1] their total points.  geo: moment tree (integer guards only).
 // mt_child/srcseg (fit tree): moment-tree ids and source segments of the new nodes.

@@ -84,6 +84,7 @@ __global__ void __launch_bounds__(k5_threads<P>(), k5_threads<P>() == 256 ? 2 : 
   uint8_t* bm = bl + L;
   uint8_t* bn = bm + L;
   __shared__ double smin_sh;
+  __shared__ double ynorm_sh;
   __shared__ double errw[K5_WARPS];
   __shared__ double sinv[KB];  // inverse pivots of the current panel
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -319,9 +320,22 @@ __global__ void __launch_bounds__(k5_threads<P>(), k5_threads<P>() == 256 ? 2 : 
         }
         __syncthreads();
       }
-      // y = row L of the factored bordered matrix
-      for (int i = tid; i < L; i += K5_THREADS) sy[i] = A[tri(L) + i];
+      // y = row L of the factored bordered matrix; ‖y‖² = bᵀG⁻¹b = the residual energy the fit removes
+      double yy = 0.0;
+      for (int i = tid; i < L; i += K5_THREADS) {
+        const double v = A[tri(L) + i];
+        sy[i] = v;
+        yy = fma(v, v, yy);
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) yy += __shfl_xor_sync(0xffffffffu, yy, o);
+      if (lane == 0) errw[warp] = yy;
       __syncthreads();
+      if (tid == 0) {
+        double t = 0.0;
+        for (int w = 0; w < K5_WARPS; ++w) t += errw[w];
+        ynorm_sh = t;
+      }
     }
 
     // ---- back substitution R̃ c̃ = y (R̃ = factorᵀ), blocked from the bottom ----------------------
@@ -388,13 +402,14 @@ __global__ void __launch_bounds__(k5_threads<P>(), k5_threads<P>() == 256 ? 2 : 
                                   : (double)nt.child_n[(int64_t)par * 8 + ((cc.x & 1) | ((cc.y & 1) << 1) | ((cc.z & 1) << 2))];
       const bool refine = refine2 > 0.0 && (smin_sh < refine2 || npts < refine_fill * L);
       const int fl = (smin_sh < kQrFlagPivot2) ? 1 : (refine ? 2 : 0);
-      // defer this node's child projections when its pre-fit RMS (the parent's octant E_RMS) is below
+      // defer this node's child projections when its predicted post-fit RMS — pre-fit block energy
+      // (the parent's octant Σr²) minus the energy the fit removes (‖y‖²), over its points — is below
       // defer_tau: its children are then unlikely to be created (K6_PROJ runs for those that are)
       int defer = 0;
       if (par >= 0 && defer_tau > 0.0) {
         const int oc = (cc.x & 1) | ((cc.y & 1) << 1) | ((cc.z & 1) << 2);
-        const double e_pre = sqrt(nt.child_ss[(int64_t)par * 8 + oc] / fmax(npts, 1.0));
-        defer = e_pre < defer_tau ? 8 : 0;
+        const double e_post2 = fmax(nt.child_ss[(int64_t)par * 8 + oc] - ynorm_sh, 0.0) / fmax(npts, 1.0);
+        defer = e_post2 < defer_tau * defer_tau ? 8 : 0;
       }
       nt.flag[first + node] = fl | defer;
       if (fl == 2) atomicAdd(reinterpret_cast<unsigned long long*>(nflag), 1ull);

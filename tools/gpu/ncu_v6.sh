@@ -1,0 +1,4 @@
+mkdir -p gpurun_out
+export PYTHONUNBUFFERED=1
+timeout 900 ncu --metrics gpu__time_duration.sum,launch__grid_size --clock-control none -k regex:k_solve --csv --log-file gpurun_out/k5_launches_v6.csv python tools/run_build.py --config 5 --reps 1 > gpurun_out/ncu_k5_v6.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_solve -s 4 -c 1 -o gpurun_out/k5_v6 -f python tools/run_build.py --config 5 --reps 1 > gpurun_out/ncu_k5f_v6.log 2>&1
