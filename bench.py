@@ -155,16 +155,32 @@ def ranks(p: int):
     return K, L
 
 
-def kernel_work(cfg, levels_points, depth_max: int):
+def projected_points(t, L: int, max_depth: int) -> int:
+    """Points whose child-frame projection K6 computes in one build, from the exported tree: blocks of
+    non-deferred nodes that may become children (n_o >= 𝓛, depth+1 <= max_depth; the kernel's guard),
+    plus, for nodes whose projections were deferred (flag bit 3), the children actually created
+    (the K6_PROJ pass)."""
+    ex = t.export()
+    cc, child = ex["child_count"], ex["child"]
+    pot = (cc >= L) & ((ex["depth"] + 1) <= max_depth)[:, None]
+    deferred = (ex["flags"] & 8) != 0
+    proj = np.where(deferred[:, None], np.where(child >= 0, cc, 0), np.where(pot, cc, 0))
+    return int(proj.sum())
+
+
+def kernel_work(cfg, levels_points, depth_max: int, projected=None):
     """Per-step algorithmic work of the main kernels: (unit, amount) — flops or bytes."""
     K, L = ranks(cfg.degree)
     N, M = cfg.n, cfg.m
     pts = [int(x) for x in levels_points]
+    if projected is None:  # every point of every level projected (upper bound)
+        projected = sum(pts)
     return {
         # K4: one FMA per raw moment per point, once per build (owner pass)
         "moments": ("flop", 2 * K * N),
-        # K6 per level: Horner (𝓛 FMA) + child projection (𝓛 FMA) + Σr² (1 FMA) per point
-        "residual": ("flop", sum(n * (4 * L + 2) for n in pts)),
+        # K6 per level: Horner (𝓛 FMA) + Σr² (1 FMA) per point, child projection (𝓛 FMA) per point
+        # of a block that may become a child (deferred blocks: only those that did)
+        "residual": ("flop", sum(n * (2 * L + 2) for n in pts) + 2 * L * projected),
         # K6 root mode: projection of f onto the root frame (𝓛 FMA per point)
         "project": ("flop", 2 * L * N),
         # K7: one Horner of the pre-summed polynomial per query
@@ -176,9 +192,9 @@ def kernel_work(cfg, levels_points, depth_max: int):
     }
 
 
-def rooflines(cfg, levels_points, depth_max, prof, steps, ms_per_step, hbm_peak):
+def rooflines(cfg, levels_points, depth_max, prof, steps, ms_per_step, hbm_peak, projected=None):
     out = {}
-    for name, (unit, work) in kernel_work(cfg, levels_points, depth_max).items():
+    for name, (unit, work) in kernel_work(cfg, levels_points, depth_max, projected).items():
         ms, n = prof.get(name, (0.0, 0))
         if not n or ms <= 0:
             continue
@@ -295,6 +311,7 @@ def main():
         tree = step_device()
     levels_nodes, levels_points = tree_of(tree).level_stats()
     node_count = tree_of(tree).node_count
+    proj_pts = projected_points(tree_of(tree), ranks(cfg.degree)[1], cfg.max_depth)
     shard_depth = getattr(tree, "shard_depth", None)
     tree.free()
 
@@ -337,7 +354,8 @@ def main():
     # stream, inside the timed region); the dominant kernel is the bench line's "roofline"
     pt_levels = int(np.sum(levels_points))
     hbm_peak = measured_hbm_peak()
-    roofs = rooflines(cfg, levels_points, len(levels_points) - 1, prof, args.steps, ms_per_step, hbm_peak)
+    roofs = rooflines(cfg, levels_points, len(levels_points) - 1, prof, args.steps, ms_per_step, hbm_peak,
+                      proj_pts)
     dominant = max(roofs, key=lambda k: roofs[k]["share_of_step"]) if roofs else None
     # DRAM traffic of one launch from an ncu --set full capture (profiles/round1_ncu_kernels_cfg5.txt):
     # k_residual at level 3 of cfg 5 (2e8 points): 6.42 GB read + 1.60 GB written = algorithmic
@@ -395,6 +413,7 @@ def main():
                        + ("no flush needed" if N * 32 + M * 24 > 2e9 else "the step's own 40 B/point/level "
                           "passes evict the inputs (no explicit flush)")),
                 "nodes": node_count, "levels": len(levels_nodes), "point_levels": pt_levels,
+                "projected_points": proj_pts,
                 "build_points_per_s": build_pts_s, "eval_points_per_s": eval_pts_s,
                 "build_ms_per_step": [round(x, 3) for x in build_ms],
                 "input_gen_s": gen_s,

@@ -40,53 +40,20 @@ struct K4Plan {
   static constexpr int MG = grp::max_size(Q, K4_LIM, 0);
 };
 
+// The point loop of one group g (compile-time): z powers, pair products and the group's FMAs, no
+// per-point dispatch.  Points stream through a per-warp shared-memory ring filled by cp.async (8-byte
+// LDGSTS): the load of point i+PD is in flight while points i..i+PD-1 are processed, without tying up
+// registers.
 template <int P, int g>
-__device__ __forceinline__ void k4_one(int gw, double x, double y, double z, double* acc) {
-  if constexpr (g < K4Plan<P>::NG) {
-    if (gw == g) grp::accum<2 * P, K4_LIM, 0, g>(x, y, z, 1.0, acc);
-  }
-}
-template <int P, int... Gs>
-__device__ __forceinline__ void k4_dispatch(int gw, double x, double y, double z, double* acc,
-                                            std::integer_sequence<int, Gs...>) {
-  (k4_one<P, Gs>(gw, x, y, z, acc), ...);
-}
-template <int P, int g>
-__device__ __forceinline__ void k4_range(int gw, int& o0, int& n) {
-  if constexpr (g < K4Plan<P>::NG) {
-    if (gw == g) { o0 = grp::out_begin(2 * P, K4_LIM, 0, g); n = grp::group_size(2 * P, K4_LIM, 0, g); }
-  }
-}
-template <int P, int... Gs>
-__device__ __forceinline__ void k4_ranges(int gw, int& o0, int& n, std::integer_sequence<int, Gs...>) {
-  (k4_range<P, Gs>(gw, o0, n), ...);
-}
-
-// Lane = chunk, warp = output group: lane l of warp w in CTA (x, y) accumulates group y·8 + w over
-// the points of chunk 32·x + l (sequentially, in the frame of node cell[owner >> shift]) and writes
-// its outputs to partial[chunk][..].  No cross-lane reduction; the 8 warps of a CTA read the same
-// 32 chunks (L1 reuse).  Chunks are <= kMomentChunk points (make_chunks).
-template <int P>
-__global__ void __launch_bounds__(K4_THREADS, 1)
-    k_moments(const double* __restrict__ ux, const double* __restrict__ uy, const double* __restrict__ uz,
-              const int4* __restrict__ cell, int shift, const Chunk* __restrict__ chunks,
-              const int64_t* __restrict__ nchunks, double* __restrict__ partial) {
-  using PL = K4Plan<P>;
-  constexpr int K = PL::K;
-  __shared__ __align__(16) double ring[K4_WARPS * K4_RING * 3 * 32];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int gw = blockIdx.y * K4_WARPS + warp;
-  const int64_t cidx = (int64_t)blockIdx.x * 32 + lane;
-  if (gw >= PL::NG || cidx >= *nchunks) return;
-  const Chunk ck = chunks[cidx];
-  const Frame fr = node_frame(cell[ck.owner >> shift]);
-  double acc[PL::MG];
+__device__ __forceinline__ void k4_loop(const double* __restrict__ ux, const double* __restrict__ uy,
+                                        const double* __restrict__ uz, const Chunk& ck, const Frame& fr, double* rg,
+                                        int lane, double* __restrict__ out) {
+  constexpr int Q = 2 * P;
+  constexpr int n = grp::group_size(Q, K4_LIM, 0, g);
+  double acc[n];
 #pragma unroll
-  for (int k = 0; k < PL::MG; ++k) acc[k] = 0.0;
-  // point stream through a per-warp shared-memory ring filled by cp.async (8-byte LDGSTS): the load of
-  // point i+PD is in flight while points i..i+PD-1 are processed, without tying up registers
+  for (int k = 0; k < n; ++k) acc[k] = 0.0;
   constexpr int R = K4_RING, PD = K4_RING - 1;
-  double* rg = ring + (size_t)warp * R * 3 * 32;
   auto issue = [&](int64_t j, int slot) {
     if (j < ck.end) {
       double* d = rg + slot * 96 + lane;
@@ -107,14 +74,41 @@ __global__ void __launch_bounds__(K4_THREADS, 1)
     const double y = __dmul_rn(__dsub_rn(sp[32], fr.cy), fr.scale);
     const double z = __dmul_rn(__dsub_rn(sp[64], fr.cz), fr.scale);
     issue(i + PD, (t + PD) % R);
-    k4_dispatch<P>(gw, x, y, z, acc, std::make_integer_sequence<int, PL::NG>{});
+    grp::accum<Q, K4_LIM, 0, g>(x, y, z, 1.0, acc);
   }
-  int o0 = 0, n = 0;
-  k4_ranges<P>(gw, o0, n, std::make_integer_sequence<int, PL::NG>{});
-  double* out = partial + cidx * (int64_t)K + o0;
+  double* o = out + grp::out_begin(Q, K4_LIM, 0, g);
 #pragma unroll
-  for (int t = 0; t < PL::MG; ++t)
-    if (t < n) out[t] = acc[t];
+  for (int k = 0; k < n; ++k) o[k] = acc[k];
+}
+
+template <int P, int... Gs>
+__device__ __forceinline__ void k4_run(int gw, const double* __restrict__ ux, const double* __restrict__ uy,
+                                       const double* __restrict__ uz, const Chunk& ck, const Frame& fr, double* rg,
+                                       int lane, double* __restrict__ out, std::integer_sequence<int, Gs...>) {
+  ((gw == Gs ? (k4_loop<P, Gs>(ux, uy, uz, ck, fr, rg, lane, out), 0) : 0), ...);
+}
+
+// Lane = chunk, warp = output group: lane l of warp w in CTA (x, y) accumulates group y·8 + w over
+// the points of chunk 32·x + l (sequentially, in the frame of node cell[owner >> shift]) and writes
+// its outputs to partial[chunk][..].  No cross-lane reduction; the 8 warps of a CTA read the same
+// 32 chunks (L1 reuse).  Chunks are <= kMomentChunk points (make_chunks).
+template <int P>
+__global__ void __launch_bounds__(K4_THREADS, 1)
+    k_moments(const double* __restrict__ ux, const double* __restrict__ uy, const double* __restrict__ uz,
+              const int4* __restrict__ cell, int shift, const Chunk* __restrict__ chunks,
+              const int64_t* __restrict__ nchunks, double* __restrict__ partial) {
+  using PL = K4Plan<P>;
+  constexpr int K = PL::K;
+  __shared__ __align__(16) double ring[K4_WARPS * K4_RING * 3 * 32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int gw = blockIdx.y * K4_WARPS + warp;
+  const int64_t cidx = (int64_t)blockIdx.x * 32 + lane;
+  if (gw >= PL::NG || cidx >= *nchunks) return;
+  const Chunk ck = chunks[cidx];
+  const Frame fr = node_frame(cell[ck.owner >> shift]);
+  double* rg = ring + (size_t)warp * K4_RING * 3 * 32;
+  k4_run<P>(gw, ux, uy, uz, ck, fr, rg, lane, partial + cidx * (int64_t)K,
+            std::make_integer_sequence<int, PL::NG>{});
 }
 
 // out[node·stride + e] = Σ of the chunk partials of the node's ranges (rpn ranges per node: 8 owner

@@ -121,15 +121,20 @@ __device__ __forceinline__ void proj_accum(double x, double y, double z, double 
   }
 }
 
+// the batch's points j = j0, j0 + step, ... < nb for the warp's group g (compile-time): no per-point
+// dispatch
 template <int P, int g>
-__device__ __forceinline__ void proj_dispatch_one(int gw, double x, double y, double z, double r, double* acc) {
-  if (gw == g) proj_accum<P, g>(x, y, z, r, acc);
+__device__ __forceinline__ void proj_loop(const double* sx, const double* sy, const double* sz, const double* sr,
+                                          int j0, int step, int nb, double* acc) {
+#pragma unroll 1
+  for (int j = j0; j < nb; j += step) proj_accum<P, g>(sx[j], sy[j], sz[j], sr[j], acc);
 }
 
 template <int P, int... Gs>
-__device__ __forceinline__ void proj_dispatch(int gw, double x, double y, double z, double r, double* acc,
-                                              std::integer_sequence<int, Gs...>) {
-  (proj_dispatch_one<P, Gs>(gw, x, y, z, r, acc), ...);
+__device__ __forceinline__ void proj_run(int gw, const double* sx, const double* sy, const double* sz,
+                                         const double* sr, int j0, int step, int nb, double* acc,
+                                         std::integer_sequence<int, Gs...>) {
+  ((gw == Gs ? (proj_loop<P, Gs>(sx, sy, sz, sr, j0, step, nb, acc), 0) : 0), ...);
 }
 
 template <int P>
@@ -235,9 +240,7 @@ __global__ void __launch_bounds__(K6_THREADS, 2)
       }
       __syncthreads();
       const int nb = (int)min((int64_t)K6_BATCH, ck.end - base);
-#pragma unroll 1
-      for (int j = sub * 32 + lane; j < nb; j += 32 * SUB)
-        proj_dispatch<P>(gw, sx[j], sy[j], sz[j], sr[j], acc, std::make_integer_sequence<int, G>{});
+      proj_run<P>(gw, sx, sy, sz, sr, sub * 32 + lane, 32 * SUB, nb, acc, std::make_integer_sequence<int, G>{});
       __syncthreads();
     }
   }
