@@ -36,7 +36,7 @@ struct K4Plan {
   static constexpr int Q = 2 * P;
   static constexpr int K = rank3(Q);
   static constexpr int NG = grp::ngroups(Q, K4_LIM, 0);
-  static constexpr int NGB = (NG + K4_WARPS - 1) / K4_WARPS;  // grid.y
+  static constexpr int NGB = (NG + K4_WARPS - 1) / K4_WARPS;  // CTAs per 32 chunks
   static constexpr int MG = grp::max_size(Q, K4_LIM, 0);
 };
 
@@ -88,8 +88,8 @@ __device__ __forceinline__ void k4_run(int gw, const double* __restrict__ ux, co
   ((gw == Gs ? (k4_loop<P, Gs>(ux, uy, uz, ck, fr, rg, lane, out), 0) : 0), ...);
 }
 
-// Lane = chunk, warp = output group: lane l of warp w in CTA (x, y) accumulates group y·8 + w over
-// the points of chunk 32·x + l (sequentially, in the frame of node cell[owner >> shift]) and writes
+// Lane = chunk, warp = output group: lane l of warp w in CTA b accumulates group (b % NGB)·8 + w over
+// the points of chunk 32·(b / NGB) + l (sequentially, in the frame of node cell[owner >> shift]) and writes
 // its outputs to partial[chunk][..].  No cross-lane reduction; the 8 warps of a CTA read the same
 // 32 chunks (L1 reuse).  Chunks are <= kMomentChunk points (make_chunks).
 template <int P>
@@ -101,8 +101,9 @@ __global__ void __launch_bounds__(K4_THREADS, 1)
   constexpr int K = PL::K;
   __shared__ __align__(16) double ring[K4_WARPS * K4_RING * 3 * 32];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int gw = blockIdx.y * K4_WARPS + warp;
-  const int64_t cidx = (int64_t)blockIdx.x * 32 + lane;
+  // the NGB CTAs that read the same 32 chunks are adjacent in launch order (their re-reads hit L2)
+  const int gw = (int)(blockIdx.x % PL::NGB) * K4_WARPS + warp;
+  const int64_t cidx = (int64_t)(blockIdx.x / PL::NGB) * 32 + lane;
   if (gw >= PL::NG || cidx >= *nchunks) return;
   const Chunk ck = chunks[cidx];
   const Frame fr = node_frame(cell[ck.owner >> shift]);
@@ -147,7 +148,7 @@ void direct_moments(const double* ux, const double* uy, const double* uz, const 
                     cudaStream_t s) {
   using PL = K4Plan<P>;
   if (max_chunks <= 0) return;
-  FMI_LAUNCH(KID_MOMENTS, s, (k_moments<P>), dim3((unsigned)((max_chunks + 31) / 32), PL::NGB), K4_THREADS, 0, ux, uy,
+  FMI_LAUNCH(KID_MOMENTS, s, (k_moments<P>), (unsigned)((max_chunks + 31) / 32 * PL::NGB), K4_THREADS, 0, ux, uy,
              uz, cell, shift, chunks, nchunks_dev, partial);
 }
 
