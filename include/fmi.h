@@ -44,7 +44,8 @@ extern "C" {
 #define FMI_ENCCL (-6)       /* a collective of a sharded build failed (the fmi_dist callback)     */
 #define FMI_ENOMEM (-7)      /* device allocation failed                                         */
 
-#define FMI_MAX_DEGREE 10    /* compiled degrees p = 0..10 (𝓛 up to 286)                        */
+#define FMI_MAX_DEGREE 14        /* degrees p = 0..14 (𝓛 up to 680); p > 10 only unscoped (below)  */
+#define FMI_MAX_LEVEL_DEGREE 10  /* the octree (level) path and sharded builds: p = 0..10 (𝓛 <= 286)  */
 #define FMI_MAX_DEPTH 20     /* keys carry max_depth+1 <= 21 levels (63-bit Morton keys)           */
 
 typedef struct fmi_tree fmi_tree; /* opaque; owned by the library until fmi_free */
@@ -56,7 +57,11 @@ typedef struct fmi_tree fmi_tree; /* opaque; owned by the library until fmi_free
  *   N          number of points, N >= 𝓛 = (p+1)(p+2)(p+3)/6 (G1).
  *   degree     total degree p of the local polynomials, 0 <= p <= FMI_MAX_DEGREE.  The basis is the
  *              geometric moments Λ_lmn(u) = u1^l u2^m u3^n/(l!m!n!) in Algorithm-2 loop order
- *              (P:185-189).
+ *              (P:185-189).  Degrees 11..14 (𝓛 up to 680) are the paper's unscoped
+ *              experiment (§3, Fig. 1) and need max_depth = 0:
+ *              FMI_EPRECOND otherwise.  Such a fit (and any max_depth = 0 fit when the environment
+ *              sets FMI_UNSCOPED_QR=1) is computed by the QR path of DESIGN.md §5 "f2": the R of the
+ *              monomial Vandermonde as R_V·C through the Legendre basis, then the same rejection walk.
  *   tol        τ >= 0: an octant block becomes a child iff E_RMS > τ and n_o >= 𝓛
  *              and depth+1 <= max_depth (G5).  E_RMS = sqrt(Σ r²/n_o) over the post-fit residual.
  *   max_depth  0..FMI_MAX_DEPTH, root depth 0.
@@ -218,7 +223,7 @@ int fmi_profile_enable(int on);
 int fmi_profile_reset(void);
 /* kernel names: "keys", "sort", "gather", "moments", "moments_reduce", "solve", "children",
  * "residual", "residual_reduce", "decide", "chunks", "scan", "eval", "misc", "project", "m2m",
- * "level_gather", "refine_solve", "refine", "presum" */
+ * "level_gather", "refine_solve", "refine", "presum", "unscoped_gram", "unscoped_solve" */
 int fmi_profile_get(const char* kernel, double* total_ms, int64_t* launches);
 /* Total kernel launches issued by the library since load (or since fmi_profile_reset). */
 int64_t fmi_launch_count(void);

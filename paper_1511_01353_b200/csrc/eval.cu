@@ -192,6 +192,7 @@ void eval_sorted(const double* q, const double4* qpk, const uint64_t* keys, cons
   template void presum_level<P>(const NodeTable&, int64_t, int64_t, cudaStream_t);
 FMI_INST(0) FMI_INST(1) FMI_INST(2) FMI_INST(3) FMI_INST(4) FMI_INST(5)
 FMI_INST(6) FMI_INST(7) FMI_INST(8) FMI_INST(9) FMI_INST(10)
+FMI_INST(11) FMI_INST(12) FMI_INST(13) FMI_INST(14)  // unscoped high-order trees (f2)
 #undef FMI_INST
 
 }  // namespace fmi

@@ -146,7 +146,8 @@ cudaEvent_t get_event() {
 const char* kNames[KID_COUNT] = {"keys",     "sort",     "gather", "moments", "moments_reduce",
                                  "solve",    "children", "residual", "residual_reduce",
                                  "decide",   "chunks",   "scan",   "eval",    "misc",
-                                 "project",  "m2m",      "level_gather", "refine_solve", "refine", "presum"};
+                                 "project",  "m2m",      "level_gather", "refine_solve", "refine", "presum",
+                                 "unscoped_gram", "unscoped_solve"};
 }  // namespace
 
 const char* kernel_name(int kid) { return (kid >= 0 && kid < KID_COUNT) ? kNames[kid] : "?"; }
@@ -590,6 +591,25 @@ void run_levels(fmi_tree* T, const uint64_t* keys, double* ux, double* uy, doubl
   free_table(mt, s);
 }
 
+// the unscoped fit (max_depth = 0) through the QR of unscoped.cu — one node, the root
+template <int P>
+void run_unscoped(fmi_tree* T, const uint64_t* keys, double* ux, double* uy, double* uz, double* r, cudaStream_t s) {
+  constexpr int L = rank3(P);
+  DBuf<int64_t> dev_small(8, s), flags(8, s), scan(8, s);
+  ensure_table(T->nt, T->cap, 16, L, true, s);
+  set_root(T->nt, T->N, true, s);
+  T->nodes = 1;
+  T->lvl_first.push_back(0);
+  T->lvl_count.push_back(1);
+  T->lvl_points.push_back(T->N);
+  T->depth_max = 0;
+  LevelCtx c{keys, ux, uy, uz, r, T->nt, 0, 1, 0, T->D, T->Dk, P, L, rank3(2 * P), T->tau};
+  level_children(c, s);
+  unscoped_fit<P>(c, nullptr, s);
+  level_decide(c, false, nullptr, nullptr, flags.p, scan.p, dev_small.p + 2, s);
+  tmark("unscoped", s);
+}
+
 template <int P>
 void run_eval(const fmi_tree* T, const double* q, const double4* qpk, const uint64_t* keys, const uint32_t* idx,
               int64_t M, int Dk, double* out, cudaStream_t s) {
@@ -612,6 +632,16 @@ void run_eval(const fmi_tree* T, const double* q, const double4* qpk, const uint
     default: fail(FMI_EPRECOND, "degree out of range"); \
   }
 
+// degrees 0..14 (the evaluation, pre-summing and unscoped-fit instantiations)
+#define FMI_DISPATCH14(p, FN, ...)                    \
+  switch (p) {                                        \
+    case 11: FN<11>(__VA_ARGS__); break;              \
+    case 12: FN<12>(__VA_ARGS__); break;              \
+    case 13: FN<13>(__VA_ARGS__); break;              \
+    case 14: FN<14>(__VA_ARGS__); break;              \
+    default: FMI_DISPATCH(p, FN, __VA_ARGS__);        \
+  }
+
 void require_device() {
   int n = 0;
   cudaError_t e = cudaGetDeviceCount(&n);
@@ -625,7 +655,9 @@ fmi_tree* build_impl(const double* pts, const double* f, int64_t N, int degree, 
                      const fmi_dist* dist) {
   if ((!pts || !f) && !(dist && N == 0)) fail(FMI_EINPUT, "null pointer argument");
   if (N < 0) fail(FMI_EINPUT, "N < 0");
-  if (degree < 0 || degree > FMI_MAX_DEGREE) fail(FMI_EPRECOND, "degree outside 0..10");
+  if (degree < 0 || degree > FMI_MAX_DEGREE) fail(FMI_EPRECOND, "degree outside 0..14");
+  if (degree > FMI_MAX_LEVEL_DEGREE && (max_depth != 0 || dist))
+    fail(FMI_EPRECOND, "degree > 10 needs max_depth = 0 (the unscoped fit, P:251-265) and no sharding");
   if (max_depth < 0 || max_depth > FMI_MAX_DEPTH) fail(FMI_EPRECOND, "max_depth outside 0..20");
   if (!(tol >= 0.0)) fail(FMI_EPRECOND, "tol must be >= 0 (and not NaN)");
   const int L = rank3(degree);
@@ -728,6 +760,8 @@ fmi_tree* build_impl(const double* pts, const double* f, int64_t N, int degree, 
     DBuf<uint32_t> perm(N, s), ptmp(N, s);
     DBuf<double4> packed(N, s);
     DBuf<double> ux(N, s), uy(N, s), uz(N, s), r(N, s);
+    // the unscoped QR path (f2): degrees 11..14, or any degree at max_depth = 0 with FMI_UNSCOPED_QR=1
+    const bool unscoped = !dist && max_depth == 0 && (degree > FMI_MAX_LEVEL_DEGREE || std::getenv("FMI_UNSCOPED_QR"));
     int Dsort = T->Dk;
     if (!dist && !std::getenv("FMI_FULL_SORT")) {
       const double fill = std::max(1.0, (double)std::max<int64_t>(Ntot, 1) / (double)L);
@@ -742,7 +776,11 @@ fmi_tree* build_impl(const double* pts, const double* f, int64_t N, int degree, 
       gather_points(packed.p, perm.p, N, ux.p, uy.p, uz.p, r.p, s);
       tmark("gather", s);
       try {
-        FMI_DISPATCH(degree, run_levels, T, keys.p, ux.p, uy.p, uz.p, r.p, s);
+        if (unscoped) {
+          FMI_DISPATCH14(degree, run_unscoped, T, keys.p, ux.p, uy.p, uz.p, r.p, s);
+        } else {
+          FMI_DISPATCH(degree, run_levels, T, keys.p, ux.p, uy.p, uz.p, r.p, s);
+        }
         break;
       } catch (const KeysShort&) {
         reset_tree(T, s);
@@ -796,14 +834,14 @@ int eval_impl(const fmi_tree* T, const double* q, int64_t M, double* out) {
   }
   const int Dk = T->depth_max;
   if (Dk == 0) {
-    FMI_DISPATCH(T->p, run_eval, T, dq, nullptr, nullptr, nullptr, M, 0, dout, s);
+    FMI_DISPATCH14(T->p, run_eval, T, dq, nullptr, nullptr, nullptr, M, 0, dout, s);
   } else {
     DBuf<uint64_t> keys(M, s), ktmp(M, s);
     DBuf<uint32_t> idx(M, s), itmp(M, s);
     DBuf<double4> qpk(M, s);
     morton_keys(dq, M, T->lo, T->width, T->unit, Dk, keys.p, idx.p, s, nullptr, qpk.p);
     radix_sort_pairs(keys.p, idx.p, ktmp.p, itmp.p, M, 3 * Dk, s);
-    FMI_DISPATCH(T->p, run_eval, T, dq, qpk.p, keys.p, idx.p, M, Dk, dout, s);
+    FMI_DISPATCH14(T->p, run_eval, T, dq, qpk.p, keys.p, idx.p, M, Dk, dout, s);
   }
   if (host_out) FMI_CK(cudaMemcpyAsync(out, dout, (size_t)M * sizeof(double), cudaMemcpyDeviceToHost, s));
   FMI_CK(cudaStreamSynchronize(s));
@@ -892,7 +930,7 @@ fmi_tree* fmi_build_dist(const double* pts, const double* f, int64_t N, int degr
 }
 
 int64_t fmi_dist_xbuf_bytes(int degree, int shard_depth) {
-  if (degree < 0 || degree > FMI_MAX_DEGREE || shard_depth < 0 || shard_depth > 6) {
+  if (degree < 0 || degree > FMI_MAX_LEVEL_DEGREE || shard_depth < 0 || shard_depth > 6) {
     set_error(FMI_EPRECOND, "degree or shard_depth out of range");
     return FMI_EPRECOND;
   }

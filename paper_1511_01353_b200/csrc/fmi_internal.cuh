@@ -47,7 +47,8 @@ void check_cuda(cudaError_t e, const char* what, const char* file, int line);
 enum KernelId {
   KID_KEYS = 0, KID_SORT, KID_GATHER, KID_MOMENTS, KID_MOMENTS_REDUCE, KID_SOLVE, KID_CHILDREN,
   KID_RESIDUAL, KID_RESIDUAL_REDUCE, KID_DECIDE, KID_CHUNKS, KID_SCAN, KID_EVAL, KID_MISC, KID_PROJECT,
-  KID_M2M, KID_LEVEL_GATHER, KID_REFINE_SOLVE, KID_REFINE, KID_PRESUM, KID_COUNT
+  KID_M2M, KID_LEVEL_GATHER, KID_REFINE_SOLVE, KID_REFINE, KID_PRESUM, KID_UNSCOPED_GRAM, KID_UNSCOPED_SOLVE,
+  KID_COUNT
 };
 const char* kernel_name(int kid);
 void prof_begin(int kid, cudaStream_t s);
@@ -262,6 +263,10 @@ constexpr double kQrFlagPivot2 = 1e-9;
 // eval.cu
 // eval.cu: pcoef of the nodes [first, first+count) of one level (parents' pcoef must be final)
 template <int P> void presum_level(const NodeTable& nt, int64_t first, int64_t count, cudaStream_t s);
+// unscoped.cu: the single-node fit up to degree 14 by QR through the Legendre basis;
+// c = the root level (count 1, child_start set); writes coef/pcoef/rank/minpiv/flag of the root, the
+// residual r (in place) and the root's octant energies child_ss.
+template <int P> void unscoped_fit(const LevelCtx& c, double* scratch_unused, cudaStream_t s);
 // qpk (optional): the queries' root-cube coordinates as 32-byte records (from morton_keys)
 template <int P> void eval_sorted(const double* q, const double4* qpk, const uint64_t* keys, const uint32_t* idx,
                                   int64_t M, const double lo[3], double width, bool unit, int Dk, const NodeTable& nt,

@@ -1,0 +1,556 @@
+// unscoped.cu — SURVEY §8(f) row f2: the unscoped high-order fit (one node, max_depth = 0) up to
+// degree 14 (𝓛 = 680), §3 / Fig. 1 (L_max = 6, 10, 14 on N_p = 8^6).
+//
+// The level path solves the normal equations from raw moments (K5), which squares the condition
+// number of the monomial Vandermonde Λ; at p >= 12 that is beyond fp64.  The paper's own solve is a QR
+// of Λ.  This path computes exactly that R without forming the monomial Gram:
+//   1. V = the Vandermonde of the tensor Legendre basis s_a s_b s_c P_a(x) P_b(y) P_c(z) (s_k = √(2k+1)),
+//      same polynomial space, well conditioned on space-filling point sets; the RHS f is its last column;
+//   2. G = [V f]ᵀ[V f] by a split-K SYRK (64×64 register-tiled tiles, fixed-order split reduction);
+//   3. bordered Cholesky G = R_Vᵀ R_V in one CTA: the last row gives y = Qᵀf and ρ = ‖f − V V⁺f‖;
+//   4. the monomial basis is Λ = V C with C upper triangular in the Algorithm-2 order (x^a = Σ_k e_ak
+//      s_k P_k(x) per axis; β ≤ α componentwise ⇒ index(β) ≤ index(α)), so Λ = Q (R_V C): the R of the
+//      paper's QR is R = R_V C — a product of triangles, its diagonal a plain product (no cancellation);
+//   5. the column-rejection walk of reading G9 on R D⁻¹ (D = column norms of R = those of Λ), the same
+//      Householder re-triangularisation as K5q, restricted to the rows a reflector can touch, and the
+//      back substitution R_S c̃ = (Qᵀf)_S;  a_α = c̃_α / D_α (monomial form, used by Horner);
+//   6. r = f − Λ(u)·a over the points (Horner) with the octant energies Σr² for the node statistics.
+// Evaluation uses the ordinary K7 path (one node).
+#include <algorithm>
+#include <cmath>
+#include <vector>
+
+#include "fmi.h"
+#include "horner.cuh"
+
+namespace fmi {
+
+namespace {
+
+constexpr int UMAXP = 14;
+constexpr int UT = 64;    // SYRK tile
+constexpr int UK = 16;    // SYRK k-slice
+constexpr int UTHREADS = 256;
+
+// x^a = Σ_k c_ue[a][k] · s_k P_k(x)
+__constant__ double c_ue[(UMAXP + 1) * (UMAXP + 1)];
+
+// ---- 1. Legendre rows: V[i][col], row-major with ld LDV (multiple of UT) --------------------------
+template <int P>
+__global__ void __launch_bounds__(UTHREADS)
+    k_leg_rows(const double* __restrict__ ux, const double* __restrict__ uy, const double* __restrict__ uz,
+               const double* __restrict__ f, int64_t r0, int64_t nr, const uint8_t* __restrict__ el,
+               const uint8_t* __restrict__ em, const uint8_t* __restrict__ en, int L, int LDV,
+               double* __restrict__ V) {
+  __shared__ double tp[3][32][P + 1];  // s_k P_k of the 32 rows' local coordinates, per axis
+  const int64_t base = (int64_t)blockIdx.x * 32;
+  if (threadIdx.x < 96) {
+    const int row = threadIdx.x & 31, ax = threadIdx.x >> 5;
+    const int64_t i = r0 + base + row;
+    double u = 0.0;
+    if (base + row < nr) {
+      const double* src = ax == 0 ? ux : (ax == 1 ? uy : uz);
+      u = __dmul_rn(__dsub_rn(src[i], 0.5), 2.0);  // root frame: centre 1/2, scale 2
+    }
+    double pm = 1.0, pk = u;  // Bonnet: (k+1) P_{k+1} = (2k+1) u P_k - k P_{k-1}
+    tp[ax][row][0] = 1.0;
+    if (P >= 1) tp[ax][row][1] = u * sqrt(3.0);
+    for (int k = 1; k < P; ++k) {
+      const double pn = ((2.0 * k + 1.0) * u * pk - k * pm) / (k + 1.0);
+      pm = pk;
+      pk = pn;
+      tp[ax][row][k + 1] = pn * sqrt(2.0 * (k + 1) + 1.0);
+    }
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < 32 * LDV; e += UTHREADS) {
+    const int row = e / LDV, col = e - row * LDV;
+    if (base + row >= nr) continue;
+    double v = 0.0;
+    if (col < L) v = tp[0][row][el[col]] * tp[1][row][em[col]] * tp[2][row][en[col]];
+    else if (col == L) v = f[r0 + base + row];
+    V[(base + row) * (int64_t)LDV + col] = v;
+  }
+}
+
+// ---- 2. split-K SYRK: part[split] (+)= V[rows of split]ᵀ V[rows of split], lower tiles only ------------
+__global__ void __launch_bounds__(UTHREADS)
+    k_syrk(const double* __restrict__ V, int64_t nr, int LDV, int nsplit, bool accumulate,
+           double* __restrict__ part) {
+  const int t = blockIdx.x;
+  int ti = (int)((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
+  while ((ti + 1) * (ti + 2) / 2 <= t) ++ti;
+  while (ti * (ti + 1) / 2 > t) --ti;
+  const int tj = t - ti * (ti + 1) / 2;
+  const int split = blockIdx.y;
+  const int64_t k0 = nr * split / nsplit, k1 = nr * (split + 1) / nsplit;
+  __shared__ __align__(16) double As[UK][UT], Bs[UK][UT];
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  double acc[4][4];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
+  // register-prefetched k-slices: the next slice's loads are in flight while this one is multiplied
+  constexpr int NQ = (UK * UT) / UTHREADS;
+  double pa[NQ], pb[NQ];
+  auto fetch = [&](int64_t kb) {
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+      const int e = threadIdx.x + q * UTHREADS;
+      const int kk = e / UT, c = e % UT;
+      const int64_t row = kb + kk;
+      pa[q] = row < k1 ? V[row * LDV + ti * UT + c] : 0.0;
+      pb[q] = row < k1 ? V[row * LDV + tj * UT + c] : 0.0;
+    }
+  };
+  if (k0 < k1) fetch(k0);
+  for (int64_t kb = k0; kb < k1; kb += UK) {
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+      const int e = threadIdx.x + q * UTHREADS;
+      As[e / UT][e % UT] = pa[q];
+      Bs[e / UT][e % UT] = pb[q];
+    }
+    __syncthreads();
+    if (kb + UK < k1) fetch(kb + UK);
+#pragma unroll
+    for (int kk = 0; kk < UK; ++kk) {
+      const double2 a01 = *reinterpret_cast<const double2*>(&As[kk][4 * ty]);
+      const double2 a23 = *reinterpret_cast<const double2*>(&As[kk][4 * ty + 2]);
+      const double2 b01 = *reinterpret_cast<const double2*>(&Bs[kk][4 * tx]);
+      const double2 b23 = *reinterpret_cast<const double2*>(&Bs[kk][4 * tx + 2]);
+      const double av[4] = {a01.x, a01.y, a23.x, a23.y};
+      const double bv[4] = {b01.x, b01.y, b23.x, b23.y};
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) acc[a][b] = fma(av[a], bv[b], acc[a][b]);
+    }
+    __syncthreads();
+  }
+  double* out = part + (int64_t)split * LDV * LDV;
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const int64_t o = (int64_t)(ti * UT + 4 * ty + a) * LDV + tj * UT + 4 * tx + b;
+      out[o] = accumulate ? out[o] + acc[a][b] : acc[a][b];
+    }
+}
+
+// G[i][j] = Σ_split part[split][i][j] (fixed order), lower triangle of the leading n×n block
+__global__ void k_sum_splits(const double* __restrict__ part, int nsplit, int LDV, int n, double* __restrict__ G) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= (int64_t)n * n) return;
+  const int i = (int)(e / n), j = (int)(e % n);
+  if (j > i) return;
+  double s = 0.0;
+  for (int p = 0; p < nsplit; ++p) s += part[(int64_t)p * LDV * LDV + (int64_t)i * LDV + j];
+  G[(int64_t)i * LDV + j] = s;
+}
+
+// ---- 3. bordered Cholesky (one CTA): lower factor in place; row n-1 = [yᵀ, ρ] -------------------------
+// Right-looking, 32-column panels (the K5 scheme with runtime n): the panel (rows j0..n-1) is staged
+// column-major in shared memory; warp 0 factors the diagonal block with each lane's row in registers
+// (shuffles, no CTA barrier per column); the rows below are solved thread-per-row in registers; the
+// trailing lower triangle (in global memory, L2-resident) is updated with 4x4 register tiles.
+constexpr int CKB = 32;
+constexpr int CTHREADS = 512;
+__host__ __device__ inline int chol_ldp(int n) {
+  const int r4 = (n + 3) & ~3;
+  return r4 % 16 == 0 ? r4 + 2 : r4;
+}
+
+__global__ void __launch_bounds__(CTHREADS) k_chol_bordered(double* __restrict__ G, int n, int LDV,
+                                                            int* __restrict__ nonpd) {
+  extern __shared__ __align__(16) double Pn[];  // [CKB][LDP]
+  __shared__ double sinv[CKB];
+  const int LDP = chol_ldp(n);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int j0 = 0; j0 < n; j0 += CKB) {
+    const int bw = min(CKB, n - j0), R = n - j0;
+    for (int e = tid; e < R * bw; e += CTHREADS) {
+      const int r = e / bw, c = e - r * bw;
+      Pn[c * LDP + r] = (r >= bw || c <= r) ? G[(int64_t)(j0 + r) * LDV + j0 + c] : 0.0;
+    }
+    __syncthreads();
+    if (warp == 0) {
+      double row[CKB];
+#pragma unroll
+      for (int c = 0; c < CKB; ++c) row[c] = (c <= lane && lane < bw) ? Pn[c * LDP + lane] : 0.0;
+#pragma unroll
+      for (int c = 0; c < CKB; ++c) {
+        if (c < bw) {
+          const int j = j0 + c;
+          const double d = __shfl_sync(0xffffffffu, row[c], c);
+          double p;
+          if (j == n - 1) {
+            p = sqrt(fmax(d, 0.0));  // ρ: residual norm of the least-squares fit
+          } else {
+            p = d > 0.0 ? sqrt(d) : 0.0;
+            if (lane == 0 && !(d > 0.0)) atomicAdd(nonpd, 1);
+          }
+          const double inv = p > 0.0 ? 1.0 / p : 0.0;
+          if (lane == 0) sinv[c] = inv;
+          row[c] = lane == c ? p : row[c] * inv;
+          if (p > 0.0) {
+#pragma unroll
+            for (int c2 = c + 1; c2 < CKB; ++c2) {
+              const double l2 = __shfl_sync(0xffffffffu, row[c], c2);
+              if (lane >= c2) row[c2] -= row[c] * l2;
+            }
+          }
+        }
+      }
+      if (lane < bw) {
+#pragma unroll
+        for (int c = 0; c < CKB; ++c)
+          if (c <= lane) Pn[c * LDP + lane] = row[c];
+      }
+    }
+    __syncthreads();
+    for (int r = bw + tid; r < R; r += CTHREADS) {
+      double x[CKB];
+#pragma unroll
+      for (int c = 0; c < CKB; ++c) x[c] = c < bw ? Pn[c * LDP + r] : 0.0;
+#pragma unroll
+      for (int c = 0; c < CKB; ++c) {
+        if (c < bw) {
+          const double inv = sinv[c];
+          const double lc = x[c] * inv;
+          x[c] = lc;
+          if (inv > 0.0) {
+#pragma unroll
+            for (int c2 = c + 1; c2 < CKB; ++c2)
+              if (c2 < bw) x[c2] -= lc * Pn[c * LDP + c2];
+          }
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < CKB; ++c)
+        if (c < bw) Pn[c * LDP + r] = x[c];
+    }
+    __syncthreads();
+    for (int e = tid; e < R * bw; e += CTHREADS) {
+      const int r = e / bw, c = e - r * bw;
+      if (r >= bw || c <= r) G[(int64_t)(j0 + r) * LDV + j0 + c] = Pn[c * LDP + r];
+    }
+    // trailing update G[i][k] -= Σ_c P[i][c] P[k][c], j1 <= k <= i < n, 4x4 tiles
+    const int j1 = j0 + bw, R2 = n - j1;
+    if (R2 > 0) {
+      const int nt4 = (R2 + 3) / 4;
+      const int ntile = nt4 * (nt4 + 1) / 2;
+      for (int t = tid; t < ntile; t += CTHREADS) {
+        int ti = (int)((sqrt(8.0 * (double)t + 1.0) - 1.0) * 0.5);
+        while ((ti + 1) * (ti + 2) / 2 <= t) ++ti;
+        while (ti * (ti + 1) / 2 > t) --ti;
+        const int tk = t - ti * (ti + 1) / 2;
+        const int i0 = j1 + 4 * ti, k0 = j1 + 4 * tk;
+        double acc[4][4];
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
+        const double* pi = Pn + (i0 - j0);
+        const double* pk = Pn + (k0 - j0);
+        for (int c = 0; c < bw; ++c) {
+          const double2 a01 = *reinterpret_cast<const double2*>(pi + c * LDP);
+          const double2 a23 = *reinterpret_cast<const double2*>(pi + c * LDP + 2);
+          const double2 b01 = *reinterpret_cast<const double2*>(pk + c * LDP);
+          const double2 b23 = *reinterpret_cast<const double2*>(pk + c * LDP + 2);
+          const double av[4] = {a01.x, a01.y, a23.x, a23.y};
+          const double bv[4] = {b01.x, b01.y, b23.x, b23.y};
+#pragma unroll
+          for (int a = 0; a < 4; ++a)
+#pragma unroll
+            for (int b = 0; b < 4; ++b) acc[a][b] = fma(av[a], bv[b], acc[a][b]);
+        }
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int b = 0; b < 4; ++b) {
+            const int i = i0 + a, k = k0 + b;
+            if (i < n && k <= i) G[(int64_t)i * LDV + k] -= acc[a][b];
+          }
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// ---- 4. R = R_V C, augmented with [y; ρ] as column L; column-major A[col * LA + row] -----------------
+__global__ void k_r_mono(const double* __restrict__ G, int L, int LDV, const uint8_t* __restrict__ el,
+                         const uint8_t* __restrict__ em, const uint8_t* __restrict__ en, int P,
+                         double* __restrict__ A) {
+  const int LA = L + 1;
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= (int64_t)LA * LA) return;
+  const int j = (int)(e / LA), i = (int)(e % LA);  // column j, row i
+  double v = 0.0;
+  if (j == L) {
+    v = G[(int64_t)L * LDV + i];  // y_i (i < L) and ρ (i = L): the factor's last row
+  } else if (i <= j) {
+    const int aj = el[j], bj = em[j], cj = en[j];
+    for (int k = i; k <= j; ++k) {
+      const int ak = el[k], bk = em[k], ck = en[k];
+      if (ak > aj || bk > bj || ck > cj) continue;
+      const double c = c_ue[aj * (UMAXP + 1) + ak] * c_ue[bj * (UMAXP + 1) + bk] * c_ue[cj * (UMAXP + 1) + ck];
+      if (c == 0.0) continue;
+      v = fma(G[(int64_t)k * LDV + i], c, v);  // R_V[i][k] = L_factor[k][i]
+    }
+  }
+  (void)P;
+  A[(int64_t)j * LA + i] = v;
+}
+
+__device__ __forceinline__ double ublock_sum(double v, double* red) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  double s = 0.0;
+  for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += red[w];
+  return s;
+}
+
+// ---- 5. equilibration, column-rejection walk (G9) and back substitution (one CTA) ---------------------
+__global__ void __launch_bounds__(UTHREADS)
+    k_unscoped_solve(double* __restrict__ A, int L, double delta, double* __restrict__ dinv, int* __restrict__ kept,
+                     double* __restrict__ piv, double* __restrict__ sol, NodeTable nt) {
+  const int LA = L + 1;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int nwarp = UTHREADS / 32;
+  __shared__ double red[UTHREADS / 32];
+  // D_j = ‖column j of R‖ = ‖column j of Λ‖ (Q orthonormal)
+  for (int j = warp; j < L; j += nwarp) {
+    double s = 0.0;
+    for (int i = lane; i <= j; i += 32) { const double t = A[(int64_t)j * LA + i]; s = fma(t, t, s); }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) dinv[j] = s > 0.0 ? 1.0 / sqrt(s) : 0.0;
+  }
+  __syncthreads();
+  for (int e = tid; e < L * LA; e += UTHREADS) A[e] *= dinv[e / LA];
+  __syncthreads();
+  // walk: k = rows consumed by the kept columns; column j's non-zeros are rows k..j
+  int k = 0;
+  for (int j = 0; j < L; ++j) {
+    double* Aj = A + (int64_t)j * LA;
+    double part = 0.0;
+    for (int i = k + tid; i <= j; i += UTHREADS) { const double t = Aj[i]; part = fma(t, t, part); }
+    const double nrm2 = ublock_sum(part, red);
+    const double nrm = sqrt(nrm2);
+    const bool keep = dinv[j] > 0.0 && nrm > delta;
+    if (tid == 0) { kept[j] = keep ? k : -1; piv[j] = keep ? nrm : 0.0; }
+    if (!keep) { __syncthreads(); continue; }
+    if (j > k) {  // a reflector over rows k..j zeroes rows k+1..j of column j
+      const double d = Aj[k];
+      const double alpha = d >= 0.0 ? -nrm : nrm;
+      const double v0 = d - alpha;
+      const double vtv = nrm2 - d * d + v0 * v0;
+      const double beta = vtv > 0.0 ? 2.0 / vtv : 0.0;
+      for (int c = j + 1 + warp; c < LA; c += nwarp) {
+        double* Ac = A + (int64_t)c * LA;
+        double w = 0.0;
+        for (int i = k + 1 + lane; i <= j; i += 32) w = fma(Aj[i], Ac[i], w);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) w += __shfl_xor_sync(0xffffffffu, w, o);
+        w = fma(v0, Ac[k], w);
+        const double bw = beta * w;
+        for (int i = k + 1 + lane; i <= j; i += 32) Ac[i] -= bw * Aj[i];
+        if (lane == 0) Ac[k] -= bw * v0;
+      }
+      __syncthreads();
+      if (tid == 0) Aj[k] = alpha;
+    }
+    __syncthreads();
+    ++k;
+  }
+  // back substitution over the kept columns (row kept[j] holds column j's pivot), rhs = column L
+  const double* Ar = A + (int64_t)L * LA;
+  for (int i = tid; i < L; i += UTHREADS) sol[i] = kept[i] >= 0 ? Ar[kept[i]] : 0.0;
+  __syncthreads();
+  for (int j = L - 1; j >= 0; --j) {
+    const int row = kept[j];
+    if (row < 0) continue;  // uniform across the block
+    const double* Aj = A + (int64_t)j * LA;
+    const double cj = sol[j] / Aj[row];
+    __syncthreads();
+    for (int i = tid; i < j; i += UTHREADS)
+      if (kept[i] >= 0) sol[i] -= Aj[kept[i]] * cj;
+    if (tid == 0) sol[j] = cj;
+    __syncthreads();
+  }
+  for (int i = tid; i < L; i += UTHREADS) {
+    const double a = sol[i] * dinv[i];
+    nt.coef[i] = a;
+    nt.pcoef[i] = a;
+  }
+  if (tid == 0) {
+    int rk = 0;
+    double mn = INFINITY;
+    for (int i = 0; i < L; ++i)
+      if (kept[i] >= 0) { ++rk; mn = fmin(mn, piv[i]); }
+    nt.rank[0] = rk;
+    nt.minpiv[0] = rk ? mn : 0.0;
+    nt.flag[0] = 0;
+  }
+}
+
+// ---- 6. residual r -= Λ(u)·a over the root's points, Σr² per chunk (chunks lie in one octant) ----------
+template <int P>
+__global__ void __launch_bounds__(UTHREADS)
+    k_unscoped_resid(const double* __restrict__ ux, const double* __restrict__ uy, const double* __restrict__ uz,
+                     double* __restrict__ r, const double* __restrict__ coef, const Chunk* __restrict__ chunks,
+                     const int64_t* __restrict__ nchunks, double* __restrict__ partial) {
+  constexpr int L = rank3(P);
+  __shared__ __align__(16) double sa[(L + 1) & ~1];
+  __shared__ double red[UTHREADS / 32];
+  const int64_t cidx = blockIdx.x;
+  if (cidx >= *nchunks) return;
+  const Chunk ck = chunks[cidx];
+  for (int i = threadIdx.x; i < L; i += UTHREADS) sa[i] = coef[i];
+  __syncthreads();
+  const SmemCoef cf(sa);
+  double ss = 0.0;
+  for (int64_t i = ck.start + threadIdx.x; i < ck.end; i += UTHREADS) {
+    const double x = __dmul_rn(__dsub_rn(ux[i], 0.5), 2.0);
+    const double y = __dmul_rn(__dsub_rn(uy[i], 0.5), 2.0);
+    const double z = __dmul_rn(__dsub_rn(uz[i], 0.5), 2.0);
+    const double v = r[i] - horner3<P>(cf, x, y, z);
+    r[i] = v;
+    ss = fma(v, v, ss);
+  }
+  const double t = ublock_sum(ss, red);
+  if (threadIdx.x == 0) partial[cidx] = t;
+}
+
+// octant energies of the root in chunk order -> child_ss[o]
+__global__ void k_octant_ss(const double* __restrict__ partial, const int64_t* __restrict__ chunk_begin,
+                            const int64_t* __restrict__ nchunks, NodeTable nt) {
+  const int o = threadIdx.x;
+  if (o >= 8) return;
+  const int64_t c0 = chunk_begin[o], c1 = o + 1 < 8 ? chunk_begin[o + 1] : *nchunks;
+  double s = 0.0;
+  for (int64_t c = c0; c < c1; ++c) s += partial[c];
+  nt.child_ss[o] = s;
+}
+
+// host: x^a = Σ_k e[a][k] · s_k P_k(x) from the monomial coefficients of the Legendre polynomials
+std::vector<double> legendre_to_monomial_table() {
+  constexpr int n = UMAXP + 1;
+  std::vector<double> pc(n * n, 0.0);  // P_k(x) = Σ_j pc[k][j] x^j
+  pc[0] = 1.0;
+  pc[1 * n + 1] = 1.0;
+  for (int k = 1; k + 1 < n; ++k)
+    for (int j = 0; j < n; ++j) {
+      double v = -k * pc[(k - 1) * n + j];
+      if (j > 0) v += (2.0 * k + 1.0) * pc[k * n + j - 1];
+      pc[(k + 1) * n + j] = v / (k + 1.0);
+    }
+  // invert the lower-triangular pc: x^a = Σ_k m[a][k] P_k  (pc[k][k] != 0)
+  std::vector<double> m(n * n, 0.0);
+  for (int a = 0; a < n; ++a) {
+    // x^a = (1/pc[a][a]) (P_a - Σ_{j<a} pc[a][j] x^j)
+    std::vector<double> row(n, 0.0);
+    row[a] = 1.0 / pc[a * n + a];
+    for (int j = 0; j < a; ++j) {
+      const double c = -pc[a * n + j] / pc[a * n + a];
+      for (int k = 0; k <= j; ++k) row[k] += c * m[j * n + k];
+    }
+    for (int k = 0; k < n; ++k) m[a * n + k] = row[k];
+  }
+  for (int a = 0; a < n; ++a)
+    for (int k = 0; k < n; ++k) m[a * n + k] /= std::sqrt(2.0 * k + 1.0);  // basis s_k P_k
+  return m;
+}
+
+}  // namespace
+
+template <int P>
+void unscoped_fit(const LevelCtx& c, double* scratch_unused, cudaStream_t s) {
+  (void)scratch_unused;
+  constexpr int L = rank3(P), LA = L + 1;
+  const int LDV = (LA + UT - 1) / UT * UT;
+  const int nt_tiles = LDV / UT;
+  const int ntile = nt_tiles * (nt_tiles + 1) / 2;
+  static bool table_set = false;
+  if (!table_set) {
+    const std::vector<double> m = legendre_to_monomial_table();
+    FMI_CK(cudaMemcpyToSymbol(c_ue, m.data(), m.size() * sizeof(double)));
+    table_set = true;
+  }
+  // exponent tables (Algorithm-2 order)
+  std::vector<uint8_t> ex(3 * L);
+  {
+    int i = 0;
+    for (int l = 0; l <= P; ++l)
+      for (int m = 0; m <= P - l; ++m)
+        for (int n = 0; n <= P - l - m; ++n) { ex[i] = (uint8_t)l; ex[L + i] = (uint8_t)m; ex[2 * L + i] = (uint8_t)n; ++i; }
+  }
+  DBuf<uint8_t> dex(3 * L, s);
+  FMI_CK(cudaMemcpyAsync(dex.p, ex.data(), 3 * L, cudaMemcpyHostToDevice, s));
+  const uint8_t *el = dex.p, *em = dex.p + L, *en = dex.p + 2 * L;
+  // the root's point range
+  int64_t se[2];
+  FMI_CK(cudaMemcpyAsync(se, c.nt.start, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  FMI_CK(cudaMemcpyAsync(se + 1, c.nt.end, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  FMI_CK(cudaStreamSynchronize(s));
+  const int64_t n = se[1] - se[0];
+  // 1-2. Legendre Gram over slabs of rows
+  const int64_t slab = std::min<int64_t>(n, std::max<int64_t>(4096, ((int64_t)1 << 28) / LDV));  // <= 2 GB
+  const int nsplit = (int)std::max<int64_t>(1, std::min<int64_t>(std::max(1, 296 / ntile), slab / 512 + 1));
+  DBuf<double> V((size_t)slab * LDV, s), part((size_t)nsplit * LDV * LDV, s), G((size_t)LDV * LDV, s);
+  for (int64_t r0 = 0; r0 < n; r0 += slab) {
+    const int64_t nr = std::min(slab, n - r0);
+    FMI_LAUNCH(KID_UNSCOPED_GRAM, s, k_leg_rows<P>, (unsigned)((nr + 31) / 32), UTHREADS, 0, c.ux + se[0],
+               c.uy + se[0], c.uz + se[0], c.r + se[0], r0, nr, el, em, en, L, LDV, V.p);
+    FMI_LAUNCH(KID_UNSCOPED_GRAM, s, k_syrk, dim3((unsigned)ntile, (unsigned)nsplit), UTHREADS, 0, V.p, nr, LDV,
+               nsplit, r0 > 0, part.p);
+  }
+  V.release();
+  FMI_LAUNCH(KID_UNSCOPED_GRAM, s, k_sum_splits, (unsigned)(((int64_t)LA * LA + 255) / 256), 256, 0, part.p, nsplit,
+             LDV, LA, G.p);
+  part.release();
+  // 3-5
+  DBuf<int> nonpd(1, s);
+  FMI_CK(cudaMemsetAsync(nonpd.p, 0, sizeof(int), s));
+  {
+    const size_t smem = (size_t)CKB * chol_ldp(LA) * sizeof(double);
+    FMI_CK(cudaFuncSetAttribute(k_chol_bordered, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    FMI_LAUNCH(KID_UNSCOPED_SOLVE, s, k_chol_bordered, 1, CTHREADS, smem, G.p, LA, LDV, nonpd.p);
+  }
+  DBuf<double> A((size_t)LA * LA, s), work((size_t)3 * L, s);
+  DBuf<int> kept(L, s);
+  FMI_LAUNCH(KID_UNSCOPED_SOLVE, s, k_r_mono, (unsigned)(((int64_t)LA * LA + 255) / 256), 256, 0, G.p, L, LDV, el, em,
+             en, P, A.p);
+  FMI_LAUNCH(KID_UNSCOPED_SOLVE, s, k_unscoped_solve, 1, UTHREADS, 0, A.p, L, kDelta, work.p, kept.p, work.p + L,
+             work.p + 2 * L, c.nt);
+  // 6. residual and octant energies
+  {
+    DBuf<int64_t> counts(8, s), begin(8, s), nch(1, s);
+    const int64_t ch = std::max<int64_t>(1024, (n + 148 * 4 - 1) / (148 * 4));
+    const int64_t maxc = n / ch + 9;
+    DBuf<Chunk> chunks(maxc, s);
+    DBuf<double> partial(maxc, s);
+    make_chunks(c.nt.child_start, nullptr, 8, ch, counts.p, begin.p, nch.p, chunks.p, maxc, s);
+    FMI_LAUNCH(KID_RESIDUAL, s, k_unscoped_resid<P>, (unsigned)maxc, UTHREADS, 0, c.ux, c.uy, c.uz, c.r, c.nt.coef,
+               chunks.p, nch.p, partial.p);
+    FMI_LAUNCH(KID_RESIDUAL_REDUCE, s, k_octant_ss, 1, 32, 0, partial.p, begin.p, nch.p, c.nt);
+    FMI_CK(cudaStreamSynchronize(s));
+  }
+  int h_nonpd = 0;
+  FMI_CK(cudaMemcpy(&h_nonpd, nonpd.p, sizeof(int), cudaMemcpyDeviceToHost));
+  if (h_nonpd > 0)
+    fail(FMI_EPRECOND, "unscoped fit: the Legendre Gram of the point set is singular (fewer distinct points than "
+                       "the basis needs, or a degenerate point set)");
+}
+
+#define FMI_INST(P) template void unscoped_fit<P>(const LevelCtx&, double*, cudaStream_t);
+FMI_INST(0) FMI_INST(1) FMI_INST(2) FMI_INST(3) FMI_INST(4) FMI_INST(5) FMI_INST(6) FMI_INST(7)
+FMI_INST(8) FMI_INST(9) FMI_INST(10) FMI_INST(11) FMI_INST(12) FMI_INST(13) FMI_INST(14)
+#undef FMI_INST
+
+}  // namespace fmi

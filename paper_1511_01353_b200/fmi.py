@@ -23,7 +23,8 @@ FMI_ENUMERIC = -4
 FMI_ECUDA = -5
 FMI_ENCCL = -6
 FMI_ENOMEM = -7
-MAX_DEGREE = 10
+MAX_DEGREE = 14        # p > MAX_LEVEL_DEGREE only with max_depth = 0 (unscoped fit, f2)
+MAX_LEVEL_DEGREE = 10
 MAX_DEPTH = 20
 
 # every symbol include/fmi.h declares (tests check the library exports all of them)
@@ -51,7 +52,7 @@ class FmiDist(ctypes.Structure):
 
 KERNELS = ("keys", "sort", "gather", "moments", "moments_reduce", "solve", "children", "residual",
            "residual_reduce", "decide", "chunks", "scan", "eval", "misc", "project", "m2m", "level_gather",
-           "refine_solve", "refine", "presum")
+           "refine_solve", "refine", "presum", "unscoped_gram", "unscoped_solve")
 
 
 class FmiNode(ctypes.Structure):

@@ -53,7 +53,9 @@ def test_argument_errors_without_gpu(lib):
     f = np.zeros(100)
     h = lib.fmi_build(None, None, 100, 2, 1e-6, 2)
     assert not h and fmi.last_error()[0] == fmi.fmi.FMI_EINPUT
-    for args, code in [((pts, f, 100, 11, 1e-6, 2), fmi.fmi.FMI_EPRECOND),
+    for args, code in [((pts, f, 100, 11, 1e-6, 2), fmi.fmi.FMI_EPRECOND),   # p > 10 needs max_depth = 0
+                       ((pts, f, 100, 15, 1e-6, 0), fmi.fmi.FMI_EPRECOND),   # p > 14
+                       ((pts, f, 100, 12, 1e-6, 0), fmi.fmi.FMI_EPRECOND),   # N < 𝓛 = 455
                        ((pts, f, 100, 2, -1.0, 2), fmi.fmi.FMI_EPRECOND),
                        ((pts, f, 100, 2, float("nan"), 2), fmi.fmi.FMI_EPRECOND),
                        ((pts, f, 100, 2, 1e-6, 21), fmi.fmi.FMI_EPRECOND),
