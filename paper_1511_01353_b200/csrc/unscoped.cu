@@ -140,7 +140,8 @@ __global__ void __launch_bounds__(UTHREADS)
 }
 
 // G[i][j] = Σ_split part[split][i][j] (fixed order), lower triangle of the leading n×n block
-__global__ void k_sum_splits(const double* __restrict__ part, int nsplit, int LDV, int n, double* __restrict__ G) {
+__global__ void k_sum_splits(const double* __restrict__ part, int nsplit, int LDV, int n, double* __restrict__ G,
+                             double* __restrict__ diag0) {
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= (int64_t)n * n) return;
   const int i = (int)(e / n), j = (int)(e % n);
@@ -148,6 +149,7 @@ __global__ void k_sum_splits(const double* __restrict__ part, int nsplit, int LD
   double s = 0.0;
   for (int p = 0; p < nsplit; ++p) s += part[(int64_t)p * LDV * LDV + (int64_t)i * LDV + j];
   G[(int64_t)i * LDV + j] = s;
+  if (i == j) diag0[i] = s;
 }
 
 // ---- 3. bordered Cholesky (one CTA): lower factor in place; row n-1 = [yᵀ, ρ] -------------------------
@@ -162,7 +164,12 @@ __host__ __device__ inline int chol_ldp(int n) {
   return r4 % 16 == 0 ? r4 + 2 : r4;
 }
 
+// A Schur pivot below kZeroPivot of the column's own squared norm (diag0) is a column in the span of the
+// previous ones up to rounding (degenerate point sets, e.g. coplanar): it is set to 0 and its monomial
+// counterparts are then rejected by the G9 walk.
+constexpr double kZeroPivot = 1e-13;
 __global__ void __launch_bounds__(CTHREADS) k_chol_bordered(double* __restrict__ G, int n, int LDV,
+                                                            const double* __restrict__ diag0,
                                                             int* __restrict__ nonpd) {
   extern __shared__ __align__(16) double Pn[];  // [CKB][LDP]
   __shared__ double sinv[CKB];
@@ -188,8 +195,9 @@ __global__ void __launch_bounds__(CTHREADS) k_chol_bordered(double* __restrict__
           if (j == n - 1) {
             p = sqrt(fmax(d, 0.0));  // ρ: residual norm of the least-squares fit
           } else {
-            p = d > 0.0 ? sqrt(d) : 0.0;
-            if (lane == 0 && !(d > 0.0)) atomicAdd(nonpd, 1);
+            const bool ok = d > kZeroPivot * diag0[j];
+            p = ok ? sqrt(d) : 0.0;
+            if (lane == 0 && !ok) atomicAdd(nonpd, 1);
           }
           const double inv = p > 0.0 ? 1.0 / p : 0.0;
           if (lane == 0) sinv[c] = inv;
@@ -511,8 +519,9 @@ void unscoped_fit(const LevelCtx& c, double* scratch_unused, cudaStream_t s) {
                nsplit, r0 > 0, part.p);
   }
   V.release();
+  DBuf<double> diag0(LA, s);
   FMI_LAUNCH(KID_UNSCOPED_GRAM, s, k_sum_splits, (unsigned)(((int64_t)LA * LA + 255) / 256), 256, 0, part.p, nsplit,
-             LDV, LA, G.p);
+             LDV, LA, G.p, diag0.p);
   part.release();
   // 3-5
   DBuf<int> nonpd(1, s);
@@ -520,7 +529,7 @@ void unscoped_fit(const LevelCtx& c, double* scratch_unused, cudaStream_t s) {
   {
     const size_t smem = (size_t)CKB * chol_ldp(LA) * sizeof(double);
     FMI_CK(cudaFuncSetAttribute(k_chol_bordered, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    FMI_LAUNCH(KID_UNSCOPED_SOLVE, s, k_chol_bordered, 1, CTHREADS, smem, G.p, LA, LDV, nonpd.p);
+    FMI_LAUNCH(KID_UNSCOPED_SOLVE, s, k_chol_bordered, 1, CTHREADS, smem, G.p, LA, LDV, diag0.p, nonpd.p);
   }
   DBuf<double> A((size_t)LA * LA, s), work((size_t)3 * L, s);
   DBuf<int> kept(L, s);
@@ -541,11 +550,6 @@ void unscoped_fit(const LevelCtx& c, double* scratch_unused, cudaStream_t s) {
     FMI_LAUNCH(KID_RESIDUAL_REDUCE, s, k_octant_ss, 1, 32, 0, partial.p, begin.p, nch.p, c.nt);
     FMI_CK(cudaStreamSynchronize(s));
   }
-  int h_nonpd = 0;
-  FMI_CK(cudaMemcpy(&h_nonpd, nonpd.p, sizeof(int), cudaMemcpyDeviceToHost));
-  if (h_nonpd > 0)
-    fail(FMI_EPRECOND, "unscoped fit: the Legendre Gram of the point set is singular (fewer distinct points than "
-                       "the basis needs, or a degenerate point set)");
 }
 
 #define FMI_INST(P) template void unscoped_fit<P>(const LevelCtx&, double*, cudaStream_t);
