@@ -29,7 +29,7 @@ namespace {
 
 constexpr int UMAXP = 14;
 constexpr int UT = 64;    // SYRK tile
-constexpr int UK = 16;    // SYRK k-slice
+constexpr int UK = 8;     // SYRK k-slice
 constexpr int UTHREADS = 256;
 
 // x^a = Σ_k c_ue[a][k] · s_k P_k(x)
@@ -74,7 +74,10 @@ __global__ void __launch_bounds__(UTHREADS)
 }
 
 // ---- 2. split-K SYRK: part[split] (+)= V[rows of split]ᵀ V[rows of split], lower tiles only ------------
-__global__ void __launch_bounds__(UTHREADS)
+// 64×64 output tile per CTA of 64 threads, 8×8 register tile per thread (per k: 4 + 4 16-byte shared
+// loads feed 64 FMAs), k-slices of UK rows staged in shared memory with register prefetch of the next.
+constexpr int SY_THREADS = 64;
+__global__ void __launch_bounds__(SY_THREADS)
     k_syrk(const double* __restrict__ V, int64_t nr, int LDV, int nsplit, bool accumulate,
            double* __restrict__ part) {
   const int t = blockIdx.x;
@@ -85,19 +88,18 @@ __global__ void __launch_bounds__(UTHREADS)
   const int split = blockIdx.y;
   const int64_t k0 = nr * split / nsplit, k1 = nr * (split + 1) / nsplit;
   __shared__ __align__(16) double As[UK][UT], Bs[UK][UT];
-  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
-  double acc[4][4];
+  const int tx = threadIdx.x & 7, ty = threadIdx.x >> 3;
+  double acc[8][8];
 #pragma unroll
-  for (int a = 0; a < 4; ++a)
+  for (int a = 0; a < 8; ++a)
 #pragma unroll
-    for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
-  // register-prefetched k-slices: the next slice's loads are in flight while this one is multiplied
-  constexpr int NQ = (UK * UT) / UTHREADS;
+    for (int b = 0; b < 8; ++b) acc[a][b] = 0.0;
+  constexpr int NQ = (UK * UT) / SY_THREADS;  // 16
   double pa[NQ], pb[NQ];
   auto fetch = [&](int64_t kb) {
 #pragma unroll
     for (int q = 0; q < NQ; ++q) {
-      const int e = threadIdx.x + q * UTHREADS;
+      const int e = threadIdx.x + q * SY_THREADS;
       const int kk = e / UT, c = e % UT;
       const int64_t row = kb + kk;
       pa[q] = row < k1 ? V[row * LDV + ti * UT + c] : 0.0;
@@ -108,33 +110,35 @@ __global__ void __launch_bounds__(UTHREADS)
   for (int64_t kb = k0; kb < k1; kb += UK) {
 #pragma unroll
     for (int q = 0; q < NQ; ++q) {
-      const int e = threadIdx.x + q * UTHREADS;
+      const int e = threadIdx.x + q * SY_THREADS;
       As[e / UT][e % UT] = pa[q];
       Bs[e / UT][e % UT] = pb[q];
     }
     __syncthreads();
     if (kb + UK < k1) fetch(kb + UK);
-#pragma unroll
+#pragma unroll 4
     for (int kk = 0; kk < UK; ++kk) {
-      const double2 a01 = *reinterpret_cast<const double2*>(&As[kk][4 * ty]);
-      const double2 a23 = *reinterpret_cast<const double2*>(&As[kk][4 * ty + 2]);
-      const double2 b01 = *reinterpret_cast<const double2*>(&Bs[kk][4 * tx]);
-      const double2 b23 = *reinterpret_cast<const double2*>(&Bs[kk][4 * tx + 2]);
-      const double av[4] = {a01.x, a01.y, a23.x, a23.y};
-      const double bv[4] = {b01.x, b01.y, b23.x, b23.y};
+      double av[8], bv[8];
 #pragma unroll
-      for (int a = 0; a < 4; ++a)
+      for (int h = 0; h < 4; ++h) {
+        const double2 a2 = *reinterpret_cast<const double2*>(&As[kk][8 * ty + 2 * h]);
+        const double2 b2 = *reinterpret_cast<const double2*>(&Bs[kk][8 * tx + 2 * h]);
+        av[2 * h] = a2.x; av[2 * h + 1] = a2.y;
+        bv[2 * h] = b2.x; bv[2 * h + 1] = b2.y;
+      }
 #pragma unroll
-        for (int b = 0; b < 4; ++b) acc[a][b] = fma(av[a], bv[b], acc[a][b]);
+      for (int a = 0; a < 8; ++a)
+#pragma unroll
+        for (int b = 0; b < 8; ++b) acc[a][b] = fma(av[a], bv[b], acc[a][b]);
     }
     __syncthreads();
   }
   double* out = part + (int64_t)split * LDV * LDV;
 #pragma unroll
-  for (int a = 0; a < 4; ++a)
+  for (int a = 0; a < 8; ++a)
 #pragma unroll
-    for (int b = 0; b < 4; ++b) {
-      const int64_t o = (int64_t)(ti * UT + 4 * ty + a) * LDV + tj * UT + 4 * tx + b;
+    for (int b = 0; b < 8; ++b) {
+      const int64_t o = (int64_t)(ti * UT + 8 * ty + a) * LDV + tj * UT + 8 * tx + b;
       out[o] = accumulate ? out[o] + acc[a][b] : acc[a][b];
     }
 }
@@ -509,13 +513,13 @@ void unscoped_fit(const LevelCtx& c, double* scratch_unused, cudaStream_t s) {
   const int64_t n = se[1] - se[0];
   // 1-2. Legendre Gram over slabs of rows
   const int64_t slab = std::min<int64_t>(n, std::max<int64_t>(4096, ((int64_t)1 << 28) / LDV));  // <= 2 GB
-  const int nsplit = (int)std::max<int64_t>(1, std::min<int64_t>(std::max(1, 296 / ntile), slab / 512 + 1));
+  const int nsplit = (int)std::max<int64_t>(1, std::min<int64_t>(std::max(1, 148 * 4 / ntile), slab / 512 + 1));
   DBuf<double> V((size_t)slab * LDV, s), part((size_t)nsplit * LDV * LDV, s), G((size_t)LDV * LDV, s);
   for (int64_t r0 = 0; r0 < n; r0 += slab) {
     const int64_t nr = std::min(slab, n - r0);
     FMI_LAUNCH(KID_UNSCOPED_GRAM, s, k_leg_rows<P>, (unsigned)((nr + 31) / 32), UTHREADS, 0, c.ux + se[0],
                c.uy + se[0], c.uz + se[0], c.r + se[0], r0, nr, el, em, en, L, LDV, V.p);
-    FMI_LAUNCH(KID_UNSCOPED_GRAM, s, k_syrk, dim3((unsigned)ntile, (unsigned)nsplit), UTHREADS, 0, V.p, nr, LDV,
+    FMI_LAUNCH(KID_UNSCOPED_GRAM, s, k_syrk, dim3((unsigned)ntile, (unsigned)nsplit), SY_THREADS, 0, V.p, nr, LDV,
                nsplit, r0 > 0, part.p);
   }
   V.release();
