@@ -27,6 +27,13 @@ constexpr int K6_THREADS = 256;
 constexpr int K6_WARPS = K6_THREADS / 32;
 constexpr int K6_PPT = 2;                       // points per thread in the Horner phase
 constexpr int K6_BATCH = K6_PPT * K6_THREADS;
+// the next batch's points stream into a shared-memory stage (cp.async) while the current one is processed
+constexpr size_t K6_STAGE_SMEM = 2 * 4 * (size_t)K6_BATCH * sizeof(double);
+
+__device__ __forceinline__ void k6_cp8(double* dst, const double* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)), "l"(src)
+               : "memory");
+}
 
 // ---- compile-time output groups ------------------------------------------------------------------
 // pairs (a,b), a+b <= P, in a-major order (= the (l,m) order of Algorithm 2); pair q owns
@@ -199,15 +206,39 @@ __global__ void __launch_bounds__(K6_THREADS, 2)
 #pragma unroll
   for (int k = 0; k < MG; ++k) acc[k] = 0.0;
   double ss = 0.0;
-  for (int64_t base = ck.start; base < ck.end; base += K6_BATCH) {
+  // stage[b & 1][array][K6_BATCH]: thread tid copies (and later reads) elements tid + k·K6_THREADS
+  extern __shared__ __align__(16) double stage[];
+  auto issue = [&](int64_t base, int buf) {
+    if (base < ck.end) {
+      double* st = stage + (size_t)buf * 4 * K6_BATCH;
+#pragma unroll
+      for (int k = 0; k < K6_PPT; ++k) {
+        const int64_t i = base + tid + k * K6_THREADS;
+        const int64_t j = i < ck.end ? i : ck.start;
+        const int e = tid + k * K6_THREADS;
+        k6_cp8(st + e, ux + j);
+        k6_cp8(st + K6_BATCH + e, uy + j);
+        k6_cp8(st + 2 * K6_BATCH + e, uz + j);
+        k6_cp8(st + 3 * K6_BATCH + e, r + j);
+      }
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  issue(ck.start, 0);
+  int buf = 0;
+  for (int64_t base = ck.start; base < ck.end; base += K6_BATCH, buf ^= 1) {
+    issue(base + K6_BATCH, buf ^ 1);
+    asm volatile("cp.async.wait_group 1;" ::: "memory");
     double X[K6_PPT], Y[K6_PPT], Z[K6_PPT], R[K6_PPT];
     bool V[K6_PPT];
+    {
+      const double* st = stage + (size_t)buf * 4 * K6_BATCH;
 #pragma unroll
-    for (int k = 0; k < K6_PPT; ++k) {
-      const int64_t i = base + tid + k * K6_THREADS;
-      V[k] = i < ck.end;
-      const int64_t j = V[k] ? i : ck.start;
-      X[k] = ux[j]; Y[k] = uy[j]; Z[k] = uz[j]; R[k] = r[j];
+      for (int k = 0; k < K6_PPT; ++k) {
+        const int e = tid + k * K6_THREADS;
+        V[k] = base + e < ck.end;
+        X[k] = st[e]; Y[k] = st[K6_BATCH + e]; Z[k] = st[2 * K6_BATCH + e]; R[k] = st[3 * K6_BATCH + e];
+      }
     }
     if (horner) {
       double hx[K6_PPT], hy[K6_PPT], hz[K6_PPT], pv[K6_PPT];
@@ -310,9 +341,14 @@ void level_residual(const LevelCtx& c, int mode, int iter, const double* delta, 
                     const int64_t* nchunks_dev, int64_t max_chunks, const int64_t* chunk_begin, int64_t nseg,
                     double* partial, double* segsum, cudaStream_t s, const int32_t* sel) {
   const int kid = mode == K6_ROOT ? KID_PROJECT : (mode == K6_OWN ? KID_REFINE : KID_RESIDUAL);
+  static bool attr = false;
+  if (!attr) {
+    FMI_CK(cudaFuncSetAttribute(k_residual<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)K6_STAGE_SMEM));
+    attr = true;
+  }
   if (max_chunks > 0)
-    FMI_LAUNCH(kid, s, k_residual<P>, (unsigned)max_chunks, K6_THREADS, 0, c.ux, c.uy, c.uz, c.r, c.nt, c.first,
-               chunks, nchunks_dev, c.depth, c.D, mode, iter, delta, partial);
+    FMI_LAUNCH(kid, s, k_residual<P>, (unsigned)max_chunks, K6_THREADS, K6_STAGE_SMEM, c.ux, c.uy, c.uz, c.r, c.nt,
+               c.first, chunks, nchunks_dev, c.depth, c.D, mode, iter, delta, partial);
   FMI_LAUNCH(KID_RESIDUAL_REDUCE, s, k_residual_reduce, (unsigned)nseg, 128, 0, partial, chunk_begin, nchunks_dev, nseg,
              c.nt, c.first, rank3(P), mode == K6_CHILD, sel, segsum);
 }
