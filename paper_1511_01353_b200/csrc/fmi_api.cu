@@ -445,7 +445,7 @@ void run_levels(fmi_tree* T, const uint64_t* keys, double* ux, double* uy, doubl
     int64_t first = 0, count = 1, points = T->N;
     {  // root projection b = Λᵀf in the root frame
       LevelCtx c{keys, ux, uy, uz, r, T->nt, 0, 1, 0, T->D, T->Dk, P, L, K, T->tau};
-      const int64_t ch = choose_chunk(T->N, 1024, 8);
+      const int64_t ch = choose_chunk(T->N, 1024, 32);
       const int64_t maxc = T->N / ch + 2;
       counts.ensure(8, s);
       begin.ensure(8, s);
@@ -520,7 +520,7 @@ void run_levels(fmi_tree* T, const uint64_t* keys, double* ux, double* uy, doubl
       tmark("solve", s);
       if (!global) level_solve_qr<P>(c, lvlmom.p, qr_scratch.p, qr_slots, s);
       // fused K6 over the level's octant segments
-      const int64_t ch6 = choose_chunk(points, 1024, 8);
+      const int64_t ch6 = choose_chunk(points, 1024, 32);
       const int64_t max6 = points / ch6 + 8 * count + 1;
       counts.ensure(count * 8, s);
       begin.ensure(count * 8, s);

@@ -105,21 +105,28 @@ __device__ __forceinline__ void horner3x4(const Coef& coef, const double* x, con
   for (int k = 0; k < 4; ++k) v[k] = px[k];
 }
 
-// Shared-memory coefficient reader that the compiler cannot hoist out of a point loop (a hoisted
-// copy of 𝓛 = 286 coefficients would not fit in registers).
+// Shared-memory coefficient reader (plain loads: the callers' point loops contain a __syncthreads, so the
+// compiler cannot hoist the 𝓛 coefficient loads out of them, but it may schedule them freely inside a
+// Horner evaluation to overlap the row chains).
 struct SmemCoef {
   static constexpr bool kPairs = true;  // coefficient 0 must be 16-byte aligned
+  const double* p;
+  __device__ __forceinline__ explicit SmemCoef(const double* q) : p(q) {}
+  __device__ __forceinline__ double operator()(int i) const { return p[i]; }
+  __device__ __forceinline__ double2 pair(int i) const {  // i even
+    return *reinterpret_cast<const double2*>(p + i);
+  }
+};
+
+// Volatile variant for point loops WITHOUT a barrier (the compiler must not hoist 𝓛 loads out of them).
+struct SmemCoefVolatile {
+  static constexpr bool kPairs = false;
   uint32_t base;  // shared-window address of coefficient 0
-  __device__ __forceinline__ explicit SmemCoef(const double* p)
+  __device__ __forceinline__ explicit SmemCoefVolatile(const double* p)
       : base((uint32_t)__cvta_generic_to_shared(p)) {}
   __device__ __forceinline__ double operator()(int i) const {
     double v;
     asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(base + 8u * (uint32_t)i));
-    return v;
-  }
-  __device__ __forceinline__ double2 pair(int i) const {  // i even
-    double2 v;
-    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(base + 8u * (uint32_t)i));
     return v;
   }
 };

@@ -316,21 +316,40 @@ __global__ void __launch_bounds__(K6_THREADS, 2)
   }
 }
 
-// segment sums: partial chunks of segment (node*8+o) in chunk order -> segsum[seg][𝓛+1]; Σr² also to
-// the node table (child_ss) for the decisions.
-__global__ void __launch_bounds__(128)
+// segment sums: partial chunks of segment (node*8+o) -> segsum[seg][𝓛+1]; Σr² also to the node table
+// (child_ss) for the decisions.  CTA per (segment, 32 consecutive entries): lane = entry, warp w
+// sums the chunks c ≡ w (mod 8) with 2 independent accumulators, the 8 warp sums are then added in warp
+// order (fixed order: deterministic).
+__global__ void __launch_bounds__(256)
     k_residual_reduce(const double* __restrict__ partial, const int64_t* __restrict__ chunk_begin,
                       const int64_t* __restrict__ nchunks, int64_t nseg, NodeTable nt, int64_t first, int L,
                       bool write_ss, const int32_t* __restrict__ sel, double* __restrict__ segsum) {
   const int64_t sgi = blockIdx.x;
   if (sel && sel[sgi] < 0) return;  // K6_PROJ: only the selected segments are (re)written
+  __shared__ double ws[8][32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t c0 = chunk_begin[sgi];
   const int64_t c1 = sgi + 1 < nseg ? chunk_begin[sgi + 1] : *nchunks;
-  for (int e = threadIdx.x; e <= L; e += blockDim.x) {
-    double s = 0.0;
-    for (int64_t c = c0; c < c1; ++c) s += partial[c * (L + 1) + e];
-    segsum[sgi * (L + 1) + e] = s;
-    if (e == L && write_ss) nt.child_ss[first * 8 + sgi] = s;
+  {  // entry group blockIdx.y: entries 32·y .. 32·y + 31
+    const int e = (int)blockIdx.y * 32 + lane;
+    double a = 0.0, b = 0.0;
+    if (e <= L) {
+      int64_t c = c0 + warp;
+      for (; c + 8 < c1; c += 16) {
+        a += partial[c * (L + 1) + e];
+        b += partial[(c + 8) * (L + 1) + e];
+      }
+      if (c < c1) a += partial[c * (L + 1) + e];
+    }
+    ws[warp][lane] = a + b;
+    __syncthreads();
+    if (warp == 0 && e <= L) {
+      double t = 0.0;
+#pragma unroll
+      for (int w = 0; w < 8; ++w) t += ws[w][lane];
+      segsum[sgi * (L + 1) + e] = t;
+      if (e == L && write_ss) nt.child_ss[first * 8 + sgi] = t;
+    }
   }
 }
 
@@ -349,7 +368,8 @@ void level_residual(const LevelCtx& c, int mode, int iter, const double* delta, 
   if (max_chunks > 0)
     FMI_LAUNCH(kid, s, k_residual<P>, (unsigned)max_chunks, K6_THREADS, K6_STAGE_SMEM, c.ux, c.uy, c.uz, c.r, c.nt,
                c.first, chunks, nchunks_dev, c.depth, c.D, mode, iter, delta, partial);
-  FMI_LAUNCH(KID_RESIDUAL_REDUCE, s, k_residual_reduce, (unsigned)nseg, 128, 0, partial, chunk_begin, nchunks_dev, nseg,
+  FMI_LAUNCH(KID_RESIDUAL_REDUCE, s, k_residual_reduce, dim3((unsigned)nseg, (unsigned)((rank3(P) + 1 + 31) / 32)), 256,
+             0, partial, chunk_begin, nchunks_dev, nseg,
              c.nt, c.first, rank3(P), mode == K6_CHILD, sel, segsum);
 }
 

@@ -425,7 +425,7 @@ __global__ void __launch_bounds__(UTHREADS)
   const Chunk ck = chunks[cidx];
   for (int i = threadIdx.x; i < L; i += UTHREADS) sa[i] = coef[i];
   __syncthreads();
-  const SmemCoef cf(sa);
+  const SmemCoefVolatile cf(sa);
   double ss = 0.0;
   for (int64_t i = ck.start + threadIdx.x; i < ck.end; i += UTHREADS) {
     const double x = __dmul_rn(__dsub_rn(ux[i], 0.5), 2.0);
