@@ -215,8 +215,9 @@ __global__ void __launch_bounds__(k5_threads<P>(), k5_threads<P>() == 256 ? 2 : 
               const int j = j0 + c;
               const double sjj = __shfl_sync(0xffffffffu, row[c], c);
               const bool keep = dinv[j] > 0.0 && sjj > delta2;
-              const double p = keep ? sqrt(sjj) : 0.0;
-              const double inv = p > 0.0 ? 1.0 / p : 0.0;
+              // one reciprocal square root on the column-to-column critical path (p = sjj·rsqrt(sjj))
+              const double inv = keep ? rsqrt(sjj) : 0.0;
+              const double p = keep ? sjj * inv : 0.0;
               if (lane == 0) {
                 piv[j] = p;
                 sinv[c] = inv;

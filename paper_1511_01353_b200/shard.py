@@ -47,6 +47,9 @@ class TorchComm:
             t.copy_(h)
         else:
             fn(t)
+            if t.is_cuda:  # the library reads the result on its own stream: complete the collective first
+                import torch
+                torch.cuda.current_stream(t.device).synchronize()
 
     def allreduce_sum(self, t):
         self._op(t, lambda x: self.dist.all_reduce(x, op=self.dist.ReduceOp.SUM, group=self.group))
