@@ -197,10 +197,25 @@ __global__ void __launch_bounds__(k5_threads<P>(), k5_threads<P>() == 256 ? 2 : 
       // ---- blocked right-looking Cholesky with column rejection, RHS row carried along ---------
       for (int j0 = 0; j0 < L; j0 += KB) {
         const int bw = min(KB, L - j0), R = L - j0 + 1;  // panel rows j0..L (row L = RHS)
-        for (int e = tid; e < R * bw; e += K5_THREADS) {
-          const int r = e / bw, c = e % bw;
-          const int i = j0 + r;
-          Pn[c * LDP + r] = (i == L || c <= r) ? A[tri(i) + j0 + c] : 0.0;
+        // panel load: 8 independent L2 loads in flight per thread before their shared-memory stores
+        for (int e0 = tid; e0 < R * bw; e0 += 8 * K5_THREADS) {
+          double v[8];
+          int pos[8];
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            const int e = e0 + k * K5_THREADS;
+            pos[k] = -1;
+            v[k] = 0.0;
+            if (e < R * bw) {
+              const int r = e / bw, c = e - r * bw;
+              const int i = j0 + r;
+              pos[k] = c * LDP + r;
+              if (i == L || c <= r) v[k] = A[tri(i) + j0 + c];
+            }
+          }
+#pragma unroll
+          for (int k = 0; k < 8; ++k)
+            if (pos[k] >= 0) Pn[pos[k]] = v[k];
         }
         __syncthreads();
         // (1) diagonal block: unblocked Cholesky with column rejection by warp 0, lane = row, the row
@@ -226,10 +241,17 @@ __global__ void __launch_bounds__(k5_threads<P>(), k5_threads<P>() == 256 ? 2 : 
               }
               row[c] = lane == c ? p : row[c] * inv;
               if (p > 0.0) {
+                // L[c2][c] from lane c2, 8 shuffles in flight before their FMAs (a shuffle->FMA pair per
+                // column entry would serialise on the shuffle latency)
 #pragma unroll
-                for (int c2 = c + 1; c2 < KB; ++c2) {
-                  const double l2 = __shfl_sync(0xffffffffu, row[c], c2);  // L[c2][c]
-                  if (lane >= c2) row[c2] -= row[c] * l2;
+                for (int b0 = c + 1; b0 < KB; b0 += 8) {
+                  double l2[8];
+#pragma unroll
+                  for (int k = 0; k < 8; ++k)
+                    if (b0 + k < KB) l2[k] = __shfl_sync(0xffffffffu, row[c], b0 + k);
+#pragma unroll
+                  for (int k = 0; k < 8; ++k)
+                    if (b0 + k < KB && lane >= b0 + k) row[b0 + k] -= row[c] * l2[k];
                 }
               }
             }
