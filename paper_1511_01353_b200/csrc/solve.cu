@@ -49,6 +49,27 @@ BasisTab make_basis() {
 
 __host__ __device__ constexpr int64_t tri(int i) { return (int64_t)i * (i + 1) / 2; }
 
+// optional phase timing (build with -DFMI_K5_TIMING): thread 0 of each CTA accumulates clock64 deltas
+// between barriers; CTA 0 prints them at exit (tools/k5_timing.sh)
+#ifdef FMI_K5_TIMING
+#define K5T_DECL long long k5t_last = clock64(), k5t_acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#define K5T(ph)                                  \
+  if (tid == 0) {                                \
+    const long long t_ = clock64();              \
+    k5t_acc[ph] += t_ - k5t_last;                \
+    k5t_last = t_;                               \
+  }
+#define K5T_PRINT                                                                                          \
+  if (tid == 0 && blockIdx.x == 0)                                                                        \
+    printf("k5 phases (cycles, CTA 0, L=%d): assemble %lld panel_load %lld diag %lld trsm %lld "          \
+           "trailing %lld backsub %lld epilogue %lld\n", L, k5t_acc[0], k5t_acc[1], k5t_acc[2], k5t_acc[3], \
+           k5t_acc[4], k5t_acc[5], k5t_acc[6]);
+#else
+#define K5T_DECL
+#define K5T(ph)
+#define K5T_PRINT
+#endif
+
 template <int P>
 struct K5Shape {
   static constexpr int Q = 2 * P;
@@ -91,7 +112,9 @@ __global__ void __launch_bounds__(k5_threads<P>(), k5_threads<P>() == 256 ? 2 : 
   for (int i = tid; i < L; i += K5_THREADS) { bl[i] = bt.l[i]; bm[i] = bt.m[i]; bn[i] = bt.n[i]; }
   __syncthreads();
 
+  K5T_DECL
   for (int64_t node = blockIdx.x; node < count; node += gridDim.x) {
+    K5T(6)
     // mode 1 (refinement): bit-1 nodes only; mode 2 (direct-moment re-solve): bit-2 nodes only
     if (mode == 1 && !(nt.flag[first + node] & 2)) continue;
     if (mode == 2 && !(nt.flag[first + node] & 4)) continue;
@@ -194,6 +217,7 @@ __global__ void __launch_bounds__(k5_threads<P>(), k5_threads<P>() == 256 ? 2 : 
           continue;
         }
       }
+      K5T(0)
       // ---- blocked right-looking Cholesky with column rejection, RHS row carried along ---------
       for (int j0 = 0; j0 < L; j0 += KB) {
         const int bw = min(KB, L - j0), R = L - j0 + 1;  // panel rows j0..L (row L = RHS)
@@ -218,6 +242,7 @@ __global__ void __launch_bounds__(k5_threads<P>(), k5_threads<P>() == 256 ? 2 : 
             if (pos[k] >= 0) Pn[pos[k]] = v[k];
         }
         __syncthreads();
+        K5T(1)
         // (1) diagonal block: unblocked Cholesky with column rejection by warp 0, lane = row, the row
         // in registers; column entries travel by shuffles (no shared-memory round trips)
         if (warp == 0) {
@@ -263,6 +288,7 @@ __global__ void __launch_bounds__(k5_threads<P>(), k5_threads<P>() == 256 ? 2 : 
           }
         }
         __syncthreads();
+        K5T(2)
         // (2) rows below the diagonal block (RHS row included): L_r = A_r L_diag⁻ᵀ, thread per row,
         // the row in registers, the same updates in the same order as the unblocked algorithm
         for (int r = bw + tid; r < R; r += K5_THREADS) {
@@ -287,6 +313,7 @@ __global__ void __launch_bounds__(k5_threads<P>(), k5_threads<P>() == 256 ? 2 : 
             if (c < bw) Pn[c * LDP + r] = x[c];
         }
         __syncthreads();
+        K5T(3)
         for (int e = tid; e < R * bw; e += K5_THREADS) {
           const int r = e / bw, c = e % bw;
           const int i = j0 + r;
@@ -342,6 +369,7 @@ __global__ void __launch_bounds__(k5_threads<P>(), k5_threads<P>() == 256 ? 2 : 
           }
         }
         __syncthreads();
+        K5T(4)
       }
       // y = row L of the factored bordered matrix; ‖y‖² = bᵀG⁻¹b = the residual energy the fit removes
       double yy = 0.0;
@@ -396,6 +424,7 @@ __global__ void __launch_bounds__(k5_threads<P>(), k5_threads<P>() == 256 ? 2 : 
       __syncthreads();
     }
 
+    K5T(5)
     double* out = nt.coef + (first + node) * (int64_t)L;
     if (mode == 1) {  // refinement correction δ (monomial form): delta[node] = δ, coef += δ
       for (int i = tid; i < L; i += K5_THREADS) {
@@ -439,6 +468,7 @@ __global__ void __launch_bounds__(k5_threads<P>(), k5_threads<P>() == 256 ? 2 : 
     }
     __syncthreads();
   }
+  K5T_PRINT
 }
 
 }  // namespace
