@@ -9,6 +9,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <functional>
 #include <atomic>
 #include <chrono>
 #include <cstdio>
@@ -52,6 +53,17 @@ __global__ void k_qr_to_refine(NodeTable nt, int64_t first, int64_t count, int64
   }
 }
 
+
+// the root node's table entries, written by a one-thread kernel (no host->device copy: a copy would
+// queue behind a large upload on the copy engine, e.g. fmi_transfer's overlapped query upload)
+__global__ void k_set_root(NodeTable t, int64_t N, bool fit) {
+  t.start[0] = 0;
+  t.end[0] = N;
+  t.cell[0] = make_int4(0, 0, 0, 0);
+  t.parent[0] = -1;
+  for (int k = 0; k < 8; ++k) t.child[k] = -1;
+  if (fit) t.mtid[0] = 0;
+}
 
 }  // namespace fmi
 
@@ -300,17 +312,7 @@ void ensure_table(NodeTable& t, int64_t& cap, int64_t need, int L, bool fit, cud
 }
 
 void set_root(NodeTable& t, int64_t N, bool fit, cudaStream_t s) {
-  int64_t st = 0, en = N;
-  int4 c = make_int4(0, 0, 0, 0);
-  int32_t par = -1, mt = 0;
-  std::vector<int32_t> ch(8, -1);
-  FMI_CK(cudaMemcpyAsync(t.start, &st, sizeof st, cudaMemcpyHostToDevice, s));
-  FMI_CK(cudaMemcpyAsync(t.end, &en, sizeof en, cudaMemcpyHostToDevice, s));
-  FMI_CK(cudaMemcpyAsync(t.cell, &c, sizeof c, cudaMemcpyHostToDevice, s));
-  FMI_CK(cudaMemcpyAsync(t.parent, &par, sizeof par, cudaMemcpyHostToDevice, s));
-  FMI_CK(cudaMemcpyAsync(t.child, ch.data(), 8 * sizeof(int32_t), cudaMemcpyHostToDevice, s));
-  if (fit) FMI_CK(cudaMemcpyAsync(t.mtid, &mt, sizeof mt, cudaMemcpyHostToDevice, s));
-  FMI_CK(cudaStreamSynchronize(s));  // host staging values above live on this frame
+  FMI_LAUNCH(KID_MISC, s, k_set_root, 1, 1, 0, t, N, fit);
 }
 
 bool is_device_ptr(const void* p) {
@@ -651,8 +653,10 @@ void require_device() {
   }
 }
 
+// after_inputs (optional): called once the host->device copies of the inputs are enqueued on the build
+// stream, before any compute (fmi_transfer starts the query upload there, overlapping the build)
 fmi_tree* build_impl(const double* pts, const double* f, int64_t N, int degree, double tol, int max_depth,
-                     const fmi_dist* dist) {
+                     const fmi_dist* dist, const std::function<void(cudaStream_t)>& after_inputs = nullptr) {
   if ((!pts || !f) && !(dist && N == 0)) fail(FMI_EINPUT, "null pointer argument");
   if (N < 0) fail(FMI_EINPUT, "N < 0");
   if (degree < 0 || degree > FMI_MAX_DEGREE) fail(FMI_EPRECOND, "degree outside 0..14");
@@ -689,6 +693,7 @@ fmi_tree* build_impl(const double* pts, const double* f, int64_t N, int degree, 
     FMI_CK(cudaMemcpyAsync(df_own.p, f, (size_t)N * sizeof(double), cudaMemcpyHostToDevice, s));
     df = df_own.p;
   }
+  if (after_inputs) after_inputs(s);
 
   // root frame (G6) + finiteness
   DBuf<double> bb(8, s);
@@ -1029,15 +1034,52 @@ int fmi_eval(const fmi_tree* tree, const double* q, int64_t M, double* out) {
 int fmi_transfer(const double* pts, const double* f, int64_t N, const double* q, int64_t M, double* out, int degree,
                  double tol, int max_depth) {
   return guard([&] {
-    fmi_tree* T = build_impl(pts, f, N, degree, tol, max_depth, nullptr);
+    // Queries in page-locked host memory are uploaded on a side stream while the build computes (the
+    // PCIe copy overlaps the fit instead of following it); other queries are copied by eval_impl.
+    cudaPointerAttributes qa{};
+    const bool q_pinned = q && M > 0 && cudaPointerGetAttributes(&qa, q) == cudaSuccess && qa.type == cudaMemoryTypeHost;
+    cudaGetLastError();
+    cudaStream_t s2 = nullptr;
+    cudaEvent_t e_in = nullptr, e_q = nullptr;
+    double* dq = nullptr;
+    auto cleanup = [&] {
+      if (e_in) cudaEventDestroy(e_in);
+      if (e_q) cudaEventDestroy(e_q);
+      if (s2) cudaStreamDestroy(s2);
+    };
+    std::function<void(cudaStream_t)> upload;
+    if (q_pinned) {
+      FMI_CK(cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking));
+      FMI_CK(cudaEventCreateWithFlags(&e_in, cudaEventDisableTiming));
+      FMI_CK(cudaEventCreateWithFlags(&e_q, cudaEventDisableTiming));
+      upload = [&](cudaStream_t s) {
+        dq = static_cast<double*>(dmalloc((size_t)M * 3 * sizeof(double), s));
+        FMI_CK(cudaEventRecord(e_in, s));         // the point upload is enqueued before this
+        FMI_CK(cudaStreamWaitEvent(s2, e_in, 0));  // one PCIe transfer at a time
+        FMI_CK(cudaMemcpyAsync(dq, q, (size_t)M * 3 * sizeof(double), cudaMemcpyHostToDevice, s2));
+        FMI_CK(cudaEventRecord(e_q, s2));
+      };
+    }
+    fmi_tree* T = nullptr;
     int rc = 0;
     try {
-      rc = eval_impl(T, q, M, out);
+      T = build_impl(pts, f, N, degree, tol, max_depth, nullptr, upload);
+      if (dq) {
+        FMI_CK(cudaStreamWaitEvent(tl_stream, e_q, 0));
+        rc = eval_impl(T, dq, M, out);
+      } else {
+        rc = eval_impl(T, q, M, out);
+      }
     } catch (...) {
-      fmi_free(T);
+      if (T) fmi_free(T);
+      if (dq) { cudaStreamSynchronize(s2); dfree(dq, tl_stream); }
+      cleanup();
       throw;
     }
     fmi_free(T);
+    if (dq) dfree(dq, tl_stream);
+    FMI_CK(cudaStreamSynchronize(tl_stream));
+    cleanup();
     return rc;
   });
 }
