@@ -817,6 +817,32 @@ fmi_tree* build_impl(const double* pts, const double* f, int64_t N, int degree, 
   return T;
 }
 
+// one evaluation pass over device queries dq[0..m) -> dout[0..m) on stream s (K1 + K2 + K7)
+void eval_device(const fmi_tree* T, const double* dq, int64_t m, double* dout, cudaStream_t s) {
+  const int Dk = T->depth_max;
+  if (Dk == 0) {
+    FMI_DISPATCH14(T->p, run_eval, T, dq, nullptr, nullptr, nullptr, m, 0, dout, s);
+  } else {
+    DBuf<uint64_t> keys(m, s), ktmp(m, s);
+    DBuf<uint32_t> idx(m, s), itmp(m, s);
+    DBuf<double4> qpk(m, s);
+    morton_keys(dq, m, T->lo, T->width, T->unit, Dk, keys.p, idx.p, s, nullptr, qpk.p);
+    radix_sort_pairs(keys.p, idx.p, ktmp.p, itmp.p, m, 3 * Dk, s);
+    FMI_DISPATCH14(T->p, run_eval, T, dq, qpk.p, keys.p, idx.p, m, Dk, dout, s);
+  }
+}
+
+bool is_pinned_host(const void* p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost;
+}
+
+constexpr int64_t kEvalChunk = (int64_t)1 << 24;  // queries per pipelined chunk (host buffers)
+
 int eval_impl(const fmi_tree* T, const double* q, int64_t M, double* out) {
   if (!T) fail(FMI_EINPUT, "null tree");
   if (M < 0) fail(FMI_EINPUT, "M < 0");
@@ -824,11 +850,85 @@ int eval_impl(const fmi_tree* T, const double* q, int64_t M, double* out) {
   if (!q || !out) fail(FMI_EINPUT, "null pointer argument");
   if (M > (int64_t)UINT32_MAX) fail(FMI_EPRECOND, "M exceeds 2^32 - 1");
   cudaStream_t s = tl_stream;
+  const bool host_q = !is_device_ptr(q), host_out = !is_device_ptr(out);
+  if (M > kEvalChunk && ((host_q && is_pinned_host(q)) || (host_out && is_pinned_host(out))) &&
+      !(host_q && !is_pinned_host(q)) && !(host_out && !is_pinned_host(out))) {
+    // Page-locked host buffers: chunks of queries flow H2D (copy stream) -> keys/sort/eval (compute
+    // stream) -> D2H (second copy stream), so the PCIe transfers of one chunk overlap the compute of
+    // its neighbours.  Query and output buffers are double-buffered.
+    const int64_t CH = kEvalChunk, nck = (M + CH - 1) / CH;
+    cudaStream_t sin = nullptr, sout = nullptr;
+    cudaEvent_t e_h2d[2] = {nullptr, nullptr}, e_comp[2] = {nullptr, nullptr}, e_d2h[2] = {nullptr, nullptr};
+    auto release = [&] {
+      for (int b = 0; b < 2; ++b) {
+        if (e_h2d[b]) cudaEventDestroy(e_h2d[b]);
+        if (e_comp[b]) cudaEventDestroy(e_comp[b]);
+        if (e_d2h[b]) cudaEventDestroy(e_d2h[b]);
+      }
+      if (sin) cudaStreamDestroy(sin);
+      if (sout) cudaStreamDestroy(sout);
+    };
+    DBuf<double> dqb[2], doutb[2];
+    try {
+      FMI_CK(cudaStreamCreateWithFlags(&sin, cudaStreamNonBlocking));
+      FMI_CK(cudaStreamCreateWithFlags(&sout, cudaStreamNonBlocking));
+      for (int b = 0; b < 2; ++b) {
+        FMI_CK(cudaEventCreateWithFlags(&e_h2d[b], cudaEventDisableTiming));
+        FMI_CK(cudaEventCreateWithFlags(&e_comp[b], cudaEventDisableTiming));
+        FMI_CK(cudaEventCreateWithFlags(&e_d2h[b], cudaEventDisableTiming));
+        if (host_q) dqb[b].alloc((size_t)CH * 3, s);
+        if (host_out) doutb[b].alloc((size_t)CH, s);
+      }
+      FMI_CK(cudaEventRecord(e_comp[0], s));  // allocations visible to the copy streams
+      FMI_CK(cudaStreamWaitEvent(sin, e_comp[0], 0));
+      FMI_CK(cudaStreamWaitEvent(sout, e_comp[0], 0));
+      for (int64_t k = 0; k < nck; ++k) {
+        const int b = (int)(k & 1);
+        const int64_t c0 = k * CH, m = std::min(CH, M - c0);
+        const double* qk = q + 3 * c0;
+        if (host_q) {
+          if (k >= 2) FMI_CK(cudaStreamWaitEvent(sin, e_comp[b], 0));  // chunk k-2 done with dqb[b]
+          FMI_CK(cudaMemcpyAsync(dqb[b].p, qk, (size_t)m * 3 * sizeof(double), cudaMemcpyHostToDevice, sin));
+          FMI_CK(cudaEventRecord(e_h2d[b], sin));
+          FMI_CK(cudaStreamWaitEvent(s, e_h2d[b], 0));
+          qk = dqb[b].p;
+        }
+        double* ok = out + c0;
+        if (host_out) {
+          if (k >= 2) FMI_CK(cudaStreamWaitEvent(s, e_d2h[b], 0));  // chunk k-2's values copied out
+          ok = doutb[b].p;
+        }
+        eval_device(T, qk, m, ok, s);
+        FMI_CK(cudaEventRecord(e_comp[b], s));
+        if (host_out) {
+          FMI_CK(cudaStreamWaitEvent(sout, e_comp[b], 0));
+          FMI_CK(cudaMemcpyAsync(out + c0, doutb[b].p, (size_t)m * sizeof(double), cudaMemcpyDeviceToHost, sout));
+          FMI_CK(cudaEventRecord(e_d2h[b], sout));
+        }
+      }
+      FMI_CK(cudaStreamSynchronize(sin));
+      FMI_CK(cudaStreamSynchronize(sout));
+      FMI_CK(cudaStreamSynchronize(s));
+    } catch (...) {
+      if (sin) cudaStreamSynchronize(sin);
+      if (sout) cudaStreamSynchronize(sout);
+      cudaStreamSynchronize(s);
+      release();
+      throw;
+    }
+    for (int b = 0; b < 2; ++b) {
+      dqb[b].release();
+      doutb[b].release();
+    }
+    FMI_CK(cudaStreamSynchronize(s));
+    release();
+    prof_collect();
+    return 0;
+  }
   DBuf<double> dq_own, dout_own;
   const double* dq = q;
   double* dout = out;
-  const bool host_out = !is_device_ptr(out);
-  if (!is_device_ptr(q)) {
+  if (host_q) {
     dq_own.alloc((size_t)M * 3, s);
     FMI_CK(cudaMemcpyAsync(dq_own.p, q, (size_t)M * 3 * sizeof(double), cudaMemcpyHostToDevice, s));
     dq = dq_own.p;
@@ -837,17 +937,7 @@ int eval_impl(const fmi_tree* T, const double* q, int64_t M, double* out) {
     dout_own.alloc((size_t)M, s);
     dout = dout_own.p;
   }
-  const int Dk = T->depth_max;
-  if (Dk == 0) {
-    FMI_DISPATCH14(T->p, run_eval, T, dq, nullptr, nullptr, nullptr, M, 0, dout, s);
-  } else {
-    DBuf<uint64_t> keys(M, s), ktmp(M, s);
-    DBuf<uint32_t> idx(M, s), itmp(M, s);
-    DBuf<double4> qpk(M, s);
-    morton_keys(dq, M, T->lo, T->width, T->unit, Dk, keys.p, idx.p, s, nullptr, qpk.p);
-    radix_sort_pairs(keys.p, idx.p, ktmp.p, itmp.p, M, 3 * Dk, s);
-    FMI_DISPATCH14(T->p, run_eval, T, dq, qpk.p, keys.p, idx.p, M, Dk, dout, s);
-  }
+  eval_device(T, dq, M, dout, s);
   if (host_out) FMI_CK(cudaMemcpyAsync(out, dout, (size_t)M * sizeof(double), cudaMemcpyDeviceToHost, s));
   FMI_CK(cudaStreamSynchronize(s));
   prof_collect();

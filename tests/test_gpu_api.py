@@ -50,3 +50,26 @@ def test_save_load_roundtrip(tmp_path):
     with pytest.raises(f_.FmiError) as ei:
         f_.load(str(bad))
     assert ei.value.code == f_.FMI_EVERSION
+
+
+def test_pipelined_host_eval_matches_device_eval():
+    """M > 2^24 queries in page-locked host memory take the chunked path (H2D / keys+sort+eval / D2H of
+    neighbouring chunks overlapped); every value equals the device-pointer evaluation bit for bit, and
+    a pageable output buffer (unpipelined path) gives the same values."""
+    import paper_1511_01353_b200 as fmi
+    cfg = workloads.CONFIGS[2]
+    pts, f, _ = workloads.make_inputs(cfg)
+    M = (1 << 24) * 2 + 12345  # three chunks, ragged tail
+    q = workloads.uniform_points(M, 7)
+    hq = torch.from_numpy(q).pin_memory()
+    hout = torch.empty(M, dtype=torch.float64).pin_memory()
+    with fmi.build(pts, f, cfg.degree, cfg.tol, cfg.max_depth) as t:
+        ref = t.eval(hq.cuda()).cpu().numpy()
+        t.eval(hq.numpy(), out=hout.numpy())
+        assert np.array_equal(hout.numpy(), ref)
+        pageable = t.eval(q)
+        assert np.array_equal(pageable, ref)
+    # transfer: queries uploaded during the fit, values pipelined back
+    out2 = torch.empty(M, dtype=torch.float64).pin_memory()
+    fmi.transfer(pts, f, hq.numpy(), cfg.degree, cfg.tol, cfg.max_depth, out=out2.numpy())
+    assert np.array_equal(out2.numpy(), ref)
