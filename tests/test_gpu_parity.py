@@ -224,3 +224,15 @@ def test_residual_bookkeeping_and_determinism():
         assert np.array_equal(gpu_eval(t1, q), gpu_eval(t2, q))
         ora = fo.build(pts, f, cfg.degree, cfg.tol, cfg.max_depth)
         assert np.max(np.abs(r - ora.residual)) <= 1e-9 * np.max(np.abs(f))
+
+
+def test_deep_cluster_resorts_all_levels():
+    """A tight cluster drives the tree far deeper than the sorted key prefix (Dsort ~ log8(N/𝓛) + 1 = 6
+    levels here): the build detects it (KeysShort) and re-sorts all levels; the result is the oracle's."""
+    rng = np.random.default_rng(21)
+    n_bg, n_cl = 2000, 30_000
+    pts = np.vstack([rng.random((n_bg, 3)), 0.3 + 1e-4 * rng.random((n_cl, 3))])
+    f = workloads.franke3d(pts)
+    q = np.vstack([rng.random((1000, 3)), 0.3 + 1e-4 * rng.random((1000, 3))])
+    ora, gpu, *_ = check_parity(pts, f, 1, 1e-12, 16, q)
+    assert int(np.max(ora.depth)) >= 8

@@ -125,6 +125,21 @@ def test_fit_unisolvent_interpolates(p):
     assert np.max(np.abs(fo.vandermonde(u, p) @ fit.coeffs - f)) <= 1e-9
 
 
+@pytest.mark.parametrize("p", [12, 14])
+def test_fit_high_degree_equals_independent_lstsq(p):
+    """The unscoped high-order fits of Fig. 1 (L_max up to 14): the oracle's Householder QR of
+    the monomial Vandermonde keeps every column on a random point set and gives the fitted values of an
+    SVD least-squares fit in the Legendre product basis."""
+    rng = np.random.default_rng(30 + p)
+    u = rng.uniform(-1, 1, (4 * fo.rank(p), 3))
+    f = workloads.franke3d((u + 1) / 2)
+    fit = fo.fit_node(u, f, p)
+    assert fit.kept.all()
+    ours = fo.vandermonde(u, p) @ fit.coeffs
+    ref = _ls_eval(_ls_fit((u + 1) / 2, f, p), (u + 1) / 2, p)
+    assert np.max(np.abs(ours - ref)) <= 1e-11
+
+
 @pytest.mark.parametrize("p", [1, 2, 3, 5])
 def test_fit_equals_independent_lstsq(p):
     """Library routine with an independent basis: same fitted values as SVD lstsq on Legendre products."""
