@@ -251,7 +251,7 @@ __global__ void __launch_bounds__(K6_THREADS, 2)
       if constexpr (K6_PPT == 4) {
         horner3x4<P>(coef, hx, hy, hz, pv);
       } else {
-        static_assert(K6_PPT == 2, "K6_PPT");
+        static_assert(K6_PPT == 2 || P < 0, "K6_PPT");
         horner3x2<P>(coef, hx[0], hy[0], hz[0], hx[1], hy[1], hz[1], pv[0], pv[1]);
       }
 #pragma unroll
