@@ -324,6 +324,15 @@ bool is_device_ptr(const void* p) {
   return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
 }
 
+bool is_pinned_host(const void* p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost;
+}
+
 int64_t choose_chunk(int64_t points, int64_t min_ch, int64_t per_sm_chunks) {
   int64_t target = (points + 148 * per_sm_chunks - 1) / (148 * per_sm_chunks);
   return std::max(min_ch, target);
@@ -653,8 +662,9 @@ void require_device() {
   }
 }
 
-// after_inputs (optional): called once the host->device copies of the inputs are enqueued on the build
-// stream, before any compute (fmi_transfer starts the query upload there, overlapping the build)
+// after_inputs (optional): called once the host->device copies of the inputs are enqueued, with the
+// stream that carries the last of them (fmi_transfer chains its query upload after it, overlapping the
+// fit)
 fmi_tree* build_impl(const double* pts, const double* f, int64_t N, int degree, double tol, int max_depth,
                      const fmi_dist* dist, const std::function<void(cudaStream_t)>& after_inputs = nullptr) {
   if ((!pts || !f) && !(dist && N == 0)) fail(FMI_EINPUT, "null pointer argument");
@@ -688,16 +698,38 @@ fmi_tree* build_impl(const double* pts, const double* f, int64_t N, int degree, 
     FMI_CK(cudaMemcpyAsync(dpts_own.p, pts, (size_t)N * 3 * sizeof(double), cudaMemcpyHostToDevice, s));
     dpts = dpts_own.p;
   }
+  // Page-locked host values (single-GPU build): uploaded on a side stream after the points, while the
+  // bounding box, keys and sort run; the gather takes them then (and checks their finiteness).
+  struct SideStream {
+    cudaStream_t st = nullptr;
+    cudaEvent_t e_pts = nullptr, e_f = nullptr;
+    ~SideStream() {
+      if (st) { cudaStreamSynchronize(st); cudaStreamDestroy(st); }
+      if (e_pts) cudaEventDestroy(e_pts);
+      if (e_f) cudaEventDestroy(e_f);
+    }
+  } side;
+  const bool late_f = !dist && N > 0 && !is_device_ptr(f) && is_pinned_host(f);
   if (N > 0 && !is_device_ptr(f)) {
     df_own.alloc((size_t)N, s);
-    FMI_CK(cudaMemcpyAsync(df_own.p, f, (size_t)N * sizeof(double), cudaMemcpyHostToDevice, s));
     df = df_own.p;
+    if (late_f) {
+      FMI_CK(cudaStreamCreateWithFlags(&side.st, cudaStreamNonBlocking));
+      FMI_CK(cudaEventCreateWithFlags(&side.e_pts, cudaEventDisableTiming));
+      FMI_CK(cudaEventCreateWithFlags(&side.e_f, cudaEventDisableTiming));
+      FMI_CK(cudaEventRecord(side.e_pts, s));  // after the point upload and the allocation
+      FMI_CK(cudaStreamWaitEvent(side.st, side.e_pts, 0));
+      FMI_CK(cudaMemcpyAsync(df_own.p, f, (size_t)N * sizeof(double), cudaMemcpyHostToDevice, side.st));
+      FMI_CK(cudaEventRecord(side.e_f, side.st));
+    } else {
+      FMI_CK(cudaMemcpyAsync(df_own.p, f, (size_t)N * sizeof(double), cudaMemcpyHostToDevice, s));
+    }
   }
-  if (after_inputs) after_inputs(s);
+  if (after_inputs) after_inputs(late_f ? side.st : s);
 
   // root frame (G6) + finiteness
   DBuf<double> bb(8, s);
-  bbox_and_check(dpts, N, bb.p, df, s);
+  bbox_and_check(dpts, N, bb.p, late_f ? nullptr : df, s);
   double hb[8];
   FMI_CK(cudaMemcpyAsync(hb, bb.p, sizeof hb, cudaMemcpyDeviceToHost, s));
   FMI_CK(cudaStreamSynchronize(s));
@@ -772,13 +804,27 @@ fmi_tree* build_impl(const double* pts, const double* f, int64_t N, int degree, 
       const double fill = std::max(1.0, (double)std::max<int64_t>(Ntot, 1) / (double)L);
       Dsort = std::min(T->Dk, (int)std::ceil(std::log(fill) / std::log(8.0)) + 1);
     }
+    DBuf<int> fbad;
+    if (late_f) {
+      fbad.alloc(1, s);
+      FMI_CK(cudaMemsetAsync(fbad.p, 0, sizeof(int), s));
+    }
     for (;;) {
-      morton_keys(dpts, N, T->lo, T->width, T->unit, T->Dk, keys.p, perm.p, s, df, packed.p);
+      morton_keys(dpts, N, T->lo, T->width, T->unit, T->Dk, keys.p, perm.p, s, late_f ? nullptr : df, packed.p);
       tmark("keys", s);
       radix_sort_pairs(keys.p, perm.p, ktmp.p, ptmp.p, N, 3 * T->Dk, s, 3 * (T->Dk - Dsort));
       T->Dsorted = Dsort;
       tmark("sort", s);
-      gather_points(packed.p, perm.p, N, ux.p, uy.p, uz.p, r.p, s);
+      if (late_f) {
+        FMI_CK(cudaStreamWaitEvent(s, side.e_f, 0));
+        gather_points(packed.p, perm.p, N, ux.p, uy.p, uz.p, r.p, s, df, fbad.p);
+        int hbad = 0;
+        FMI_CK(cudaMemcpyAsync(&hbad, fbad.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+        FMI_CK(cudaStreamSynchronize(s));
+        if (hbad) fail(FMI_EINPUT, "non-finite coordinate or value");
+      } else {
+        gather_points(packed.p, perm.p, N, ux.p, uy.p, uz.p, r.p, s);
+      }
       tmark("gather", s);
       try {
         if (unscoped) {
@@ -830,15 +876,6 @@ void eval_device(const fmi_tree* T, const double* dq, int64_t m, double* dout, c
     radix_sort_pairs(keys.p, idx.p, ktmp.p, itmp.p, m, 3 * Dk, s);
     FMI_DISPATCH14(T->p, run_eval, T, dq, qpk.p, keys.p, idx.p, m, Dk, dout, s);
   }
-}
-
-bool is_pinned_host(const void* p) {
-  cudaPointerAttributes a;
-  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
-    cudaGetLastError();
-    return false;
-  }
-  return a.type == cudaMemoryTypeHost;
 }
 
 constexpr int64_t kEvalChunk = (int64_t)1 << 24;  // queries per pipelined chunk (host buffers)
@@ -1142,9 +1179,9 @@ int fmi_transfer(const double* pts, const double* f, int64_t N, const double* q,
       FMI_CK(cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking));
       FMI_CK(cudaEventCreateWithFlags(&e_in, cudaEventDisableTiming));
       FMI_CK(cudaEventCreateWithFlags(&e_q, cudaEventDisableTiming));
-      upload = [&](cudaStream_t s) {
-        dq = static_cast<double*>(dmalloc((size_t)M * 3 * sizeof(double), s));
-        FMI_CK(cudaEventRecord(e_in, s));         // the point upload is enqueued before this
+      upload = [&](cudaStream_t cs) {
+        dq = static_cast<double*>(dmalloc((size_t)M * 3 * sizeof(double), s2));
+        FMI_CK(cudaEventRecord(e_in, cs));        // the input uploads are enqueued before this
         FMI_CK(cudaStreamWaitEvent(s2, e_in, 0));  // one PCIe transfer at a time
         FMI_CK(cudaMemcpyAsync(dq, q, (size_t)M * 3 * sizeof(double), cudaMemcpyHostToDevice, s2));
         FMI_CK(cudaEventRecord(e_q, s2));

@@ -139,8 +139,10 @@ void morton_keys(const double* pts, int64_t n, const double lo[3], double width,
 // sorted data and keys_tmp/vals_tmp at the scratch (the pointers may have been swapped).
 void radix_sort_pairs(uint64_t*& keys, uint32_t*& vals, uint64_t*& keys_tmp, uint32_t*& vals_tmp, int64_t n,
                       int nbits, cudaStream_t s, int bit_lo = 0);
+// f (optional): take the values from f[perm[i]] instead of the records (values uploaded after the keys
+// were built); *bad is set if one is non-finite
 void gather_points(const double4* packed, const uint32_t* perm, int64_t n, double* ux, double* uy, double* uz,
-                   double* r, cudaStream_t s);
+                   double* r, cudaStream_t s, const double* f = nullptr, int* bad = nullptr);
 
 // sharded build helpers (keys.cu): depth-s cell histogram, partition by owner shard, scatter
 void cell_counts(const double* pts, int64_t n, const double lo[3], double width, bool unit, int s, int64_t* counts,

@@ -54,18 +54,34 @@ __global__ void __launch_bounds__(BB_THREADS) k_bbox_partial(const double* __res
   if (threadIdx.x < 7) part[blockIdx.x * 8 + threadIdx.x] = sm[threadIdx.x][0];
 }
 
-__global__ void k_bbox_final(const double* __restrict__ part, int nb, double* __restrict__ out) {
-  if (threadIdx.x != 0) return;
+__global__ void __launch_bounds__(BB_THREADS) k_bbox_final(const double* __restrict__ part, int nb,
+                                                           double* __restrict__ out) {
   double r[7] = {INFINITY, INFINITY, INFINITY, -INFINITY, -INFINITY, -INFINITY, 0.0};
-  for (int b = 0; b < nb; ++b) {
+  for (int b = threadIdx.x; b < nb; b += BB_THREADS) {
+#pragma unroll
     for (int a = 0; a < 3; ++a) {
       r[a] = fmin(r[a], part[b * 8 + a]);
       r[3 + a] = fmax(r[3 + a], part[b * 8 + 3 + a]);
     }
     r[6] = fmax(r[6], part[b * 8 + 6]);
   }
-  for (int a = 0; a < 7; ++a) out[a] = r[a];
-  out[7] = 0.0;
+  __shared__ double sm[7][BB_THREADS];
+#pragma unroll
+  for (int a = 0; a < 7; ++a) sm[a][threadIdx.x] = r[a];
+  __syncthreads();
+  for (int w = BB_THREADS / 2; w > 0; w >>= 1) {
+    if (threadIdx.x < w) {
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        sm[a][threadIdx.x] = fmin(sm[a][threadIdx.x], sm[a][threadIdx.x + w]);
+        sm[3 + a][threadIdx.x] = fmax(sm[3 + a][threadIdx.x], sm[3 + a][threadIdx.x + w]);
+      }
+      sm[6][threadIdx.x] = fmax(sm[6][threadIdx.x], sm[6][threadIdx.x + w]);
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x < 7) out[threadIdx.x] = sm[threadIdx.x][0];
+  if (threadIdx.x == 7) out[7] = 0.0;
 }
 
 // ------------------------------------------------------------------------------------------------
@@ -243,6 +259,25 @@ __global__ void __launch_bounds__(256) k_gather(const double4* __restrict__ pack
   r[i] = b.y;
 }
 
+// variant for values uploaded after the keys were built (fmi_build with page-locked host f): the value
+// comes from f[perm[i]]; a non-finite value raises *bad
+__global__ void __launch_bounds__(256) k_gather_f(const double4* __restrict__ packed, const uint32_t* __restrict__ perm,
+                                                  const double* __restrict__ f, int64_t n, double* __restrict__ ux,
+                                                  double* __restrict__ uy, double* __restrict__ uz,
+                                                  double* __restrict__ r, int* __restrict__ bad) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const uint32_t j = perm[i];
+  const double2* p = reinterpret_cast<const double2*>(packed + j);
+  const double2 a = __ldg(p), b = __ldg(p + 1);
+  const double v = __ldg(f + j);
+  ux[i] = a.x;
+  uy[i] = a.y;
+  uz[i] = b.x;
+  r[i] = v;
+  if (!isfinite(v)) *bad = 1;
+}
+
 // sharded build helpers ---------------------------------------------------------------------------
 __device__ __forceinline__ uint32_t cell_label(double ux, double uy, double uz, int s) {
   return (uint32_t)(spread3(quantize(ux, s)) | (spread3(quantize(uy, s)) << 1) | (spread3(quantize(uz, s)) << 2));
@@ -325,7 +360,7 @@ void bbox_and_check(const double* pts, int64_t n, double* out8, const double* f,
   if (nb < 1) nb = 1;
   DBuf<double> part((size_t)nb * 8, s);
   FMI_LAUNCH(KID_MISC, s, k_bbox_partial, nb, BB_THREADS, 0, pts, n, f, part.p);
-  FMI_LAUNCH(KID_MISC, s, k_bbox_final, 1, 32, 0, part.p, nb, out8);
+  FMI_LAUNCH(KID_MISC, s, k_bbox_final, 1, BB_THREADS, 0, part.p, nb, out8);
 }
 
 void morton_keys(const double* pts, int64_t n, const double lo[3], double width, bool unit, int D, uint64_t* keys,
@@ -360,10 +395,13 @@ void radix_sort_pairs(uint64_t*& keys, uint32_t*& vals, uint64_t*& keys_tmp, uin
 }
 
 void gather_points(const double4* packed, const uint32_t* perm, int64_t n, double* ux, double* uy, double* uz,
-                   double* r, cudaStream_t s) {
+                   double* r, cudaStream_t s, const double* f, int* bad) {
   if (n <= 0) return;
   unsigned grid = (unsigned)((n + 255) / 256);
-  FMI_LAUNCH(KID_GATHER, s, k_gather, grid, 256, 0, packed, perm, n, ux, uy, uz, r);
+  if (f)
+    FMI_LAUNCH(KID_GATHER, s, k_gather_f, grid, 256, 0, packed, perm, f, n, ux, uy, uz, r, bad);
+  else
+    FMI_LAUNCH(KID_GATHER, s, k_gather, grid, 256, 0, packed, perm, n, ux, uy, uz, r);
 }
 
 }  // namespace fmi

@@ -73,3 +73,22 @@ def test_pipelined_host_eval_matches_device_eval():
     out2 = torch.empty(M, dtype=torch.float64).pin_memory()
     fmi.transfer(pts, f, hq.numpy(), cfg.degree, cfg.tol, cfg.max_depth, out=out2.numpy())
     assert np.array_equal(out2.numpy(), ref)
+
+
+def test_pinned_host_values_uploaded_late():
+    """Page-locked host values take the side-stream upload (checked for finiteness at the gather): same
+    tree and values as device inputs; a NaN is still rejected with FMI_EINPUT."""
+    import paper_1511_01353_b200 as fmi
+    cfg = workloads.CONFIGS[2]
+    pts, f, q = workloads.make_inputs(cfg)
+    q = q[:20_000]
+    hp = torch.from_numpy(pts).pin_memory()
+    hf = torch.from_numpy(f).pin_memory()
+    with fmi.build(hp.numpy(), hf.numpy(), cfg.degree, cfg.tol, cfg.max_depth) as a, \
+            fmi.build(hp.cuda(), hf.cuda(), cfg.degree, cfg.tol, cfg.max_depth) as b:
+        assert a.node_count == b.node_count
+        assert np.array_equal(a.eval(q), b.eval(q))
+    hf[123] = float("nan")
+    with pytest.raises(fmi.FmiError) as ei:
+        fmi.build(hp.numpy(), hf.numpy(), cfg.degree, cfg.tol, cfg.max_depth)
+    assert ei.value.code == -1
