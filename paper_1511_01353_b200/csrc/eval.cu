@@ -128,9 +128,9 @@ __device__ __forceinline__ void eval_locate(const double* __restrict__ q, const 
     }
   }
   const Frame fr = node_frame(nt.cell[node]);
-  x = __dmul_rn(__dsub_rn(ux, fr.cx), fr.scale);
-  y = __dmul_rn(__dsub_rn(uy, fr.cy), fr.scale);
-  z = __dmul_rn(__dsub_rn(uz, fr.cz), fr.scale);
+  x = to_local(ux, fr.cx, fr.scale);
+  y = to_local(uy, fr.cy, fr.scale);
+  z = to_local(uz, fr.cz, fr.scale);
 }
 
 template <int P>

@@ -70,9 +70,9 @@ __device__ __forceinline__ void k4_loop(const double* __restrict__ ux, const dou
   for (int64_t i = ck.start; i < ck.end; ++i, t = (t + 1 == R) ? 0 : t + 1) {
     asm volatile("cp.async.wait_group %0;" ::"n"(PD - 1) : "memory");
     const double* sp = rg + t * 96 + lane;
-    const double x = __dmul_rn(__dsub_rn(sp[0], fr.cx), fr.scale);
-    const double y = __dmul_rn(__dsub_rn(sp[32], fr.cy), fr.scale);
-    const double z = __dmul_rn(__dsub_rn(sp[64], fr.cz), fr.scale);
+    const double x = to_local(sp[0], fr.cx, fr.scale);
+    const double y = to_local(sp[32], fr.cy, fr.scale);
+    const double z = to_local(sp[64], fr.cz, fr.scale);
     issue(i + PD, (t + PD) % R);
     grp::accum<Q, K4_LIM, 0, g>(x, y, z, 1.0, acc);
   }

@@ -244,9 +244,9 @@ __global__ void __launch_bounds__(K6_THREADS, 2)
       double hx[K6_PPT], hy[K6_PPT], hz[K6_PPT], pv[K6_PPT];
 #pragma unroll
       for (int k = 0; k < K6_PPT; ++k) {
-        hx[k] = __dmul_rn(__dsub_rn(X[k], fn.cx), fn.scale);
-        hy[k] = __dmul_rn(__dsub_rn(Y[k], fn.cy), fn.scale);
-        hz[k] = __dmul_rn(__dsub_rn(Z[k], fn.cz), fn.scale);
+        hx[k] = to_local(X[k], fn.cx, fn.scale);
+        hy[k] = to_local(Y[k], fn.cy, fn.scale);
+        hz[k] = to_local(Z[k], fn.cz, fn.scale);
       }
       if constexpr (K6_PPT == 4) {
         horner3x4<P>(coef, hx, hy, hz, pv);
@@ -264,9 +264,9 @@ __global__ void __launch_bounds__(K6_THREADS, 2)
 #pragma unroll
       for (int k = 0; k < K6_PPT; ++k) {
         const int j = tid + k * K6_THREADS;
-        sx[j] = __dmul_rn(__dsub_rn(X[k], fc.cx), fc.scale);
-        sy[j] = __dmul_rn(__dsub_rn(Y[k], fc.cy), fc.scale);
-        sz[j] = __dmul_rn(__dsub_rn(Z[k], fc.cz), fc.scale);
+        sx[j] = to_local(X[k], fc.cx, fc.scale);
+        sy[j] = to_local(Y[k], fc.cy, fc.scale);
+        sz[j] = to_local(Z[k], fc.cz, fc.scale);
         sr[j] = V[k] ? R[k] : 0.0;
       }
       __syncthreads();

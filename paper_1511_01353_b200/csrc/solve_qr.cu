@@ -14,7 +14,7 @@
 // (L2-resident).  Non-flagged nodes exit immediately.
 #include <algorithm>
 
-#include "fmi_internal.cuh"
+#include "horner.cuh"
 
 namespace fmi {
 
@@ -96,9 +96,9 @@ __global__ void __launch_bounds__(KQ_THREADS)
         if (row < nb) {
           const int64_t pi = b0 + row;
           if (col < L) {
-            const double x = __dmul_rn(__dsub_rn(ux[pi], cx), scale);
-            const double y = __dmul_rn(__dsub_rn(uy[pi], cy), scale);
-            const double z = __dmul_rn(__dsub_rn(uz[pi], cz), scale);
+            const double x = to_local(ux[pi], cx, scale);
+            const double y = to_local(uy[pi], cy, scale);
+            const double z = to_local(uz[pi], cz, scale);
             double m = 1.0;
             for (int k = 0; k < bl[col]; ++k) m *= x;
             for (int k = 0; k < bm[col]; ++k) m *= y;

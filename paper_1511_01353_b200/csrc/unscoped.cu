@@ -50,7 +50,7 @@ __global__ void __launch_bounds__(UTHREADS)
     double u = 0.0;
     if (base + row < nr) {
       const double* src = ax == 0 ? ux : (ax == 1 ? uy : uz);
-      u = __dmul_rn(__dsub_rn(src[i], 0.5), 2.0);  // root frame: centre 1/2, scale 2
+      u = to_local(src[i], 0.5, 2.0);  // root frame: centre 1/2, scale 2
     }
     double pm = 1.0, pk = u;  // Bonnet: (k+1) P_{k+1} = (2k+1) u P_k - k P_{k-1}
     tp[ax][row][0] = 1.0;
@@ -428,9 +428,9 @@ __global__ void __launch_bounds__(UTHREADS)
   const SmemCoefVolatile cf(sa);
   double ss = 0.0;
   for (int64_t i = ck.start + threadIdx.x; i < ck.end; i += UTHREADS) {
-    const double x = __dmul_rn(__dsub_rn(ux[i], 0.5), 2.0);
-    const double y = __dmul_rn(__dsub_rn(uy[i], 0.5), 2.0);
-    const double z = __dmul_rn(__dsub_rn(uz[i], 0.5), 2.0);
+    const double x = to_local(ux[i], 0.5, 2.0);
+    const double y = to_local(uy[i], 0.5, 2.0);
+    const double z = to_local(uz[i], 0.5, 2.0);
     const double v = r[i] - horner3<P>(cf, x, y, z);
     r[i] = v;
     ss = fma(v, v, ss);
