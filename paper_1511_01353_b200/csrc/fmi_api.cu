@@ -616,7 +616,7 @@ void run_unscoped(fmi_tree* T, const uint64_t* keys, double* ux, double* uy, dou
   T->depth_max = 0;
   LevelCtx c{keys, ux, uy, uz, r, T->nt, 0, 1, 0, T->D, T->Dk, P, L, rank3(2 * P), T->tau};
   level_children(c, s);
-  unscoped_fit<P>(c, nullptr, s);
+  unscoped_fit<P>(c, s);
   level_decide(c, false, nullptr, nullptr, flags.p, scan.p, dev_small.p + 2, s);
   tmark("unscoped", s);
 }

@@ -268,7 +268,7 @@ template <int P> void presum_level(const NodeTable& nt, int64_t first, int64_t c
 // unscoped.cu: the single-node fit up to degree 14 by QR through the Legendre basis;
 // c = the root level (count 1, child_start set); writes coef/pcoef/rank/minpiv/flag of the root, the
 // residual r (in place) and the root's octant energies child_ss.
-template <int P> void unscoped_fit(const LevelCtx& c, double* scratch_unused, cudaStream_t s);
+template <int P> void unscoped_fit(const LevelCtx& c, cudaStream_t s);
 // qpk (optional): the queries' root-cube coordinates as 32-byte records (from morton_keys)
 template <int P> void eval_sorted(const double* q, const double4* qpk, const uint64_t* keys, const uint32_t* idx,
                                   int64_t M, const double lo[3], double width, bool unit, int Dk, const NodeTable& nt,

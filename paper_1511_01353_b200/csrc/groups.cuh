@@ -116,30 +116,6 @@ __device__ __forceinline__ void accum(double x, double y, double z, double w, do
   }
 }
 
-// Split form of accum(): prep() does the per-point setup (z powers, first pair's x^a y^b w), apply()
-// the FMAs — so a caller can prepare the next point while the current one's FMAs issue.
-template <int Q, int LIM, int TARGET, int g>
-struct Prep {
-  static constexpr int q0 = pair_begin(Q, LIM, TARGET, g), q1 = pair_begin(Q, LIM, TARGET, g + 1);
-  static constexpr int o0 = out_begin(Q, LIM, TARGET, g);
-  static constexpr int CM = group_cmax(Q, LIM, TARGET, g);
-  double zp[CM + 1];
-  double x, y, xw, yb;
-  __device__ __forceinline__ void prep(double x_, double y_, double z, double w) {
-    x = x_;
-    y = y_;
-    zp[0] = 1.0;
-    if constexpr (CM >= 1) zp[1] = z;
-#pragma unroll
-    for (int c = 2; c <= CM; ++c) zp[c] = zp[c / 2] * zp[c - c / 2];
-    xw = cpow<pair_a(Q, q0)>(x) * w;
-    yb = xw * cpow<pair_b(Q, q0)>(y);  // first pair's x^a y^b w
-  }
-  __device__ __forceinline__ void apply(double* acc) const {
-    if constexpr (q0 < q1) pairs<Q, q0, q1, o0>(x, y, zp, xw, yb, acc);
-  }
-};
-
 // Butterfly reduce-scatter of N = 32·M values per lane over the 32 lanes of a warp: afterwards lane l
 // holds the warp totals of entries M·l .. M·l+M-1 in v[0..M).  31·M shuffles instead of 5·N.
 template <int N>

@@ -7,6 +7,7 @@
 // Octant digit of level t (1..D): o = bx + 2·by + 4·bz (x fastest), b* = bit (D-t) of
 // q* = min(floor(u*·2^D), 2^D - 1).  u* is the root-cube unit coordinate; u* >= split plane <=> the
 // bit is set (tie -> upper side) because u·2^D is an exact power-of-two scaling (G7, G18).
+#include <mutex>
 #include <algorithm>
 
 #include "fmi_internal.cuh"
@@ -373,11 +374,11 @@ void morton_keys(const double* pts, int64_t n, const double lo[3], double width,
 void radix_sort_pairs(uint64_t*& keys, uint32_t*& vals, uint64_t*& keys_tmp, uint32_t*& vals_tmp, int64_t n,
                       int nbits, cudaStream_t s, int bit_lo) {
   if (n <= 1 || nbits <= 0) return;
-  static bool attr = false;
-  if (!attr) {
-    FMI_CK(cudaFuncSetAttribute(k_rs_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kScatterSmem));
-    attr = true;
-  }
+  static std::once_flag attr_once;  // one opt-in per kernel instantiation (thread-safe)
+  std::call_once(attr_once, [&] {
+    FMI_CK(cudaFuncSetAttribute(
+        k_rs_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kScatterSmem));
+  });
   const int64_t nblk = (n + RS_TILE - 1) / RS_TILE;
   DBuf<int64_t> counts((size_t)nblk * 256, s);
   uint64_t* ka = keys; uint32_t* va = vals; uint64_t* kb = keys_tmp; uint32_t* vb = vals_tmp;

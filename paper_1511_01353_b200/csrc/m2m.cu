@@ -17,6 +17,7 @@
 //     B_p = B_own + T+( Σ_c (B_c + (3Q+3)·eps·|M_c|) ).
 // The solve rejects a translated Gram whose equilibrated bound exceeds kMomentTol (catastrophic
 // cancellation, e.g. points clustered at the parent's centre) and the node is re-accumulated directly.
+#include <mutex>
 #include "fmi_internal.cuh"
 
 namespace fmi {
@@ -240,11 +241,11 @@ void bound_init(const NodeTable& mt, int64_t n, int K, int KS, float* bnd, cudaS
 template <int P>
 void m2m_level(double* mom, float* bnd, const int32_t* child, int64_t first, int64_t count, cudaStream_t s) {
   constexpr size_t smem = M2MLayout<P>::BYTES;
-  static bool attr = false;
-  if (!attr) {
-    FMI_CK(cudaFuncSetAttribute(k_m2m<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr = true;
-  }
+  static std::once_flag attr_once;  // one opt-in per kernel instantiation (thread-safe)
+  std::call_once(attr_once, [&] {
+    FMI_CK(cudaFuncSetAttribute(
+        k_m2m<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  });
   if (count <= 0) return;
   FMI_LAUNCH(KID_M2M, s, k_m2m<P>, (unsigned)count, M2M_THREADS, smem, mom, bnd, child, first, count);
 }

@@ -15,6 +15,7 @@
 // a fixed group of outputs (a contiguous range of the Algorithm-2 basis order) and its lanes walk the
 // batch's points: per point, z^0..z^cmax are formed once and every output (a,b,c) of the group costs
 // one FMA  acc += (x^a y^b r) · z^c.  Lane partials are reduced in a fixed order (deterministic).
+#include <mutex>
 #include <utility>
 
 #include "horner.cuh"
@@ -360,11 +361,11 @@ void level_residual(const LevelCtx& c, int mode, int iter, const double* delta, 
                     const int64_t* nchunks_dev, int64_t max_chunks, const int64_t* chunk_begin, int64_t nseg,
                     double* partial, double* segsum, cudaStream_t s, const int32_t* sel) {
   const int kid = mode == K6_ROOT ? KID_PROJECT : (mode == K6_OWN ? KID_REFINE : KID_RESIDUAL);
-  static bool attr = false;
-  if (!attr) {
-    FMI_CK(cudaFuncSetAttribute(k_residual<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)K6_STAGE_SMEM));
-    attr = true;
-  }
+  static std::once_flag attr_once;  // one opt-in per kernel instantiation (thread-safe)
+  std::call_once(attr_once, [&] {
+    FMI_CK(cudaFuncSetAttribute(
+        k_residual<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)K6_STAGE_SMEM));
+  });
   if (max_chunks > 0)
     FMI_LAUNCH(kid, s, k_residual<P>, (unsigned)max_chunks, K6_THREADS, K6_STAGE_SMEM, c.ux, c.uy, c.uz, c.r, c.nt,
                c.first, chunks, nchunks_dev, c.depth, c.D, mode, iter, delta, partial);

@@ -19,6 +19,7 @@
 // as the unblocked algorithm), written back, and the trailing triangle is updated once with 4x4
 // register tiles.  The back substitution R̃ c̃ = y is blocked the same way (small triangular solve of
 // the diagonal block, then a row-contiguous GEMV update of the rows above).
+#include <mutex>
 #include <algorithm>
 #include <vector>
 
@@ -478,11 +479,11 @@ void level_solve(const LevelCtx& c, const double* mom, int mode, const double* s
                  double refine_fill, int64_t n_root, int64_t* nflag, double* fac, cudaStream_t s, double defer_tau) {
   using S = K5Shape<P>;
   static const BasisTab bt = make_basis<P>();
-  static bool attr = false;
-  if (!attr) {
-    FMI_CK(cudaFuncSetAttribute(k_solve<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::SMEM));
-    attr = true;
-  }
+  static std::once_flag attr_once;  // one opt-in per kernel instantiation (thread-safe)
+  std::call_once(attr_once, [&] {
+    FMI_CK(cudaFuncSetAttribute(
+        k_solve<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::SMEM));
+  });
   const int64_t grid = std::min<int64_t>(c.count, 1 << 20);
   if (grid <= 0) return;
   FMI_LAUNCH(mode == 1 ? KID_REFINE_SOLVE : KID_SOLVE, s, k_solve<P>, (unsigned)grid, k5_threads<P>(), S::SMEM, mom, mode,

@@ -18,6 +18,7 @@
 // Evaluation uses the ordinary K7 path (one node).
 #include <algorithm>
 #include <cmath>
+#include <mutex>
 #include <vector>
 
 #include "fmi.h"
@@ -482,18 +483,16 @@ std::vector<double> legendre_to_monomial_table() {
 }  // namespace
 
 template <int P>
-void unscoped_fit(const LevelCtx& c, double* scratch_unused, cudaStream_t s) {
-  (void)scratch_unused;
+void unscoped_fit(const LevelCtx& c, cudaStream_t s) {
   constexpr int L = rank3(P), LA = L + 1;
   const int LDV = (LA + UT - 1) / UT * UT;
   const int nt_tiles = LDV / UT;
   const int ntile = nt_tiles * (nt_tiles + 1) / 2;
-  static bool table_set = false;
-  if (!table_set) {
+  static std::once_flag table_once;  // the constant table of this device (one process per GPU)
+  std::call_once(table_once, [] {
     const std::vector<double> m = legendre_to_monomial_table();
     FMI_CK(cudaMemcpyToSymbol(c_ue, m.data(), m.size() * sizeof(double)));
-    table_set = true;
-  }
+  });
   // exponent tables (Algorithm-2 order)
   std::vector<uint8_t> ex(3 * L);
   {
@@ -556,7 +555,7 @@ void unscoped_fit(const LevelCtx& c, double* scratch_unused, cudaStream_t s) {
   }
 }
 
-#define FMI_INST(P) template void unscoped_fit<P>(const LevelCtx&, double*, cudaStream_t);
+#define FMI_INST(P) template void unscoped_fit<P>(const LevelCtx&, cudaStream_t);
 FMI_INST(0) FMI_INST(1) FMI_INST(2) FMI_INST(3) FMI_INST(4) FMI_INST(5) FMI_INST(6) FMI_INST(7)
 FMI_INST(8) FMI_INST(9) FMI_INST(10) FMI_INST(11) FMI_INST(12) FMI_INST(13) FMI_INST(14)
 #undef FMI_INST
