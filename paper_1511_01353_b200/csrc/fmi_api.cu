@@ -324,6 +324,14 @@ bool is_device_ptr(const void* p) {
   return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
 }
 
+// host-buffer overlaps (late value upload, query upload during the fit) only pay off on large inputs;
+// FMI_NO_OVERLAP=1 disables them (diagnostics)
+constexpr int64_t kOverlapMin = (int64_t)1 << 20;
+bool no_overlap() {
+  static const bool v = std::getenv("FMI_NO_OVERLAP") != nullptr;
+  return v;
+}
+
 bool is_pinned_host(const void* p) {
   cudaPointerAttributes a;
   if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
@@ -709,7 +717,8 @@ fmi_tree* build_impl(const double* pts, const double* f, int64_t N, int degree, 
       if (e_f) cudaEventDestroy(e_f);
     }
   } side;
-  const bool late_f = !dist && N > 0 && !is_device_ptr(f) && is_pinned_host(f);
+  // (large inputs only: the side stream costs more than it hides on small builds)
+  const bool late_f = !dist && N >= kOverlapMin && !is_device_ptr(f) && is_pinned_host(f) && !no_overlap();
   if (N > 0 && !is_device_ptr(f)) {
     df_own.alloc((size_t)N, s);
     df = df_own.p;
@@ -1164,7 +1173,8 @@ int fmi_transfer(const double* pts, const double* f, int64_t N, const double* q,
     // Queries in page-locked host memory are uploaded on a side stream while the build computes (the
     // PCIe copy overlaps the fit instead of following it); other queries are copied by eval_impl.
     cudaPointerAttributes qa{};
-    const bool q_pinned = q && M > 0 && cudaPointerGetAttributes(&qa, q) == cudaSuccess && qa.type == cudaMemoryTypeHost;
+    const bool q_pinned = q && M >= kOverlapMin && !no_overlap() && cudaPointerGetAttributes(&qa, q) == cudaSuccess &&
+                          qa.type == cudaMemoryTypeHost;
     cudaGetLastError();
     cudaStream_t s2 = nullptr;
     cudaEvent_t e_in = nullptr, e_q = nullptr;
