@@ -31,7 +31,7 @@ namespace {
 
 // threads per node: 128 for the small systems (more nodes per SM), 256 for 𝓛 >= 220 (p >= 9)
 template <int P>
-constexpr int k5_threads() { return rank3(P) >= 220 ? 256 : 128; }
+constexpr int k5_threads() { return rank3(P) >= 220 ? 256 : (rank3(P) >= 100 ? 128 : 64); }
 constexpr int KB = 32;
 
 struct BasisTab {
@@ -85,7 +85,7 @@ struct K5Shape {
 };
 
 template <int P>
-__global__ void __launch_bounds__(k5_threads<P>(), k5_threads<P>() == 256 ? 2 : 3)
+__global__ void __launch_bounds__(k5_threads<P>(), k5_threads<P>() == 256 ? 2 : (k5_threads<P>() == 128 ? 3 : 6))
     k_solve(const double* __restrict__ mom, int mode, const double* __restrict__ segrhs, double* __restrict__ delta,
             NodeTable nt, int64_t first, int64_t count, double* __restrict__ fac,
             const __grid_constant__ BasisTab bt, double delta2, double refine2, double refine_fill,
