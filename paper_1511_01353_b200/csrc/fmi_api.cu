@@ -65,6 +65,12 @@ __global__ void k_set_root(NodeTable t, int64_t N, bool fit) {
   if (fit) t.mtid[0] = 0;
 }
 
+// mark every node of a level as deferred (flag bit 3): its child projections run in K6_PROJ
+__global__ void k_defer_all(NodeTable nt, int64_t first, int64_t count) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < count) nt.flag[first + t] |= 8;
+}
+
 }  // namespace fmi
 
 using namespace fmi;
@@ -210,6 +216,7 @@ struct fmi_tree {
   double refine_fill = kRefineFill;  // env FMI_REFINE_FILL
   int64_t mt_min = 0;                // moment-tree cell minimum (points); env FMI_MT_FILL (multiple of 𝓛)
   double defer_theta = kDeferTheta;  // env FMI_DEFER_THETA (0: never defer)
+  bool k6_split = true;              // env FMI_K6_SPLIT=0: fused K6 (Horner + projections in one pass)
   int64_t deferred_children = 0;     // children whose projections ran in a K6_PROJ pass
   double tau = 0;
   double lo[3] = {0, 0, 0};
@@ -386,7 +393,7 @@ void dist_sum(const fmi_tree* T, void* dev, int64_t n, int dtype, cudaStream_t s
 template <int P>
 void run_levels(fmi_tree* T, const uint64_t* keys, double* ux, double* uy, double* uz, double* r, cudaStream_t s) {
   constexpr int L = rank3(P), K = rank3(2 * P);
-  DBuf<int64_t> counts, begin, flags, scan, dev_small(8, s), nflag(2, s), gcnt;
+  DBuf<int64_t> counts, begin, flags, scan, dev_small(8, s), nflag(3, s), gcnt;
   DBuf<int32_t> dsel;
   DBuf<Chunk> chunks;
   DBuf<double> partial, mtmom, segsum, lvlmom, scratch, delta;
@@ -492,12 +499,13 @@ void run_levels(fmi_tree* T, const uint64_t* keys, double* ux, double* uy, doubl
       level_children(c, s);
       const bool global = T->dist && depth < T->shard_depth;  // nodes summed over the shards
       // K5: solve; nodes whose translated moments fail the rounding check are re-accumulated directly
-      FMI_CK(cudaMemsetAsync(nflag.p, 0, 2 * sizeof(int64_t), s));
+      FMI_CK(cudaMemsetAsync(nflag.p, 0, 3 * sizeof(int64_t), s));
       scratch.ensure((size_t)count * fac_per_node, s);
-      const double defer_tau = global ? 0.0 : T->defer_theta * T->tau;  // deferral: single shard only
+      // deferral: single shard only; split mode defers every node (Horner-only K6 + K6_PROJ)
+      const double defer_tau = global ? 0.0 : (T->k6_split ? INFINITY : T->defer_theta * T->tau);
       level_solve<P>(c, lvlmom.p, 0, nullptr, nullptr, T->refine2, T->refine_fill, T->Ntot, nflag.p, scratch.p, s,
                      defer_tau);
-      FMI_CK(cudaMemcpyAsync(&host_small[2], nflag.p, 2 * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+      FMI_CK(cudaMemcpyAsync(&host_small[2], nflag.p, 3 * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
       FMI_CK(cudaStreamSynchronize(s));
       if (host_small[3] > 0) {
         // few flagged nodes, possibly huge (a root): longer chunks keep the chunk count (and the
@@ -526,17 +534,27 @@ void run_levels(fmi_tree* T, const uint64_t* keys, double* ux, double* uy, doubl
         }
         level_solve<P>(c, lvlmom.p, 2, nullptr, nullptr, T->refine2, T->refine_fill, T->Ntot, nflag.p, scratch.p, s,
                        defer_tau);
-        FMI_CK(cudaMemcpyAsync(&host_small[2], nflag.p, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
-        FMI_CK(cudaStreamSynchronize(s));
         T->direct_nodes += host_small[3];
+        FMI_CK(cudaMemcpyAsync(&host_small[2], nflag.p, 3 * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+        FMI_CK(cudaStreamSynchronize(s));
       }
       if (global) {  // K5q needs all of a node's points: global nodes take refinement steps instead
         FMI_LAUNCH(KID_MISC, s, k_qr_to_refine, (unsigned)((count + 255) / 256), 256, 0, T->nt, first, count, nflag.p);
         FMI_CK(cudaMemcpyAsync(&host_small[2], nflag.p, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
         FMI_CK(cudaStreamSynchronize(s));
       }
-      const int64_t nref = host_small[2];
+      const int64_t nref = host_small[2], ndefer_nodes = host_small[4];
       tmark("solve", s);
+      // K6 form of this level: fused (Horner + Σr² + child projections) when most nodes may have
+      // children; when at least half of the nodes deferred their projections (predicted leaves), all are
+      // deferred and the level runs the Horner-only K6 (more points in flight per thread, no projection
+      // registers) followed by K6_PROJ for the children actually created
+      bool horner_only = T->k6_split && !global;
+      if (!global && !horner_only && ndefer_nodes * 2 >= count && ndefer_nodes > 0) {
+        if (ndefer_nodes < count)
+          FMI_LAUNCH(KID_MISC, s, k_defer_all, (unsigned)((count + 255) / 256), 256, 0, T->nt, first, count);
+        horner_only = true;
+      }
       if (!global) level_solve_qr<P>(c, lvlmom.p, qr_scratch.p, qr_slots, s);
       // fused K6 over the level's octant segments
       const int64_t ch6 = choose_chunk(points, 1024, 32);
@@ -562,7 +580,7 @@ void run_levels(fmi_tree* T, const uint64_t* keys, double* ux, double* uy, doubl
       }
       tmark("qr+refine", s);
       level_residual<P>(c, K6_CHILD, 0, delta.p, chunks.p, dev_small.p + 1, max6, begin.p, count * 8, partial.p,
-                        segsum.p, s);
+                        segsum.p, s, nullptr, horner_only);
       tmark("residual", s);
       flags.ensure(count * 8, s);
       scan.ensure(count * 8, s);
@@ -777,6 +795,7 @@ fmi_tree* build_impl(const double* pts, const double* f, int64_t N, int degree, 
     if (const char* e = std::getenv("FMI_REFINE_PIVOT2")) T->refine2 = std::atof(e);
     if (const char* e = std::getenv("FMI_REFINE_FILL")) T->refine_fill = std::atof(e);
     if (const char* e = std::getenv("FMI_DEFER_THETA")) T->defer_theta = std::atof(e);
+    if (const char* e = std::getenv("FMI_K6_SPLIT")) T->k6_split = std::atoi(e) != 0;
     {
       double mf = kMomentTreeFill;
       if (const char* e = std::getenv("FMI_MT_FILL")) mf = std::atof(e);

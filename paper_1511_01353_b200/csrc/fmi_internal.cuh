@@ -236,7 +236,7 @@ enum K6Mode { K6_CHILD = 0, K6_ROOT = 1, K6_OWN = 2, K6_PROJ = 3 };
 template <int P> void level_residual(const LevelCtx& c, int mode, int iter, const double* delta, const Chunk* chunks,
                                      const int64_t* nchunks_dev, int64_t max_chunks, const int64_t* chunk_begin,
                                      int64_t nseg, double* partial, double* segsum, cudaStream_t s,
-                                     const int32_t* sel = nullptr);
+                                     const int32_t* sel = nullptr, bool horner_only = false);
 // child projections of a node are deferred (flag bit 3) when its predicted post-fit RMS (pre-fit energy
 // minus the energy the fit removes) is below kDeferTheta·τ: its children are then unlikely to be
 // created, and the projection pass runs only for those that are

@@ -26,10 +26,12 @@ namespace {
 
 constexpr int K6_THREADS = 256;
 constexpr int K6_WARPS = K6_THREADS / 32;
-constexpr int K6_PPT = 2;                       // points per thread in the Horner phase
-constexpr int K6_BATCH = K6_PPT * K6_THREADS;
+// points per thread in the Horner phase: 2 in the fused kernel (register budget shared with the
+// projection accumulators), 4 in the Horner-only variant (four independent Horner chains per thread)
+__host__ __device__ constexpr int k6_ppt(int var) { return var == 1 ? 4 : 2; }
+__host__ __device__ constexpr int k6_batch(int var) { return k6_ppt(var) * 256; }
 // the next batch's points stream into a shared-memory stage (cp.async) while the current one is processed
-constexpr size_t K6_STAGE_SMEM = 2 * 4 * (size_t)K6_BATCH * sizeof(double);
+__host__ __device__ constexpr size_t k6_stage_smem(int var) { return 2 * 4 * (size_t)k6_batch(var) * sizeof(double); }
 
 __device__ __forceinline__ void k6_cp8(double* dst, const double* src) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)), "l"(src)
@@ -145,8 +147,10 @@ __device__ __forceinline__ void proj_run(int gw, const double* sx, const double*
   ((gw == Gs ? (proj_loop<P, Gs>(sx, sy, sz, sr, j0, step, nb, acc), 0) : 0), ...);
 }
 
-template <int P>
-__global__ void __launch_bounds__(K6_THREADS, 2)
+// VAR: 0 = fused (Horner + Σr² + projections), 1 = Horner + Σr² only, 2 = projections only — the
+// specialised variants carry no registers for the part they skip
+template <int P, int VAR>
+__global__ void __launch_bounds__(K6_THREADS, VAR == 1 ? 3 : 2)
     k_residual(const double* __restrict__ ux, const double* __restrict__ uy, const double* __restrict__ uz,
                double* __restrict__ r, NodeTable nt, int64_t first, const Chunk* __restrict__ chunks,
                const int64_t* __restrict__ nchunks, int depth, int D, int mode, int iter,
@@ -155,13 +159,14 @@ __global__ void __launch_bounds__(K6_THREADS, 2)
   constexpr int G = proj_groups(P);
   constexpr int SUB = K6_WARPS / G;  // warps per output group (split the batch's points)
   constexpr int MG = max_group(P);
+  constexpr int K6_PPT = k6_ppt(VAR), K6_BATCH = k6_batch(VAR);
   __shared__ __align__(16) double sa[L];
-  __shared__ double sbuf[4 * K6_BATCH];  // batch coordinates in the child frame + residuals
+  __shared__ double sbuf[VAR == 1 ? 2 * L : 4 * K6_BATCH];  // batch coordinates in the child frame + residuals
   double* sx = sbuf;
   double* sy = sbuf + K6_BATCH;
   double* sz = sbuf + 2 * K6_BATCH;
   double* sr = sbuf + 3 * K6_BATCH;
-  static_assert(SUB * L <= 4 * K6_BATCH, "reduction buffer");
+  static_assert(VAR == 1 || SUB * L <= 4 * K6_BATCH, "reduction buffer");
   double (*red)[L] = reinterpret_cast<double (*)[L]>(sbuf);  // after the point loop
   __shared__ double redw[K6_WARPS];
   const int64_t cidx = blockIdx.x;
@@ -172,7 +177,8 @@ __global__ void __launch_bounds__(K6_THREADS, 2)
   const int64_t node = first + ln;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   double* out = partial + cidx * (int64_t)(L + 1);
-  const bool horner = mode != K6_ROOT && mode != K6_PROJ;
+  constexpr bool kHorner = VAR != 2, kProj = VAR != 1;
+  const bool horner = kHorner && mode != K6_ROOT && mode != K6_PROJ;
   const bool refined = horner && (nt.flag[node] & 2);
   if (mode == K6_OWN && !refined) {  // refinement pass: this node takes no step
     for (int e = tid; e <= L; e += K6_THREADS) out[e] = 0.0;
@@ -181,18 +187,18 @@ __global__ void __launch_bounds__(K6_THREADS, 2)
   bool project;
   Frame fn{}, fc{};
   if (mode == K6_ROOT) {
-    project = true;
+    project = kProj;
     fc = node_frame(nt.cell[node]);
   } else {
     const int4 c = nt.cell[node];
     fn = node_frame(c);
     if (mode == K6_OWN) {
-      project = true;
+      project = kProj;
       fc = fn;
     } else {
       const int64_t n_o = nt.child_start[node * 9 + o + 1] - nt.child_start[node * 9 + o];
       // potential child (P:306 integer guard + G5), unless deferred (flag bit 3: see K6_PROJ)
-      project = mode == K6_PROJ || (n_o >= L && depth + 1 <= D && !(nt.flag[node] & 8));
+      project = kProj && (mode == K6_PROJ || (n_o >= L && depth + 1 <= D && !(nt.flag[node] & 8)));
       fc = node_frame(make_int4(2 * c.x + (o & 1), 2 * c.y + ((o >> 1) & 1), 2 * c.z + ((o >> 2) & 1), c.w + 1));
     }
     // polynomial to subtract: the fit, or (refined nodes) the last refinement correction
@@ -203,7 +209,7 @@ __global__ void __launch_bounds__(K6_THREADS, 2)
   __syncthreads();
   const SmemCoef coef(sa);
   const int gw = warp % G, sub = warp / G;
-  double acc[MG > 0 ? MG : 1];
+  double acc[(kProj && MG > 0) ? MG : 1];
 #pragma unroll
   for (int k = 0; k < MG; ++k) acc[k] = 0.0;
   double ss = 0.0;
@@ -241,7 +247,7 @@ __global__ void __launch_bounds__(K6_THREADS, 2)
         X[k] = st[e]; Y[k] = st[K6_BATCH + e]; Z[k] = st[2 * K6_BATCH + e]; R[k] = st[3 * K6_BATCH + e];
       }
     }
-    if (horner) {
+    if (kHorner && horner) {
       double hx[K6_PPT], hy[K6_PPT], hz[K6_PPT], pv[K6_PPT];
 #pragma unroll
       for (int k = 0; k < K6_PPT; ++k) {
@@ -252,7 +258,7 @@ __global__ void __launch_bounds__(K6_THREADS, 2)
       if constexpr (K6_PPT == 4) {
         horner3x4<P>(coef, hx, hy, hz, pv);
       } else {
-        static_assert(K6_PPT == 2 || P < 0, "K6_PPT");
+        static_assert(K6_PPT == 2 || P < 0, "points per thread");
         horner3x2<P>(coef, hx[0], hy[0], hz[0], hx[1], hy[1], hz[1], pv[0], pv[1]);
       }
 #pragma unroll
@@ -261,7 +267,7 @@ __global__ void __launch_bounds__(K6_THREADS, 2)
         if (V[k]) { r[base + tid + k * K6_THREADS] = R[k]; ss = fma(R[k], R[k], ss); }
       }
     }
-    if (project) {
+    if constexpr (kProj) if (project) {
 #pragma unroll
       for (int k = 0; k < K6_PPT; ++k) {
         const int j = tid + k * K6_THREADS;
@@ -281,7 +287,7 @@ __global__ void __launch_bounds__(K6_THREADS, 2)
   for (int s = 16; s > 0; s >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, s);
   if (lane == 0) redw[warp] = ss;
   // projection: lane reduction per output, then over the SUB warps of a group in fixed order
-  if (project) {
+  if constexpr (kProj) if (project) {
     const int ob = [&] {
       int v = 0;
 #pragma unroll
@@ -356,27 +362,38 @@ __global__ void __launch_bounds__(256)
 
 }  // namespace
 
-template <int P>
-void level_residual(const LevelCtx& c, int mode, int iter, const double* delta, const Chunk* chunks,
-                    const int64_t* nchunks_dev, int64_t max_chunks, const int64_t* chunk_begin, int64_t nseg,
-                    double* partial, double* segsum, cudaStream_t s, const int32_t* sel) {
-  const int kid = mode == K6_ROOT ? KID_PROJECT : (mode == K6_OWN ? KID_REFINE : KID_RESIDUAL);
+template <int P, int VAR>
+void launch_residual(int kid, const LevelCtx& c, int mode, int iter, const double* delta, const Chunk* chunks,
+                     const int64_t* nchunks_dev, int64_t max_chunks, double* partial, cudaStream_t s) {
   static std::once_flag attr_once;  // one opt-in per kernel instantiation (thread-safe)
   std::call_once(attr_once, [&] {
     FMI_CK(cudaFuncSetAttribute(
-        k_residual<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)K6_STAGE_SMEM));
+        k_residual<P, VAR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k6_stage_smem(VAR)));
   });
-  if (max_chunks > 0)
-    FMI_LAUNCH(kid, s, k_residual<P>, (unsigned)max_chunks, K6_THREADS, K6_STAGE_SMEM, c.ux, c.uy, c.uz, c.r, c.nt,
-               c.first, chunks, nchunks_dev, c.depth, c.D, mode, iter, delta, partial);
+  FMI_LAUNCH(kid, s, (k_residual<P, VAR>), (unsigned)max_chunks, K6_THREADS, k6_stage_smem(VAR), c.ux, c.uy, c.uz, c.r,
+             c.nt, c.first, chunks, nchunks_dev, c.depth, c.D, mode, iter, delta, partial);
+}
+
+template <int P>
+void level_residual(const LevelCtx& c, int mode, int iter, const double* delta, const Chunk* chunks,
+                    const int64_t* nchunks_dev, int64_t max_chunks, const int64_t* chunk_begin, int64_t nseg,
+                    double* partial, double* segsum, cudaStream_t s, const int32_t* sel, bool horner_only) {
+  const int kid = mode == K6_ROOT ? KID_PROJECT : (mode == K6_OWN ? KID_REFINE : KID_RESIDUAL);
+  if (max_chunks > 0) {
+    if (mode == K6_ROOT || mode == K6_PROJ)
+      launch_residual<P, 2>(kid, c, mode, iter, delta, chunks, nchunks_dev, max_chunks, partial, s);
+    else if (mode == K6_CHILD && horner_only)
+      launch_residual<P, 1>(kid, c, mode, iter, delta, chunks, nchunks_dev, max_chunks, partial, s);
+    else
+      launch_residual<P, 0>(kid, c, mode, iter, delta, chunks, nchunks_dev, max_chunks, partial, s);
+  }
   FMI_LAUNCH(KID_RESIDUAL_REDUCE, s, k_residual_reduce, dim3((unsigned)nseg, (unsigned)((rank3(P) + 1 + 31) / 32)), 256,
-             0, partial, chunk_begin, nchunks_dev, nseg,
-             c.nt, c.first, rank3(P), mode == K6_CHILD, sel, segsum);
+             0, partial, chunk_begin, nchunks_dev, nseg, c.nt, c.first, rank3(P), mode == K6_CHILD, sel, segsum);
 }
 
 #define FMI_INST(P)                                                                                            \
   template void level_residual<P>(const LevelCtx&, int, int, const double*, const Chunk*, const int64_t*, int64_t, \
-                                  const int64_t*, int64_t, double*, double*, cudaStream_t, const int32_t*);
+                                  const int64_t*, int64_t, double*, double*, cudaStream_t, const int32_t*, bool);
 FMI_INST(0) FMI_INST(1) FMI_INST(2) FMI_INST(3) FMI_INST(4) FMI_INST(5)
 FMI_INST(6) FMI_INST(7) FMI_INST(8) FMI_INST(9) FMI_INST(10)
 #undef FMI_INST

@@ -459,13 +459,16 @@ __global__ void __launch_bounds__(k5_threads<P>(), k5_threads<P>() == 256 ? 2 : 
       // (the parent's octant Σr²) minus the energy the fit removes (‖y‖²), over its points — is below
       // defer_tau: its children are then unlikely to be created (K6_PROJ runs for those that are)
       int defer = 0;
-      if (par >= 0 && defer_tau > 0.0) {
+      if (isinf(defer_tau)) {  // split K6 (FMI_K6_SPLIT): every node's projections run in K6_PROJ
+        defer = 8;
+      } else if (par >= 0 && defer_tau > 0.0) {
         const int oc = (cc.x & 1) | ((cc.y & 1) << 1) | ((cc.z & 1) << 2);
         const double e_post2 = fmax(nt.child_ss[(int64_t)par * 8 + oc] - ynorm_sh, 0.0) / fmax(npts, 1.0);
         defer = e_post2 < defer_tau * defer_tau ? 8 : 0;
       }
       nt.flag[first + node] = fl | defer;
       if (fl == 2) atomicAdd(reinterpret_cast<unsigned long long*>(nflag), 1ull);
+      if (defer) atomicAdd(reinterpret_cast<unsigned long long*>(nflag + 2), 1ull);
     }
     __syncthreads();
   }
