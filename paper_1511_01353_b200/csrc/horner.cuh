@@ -7,7 +7,9 @@
 
 namespace fmi {
 
-// COEF(i) must yield coefficient i (e.g. a shared-memory read or an __ldg).
+// COEF(i) must yield coefficient i (e.g. a shared-memory read or an __ldg).  Every Horner chain starts
+// at its highest coefficient (no fma(0, z, a) = a step: that product is not foldable by the compiler,
+// z may be non-finite, and would cost one FP64 instruction per row).
 template <int P, typename Coef>
 __device__ __forceinline__ double horner3(const Coef& coef, double x, double y, double z) {
   double px = 0.0;
@@ -20,12 +22,12 @@ __device__ __forceinline__ double horner3(const Coef& coef, double x, double y, 
       double cr[P + 1];
 #pragma unroll
       for (int n = 0; n <= P - l - m; ++n) cr[n] = coef(basis_index(P, l, m, n));
-      double pz = 0.0;
+      double pz = cr[P - l - m];
 #pragma unroll
-      for (int n = P - l - m; n >= 0; --n) pz = fma(pz, z, cr[n]);
-      py = fma(py, y, pz);
+      for (int n = P - l - m - 1; n >= 0; --n) pz = fma(pz, z, cr[n]);
+      py = (m == P - l) ? pz : fma(py, y, pz);
     }
-    px = fma(px, x, py);
+    px = (l == P) ? py : fma(px, x, py);
   }
   return px;
 }
@@ -62,17 +64,17 @@ __device__ __forceinline__ void horner3x2(const Coef& coef, double x0, double y0
     for (int m = P - l; m >= 0; --m) {
       double cr[P + 1];
       load_row<P>(coef, basis_index(P, l, m, 0), P - l - m + 1, cr);
-      double pz0 = 0.0, pz1 = 0.0;
+      double pz0 = cr[P - l - m], pz1 = cr[P - l - m];
 #pragma unroll
-      for (int n = P - l - m; n >= 0; --n) {
+      for (int n = P - l - m - 1; n >= 0; --n) {
         pz0 = fma(pz0, z0, cr[n]);
         pz1 = fma(pz1, z1, cr[n]);
       }
-      py0 = fma(py0, y0, pz0);
-      py1 = fma(py1, y1, pz1);
+      py0 = (m == P - l) ? pz0 : fma(py0, y0, pz0);
+      py1 = (m == P - l) ? pz1 : fma(py1, y1, pz1);
     }
-    px0 = fma(px0, x0, py0);
-    px1 = fma(px1, x1, py1);
+    px0 = (l == P) ? py0 : fma(px0, x0, py0);
+    px1 = (l == P) ? py1 : fma(px1, x1, py1);
   }
   v0 = px0;
   v1 = px1;
@@ -88,18 +90,21 @@ __device__ __forceinline__ void horner3x4(const Coef& coef, const double* x, con
     double py[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
     for (int m = P - l; m >= 0; --m) {
-      double pz[4] = {0.0, 0.0, 0.0, 0.0};
+      double cr[P + 1];
+      load_row<P>(coef, basis_index(P, l, m, 0), P - l - m + 1, cr);
+      double pz[4];
 #pragma unroll
-      for (int n = P - l - m; n >= 0; --n) {
-        const double a = coef(basis_index(P, l, m, n));
+      for (int k = 0; k < 4; ++k) pz[k] = cr[P - l - m];
 #pragma unroll
-        for (int k = 0; k < 4; ++k) pz[k] = fma(pz[k], z[k], a);
+      for (int n = P - l - m - 1; n >= 0; --n) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) pz[k] = fma(pz[k], z[k], cr[n]);
       }
 #pragma unroll
-      for (int k = 0; k < 4; ++k) py[k] = fma(py[k], y[k], pz[k]);
+      for (int k = 0; k < 4; ++k) py[k] = (m == P - l) ? pz[k] : fma(py[k], y[k], pz[k]);
     }
 #pragma unroll
-    for (int k = 0; k < 4; ++k) px[k] = fma(px[k], x[k], py[k]);
+    for (int k = 0; k < 4; ++k) px[k] = (l == P) ? py[k] : fma(px[k], x[k], py[k]);
   }
 #pragma unroll
   for (int k = 0; k < 4; ++k) v[k] = px[k];

@@ -150,7 +150,7 @@ __device__ __forceinline__ void proj_run(int gw, const double* sx, const double*
 // VAR: 0 = fused (Horner + Σr² + projections), 1 = Horner + Σr² only, 2 = projections only — the
 // specialised variants carry no registers for the part they skip
 template <int P, int VAR>
-__global__ void __launch_bounds__(K6_THREADS, VAR == 1 ? 3 : 2)
+__global__ void __launch_bounds__(K6_THREADS, 2)
     k_residual(const double* __restrict__ ux, const double* __restrict__ uy, const double* __restrict__ uz,
                double* __restrict__ r, NodeTable nt, int64_t first, const Chunk* __restrict__ chunks,
                const int64_t* __restrict__ nchunks, int depth, int D, int mode, int iter,
