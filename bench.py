@@ -357,13 +357,18 @@ def main():
     roofs = rooflines(cfg, levels_points, len(levels_points) - 1, prof, args.steps, ms_per_step, hbm_peak,
                       proj_pts)
     dominant = max(roofs, key=lambda k: roofs[k]["share_of_step"]) if roofs else None
-    # DRAM traffic of one launch from an ncu --set full capture (profiles/round1_ncu_kernels_cfg5.txt):
-    # k_residual at level 3 of cfg 5 (2e8 points): 6.42 GB read + 1.60 GB written = algorithmic
-    # 40 B/point (ux, uy, uz, r read; r written) — no wasted re-reads
-    if dominant == "residual" and cfg.cfg == 5 and roofs.get("residual"):
-        roofs["residual"]["traffic"] = 8.03e9
-        roofs["residual"]["traffic_note"] = ("ncu dram__bytes_read+write of the level-3 launch (2e8 points); "
-                                             "algorithmic 40 B/point = 8.0e9")
+    # DRAM traffic per k_residual launch from an ncu capture of one cfg-5 build (tools/gpu/run48.sh,
+    # profiles/round1_k6_traffic_cfg5.csv): the step's 11 launches (6 Horner-only passes, 5 projection
+    # passes) move 63.45 GB = the algorithmic 40 B per point-level + 32 B per projected point (no re-reads)
+    if cfg.cfg == 5 and roofs.get("residual"):
+        roofs["residual"]["traffic"] = 63.45e9 / 11
+        roofs["residual"]["traffic_note"] = ("ncu dram__bytes_read+write summed over the 11 k_residual launches of a "
+                                             "cfg-5 build / 11; algorithmic 40 B/point-level + 32 B/projected point")
+    # k_moments (one launch per build): 4.82 GB read (= the algorithmic 24 B/point) + 2.90 GB of per-chunk
+    # partial sums written (profiles/round1_ncu_k4_traffic.txt)
+    if cfg.cfg == 5 and roofs.get("moments"):
+        roofs["moments"]["traffic"] = 7.71e9
+        roofs["moments"]["traffic_note"] = "ncu dram__bytes_read+write of the cfg-5 launch: 4.82 GB read + 2.90 GB written"
     step_kernel_ms = sum(v[0] for v in prof.values()) / args.steps
 
     # ---- e2e through the C ABI with pinned host buffers -----------------------------------------
