@@ -18,6 +18,7 @@
 #include <mutex>
 #include <utility>
 
+#include "groups.cuh"
 #include "horner.cuh"
 
 namespace fmi {
@@ -121,12 +122,9 @@ __device__ __forceinline__ void proj_accum(double x, double y, double z, double 
     if constexpr (CM >= 1) zp[1] = z;
 #pragma unroll
     for (int c = 2; c <= CM; ++c) zp[c] = zp[c / 2] * zp[c - c / 2];  // log-depth power tree
-    double xr = r;
-#pragma unroll
-    for (int e = 0; e < pair_a(P, q0); ++e) xr *= x;
-    double v = xr;
-#pragma unroll
-    for (int e = 0; e < pair_b(P, q0); ++e) v *= y;
+    // first pair's x^a r and x^a y^b r by square-and-multiply (log-depth)
+    const double xr = grp::cpow<pair_a(P, q0)>(x) * r;
+    const double v = xr * grp::cpow<pair_b(P, q0)>(y);
     proj_pairs<P, q0, q1, o0>(x, y, zp, xr, v, acc);
   }
 }
