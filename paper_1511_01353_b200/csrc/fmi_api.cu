@@ -334,6 +334,8 @@ bool is_device_ptr(const void* p) {
 // host-buffer overlaps (late value upload, query upload during the fit) only pay off on large inputs;
 // FMI_NO_OVERLAP=1 disables them (diagnostics)
 constexpr int64_t kOverlapMin = (int64_t)1 << 20;
+// K6 split (Horner-only pass + projections of created children) from this many points per level on
+constexpr int64_t kSplitMinPoints = (int64_t)1 << 25;
 bool no_overlap() {
   static const bool v = std::getenv("FMI_NO_OVERLAP") != nullptr;
   return v;
@@ -502,7 +504,8 @@ void run_levels(fmi_tree* T, const uint64_t* keys, double* ux, double* uy, doubl
       FMI_CK(cudaMemsetAsync(nflag.p, 0, 3 * sizeof(int64_t), s));
       scratch.ensure((size_t)count * fac_per_node, s);
       // deferral: single shard only; split mode defers every node (Horner-only K6 + K6_PROJ)
-      const double defer_tau = global ? 0.0 : (T->k6_split ? INFINITY : T->defer_theta * T->tau);
+      const double defer_tau =
+          global ? 0.0 : ((T->k6_split && points >= kSplitMinPoints) ? INFINITY : T->defer_theta * T->tau);
       level_solve<P>(c, lvlmom.p, 0, nullptr, nullptr, T->refine2, T->refine_fill, T->Ntot, nflag.p, scratch.p, s,
                      defer_tau);
       FMI_CK(cudaMemcpyAsync(&host_small[2], nflag.p, 3 * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
@@ -549,8 +552,9 @@ void run_levels(fmi_tree* T, const uint64_t* keys, double* ux, double* uy, doubl
       // children; when at least half of the nodes deferred their projections (predicted leaves), all are
       // deferred and the level runs the Horner-only K6 (more points in flight per thread, no projection
       // registers) followed by K6_PROJ for the children actually created
-      bool horner_only = T->k6_split && !global;
-      if (!global && !horner_only && ndefer_nodes * 2 >= count && ndefer_nodes > 0) {
+      // the split pays on big levels (cfg 5: 2e8 points); small adaptive levels keep the fused pass
+      bool horner_only = T->k6_split && !global && points >= kSplitMinPoints;
+      if (!global && !horner_only && points >= kSplitMinPoints && ndefer_nodes * 2 >= count && ndefer_nodes > 0) {
         if (ndefer_nodes < count)
           FMI_LAUNCH(KID_MISC, s, k_defer_all, (unsigned)((count + 255) / 256), 256, 0, T->nt, first, count);
         horner_only = true;
