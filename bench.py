@@ -84,6 +84,9 @@ class ClockSampler:
     def __init__(self, index: int):
         self.samples, self.reasons, self.max_mhz = [], set(), None
         self._stop = threading.Event()
+        if os.environ.get("FMI_BENCH_NO_CLOCKS"):  # diagnostics: no NVML sampling
+            self.nv = None
+            return
         try:
             import pynvml
             pynvml.nvmlInit()
