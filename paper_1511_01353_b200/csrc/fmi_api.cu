@@ -217,6 +217,7 @@ struct fmi_tree {
   int64_t mt_min = 0;                // moment-tree cell minimum (points); env FMI_MT_FILL (multiple of 𝓛)
   double defer_theta = kDeferTheta;  // env FMI_DEFER_THETA (0: never defer)
   bool k6_split = true;              // env FMI_K6_SPLIT=0: fused K6 (Horner + projections in one pass)
+  int64_t split_min = 0;             // levels with at least this many points run the split K6
   int64_t deferred_children = 0;     // children whose projections ran in a K6_PROJ pass
   double tau = 0;
   double lo[3] = {0, 0, 0};
@@ -335,7 +336,8 @@ bool is_device_ptr(const void* p) {
 // FMI_NO_OVERLAP=1 disables them (diagnostics)
 constexpr int64_t kOverlapMin = (int64_t)1 << 20;
 // K6 split (Horner-only pass + projections of created children) from this many points per level on
-constexpr int64_t kSplitMinPoints = (int64_t)1 << 25;
+// (env FMI_K6_SPLIT_MIN overrides: the parity tests force the split at small sizes)
+constexpr int64_t kSplitMinPointsDefault = (int64_t)1 << 25;
 bool no_overlap() {
   static const bool v = std::getenv("FMI_NO_OVERLAP") != nullptr;
   return v;
@@ -505,7 +507,7 @@ void run_levels(fmi_tree* T, const uint64_t* keys, double* ux, double* uy, doubl
       scratch.ensure((size_t)count * fac_per_node, s);
       // deferral: single shard only; split mode defers every node (Horner-only K6 + K6_PROJ)
       const double defer_tau =
-          global ? 0.0 : ((T->k6_split && points >= kSplitMinPoints) ? INFINITY : T->defer_theta * T->tau);
+          global ? 0.0 : ((T->k6_split && points >= T->split_min) ? INFINITY : T->defer_theta * T->tau);
       level_solve<P>(c, lvlmom.p, 0, nullptr, nullptr, T->refine2, T->refine_fill, T->Ntot, nflag.p, scratch.p, s,
                      defer_tau);
       FMI_CK(cudaMemcpyAsync(&host_small[2], nflag.p, 3 * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
@@ -553,8 +555,8 @@ void run_levels(fmi_tree* T, const uint64_t* keys, double* ux, double* uy, doubl
       // deferred and the level runs the Horner-only K6 (more points in flight per thread, no projection
       // registers) followed by K6_PROJ for the children actually created
       // the split pays on big levels (cfg 5: 2e8 points); small adaptive levels keep the fused pass
-      bool horner_only = T->k6_split && !global && points >= kSplitMinPoints;
-      if (!global && !horner_only && points >= kSplitMinPoints && ndefer_nodes * 2 >= count && ndefer_nodes > 0) {
+      bool horner_only = T->k6_split && !global && points >= T->split_min;
+      if (!global && !horner_only && points >= T->split_min && ndefer_nodes * 2 >= count && ndefer_nodes > 0) {
         if (ndefer_nodes < count)
           FMI_LAUNCH(KID_MISC, s, k_defer_all, (unsigned)((count + 255) / 256), 256, 0, T->nt, first, count);
         horner_only = true;
@@ -800,6 +802,8 @@ fmi_tree* build_impl(const double* pts, const double* f, int64_t N, int degree, 
     if (const char* e = std::getenv("FMI_REFINE_FILL")) T->refine_fill = std::atof(e);
     if (const char* e = std::getenv("FMI_DEFER_THETA")) T->defer_theta = std::atof(e);
     if (const char* e = std::getenv("FMI_K6_SPLIT")) T->k6_split = std::atoi(e) != 0;
+    T->split_min = kSplitMinPointsDefault;
+    if (const char* e = std::getenv("FMI_K6_SPLIT_MIN")) T->split_min = std::atoll(e);
     {
       double mf = kMomentTreeFill;
       if (const char* e = std::getenv("FMI_MT_FILL")) mf = std::atof(e);

@@ -236,3 +236,16 @@ def test_deep_cluster_resorts_all_levels():
     q = np.vstack([rng.random((1000, 3)), 0.3 + 1e-4 * rng.random((1000, 3))])
     ora, gpu, *_ = check_parity(pts, f, 1, 1e-12, 16, q)
     assert int(np.max(ora.depth)) >= 8
+
+
+@pytest.mark.parametrize("split_min", ["0", "1000000000000"])
+def test_k6_split_and_fused_match_the_oracle(split_min, monkeypatch):
+    """The split K6 (Horner-only pass + projections of the created children; used on levels of >= 2^25
+    points) and the fused pass (Horner + projections of every potential child) give the oracle's tree at
+    a size where every level is small: FMI_K6_SPLIT_MIN forces the choice."""
+    monkeypatch.setenv("FMI_K6_SPLIT_MIN", split_min)
+    cfg = workloads.CONFIGS[2]
+    pts, f, q = workloads.make_inputs(cfg)
+    q = q[:50_000]
+    ora, gpu, *_ = check_parity(pts, f, cfg.degree, cfg.tol, cfg.max_depth, q, erms_vs=workloads.franke3d)
+    assert ora.node_count == 585
