@@ -6,7 +6,8 @@
 // of Λ.  This path computes exactly that R without forming the monomial Gram:
 //   1. V = the Vandermonde of the tensor Legendre basis s_a s_b s_c P_a(x) P_b(y) P_c(z) (s_k = √(2k+1)),
 //      same polynomial space, well conditioned on space-filling point sets; the RHS f is its last column;
-//   2. G = [V f]ᵀ[V f] by a split-K SYRK (64×64 register-tiled tiles, fixed-order split reduction);
+//   2. G = [V f]ᵀ[V f] by a split-K SYRK on the FP64 tensor cores (DMMA m8n8k4; fixed-order split
+//      reduction);
 //   3. bordered Cholesky G = R_Vᵀ R_V in one CTA: the last row gives y = Qᵀf and ρ = ‖f − V V⁺f‖;
 //   4. the monomial basis is Λ = V C with C upper triangular in the Algorithm-2 order (x^a = Σ_k e_ak
 //      s_k P_k(x) per axis; β ≤ α componentwise ⇒ index(β) ≤ index(α)), so Λ = Q (R_V C): the R of the
@@ -30,7 +31,6 @@ namespace {
 
 constexpr int UMAXP = 14;
 constexpr int UT = 64;    // SYRK tile
-constexpr int UK = 8;     // SYRK k-slice
 constexpr int UTHREADS = 256;
 
 // x^a = Σ_k c_ue[a][k] · s_k P_k(x)
@@ -75,12 +75,19 @@ __global__ void __launch_bounds__(UTHREADS)
 }
 
 // ---- 2. split-K SYRK: part[split] (+)= V[rows of split]ᵀ V[rows of split], lower tiles only ------------
-// 64×64 output tile per CTA of 64 threads, 8×8 register tile per thread (per k: 4 + 4 16-byte shared
-// loads feed 64 FMAs), k-slices of UK rows staged in shared memory with register prefetch of the next.
-constexpr int SY_THREADS = 64;
-__global__ void __launch_bounds__(SY_THREADS)
-    k_syrk(const double* __restrict__ V, int64_t nr, int LDV, int nsplit, bool accumulate,
-           double* __restrict__ part) {
+// Tensor-core variant (FP64 DMMA, mma.sync m8n8k4): the Gram is a dense contraction, so each warp
+// issues 8x8x4 double MMAs — 256 FMAs per instruction instead of 32.  CTA = 4 warps on a 64x64 tile
+// (2x2 warps of 32x32 = 4x4 MMA sub-tiles), k-slices of 16 rows staged in shared memory (rows padded to
+// 72 doubles: the four rows a fragment load touches fall in two bank phases).
+constexpr int SYD_THREADS = 128, SYD_K = 16, SYD_LD = 72;
+__device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+               : "+d"(d0), "+d"(d1) : "d"(a), "d"(b));
+}
+
+__global__ void __launch_bounds__(SYD_THREADS)
+    k_syrk_dmma(const double* __restrict__ V, int64_t nr, int LDV, int nsplit, bool accumulate,
+                double* __restrict__ part) {
   const int t = blockIdx.x;
   int ti = (int)((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
   while ((ti + 1) * (ti + 2) / 2 <= t) ++ti;
@@ -88,19 +95,21 @@ __global__ void __launch_bounds__(SY_THREADS)
   const int tj = t - ti * (ti + 1) / 2;
   const int split = blockIdx.y;
   const int64_t k0 = nr * split / nsplit, k1 = nr * (split + 1) / nsplit;
-  __shared__ __align__(16) double As[UK][UT], Bs[UK][UT];
-  const int tx = threadIdx.x & 7, ty = threadIdx.x >> 3;
-  double acc[8][8];
+  __shared__ __align__(16) double As[SYD_K][SYD_LD], Bs[SYD_K][SYD_LD];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int wm = warp >> 1, wn = warp & 1;  // the warp's 32x32 quadrant
+  const int fr = lane & 3, fc = lane >> 2;  // fragment row (k) and column (m or n) of this lane
+  double acc[4][4][2];
 #pragma unroll
-  for (int a = 0; a < 8; ++a)
+  for (int a = 0; a < 4; ++a)
 #pragma unroll
-    for (int b = 0; b < 8; ++b) acc[a][b] = 0.0;
-  constexpr int NQ = (UK * UT) / SY_THREADS;  // 16
+    for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+  constexpr int NQ = (SYD_K * UT) / SYD_THREADS;  // 8 loads per operand per thread
   double pa[NQ], pb[NQ];
   auto fetch = [&](int64_t kb) {
 #pragma unroll
     for (int q = 0; q < NQ; ++q) {
-      const int e = threadIdx.x + q * SY_THREADS;
+      const int e = threadIdx.x + q * SYD_THREADS;
       const int kk = e / UT, c = e % UT;
       const int64_t row = kb + kk;
       pa[q] = row < k1 ? V[row * LDV + ti * UT + c] : 0.0;
@@ -108,40 +117,39 @@ __global__ void __launch_bounds__(SY_THREADS)
     }
   };
   if (k0 < k1) fetch(k0);
-  for (int64_t kb = k0; kb < k1; kb += UK) {
+  for (int64_t kb = k0; kb < k1; kb += SYD_K) {
 #pragma unroll
     for (int q = 0; q < NQ; ++q) {
-      const int e = threadIdx.x + q * SY_THREADS;
+      const int e = threadIdx.x + q * SYD_THREADS;
       As[e / UT][e % UT] = pa[q];
       Bs[e / UT][e % UT] = pb[q];
     }
     __syncthreads();
-    if (kb + UK < k1) fetch(kb + UK);
-#pragma unroll 4
-    for (int kk = 0; kk < UK; ++kk) {
-      double av[8], bv[8];
+    if (kb + SYD_K < k1) fetch(kb + SYD_K);
 #pragma unroll
-      for (int h = 0; h < 4; ++h) {
-        const double2 a2 = *reinterpret_cast<const double2*>(&As[kk][8 * ty + 2 * h]);
-        const double2 b2 = *reinterpret_cast<const double2*>(&Bs[kk][8 * tx + 2 * h]);
-        av[2 * h] = a2.x; av[2 * h + 1] = a2.y;
-        bv[2 * h] = b2.x; bv[2 * h + 1] = b2.y;
-      }
+    for (int ks = 0; ks < SYD_K; ks += 4) {
+      double af[4], bf[4];  // A[m][k] = V[k][m], B[k][n] = V[k][n]
 #pragma unroll
-      for (int a = 0; a < 8; ++a)
+      for (int ms = 0; ms < 4; ++ms) af[ms] = As[ks + fr][wm * 32 + ms * 8 + fc];
 #pragma unroll
-        for (int b = 0; b < 8; ++b) acc[a][b] = fma(av[a], bv[b], acc[a][b]);
+      for (int ns = 0; ns < 4; ++ns) bf[ns] = Bs[ks + fr][wn * 32 + ns * 8 + fc];
+#pragma unroll
+      for (int ms = 0; ms < 4; ++ms)
+#pragma unroll
+        for (int ns = 0; ns < 4; ++ns) dmma884(acc[ms][ns][0], acc[ms][ns][1], af[ms], bf[ns]);
     }
     __syncthreads();
   }
   double* out = part + (int64_t)split * LDV * LDV;
 #pragma unroll
-  for (int a = 0; a < 8; ++a)
+  for (int ms = 0; ms < 4; ++ms)
 #pragma unroll
-    for (int b = 0; b < 8; ++b) {
-      const int64_t o = (int64_t)(ti * UT + 8 * ty + a) * LDV + tj * UT + 8 * tx + b;
-      out[o] = accumulate ? out[o] + acc[a][b] : acc[a][b];
-    }
+    for (int ns = 0; ns < 4; ++ns)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int64_t o = (int64_t)(ti * UT + wm * 32 + ms * 8 + fc) * LDV + tj * UT + wn * 32 + ns * 8 + 2 * fr + h;
+        out[o] = accumulate ? out[o] + acc[ms][ns][h] : acc[ms][ns][h];
+      }
 }
 
 // G[i][j] = Σ_split part[split][i][j] (fixed order), lower triangle of the leading n×n block
@@ -512,13 +520,13 @@ void unscoped_fit(const LevelCtx& c, cudaStream_t s) {
   const int64_t n = se[1] - se[0];
   // 1-2. Legendre Gram over slabs of rows
   const int64_t slab = std::min<int64_t>(n, std::max<int64_t>(4096, ((int64_t)1 << 28) / LDV));  // <= 2 GB
-  const int nsplit = (int)std::max<int64_t>(1, std::min<int64_t>(std::max(1, 148 * 4 / ntile), slab / 512 + 1));
+  const int nsplit = (int)std::max<int64_t>(1, std::min<int64_t>(std::max(1, 148 * 3 / ntile), slab / 512 + 1));
   DBuf<double> V((size_t)slab * LDV, s), part((size_t)nsplit * LDV * LDV, s), G((size_t)LDV * LDV, s);
   for (int64_t r0 = 0; r0 < n; r0 += slab) {
     const int64_t nr = std::min(slab, n - r0);
     FMI_LAUNCH(KID_UNSCOPED_GRAM, s, k_leg_rows<P>, (unsigned)((nr + 31) / 32), UTHREADS, 0, c.ux + se[0],
                c.uy + se[0], c.uz + se[0], c.r + se[0], r0, nr, el, em, en, L, LDV, V.p);
-    FMI_LAUNCH(KID_UNSCOPED_GRAM, s, k_syrk, dim3((unsigned)ntile, (unsigned)nsplit), SY_THREADS, 0, V.p, nr, LDV,
+    FMI_LAUNCH(KID_UNSCOPED_GRAM, s, k_syrk_dmma, dim3((unsigned)ntile, (unsigned)nsplit), SYD_THREADS, 0, V.p, nr, LDV,
                nsplit, r0 > 0, part.p);
   }
   V.release();
