@@ -79,7 +79,9 @@ struct K5Shape {
   static constexpr int64_t NAB = tri(L) + L;  // packed lower factor + RHS row
   // panel column stride: rows padded to 4 (16-byte vectors of 4 rows), and not a multiple of 16 so that
   // consecutive columns of one row fall in different banks
-  static constexpr int LDP = ((L + 1 + 3) & ~3) % 16 == 0 ? ((L + 1 + 3) & ~3) + 2 : ((L + 1 + 3) & ~3);
+  // (>= L + 8: the 8-row MMA tiles of the trailing update read up to 7 rows past the last one)
+  static constexpr int LDP0 = (L + 8 + 1) & ~1;
+  static constexpr int LDP = LDP0 % 16 == 0 ? LDP0 + 2 : LDP0;
   // shared: moments [K], dinv, piv, 1/piv, y/c [L], column-major panel [KB x LDP], exponents
   static constexpr size_t SMEM = ((size_t)K + 4 * L + (size_t)KB * LDP + 8) * sizeof(double) + 3 * L + 16;
 };
@@ -320,53 +322,60 @@ __global__ void __launch_bounds__(k5_threads<P>(), k5_threads<P>() == 256 ? 2 : 
           const int i = j0 + r;
           if (i == L || c <= r) A[tri(i) + j0 + c] = Pn[c * LDP + r];
         }
-        // trailing update A[i][k] -= Σ_c Pn[i-j0][c] Pn[k-j0][c], j1 <= k <= min(i, L-1), j1 <= i <= L;
-        // 4x4 register tiles, 16-byte vector loads of 4 consecutive panel rows (conflict-free)
+        // trailing update A[i][k] -= Σ_c Pn[i-j0][c] Pn[k-j0][c], j1 <= k <= min(i, L-1), j1 <= i <= L:
+        // a rank-bw SYRK on the FP64 tensor cores — warp = one 8x8 tile of the lower triangle at a time,
+        // bw/4 DMMA (m8n8k4) steps with the fragments read from the column-major panel, the tile's old
+        // values loaded first so their L2 latency overlaps the MMAs
         const int j1 = j0 + bw, R2 = L + 1 - j1;
         if (j1 < L) {
-          const int nt4 = (R2 + 3) / 4;
-          const int ntile = nt4 * (nt4 + 1) / 2;
-          for (int t = tid; t < ntile; t += K5_THREADS) {
-            int ti = (int)((sqrt(8.0 * (double)t + 1.0) - 1.0) * 0.5);
-            while ((ti + 1) * (ti + 2) / 2 <= t) ++ti;
-            while (ti * (ti + 1) / 2 > t) --ti;
-            const int tk = t - ti * (ti + 1) / 2;
-            const int i0 = j1 + 4 * ti, k0 = j1 + 4 * tk;
-            // the old values first: their L2 latency overlaps the register-tile FMAs below
-            double old[4][4];
+          const int nt8 = (R2 + 7) / 8;
+          const int ntile = nt8 * (nt8 + 1) / 2;
+          const int fr = lane & 3, fc = lane >> 2;  // fragment k-row and m/n-column of this lane
+          constexpr int TPW = 4;  // tiles per warp in flight: independent MMA chains and old-value loads
+          for (int t0 = warp * TPW; t0 < ntile; t0 += K5_WARPS * TPW) {
+            int ci[TPW], ck0[TPW];
+            bool v0[TPW], v1[TPW];
+            double old0[TPW], old1[TPW], d0[TPW], d1[TPW];
+            const double* pa[TPW];
+            const double* pb[TPW];
 #pragma unroll
-            for (int a = 0; a < 4; ++a)
-#pragma unroll
-              for (int b = 0; b < 4; ++b) {
-                const int i = i0 + a, k = k0 + b;
-                old[a][b] = (i <= L && k < L && (k <= i || i == L)) ? A[tri(i) + k] : 0.0;
-              }
-            double acc[4][4];
-#pragma unroll
-            for (int a = 0; a < 4; ++a)
-#pragma unroll
-              for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
-            const double* pi = Pn + (i0 - j0);
-            const double* pk = Pn + (k0 - j0);
-            for (int c = 0; c < bw; ++c) {
-              const double2 a01 = *reinterpret_cast<const double2*>(pi + c * LDP);
-              const double2 a23 = *reinterpret_cast<const double2*>(pi + c * LDP + 2);
-              const double2 b01 = *reinterpret_cast<const double2*>(pk + c * LDP);
-              const double2 b23 = *reinterpret_cast<const double2*>(pk + c * LDP + 2);
-              const double av[4] = {a01.x, a01.y, a23.x, a23.y};
-              const double bv[4] = {b01.x, b01.y, b23.x, b23.y};
-#pragma unroll
-              for (int a = 0; a < 4; ++a)
-#pragma unroll
-                for (int b = 0; b < 4; ++b) acc[a][b] = fma(av[a], bv[b], acc[a][b]);
+            for (int u = 0; u < TPW; ++u) {
+              const int t = min(t0 + u, ntile - 1);  // a duplicate of the last tile is computed, not stored
+              int ti = (int)((sqrt(8.0 * (double)t + 1.0) - 1.0) * 0.5);
+              while ((ti + 1) * (ti + 2) / 2 <= t) ++ti;
+              while (ti * (ti + 1) / 2 > t) --ti;
+              const int tk = t - ti * (ti + 1) / 2;
+              const int i0 = j1 + 8 * ti, k0 = j1 + 8 * tk;
+              // this lane's two C elements: row i0 + fc, columns k0 + 2 fr + {0, 1}
+              ci[u] = i0 + fc;
+              ck0[u] = k0 + 2 * fr;
+              const bool own = t0 + u < ntile;
+              v0[u] = own && ci[u] <= L && ck0[u] < L && (ck0[u] <= ci[u] || ci[u] == L);
+              v1[u] = own && ci[u] <= L && ck0[u] + 1 < L && (ck0[u] + 1 <= ci[u] || ci[u] == L);
+              old0[u] = v0[u] ? A[tri(ci[u]) + ck0[u]] : 0.0;
+              old1[u] = v1[u] ? A[tri(ci[u]) + ck0[u] + 1] : 0.0;
+              d0[u] = d1[u] = 0.0;
+              pa[u] = Pn + (i0 - j0) + fc + fr * LDP;
+              pb[u] = Pn + (k0 - j0) + fc + fr * LDP;
             }
 #pragma unroll
-            for (int a = 0; a < 4; ++a)
+            for (int c = 0; c < KB; c += 4) {
+              if (c < bw) {  // columns past bw (last panel) enter as zeros
+                const bool in = c + fr < bw;
 #pragma unroll
-              for (int b = 0; b < 4; ++b) {
-                const int i = i0 + a, k = k0 + b;
-                if (i <= L && k < L && (k <= i || i == L)) A[tri(i) + k] = old[a][b] - acc[a][b];
+                for (int u = 0; u < TPW; ++u) {
+                  const double a = in ? pa[u][c * LDP] : 0.0;
+                  const double b = in ? pb[u][c * LDP] : 0.0;
+                  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+                               : "+d"(d0[u]), "+d"(d1[u]) : "d"(a), "d"(b));
+                }
               }
+            }
+#pragma unroll
+            for (int u = 0; u < TPW; ++u) {
+              if (v0[u]) A[tri(ci[u]) + ck0[u]] = old0[u] - d0[u];
+              if (v1[u]) A[tri(ci[u]) + ck0[u] + 1] = old1[u] - d1[u];
+            }
           }
         }
         __syncthreads();
