@@ -111,6 +111,7 @@ __global__ void __launch_bounds__(k5_threads<P>(), k5_threads<P>() == 256 ? 2 : 
   __shared__ double ynorm_sh;
   __shared__ double errw[K5_WARPS];
   __shared__ double sinv[KB];  // inverse pivots of the current panel
+  __shared__ double Dg[KB * KB];  // lookahead: the next panel's diagonal block (column-major, ld KB)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   for (int i = tid; i < L; i += K5_THREADS) { bl[i] = bt.l[i]; bm[i] = bt.m[i]; bn[i] = bt.n[i]; }
   __syncthreads();
@@ -222,6 +223,51 @@ __global__ void __launch_bounds__(k5_threads<P>(), k5_threads<P>() == 256 ? 2 : 
       }
       K5T(0)
       // ---- blocked right-looking Cholesky with column rejection, RHS row carried along ---------
+      auto diag = [&](double* buf, int ld, int jb, int bwd) {
+        // diagonal block: unblocked Cholesky with column rejection by warp 0, lane = row, the row in
+        // registers; column entries travel by shuffles (no shared-memory round trips)
+        double row[KB];
+#pragma unroll
+        for (int c = 0; c < KB; ++c) row[c] = (c <= lane && lane < bwd) ? buf[c * ld + lane] : 0.0;
+#pragma unroll
+        for (int c = 0; c < KB; ++c) {
+          if (c < bwd) {
+            const int j = jb + c;
+            const double sjj = __shfl_sync(0xffffffffu, row[c], c);
+            const bool keep = dinv[j] > 0.0 && sjj > delta2;
+            // one reciprocal square root on the column-to-column critical path (p = sjj·rsqrt(sjj))
+            const double inv = keep ? rsqrt(sjj) : 0.0;
+            const double p = keep ? sjj * inv : 0.0;
+            if (lane == 0) {
+              piv[j] = p;
+              sinv[c] = inv;
+              pinv[j] = inv;
+              if (dinv[j] > 0.0 && !(sjj >= smin_sh)) smin_sh = sjj;  // also catches NaN
+            }
+            row[c] = lane == c ? p : row[c] * inv;
+            if (p > 0.0) {
+              // L[c2][c] from lane c2, 8 shuffles in flight before their FMAs (a shuffle->FMA pair per
+              // column entry would serialise on the shuffle latency)
+#pragma unroll
+              for (int b0 = c + 1; b0 < KB; b0 += 8) {
+                double l2[8];
+#pragma unroll
+                for (int k = 0; k < 8; ++k)
+                  if (b0 + k < KB) l2[k] = __shfl_sync(0xffffffffu, row[c], b0 + k);
+#pragma unroll
+                for (int k = 0; k < 8; ++k)
+                  if (b0 + k < KB && lane >= b0 + k) row[b0 + k] -= row[c] * l2[k];
+              }
+            }
+          }
+        }
+        if (lane < bwd) {
+#pragma unroll
+          for (int c = 0; c < KB; ++c)
+            if (c <= lane) buf[c * ld + lane] = row[c];
+        }
+      };
+      bool dg_ready = false;  // Dg holds the factored diagonal block of the current panel
       for (int j0 = 0; j0 < L; j0 += KB) {
         const int bw = min(KB, L - j0), R = L - j0 + 1;  // panel rows j0..L (row L = RHS)
         // panel load: 8 independent L2 loads in flight per thread before their shared-memory stores
@@ -237,7 +283,11 @@ __global__ void __launch_bounds__(k5_threads<P>(), k5_threads<P>() == 256 ? 2 : 
               const int r = e / bw, c = e - r * bw;
               const int i = j0 + r;
               pos[k] = c * LDP + r;
-              if (i == L || c <= r) v[k] = A[tri(i) + j0 + c];
+              if (r < bw && dg_ready) {
+                if (c <= r) v[k] = Dg[c * KB + r];
+              } else if (i == L || c <= r) {
+                v[k] = A[tri(i) + j0 + c];
+              }
             }
           }
 #pragma unroll
@@ -246,49 +296,10 @@ __global__ void __launch_bounds__(k5_threads<P>(), k5_threads<P>() == 256 ? 2 : 
         }
         __syncthreads();
         K5T(1)
-        // (1) diagonal block: unblocked Cholesky with column rejection by warp 0, lane = row, the row
-        // in registers; column entries travel by shuffles (no shared-memory round trips)
-        if (warp == 0) {
-          double row[KB];
-#pragma unroll
-          for (int c = 0; c < KB; ++c) row[c] = (c <= lane && lane < bw) ? Pn[c * LDP + lane] : 0.0;
-#pragma unroll
-          for (int c = 0; c < KB; ++c) {
-            if (c < bw) {
-              const int j = j0 + c;
-              const double sjj = __shfl_sync(0xffffffffu, row[c], c);
-              const bool keep = dinv[j] > 0.0 && sjj > delta2;
-              // one reciprocal square root on the column-to-column critical path (p = sjj·rsqrt(sjj))
-              const double inv = keep ? rsqrt(sjj) : 0.0;
-              const double p = keep ? sjj * inv : 0.0;
-              if (lane == 0) {
-                piv[j] = p;
-                sinv[c] = inv;
-                pinv[j] = inv;
-                if (dinv[j] > 0.0 && !(sjj >= smin_sh)) smin_sh = sjj;  // also catches NaN
-              }
-              row[c] = lane == c ? p : row[c] * inv;
-              if (p > 0.0) {
-                // L[c2][c] from lane c2, 8 shuffles in flight before their FMAs (a shuffle->FMA pair per
-                // column entry would serialise on the shuffle latency)
-#pragma unroll
-                for (int b0 = c + 1; b0 < KB; b0 += 8) {
-                  double l2[8];
-#pragma unroll
-                  for (int k = 0; k < 8; ++k)
-                    if (b0 + k < KB) l2[k] = __shfl_sync(0xffffffffu, row[c], b0 + k);
-#pragma unroll
-                  for (int k = 0; k < 8; ++k)
-                    if (b0 + k < KB && lane >= b0 + k) row[b0 + k] -= row[c] * l2[k];
-                }
-              }
-            }
-          }
-          if (lane < bw) {
-#pragma unroll
-            for (int c = 0; c < KB; ++c)
-              if (c <= lane) Pn[c * LDP + lane] = row[c];
-          }
+        // (1) diagonal block (warp 0, lane = row, registers + shuffles) — already factored into Dg by
+        // the lookahead of the previous panel, except for the first panel
+        if (!dg_ready) {
+          if (warp == 0) diag(Pn, LDP, j0, bw);
         }
         __syncthreads();
         K5T(2)
@@ -328,11 +339,31 @@ __global__ void __launch_bounds__(k5_threads<P>(), k5_threads<P>() == 256 ? 2 : 
         // values loaded first so their L2 latency overlaps the MMAs
         const int j1 = j0 + bw, R2 = L + 1 - j1;
         if (j1 < L) {
+          // lookahead (8-warp CTAs, p >= 9): the next panel's diagonal block (updated by this panel)
+          // into Dg, then warp 0 factors it while the other warps apply the rest of the trailing update;
+          // smaller CTAs keep every warp on the trailing update
+          constexpr bool kLook = K5_WARPS >= 8;
+          const int bw2 = kLook ? min(KB, L - j1) : 0;
+          for (int e = tid; e < bw2 * bw2; e += K5_THREADS) {
+            const int r = e / bw2, c = e - r * bw2;
+            if (c > r) continue;
+            const double* pr = Pn + (j1 - j0 + r);
+            const double* pc = Pn + (j1 - j0 + c);
+            double acc = 0.0;
+            for (int q = 0; q < bw; ++q) acc = fma(pr[q * LDP], pc[q * LDP], acc);
+            Dg[c * KB + r] = A[tri(j1 + r) + j1 + c] - acc;
+          }
+          if constexpr (kLook) {
+            __syncthreads();
+            if (warp == 0) diag(Dg, KB, j1, bw2);
+          }
+          const int iend = j1 + bw2;  // rows j1..iend-1 (cols <= row): the next diagonal block (in Dg)
           const int nt8 = (R2 + 7) / 8;
           const int ntile = nt8 * (nt8 + 1) / 2;
           const int fr = lane & 3, fc = lane >> 2;  // fragment k-row and m/n-column of this lane
           constexpr int TPW = 4;  // tiles per warp in flight: independent MMA chains and old-value loads
-          for (int t0 = warp * TPW; t0 < ntile; t0 += K5_WARPS * TPW) {
+          const int tw = kLook ? warp - 1 : warp, nw = kLook ? K5_WARPS - 1 : K5_WARPS;  // trailing warps
+          for (int t0 = tw * TPW; tw >= 0 && t0 < ntile; t0 += nw * TPW) {
             int ci[TPW], ck0[TPW];
             bool v0[TPW], v1[TPW];
             double old0[TPW], old1[TPW], d0[TPW], d1[TPW];
@@ -349,7 +380,7 @@ __global__ void __launch_bounds__(k5_threads<P>(), k5_threads<P>() == 256 ? 2 : 
               // this lane's two C elements: row i0 + fc, columns k0 + 2 fr + {0, 1}
               ci[u] = i0 + fc;
               ck0[u] = k0 + 2 * fr;
-              const bool own = t0 + u < ntile;
+              const bool own = t0 + u < ntile && i0 + 7 >= iend;  // not entirely in the next diagonal block
               v0[u] = own && ci[u] <= L && ck0[u] < L && (ck0[u] <= ci[u] || ci[u] == L);
               v1[u] = own && ci[u] <= L && ck0[u] + 1 < L && (ck0[u] + 1 <= ci[u] || ci[u] == L);
               old0[u] = v0[u] ? A[tri(ci[u]) + ck0[u]] : 0.0;
@@ -373,11 +404,12 @@ __global__ void __launch_bounds__(k5_threads<P>(), k5_threads<P>() == 256 ? 2 : 
             }
 #pragma unroll
             for (int u = 0; u < TPW; ++u) {
-              if (v0[u]) A[tri(ci[u]) + ck0[u]] = old0[u] - d0[u];
-              if (v1[u]) A[tri(ci[u]) + ck0[u] + 1] = old1[u] - d1[u];
+              if (v0[u] && ci[u] >= iend) A[tri(ci[u]) + ck0[u]] = old0[u] - d0[u];
+              if (v1[u] && ci[u] >= iend) A[tri(ci[u]) + ck0[u] + 1] = old1[u] - d1[u];
             }
           }
         }
+        dg_ready = (K5_WARPS >= 8) && j1 < L;
         __syncthreads();
         K5T(4)
       }
