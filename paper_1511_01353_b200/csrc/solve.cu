@@ -124,9 +124,14 @@ __global__ void __launch_bounds__(k5_threads<P>(), k5_threads<P>() == 256 ? 2 : 
     if (mode == 2 && !(nt.flag[first + node] & 4)) continue;
     double* A = fac + node * S::NAB;
     const double* mp = mom + node * (int64_t)(2 * K + L);
-    const double* bnd = mp + K + L;
+    const double* bndg = mp + K + L;
+    const double* bnd = Pn;  // the panel area is free until the factorisation: the bounds staged there
     if (tid == 0) smin_sh = INFINITY;
-    for (int e = tid; e < K; e += K5_THREADS) sM[e] = mp[e];
+    for (int e = tid; e < K; e += K5_THREADS) {
+      sM[e] = mp[e];
+      if (mode == 0) Pn[e] = bndg[e];
+    }
+    static_assert(KB * S::LDP >= K, "the bound staging needs the panel area");
     __syncthreads();
     if (mode == 0 && !(sM[0] > 0.0)) {  // below the moment tree (M_000 = 0): accumulate directly
       if (tid == 0) {
