@@ -439,10 +439,22 @@ __global__ void __launch_bounds__(k5_threads<P>(), k5_threads<P>() == 256 ? 2 : 
     // ---- back substitution R̃ c̃ = y (R̃ = factorᵀ), blocked from the bottom ----------------------
     for (int j1 = L; j1 > 0; j1 -= KB) {
       const int j0 = max(0, j1 - KB), bw = j1 - j0;
-      // diagonal block L[j0..j1)[j0..j1) into shared memory (panel area, row-major bw x KB)
-      for (int e = tid; e < bw * bw; e += K5_THREADS) {
-        const int r = e / bw, c = e % bw;
-        Pn[r * KB + c] = (c <= r) ? A[tri(j0 + r) + j0 + c] : 0.0;
+      // diagonal block L[j0..j1)[j0..j1) into shared memory (panel area, row-major bw x KB); the
+      // thread's loads are issued together (KB*KB / K5_THREADS of them)
+      {
+        constexpr int NL = (KB * KB + K5_THREADS - 1) / K5_THREADS;
+        double v[NL];
+#pragma unroll
+        for (int q = 0; q < NL; ++q) {
+          const int e = tid + q * K5_THREADS;
+          const int r = e / KB, c = e % KB;
+          v[q] = (r < bw && c <= r) ? A[tri(j0 + r) + j0 + c] : 0.0;
+        }
+#pragma unroll
+        for (int q = 0; q < NL; ++q) {
+          const int e = tid + q * K5_THREADS;
+          if (e < KB * KB && e / KB < bw) Pn[e] = v[q];  // rows < bw only (the panel area holds KB·LDP)
+        }
       }
       __syncthreads();
       if (warp == 0) {  // c_j = (y_j - Σ_{j<i<j1} L[i][j] c_i) / L[j][j]; lane t holds y_t, right-looking
