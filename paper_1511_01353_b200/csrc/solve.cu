@@ -83,7 +83,9 @@ struct K5Shape {
   static constexpr int LDP0 = (L + 8 + 1) & ~1;
   static constexpr int LDP = LDP0 % 16 == 0 ? LDP0 + 2 : LDP0;
   // shared: moments [K], dinv, piv, 1/piv, y/c [L], column-major panel [KB x LDP], exponents
-  static constexpr size_t SMEM = ((size_t)K + 4 * L + (size_t)KB * LDP + 8) * sizeof(double) + 3 * L + 16;
+  // the panel area also holds two 32x32 diagonal blocks in the back substitution
+  static constexpr int PN = KB * LDP > 2 * KB * KB ? KB * LDP : 2 * KB * KB;
+  static constexpr size_t SMEM = ((size_t)K + 4 * L + (size_t)PN + 8) * sizeof(double) + 3 * L + 16;
 };
 
 template <int P>
@@ -104,7 +106,7 @@ __global__ void __launch_bounds__(k5_threads<P>(), k5_threads<P>() == 256 ? 2 : 
   constexpr int LDP = S::LDP;
   // column-major panel, 16-byte aligned: Pn[c * LDP + r] = row j0 + r, column j0 + c
   double* Pn = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(sy + L) + 15) & ~uintptr_t(15));
-  uint8_t* bl = reinterpret_cast<uint8_t*>(Pn + KB * LDP);
+  uint8_t* bl = reinterpret_cast<uint8_t*>(Pn + S::PN);
   uint8_t* bm = bl + L;
   uint8_t* bn = bm + L;
   __shared__ double smin_sh;
@@ -437,11 +439,12 @@ __global__ void __launch_bounds__(k5_threads<P>(), k5_threads<P>() == 256 ? 2 : 
     }
 
     // ---- back substitution R̃ c̃ = y (R̃ = factorᵀ), blocked from the bottom ----------------------
-    for (int j1 = L; j1 > 0; j1 -= KB) {
-      const int j0 = max(0, j1 - KB), bw = j1 - j0;
-      // diagonal block L[j0..j1)[j0..j1) into shared memory (panel area, row-major bw x KB); the
-      // thread's loads are issued together (KB*KB / K5_THREADS of them)
-      {
+    // Lookahead: after a 32-row block is solved, the rows of the next block take its contribution and
+    // the next diagonal block is staged; then warp 0 solves the next block while the other warps apply
+    // the finished block to all rows above it (the GEMV runs off the critical path).
+    {
+      // diagonal block L[j0..j1)[j0..j1) -> buf (row-major bw x KB); the thread's loads issued together
+      auto load_diag = [&](double* buf, int j0, int bw) {
         constexpr int NL = (KB * KB + K5_THREADS - 1) / K5_THREADS;
         double v[NL];
 #pragma unroll
@@ -453,34 +456,52 @@ __global__ void __launch_bounds__(k5_threads<P>(), k5_threads<P>() == 256 ? 2 : 
 #pragma unroll
         for (int q = 0; q < NL; ++q) {
           const int e = tid + q * K5_THREADS;
-          if (e < KB * KB && e / KB < bw) Pn[e] = v[q];  // rows < bw only (the panel area holds KB·LDP)
+          if (e < KB * KB && e / KB < bw) buf[e] = v[q];
         }
-      }
-      __syncthreads();
-      if (warp == 0) {  // c_j = (y_j - Σ_{j<i<j1} L[i][j] c_i) / L[j][j]; lane t holds y_t, right-looking
+      };
+      // c_j = (y_j - Σ_{j<i<j1} L[i][j] c_i) / L[j][j]: warp 0, lane t holds y_t, right-looking
+      auto solve_diag = [&](const double* buf, int j0, int bw) {
         double yv = lane < bw ? sy[j0 + lane] : 0.0;
         const double pl = lane < bw ? pinv[j0 + lane] : 0.0;
         for (int j = bw - 1; j >= 0; --j) {
           const double cj = __shfl_sync(0xffffffffu, pl > 0.0 ? yv * pl : 0.0, j);
-          if (lane < j) yv -= Pn[j * KB + lane] * cj;
+          if (lane < j) yv -= buf[j * KB + lane] * cj;
           if (lane == j) yv = cj;
         }
         if (lane < bw) sy[j0 + lane] = yv;
-      }
-      __syncthreads();
-      // rows above: y_k -= Σ_{i in [j0,j1)} L[i][k] c_i, k < j0 (rows i are contiguous in k); the
-      // block's loads are issued together (one L2 latency, not bw)
-      for (int k = tid; k < j0; k += K5_THREADS) {
-        double a[KB];
+      };
+      // y_k -= Σ_{i in [j0,j1)} L[i][k] c_i for k in [klo, khi), thread t of T (rows i contiguous in k)
+      auto gemv = [&](int j0, int bw, int klo, int khi, int t, int T) {
+        for (int k = klo + t; k < khi; k += T) {
+          double a[KB];
 #pragma unroll
-        for (int t = 0; t < KB; ++t) a[t] = t < bw ? A[tri(j0 + t) + k] : 0.0;
-        double v = 0.0;
+          for (int q = 0; q < KB; ++q) a[q] = q < bw ? A[tri(j0 + q) + k] : 0.0;
+          double v = 0.0;
 #pragma unroll
-        for (int t = 0; t < KB; ++t)
-          if (t < bw) v = fma(a[t], sy[j0 + t], v);
-        sy[k] -= v;
-      }
+          for (int q = 0; q < KB; ++q)
+            if (q < bw) v = fma(a[q], sy[j0 + q], v);
+          sy[k] -= v;
+        }
+      };
+      int j1 = L, j0 = max(0, L - KB);
+      load_diag(Pn, j0, j1 - j0);
       __syncthreads();
+      if (warp == 0) solve_diag(Pn, j0, j1 - j0);
+      __syncthreads();
+      int cur = 0;
+      while (j0 > 0) {
+        const int bw = j1 - j0, jn0 = max(0, j0 - KB);
+        double* nbuf = Pn + (cur ^ 1) * KB * KB;
+        gemv(j0, bw, jn0, j0, tid, K5_THREADS);  // the next block's rows first
+        load_diag(nbuf, jn0, j0 - jn0);
+        __syncthreads();
+        if (warp == 0) solve_diag(nbuf, jn0, j0 - jn0);
+        else gemv(j0, bw, 0, jn0, tid - 32, K5_THREADS - 32);  // all rows above the next block
+        __syncthreads();
+        j1 = j0;
+        j0 = jn0;
+        cur ^= 1;
+      }
     }
 
     K5T(5)
