@@ -337,12 +337,13 @@ __global__ void __launch_bounds__(256)
   const int64_t c1 = sgi + 1 < nseg ? chunk_begin[sgi + 1] : *nchunks;
   {  // entry group blockIdx.y: entries 32·y .. 32·y + 31
     const int e = (int)blockIdx.y * 32 + lane;
+    const int nw = (int)(blockDim.x >> 5);  // 1..8 warps, sized to the chunks per segment
     double a = 0.0, b = 0.0;
     if (e <= L) {
       int64_t c = c0 + warp;
-      for (; c + 8 < c1; c += 16) {
+      for (; c + nw < c1; c += 2 * nw) {
         a += partial[c * (L + 1) + e];
-        b += partial[(c + 8) * (L + 1) + e];
+        b += partial[(c + nw) * (L + 1) + e];
       }
       if (c < c1) a += partial[c * (L + 1) + e];
     }
@@ -350,8 +351,7 @@ __global__ void __launch_bounds__(256)
     __syncthreads();
     if (warp == 0 && e <= L) {
       double t = 0.0;
-#pragma unroll
-      for (int w = 0; w < 8; ++w) t += ws[w][lane];
+      for (int w = 0; w < nw; ++w) t += ws[w][lane];
       segsum[sgi * (L + 1) + e] = t;
       if (e == L && write_ss) nt.child_ss[first * 8 + sgi] = t;
     }
@@ -385,8 +385,13 @@ void level_residual(const LevelCtx& c, int mode, int iter, const double* delta, 
     else
       launch_residual<P, 0>(kid, c, mode, iter, delta, chunks, nchunks_dev, max_chunks, partial, s);
   }
-  FMI_LAUNCH(KID_RESIDUAL_REDUCE, s, k_residual_reduce, dim3((unsigned)nseg, (unsigned)((rank3(P) + 1 + 31) / 32)), 256,
-             0, partial, chunk_begin, nchunks_dev, nseg, c.nt, c.first, rank3(P), mode == K6_CHILD, sel, segsum);
+  // warps per segment CTA: about the chunks per segment (one warp for the many small segments of deep
+  // adaptive levels, eight for the few huge ones of the top levels)
+  int nw = 1;
+  while (nw < 8 && (int64_t)nw * nseg < max_chunks) nw *= 2;
+  FMI_LAUNCH(KID_RESIDUAL_REDUCE, s, k_residual_reduce, dim3((unsigned)nseg, (unsigned)((rank3(P) + 1 + 31) / 32)),
+             32 * nw, 0, partial, chunk_begin, nchunks_dev, nseg, c.nt, c.first, rank3(P), mode == K6_CHILD, sel,
+             segsum);
 }
 
 #define FMI_INST(P)                                                                                            \
