@@ -71,6 +71,12 @@ __global__ void k_defer_all(NodeTable nt, int64_t first, int64_t count) {
   if (t < count) nt.flag[first + t] |= 8;
 }
 
+// the range [0, n) of the root segment (a kernel: no host->device copy behind an upload)
+__global__ void k_fill_range(int64_t* se, int64_t n) {
+  se[0] = 0;
+  se[1] = n;
+}
+
 }  // namespace fmi
 
 using namespace fmi;
@@ -395,7 +401,8 @@ void dist_sum(const fmi_tree* T, void* dev, int64_t n, int dtype, cudaStream_t s
 //     (+ K5q QR re-fit of flagged nodes) -> fused K6 (residual, block energies, child projections)
 //     -> decisions + compaction.  One 16-byte D2H per level (the next level's size).
 template <int P>
-void run_levels(fmi_tree* T, const uint64_t* keys, double* ux, double* uy, double* uz, double* r, cudaStream_t s) {
+void run_levels(fmi_tree* T, const uint64_t* keys, double* ux, double* uy, double* uz, double* r, cudaStream_t s,
+                const double* root_b) {
   constexpr int L = rank3(P), K = rank3(2 * P);
   DBuf<int64_t> counts, begin, flags, scan, dev_small(8, s), nflag(3, s), gcnt;
   DBuf<int32_t> dsel;
@@ -473,7 +480,12 @@ void run_levels(fmi_tree* T, const uint64_t* keys, double* ux, double* uy, doubl
     set_root(T->nt, T->N, true, s);
     T->nodes = 1;
     int64_t first = 0, count = 1, points = T->N;
-    {  // root projection b = Λᵀf in the root frame
+    if (root_b) {  // root projection already taken by the fused gather (fused_gather_root)
+      segsum.ensure((size_t)(L + 1), s);
+      FMI_CK(cudaMemcpyAsync(segsum.p, root_b, (size_t)(L + 1) * sizeof(double), cudaMemcpyDeviceToDevice, s));
+      lvlmom.ensure((size_t)(2 * K + L), s);
+      gather_level(mtmom.p, mtbnd.p, T->nt.mtid, segsum.p, nullptr, 0, 1, K, KS, L, lvlmom.p, s);
+    } else {  // root projection b = Λᵀf in the root frame
       LevelCtx c{keys, ux, uy, uz, r, T->nt, 0, 1, 0, T->D, T->Dk, P, L, K, T->tau};
       const int64_t ch = choose_chunk(T->N, 1024, 32);
       const int64_t maxc = T->N / ch + 2;
@@ -632,6 +644,22 @@ void run_levels(fmi_tree* T, const uint64_t* keys, double* ux, double* uy, doubl
     throw;
   }
   free_table(mt, s);
+}
+
+// the gather of the sorted points fused with the root projection (single-GPU builds): chunks over [0, N)
+template <int P>
+void fused_gather_root(const double4* packed, const uint32_t* perm, const double* f, int* bad, int64_t N,
+                       double* ux, double* uy, double* uz, double* r, double* root_b, cudaStream_t s) {
+  constexpr int L = rank3(P);
+  DBuf<int64_t> se(2, s), counts(1, s), begin(1, s), nch(1, s);
+  FMI_LAUNCH(KID_MISC, s, k_fill_range, 1, 1, 0, se.p, N);
+  const int64_t ch = choose_chunk(N, 1024, 32);
+  const int64_t maxc = N / ch + 2;
+  DBuf<Chunk> chunks(maxc, s);
+  DBuf<double> partial((size_t)maxc * (L + 1), s);
+  make_chunks(se.p, se.p + 1, 1, ch, counts.p, begin.p, nch.p, chunks.p, maxc, s);
+  gather_root_projection<P>(packed, perm, f, bad, N, ux, uy, uz, r, chunks.p, nch.p, maxc, begin.p, partial.p,
+                            root_b, s);
 }
 
 // the unscoped fit (max_depth = 0) through the QR of unscoped.cu — one node, the root
@@ -841,6 +869,7 @@ fmi_tree* build_impl(const double* pts, const double* f, int64_t N, int degree, 
       Dsort = std::min(T->Dk, (int)std::ceil(std::log(fill) / std::log(8.0)) + 1);
     }
     DBuf<int> fbad;
+    DBuf<double> rootb;  // the root projection from the fused gather
     if (late_f) {
       fbad.alloc(1, s);
       FMI_CK(cudaMemsetAsync(fbad.p, 0, sizeof(int), s));
@@ -851,13 +880,23 @@ fmi_tree* build_impl(const double* pts, const double* f, int64_t N, int degree, 
       radix_sort_pairs(keys.p, perm.p, ktmp.p, ptmp.p, N, 3 * T->Dk, s, 3 * (T->Dk - Dsort));
       T->Dsorted = Dsort;
       tmark("sort", s);
+      // single-GPU level path: the gather fused with the root projection (it needs no tree)
+      const bool fuse_root = !unscoped && !dist;
+      if (fuse_root) rootb.ensure((size_t)L + 1, s);
       if (late_f) {
         FMI_CK(cudaStreamWaitEvent(s, side.e_f, 0));
-        gather_points(packed.p, perm.p, N, ux.p, uy.p, uz.p, r.p, s, df, fbad.p);
+        if (fuse_root) {
+          FMI_DISPATCH(degree, fused_gather_root, packed.p, perm.p, df, fbad.p, N, ux.p, uy.p, uz.p, r.p, rootb.p, s);
+        } else {
+          gather_points(packed.p, perm.p, N, ux.p, uy.p, uz.p, r.p, s, df, fbad.p);
+        }
         int hbad = 0;
         FMI_CK(cudaMemcpyAsync(&hbad, fbad.p, sizeof(int), cudaMemcpyDeviceToHost, s));
         FMI_CK(cudaStreamSynchronize(s));
         if (hbad) fail(FMI_EINPUT, "non-finite coordinate or value");
+      } else if (fuse_root) {
+        FMI_DISPATCH(degree, fused_gather_root, packed.p, perm.p, nullptr, nullptr, N, ux.p, uy.p, uz.p, r.p, rootb.p,
+                     s);
       } else {
         gather_points(packed.p, perm.p, N, ux.p, uy.p, uz.p, r.p, s);
       }
@@ -866,7 +905,7 @@ fmi_tree* build_impl(const double* pts, const double* f, int64_t N, int degree, 
         if (unscoped) {
           FMI_DISPATCH14(degree, run_unscoped, T, keys.p, ux.p, uy.p, uz.p, r.p, s);
         } else {
-          FMI_DISPATCH(degree, run_levels, T, keys.p, ux.p, uy.p, uz.p, r.p, s);
+          FMI_DISPATCH(degree, run_levels, T, keys.p, ux.p, uy.p, uz.p, r.p, s, fuse_root ? rootb.p : nullptr);
         }
         break;
       } catch (const KeysShort&) {

@@ -237,6 +237,14 @@ template <int P> void level_residual(const LevelCtx& c, int mode, int iter, cons
                                      const int64_t* nchunks_dev, int64_t max_chunks, const int64_t* chunk_begin,
                                      int64_t nseg, double* partial, double* segsum, cudaStream_t s,
                                      const int32_t* sel = nullptr, bool horner_only = false);
+// the gather of the sorted points (ux, uy, uz, r from packed[perm]) fused with the root projection
+// b = Λᵀf in the root frame -> segsum[0..𝓛] (chunks over [0, n)); f (optional): separately uploaded
+// values with the finiteness flag *bad
+template <int P> void gather_root_projection(const double4* packed, const uint32_t* perm, const double* f, int* bad,
+                                             int64_t n, double* ux, double* uy, double* uz, double* r,
+                                             const Chunk* chunks, const int64_t* nchunks_dev, int64_t max_chunks,
+                                             const int64_t* chunk_begin, double* partial, double* segsum,
+                                             cudaStream_t s);
 // child projections of a node are deferred (flag bit 3) when its predicted post-fit RMS (pre-fit energy
 // minus the energy the fit removes) is below kDeferTheta·τ: its children are then unlikely to be
 // created, and the projection pass runs only for those that are

@@ -321,6 +321,127 @@ __global__ void __launch_bounds__(K6_THREADS, 2)
   }
 }
 
+// The gather of the sorted points fused with the root projection (b = Λᵀf in the root frame, which
+// needs no tree): every batch's 32-byte records packed[perm[i]] are gathered by cp.async (per-thread
+// random addresses, in flight while the previous batch is projected), written out as the SoA arrays
+// ux, uy, uz, r of the later passes, and projected.  f (optional): values uploaded separately
+// (late-value path), taken from f[perm[i]] with the finiteness flag *bad.
+template <int P>
+__global__ void __launch_bounds__(K6_THREADS, 2)
+    k_gather_root(const double4* __restrict__ packed, const uint32_t* __restrict__ perm,
+                  const double* __restrict__ f, int* __restrict__ bad, double* __restrict__ ux,
+                  double* __restrict__ uy, double* __restrict__ uz, double* __restrict__ r,
+                  const Chunk* __restrict__ chunks, const int64_t* __restrict__ nchunks,
+                  double* __restrict__ partial) {
+  constexpr int L = rank3(P);
+  constexpr int G = proj_groups(P);
+  constexpr int SUB = K6_WARPS / G;
+  constexpr int MG = max_group(P);
+  constexpr int PPT = 2, BATCH = PPT * K6_THREADS;
+  __shared__ double sbuf[4 * BATCH];  // batch coordinates in the root frame + values
+  double* sx = sbuf;
+  double* sy = sbuf + BATCH;
+  double* sz = sbuf + 2 * BATCH;
+  double* sr = sbuf + 3 * BATCH;
+  static_assert(SUB * L <= 4 * BATCH, "reduction buffer");
+  double (*red)[L] = reinterpret_cast<double (*)[L]>(sbuf);
+  extern __shared__ __align__(16) double stage[];  // [2][BATCH] records (4 doubles) + [2][BATCH] values
+  const int64_t cidx = blockIdx.x;
+  if (cidx >= *nchunks) return;
+  const Chunk ck = chunks[cidx];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int gw = warp % G, sub = warp / G;
+  double* out = partial + cidx * (int64_t)(L + 1);
+  double acc[MG > 0 ? MG : 1];
+#pragma unroll
+  for (int k = 0; k < MG; ++k) acc[k] = 0.0;
+  double* srec = stage;                    // [2][BATCH][4]
+  double* sval = stage + 2 * BATCH * 4;    // [2][BATCH]
+  uint32_t pn[PPT];                        // perm of the next batch (loaded one batch ahead)
+  auto load_perm = [&](int64_t base) {
+#pragma unroll
+    for (int k = 0; k < PPT; ++k) {
+      const int64_t i = base + tid + k * K6_THREADS;
+      pn[k] = i < ck.end ? perm[i] : perm[ck.start];
+    }
+  };
+  auto issue = [&](int64_t base, int buf) {
+    if (base < ck.end) {
+#pragma unroll
+      for (int k = 0; k < PPT; ++k) {
+        const int e = tid + k * K6_THREADS;
+        double* d = srec + ((size_t)buf * BATCH + e) * 4;
+        const double* src = reinterpret_cast<const double*>(packed + pn[k]);
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(d)),
+                     "l"(src) : "memory");
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(d + 2)),
+                     "l"(src + 2) : "memory");
+        if (f) k6_cp8(sval + (size_t)buf * BATCH + e, f + pn[k]);
+      }
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  load_perm(ck.start);
+  issue(ck.start, 0);
+  load_perm(ck.start + BATCH);
+  int buf = 0;
+  const Frame fc = node_frame(make_int4(0, 0, 0, 0));
+  int nbad = 0;
+  for (int64_t base = ck.start; base < ck.end; base += BATCH, buf ^= 1) {
+    issue(base + BATCH, buf ^ 1);
+    load_perm(base + 2 * BATCH);
+    asm volatile("cp.async.wait_group 1;" ::: "memory");
+#pragma unroll
+    for (int k = 0; k < PPT; ++k) {
+      const int e = tid + k * K6_THREADS;
+      const int64_t i = base + e;
+      const bool v = i < ck.end;
+      const double* rec = srec + ((size_t)buf * BATCH + e) * 4;
+      const double X = rec[0], Y = rec[1], Z = rec[2];
+      const double R = f ? sval[(size_t)buf * BATCH + e] : rec[3];
+      if (v) {
+        ux[i] = X; uy[i] = Y; uz[i] = Z; r[i] = R;
+        if (f && !isfinite(R)) nbad = 1;
+      }
+      sx[e] = to_local(X, fc.cx, fc.scale);
+      sy[e] = to_local(Y, fc.cy, fc.scale);
+      sz[e] = to_local(Z, fc.cz, fc.scale);
+      sr[e] = v ? R : 0.0;
+    }
+    __syncthreads();
+    const int nb = (int)min((int64_t)BATCH, ck.end - base);
+    proj_run<P>(gw, sx, sy, sz, sr, sub * 32 + lane, 32 * SUB, nb, acc, std::make_integer_sequence<int, G>{});
+    __syncthreads();
+  }
+  if (nbad) *bad = 1;
+  const int ob = [&] {
+    int v = 0;
+#pragma unroll
+    for (int g = 0; g < G; ++g) if (g == gw) v = group_out_begin(P, g);
+    return v;
+  }();
+  const int on = [&] {
+    int v = 0;
+#pragma unroll
+    for (int g = 0; g < G; ++g) if (g == gw) v = group_size(P, g);
+    return v;
+  }();
+#pragma unroll
+  for (int k = 0; k < MG; ++k) {
+    double v = acc[k];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0 && k < on) red[sub][ob + k] = v;
+  }
+  __syncthreads();
+  for (int e = tid; e < L; e += K6_THREADS) {
+    double v = 0.0;
+    for (int q = 0; q < SUB; ++q) v += red[q][e];
+    out[e] = v;
+  }
+  if (tid == 0) out[L] = 0.0;
+}
+
 // segment sums: partial chunks of segment (node*8+o) -> segsum[seg][𝓛+1]; Σr² also to the node table
 // (child_ss) for the decisions.  CTA per (segment, 32 consecutive entries): lane = entry, warp w
 // sums the chunks c ≡ w (mod 8) with 2 independent accumulators, the 8 warp sums are then added in warp
@@ -394,9 +515,30 @@ void level_residual(const LevelCtx& c, int mode, int iter, const double* delta, 
              segsum);
 }
 
+template <int P>
+void gather_root_projection(const double4* packed, const uint32_t* perm, const double* f, int* bad, int64_t n,
+                            double* ux, double* uy, double* uz, double* r, const Chunk* chunks,
+                            const int64_t* nchunks_dev, int64_t max_chunks, const int64_t* chunk_begin,
+                            double* partial, double* segsum, cudaStream_t s) {
+  constexpr size_t smem = 2 * (size_t)(2 * K6_THREADS) * 5 * sizeof(double);
+  static std::once_flag attr_once;
+  std::call_once(attr_once, [&] {
+    FMI_CK(cudaFuncSetAttribute(k_gather_root<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  });
+  if (max_chunks > 0)
+    FMI_LAUNCH(KID_PROJECT, s, k_gather_root<P>, (unsigned)max_chunks, K6_THREADS, smem, packed, perm, f, bad, ux, uy,
+               uz, r, chunks, nchunks_dev, partial);
+  FMI_LAUNCH(KID_RESIDUAL_REDUCE, s, k_residual_reduce, dim3(1u, (unsigned)((rank3(P) + 1 + 31) / 32)), 256, 0,
+             partial, chunk_begin, nchunks_dev, (int64_t)1, NodeTable{}, (int64_t)0, rank3(P), false, nullptr, segsum);
+  (void)n;
+}
+
 #define FMI_INST(P)                                                                                            \
   template void level_residual<P>(const LevelCtx&, int, int, const double*, const Chunk*, const int64_t*, int64_t, \
-                                  const int64_t*, int64_t, double*, double*, cudaStream_t, const int32_t*, bool);
+                                  const int64_t*, int64_t, double*, double*, cudaStream_t, const int32_t*, bool); \
+  template void gather_root_projection<P>(const double4*, const uint32_t*, const double*, int*, int64_t, double*,    \
+                                          double*, double*, double*, const Chunk*, const int64_t*, int64_t,           \
+                                          const int64_t*, double*, double*, cudaStream_t);
 FMI_INST(0) FMI_INST(1) FMI_INST(2) FMI_INST(3) FMI_INST(4) FMI_INST(5)
 FMI_INST(6) FMI_INST(7) FMI_INST(8) FMI_INST(9) FMI_INST(10)
 #undef FMI_INST
