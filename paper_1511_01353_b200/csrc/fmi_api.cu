@@ -392,6 +392,21 @@ void dist_sum(const fmi_tree* T, void* dev, int64_t n, int dtype, cudaStream_t s
   FMI_CK(cudaMemcpyAsync(dev, d->xbuf, bytes, cudaMemcpyDeviceToDevice, s));
 }
 
+// values still uploading when the level build starts (fmi_build with page-locked host f): the moment
+// tree, K4 and M2M need only the coordinates; the values are gathered (with the root projection) once
+// the upload event has completed
+struct LateValues {
+  const double4* packed;
+  const uint32_t* perm;
+  const double* f;
+  int* bad;
+  cudaEvent_t ready;
+};
+
+template <int P>
+void fused_gather_root(const double4* packed, const uint32_t* perm, const double* f, int* bad, int64_t N,
+                       double* ux, double* uy, double* uz, double* r, double* root_b, cudaStream_t s);
+
 // Level-synchronous build:
 //  A. moment tree: every cell with >= 𝓛 points down to max_depth (integer guards of P:306 + G5,
 //     ignoring τ) — the fit tree is a subtree of it;
@@ -402,7 +417,7 @@ void dist_sum(const fmi_tree* T, void* dev, int64_t n, int dtype, cudaStream_t s
 //     -> decisions + compaction.  One 16-byte D2H per level (the next level's size).
 template <int P>
 void run_levels(fmi_tree* T, const uint64_t* keys, double* ux, double* uy, double* uz, double* r, cudaStream_t s,
-                const double* root_b) {
+                const double* root_b, const LateValues* late) {
   constexpr int L = rank3(P), K = rank3(2 * P);
   DBuf<int64_t> counts, begin, flags, scan, dev_small(8, s), nflag(3, s), gcnt;
   DBuf<int32_t> dsel;
@@ -480,7 +495,16 @@ void run_levels(fmi_tree* T, const uint64_t* keys, double* ux, double* uy, doubl
     set_root(T->nt, T->N, true, s);
     T->nodes = 1;
     int64_t first = 0, count = 1, points = T->N;
-    if (root_b) {  // root projection already taken by the fused gather (fused_gather_root)
+    if (late) {  // values uploaded meanwhile: gather them with the root projection, check finiteness
+      FMI_CK(cudaStreamWaitEvent(s, late->ready, 0));
+      segsum.ensure((size_t)(L + 1), s);
+      fused_gather_root<P>(late->packed, late->perm, late->f, late->bad, T->N, ux, uy, uz, r, segsum.p, s);
+      FMI_CK(cudaMemcpyAsync(host_small, late->bad, sizeof(int), cudaMemcpyDeviceToHost, s));
+      FMI_CK(cudaStreamSynchronize(s));
+      if (*reinterpret_cast<int*>(host_small)) fail(FMI_EINPUT, "non-finite coordinate or value");
+      lvlmom.ensure((size_t)(2 * K + L), s);
+      gather_level(mtmom.p, mtbnd.p, T->nt.mtid, segsum.p, nullptr, 0, 1, K, KS, L, lvlmom.p, s);
+    } else if (root_b) {  // root projection already taken by the fused gather (fused_gather_root)
       segsum.ensure((size_t)(L + 1), s);
       FMI_CK(cudaMemcpyAsync(segsum.p, root_b, (size_t)(L + 1) * sizeof(double), cudaMemcpyDeviceToDevice, s));
       lvlmom.ensure((size_t)(2 * K + L), s);
@@ -883,13 +907,13 @@ fmi_tree* build_impl(const double* pts, const double* f, int64_t N, int degree, 
       // single-GPU level path: the gather fused with the root projection (it needs no tree)
       const bool fuse_root = !unscoped && !dist;
       if (fuse_root) rootb.ensure((size_t)L + 1, s);
-      if (late_f) {
+      LateValues late{packed.p, perm.p, df, fbad.p, side.e_f};
+      const bool late_levels = late_f && fuse_root;  // values join inside run_levels (after K4/M2M)
+      if (late_levels) {
+        gather_points(packed.p, perm.p, N, ux.p, uy.p, uz.p, r.p, s);  // coordinates now (r: placeholder)
+      } else if (late_f) {
         FMI_CK(cudaStreamWaitEvent(s, side.e_f, 0));
-        if (fuse_root) {
-          FMI_DISPATCH(degree, fused_gather_root, packed.p, perm.p, df, fbad.p, N, ux.p, uy.p, uz.p, r.p, rootb.p, s);
-        } else {
-          gather_points(packed.p, perm.p, N, ux.p, uy.p, uz.p, r.p, s, df, fbad.p);
-        }
+        gather_points(packed.p, perm.p, N, ux.p, uy.p, uz.p, r.p, s, df, fbad.p);
         int hbad = 0;
         FMI_CK(cudaMemcpyAsync(&hbad, fbad.p, sizeof(int), cudaMemcpyDeviceToHost, s));
         FMI_CK(cudaStreamSynchronize(s));
@@ -905,7 +929,8 @@ fmi_tree* build_impl(const double* pts, const double* f, int64_t N, int degree, 
         if (unscoped) {
           FMI_DISPATCH14(degree, run_unscoped, T, keys.p, ux.p, uy.p, uz.p, r.p, s);
         } else {
-          FMI_DISPATCH(degree, run_levels, T, keys.p, ux.p, uy.p, uz.p, r.p, s, fuse_root ? rootb.p : nullptr);
+          FMI_DISPATCH(degree, run_levels, T, keys.p, ux.p, uy.p, uz.p, r.p, s,
+                       (fuse_root && !late_levels) ? rootb.p : nullptr, late_levels ? &late : nullptr);
         }
         break;
       } catch (const KeysShort&) {

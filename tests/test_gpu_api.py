@@ -76,12 +76,15 @@ def test_pipelined_host_eval_matches_device_eval():
 
 
 def test_pinned_host_values_uploaded_late():
-    """Page-locked host values take the side-stream upload (checked for finiteness at the gather): same
-    tree and values as device inputs; a NaN is still rejected with FMI_EINPUT."""
+    """Page-locked host values (N >= 2^20) take the side-stream upload and join the build after the
+    moment passes (gathered with the root projection, checked for finiteness there): same tree and
+    values as device inputs; a NaN is still rejected with FMI_EINPUT."""
     import paper_1511_01353_b200 as fmi
-    cfg = workloads.CONFIGS[2]
-    pts, f, q = workloads.make_inputs(cfg)
-    q = q[:20_000]
+    from types import SimpleNamespace
+    cfg = SimpleNamespace(degree=4, tol=1e-7, max_depth=5)
+    pts = workloads.uniform_points((1 << 20) + 12345, 3)
+    f = workloads.franke3d(pts)
+    q = workloads.uniform_points(20_000, 4)
     hp = torch.from_numpy(pts).pin_memory()
     hf = torch.from_numpy(f).pin_memory()
     with fmi.build(hp.numpy(), hf.numpy(), cfg.degree, cfg.tol, cfg.max_depth) as a, \
