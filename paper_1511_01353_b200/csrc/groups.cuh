@@ -78,10 +78,12 @@ __device__ __forceinline__ double cpow(double x) {
   else return x * cpow<E - 1>(x);
 }
 
-// pairs q..q1-1 of a group: acc[pair_first(q) - o0 + c] += v z^c with v = x^a y^b w, advanced by ONE
-// multiply per pair (v·y within a row of equal a; xw·x, the row start, at a new a)
+// pairs q..q1-1 of a group: acc[pair_first(q) - o0 + c] += v z^c with v = x^a y^b w.  Along a row of
+// equal a the pair values advance as two interleaved chains (v_{b+2} = v_b·y², one multiply per pair):
+// half the dependent-multiply latency of a single chain; vn = the next pair's value.
 template <int Q, int q, int q1, int o0>
-__device__ __forceinline__ void pairs(double x, double y, const double* zp, double xw, double v, double* acc) {
+__device__ __forceinline__ void pairs(double x, double y, double y2, const double* zp, double xw, double v, double vn,
+                                      double* acc) {
   if constexpr (q < q1) {
     constexpr int base = pair_first(Q, q) - o0;
     constexpr int n = pair_out(Q, q);
@@ -89,10 +91,10 @@ __device__ __forceinline__ void pairs(double x, double y, const double* zp, doub
     for (int c = 0; c < n; ++c) acc[base + c] = fma(v, zp[c], acc[base + c]);
     if constexpr (q + 1 < q1) {
       if constexpr (pair_a(Q, q + 1) == pair_a(Q, q)) {
-        pairs<Q, q + 1, q1, o0>(x, y, zp, xw, v * y, acc);
+        pairs<Q, q + 1, q1, o0>(x, y, y2, zp, xw, vn, v * y2, acc);
       } else {
         const double xn = xw * x;
-        pairs<Q, q + 1, q1, o0>(x, y, zp, xn, xn, acc);
+        pairs<Q, q + 1, q1, o0>(x, y, y2, zp, xn, xn, xn * y, acc);
       }
     }
   }
@@ -112,7 +114,8 @@ __device__ __forceinline__ void accum(double x, double y, double z, double w, do
 #pragma unroll
     for (int c = 2; c <= CM; ++c) zp[c] = zp[c / 2] * zp[c - c / 2];
     const double xw = cpow<pair_a(Q, q0)>(x) * w;
-    pairs<Q, q0, q1, o0>(x, y, zp, xw, xw * cpow<pair_b(Q, q0)>(y), acc);
+    const double v0 = xw * cpow<pair_b(Q, q0)>(y);
+    pairs<Q, q0, q1, o0>(x, y, y * y, zp, xw, v0, v0 * y, acc);
   }
 }
 

@@ -90,11 +90,12 @@ __host__ __device__ constexpr int group_cmax(int P, int g) {  // highest z power
   return smin > P ? 0 : P - smin;
 }
 
-// pair q of a group: acc[pair_first(q) - o0 + c] += v z^c, c = 0..P-a-b, v = x^a y^b r; then advance
-// v to pair q+1 with one multiply (v·y in a row of equal a, the row start x^(a+1) r at a new a)
-// (compile-time recursion: every index is a constant)
+// pair q of a group: acc[pair_first(q) - o0 + c] += v z^c, c = 0..P-a-b, v = x^a y^b r; along a row of
+// equal a the pair values advance as two interleaved chains (v_{b+2} = v_b·y²); vn = the next pair's
+// value (compile-time recursion: every index is a constant)
 template <int P, int q, int q1, int o0>
-__device__ __forceinline__ void proj_pairs(double x, double y, const double* zp, double xr, double v, double* acc) {
+__device__ __forceinline__ void proj_pairs(double x, double y, double y2, const double* zp, double xr, double v,
+                                           double vn, double* acc) {
   if constexpr (q < q1) {
     constexpr int base = pair_first(P, q) - o0;
     constexpr int n = pair_out(P, q);
@@ -102,10 +103,10 @@ __device__ __forceinline__ void proj_pairs(double x, double y, const double* zp,
     for (int c = 0; c < n; ++c) acc[base + c] = fma(v, zp[c], acc[base + c]);
     if constexpr (q + 1 < q1) {
       if constexpr (pair_a(P, q + 1) == pair_a(P, q)) {
-        proj_pairs<P, q + 1, q1, o0>(x, y, zp, xr, v * y, acc);
+        proj_pairs<P, q + 1, q1, o0>(x, y, y2, zp, xr, vn, v * y2, acc);
       } else {
         const double xn = xr * x;
-        proj_pairs<P, q + 1, q1, o0>(x, y, zp, xn, xn, acc);
+        proj_pairs<P, q + 1, q1, o0>(x, y, y2, zp, xn, xn, xn * y, acc);
       }
     }
   }
@@ -125,7 +126,7 @@ __device__ __forceinline__ void proj_accum(double x, double y, double z, double 
     // first pair's x^a r and x^a y^b r by square-and-multiply (log-depth)
     const double xr = grp::cpow<pair_a(P, q0)>(x) * r;
     const double v = xr * grp::cpow<pair_b(P, q0)>(y);
-    proj_pairs<P, q0, q1, o0>(x, y, zp, xr, v, acc);
+    proj_pairs<P, q0, q1, o0>(x, y, y * y, zp, xr, v, v * y, acc);
   }
 }
 
