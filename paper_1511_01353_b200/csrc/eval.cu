@@ -150,8 +150,22 @@ __global__ void __launch_bounds__(256) k_eval(const double* __restrict__ q, cons
   eval_locate<P>(q, qpk, keys, idx, i1, M, lo0, lo1, lo2, w, unit, Dk, nt, qi1, n1, x1, y1, z1);
   const int64_t node0 = __shfl_sync(0xffffffffu, n0, 0);
   const bool uniform = __all_sync(0xffffffffu, (i0 >= M || n0 == node0) && (i1 >= M || n1 == node0));
+  // CTA-wide node (the usual case: a node holds thousands of sorted queries): one coefficient copy for
+  // all 8 warps, loaded by all 256 threads at once
+  __shared__ long long cta_node[256 / 32];
+  if (lane == 0) cta_node[warp] = uniform ? (long long)node0 : -1ll;
+  __syncthreads();
+  bool cta_uniform = true;
+#pragma unroll
+  for (int w8 = 0; w8 < 256 / 32; ++w8) cta_uniform = cta_uniform && cta_node[w8] == cta_node[0] && cta_node[w8] >= 0;
   double v0, v1;
-  if (uniform) {
+  if (cta_uniform) {
+    const double* a = nt.pcoef + node0 * L;
+    for (int k = threadIdx.x; k < L; k += 256) cs[0][k] = __ldg(a + k);
+    __syncthreads();
+    const SmemCoef coef(cs[0]);
+    horner3x2<P>(coef, x0, y0, z0, x1, y1, z1, v0, v1);
+  } else if (uniform) {
     const double* a = nt.pcoef + node0 * L;
     for (int k = lane; k < L; k += 32) cs[warp][k] = __ldg(a + k);
     __syncwarp();
