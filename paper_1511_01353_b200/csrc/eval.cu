@@ -95,18 +95,20 @@ __global__ void __launch_bounds__(PS_THREADS) k_presum(NodeTable nt, int64_t fir
 // stages that node's pre-summed coefficients in shared memory once (coalesced) and every lane
 // evaluates its two queries with one coefficient read per two FMAs (horner3x2); otherwise each query
 // reads its own node's coefficients through L1.
-template <int P>
-__device__ __forceinline__ void eval_locate(const double* __restrict__ q, const double4* __restrict__ qpk,
-                                            const uint64_t* __restrict__ keys, const uint32_t* __restrict__ idx,
-                                            int64_t i, int64_t M, double lo0, double lo1, double lo2, double w,
-                                            bool unit, int Dk, const NodeTable& nt, int64_t& qi, int64_t& node,
-                                            double& x, double& y, double& z) {
+// query i: its root-cube coordinates (the 32-byte record written by the key kernel, or the raw point)
+// and its key — issued for both of a thread's queries before either is used (independent loads in flight)
+__device__ __forceinline__ void eval_fetch(const double* __restrict__ q, const double4* __restrict__ qpk,
+                                           const uint64_t* __restrict__ keys, const uint32_t* __restrict__ idx,
+                                           int64_t i, int64_t M, double lo0, double lo1, double lo2, double w,
+                                           bool unit, int64_t& qi, double& ux, double& uy, double& uz,
+                                           uint64_t& key) {
   qi = 0;
-  node = 0;
-  double ux = 0.0, uy = 0.0, uz = 0.0;
+  ux = uy = uz = 0.0;
+  key = 0;
   if (i < M) {
     qi = idx ? (int64_t)idx[i] : i;
-    if (qpk) {  // root-cube coordinates written by the key kernel: one 32-byte record per query
+    if (keys) key = keys[i];
+    if (qpk) {
       const double2* p = reinterpret_cast<const double2*>(qpk + qi);
       const double2 a = __ldg(p), b = __ldg(p + 1);
       ux = a.x; uy = a.y; uz = b.x;
@@ -115,16 +117,21 @@ __device__ __forceinline__ void eval_locate(const double* __restrict__ q, const 
       uy = to_unit_e(q[3 * qi + 1], lo1, w, unit);
       uz = to_unit_e(q[3 * qi + 2], lo2, w, unit);
     }
-    const bool inside = ux >= 0.0 && ux <= 1.0 && uy >= 0.0 && uy <= 1.0 && uz >= 0.0 && uz <= 1.0;
-    // descend to the deepest existing node containing the query
-    if (inside && keys) {
-      const uint64_t key = keys[i];
-      for (int level = 0; level < Dk; ++level) {
-        const int o = (int)((key >> (3 * (Dk - level - 1))) & 7ull);
-        const int32_t ch = __ldg(nt.child + node * 8 + o);
-        if (ch < 0) break;
-        node = ch;
-      }
+  }
+}
+
+// descend to the deepest existing node containing the query; local coordinates in its frame
+__device__ __forceinline__ void eval_descend(int64_t i, int64_t M, bool have_keys, int Dk, const NodeTable& nt,
+                                             double ux, double uy, double uz, uint64_t key, int64_t& node,
+                                             double& x, double& y, double& z) {
+  node = 0;
+  const bool inside = ux >= 0.0 && ux <= 1.0 && uy >= 0.0 && uy <= 1.0 && uz >= 0.0 && uz <= 1.0;
+  if (i < M && inside && have_keys) {
+    for (int level = 0; level < Dk; ++level) {
+      const int o = (int)((key >> (3 * (Dk - level - 1))) & 7ull);
+      const int32_t ch = __ldg(nt.child + node * 8 + o);
+      if (ch < 0) break;
+      node = ch;
     }
   }
   const Frame fr = node_frame(nt.cell[node]);
@@ -145,9 +152,12 @@ __global__ void __launch_bounds__(256) k_eval(const double* __restrict__ q, cons
   const int64_t base = ((int64_t)blockIdx.x * 8 + warp) * 64;
   const int64_t i0 = base + lane, i1 = base + 32 + lane;
   int64_t qi0, qi1, n0, n1;
-  double x0, y0, z0, x1, y1, z1;
-  eval_locate<P>(q, qpk, keys, idx, i0, M, lo0, lo1, lo2, w, unit, Dk, nt, qi0, n0, x0, y0, z0);
-  eval_locate<P>(q, qpk, keys, idx, i1, M, lo0, lo1, lo2, w, unit, Dk, nt, qi1, n1, x1, y1, z1);
+  double x0, y0, z0, x1, y1, z1, ux0, uy0, uz0, ux1, uy1, uz1;
+  uint64_t k0, k1;
+  eval_fetch(q, qpk, keys, idx, i0, M, lo0, lo1, lo2, w, unit, qi0, ux0, uy0, uz0, k0);
+  eval_fetch(q, qpk, keys, idx, i1, M, lo0, lo1, lo2, w, unit, qi1, ux1, uy1, uz1, k1);
+  eval_descend(i0, M, keys != nullptr, Dk, nt, ux0, uy0, uz0, k0, n0, x0, y0, z0);
+  eval_descend(i1, M, keys != nullptr, Dk, nt, ux1, uy1, uz1, k1, n1, x1, y1, z1);
   const int64_t node0 = __shfl_sync(0xffffffffu, n0, 0);
   const bool uniform = __all_sync(0xffffffffu, (i0 >= M || n0 == node0) && (i1 >= M || n1 == node0));
   // CTA-wide node (the usual case: a node holds thousands of sorted queries): one coefficient copy for
