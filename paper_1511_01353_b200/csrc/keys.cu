@@ -158,7 +158,7 @@ __global__ void __launch_bounds__(RS_THREADS) k_rs_hist(const uint64_t* __restri
 // Downsweep: stable rank of every item of the tile (per-warp match.any ranking + prefix over warps and
 // digits), the tile is rearranged in shared memory in digit order, then written out so that
 // consecutive threads store consecutive positions of each digit's global run (coalesced).
-__global__ void __launch_bounds__(RS_THREADS) k_rs_scatter(const uint64_t* __restrict__ kin,
+__global__ void __launch_bounds__(RS_THREADS, 3) k_rs_scatter(const uint64_t* __restrict__ kin,
                                                            const uint32_t* __restrict__ vin, int64_t n, int shift,
                                                            int64_t nblk, const int64_t* __restrict__ offs,
                                                            uint64_t* __restrict__ kout, uint32_t* __restrict__ vout) {
@@ -175,27 +175,28 @@ __global__ void __launch_bounds__(RS_THREADS) k_rs_scatter(const uint64_t* __res
   const int64_t tbase = (int64_t)blockIdx.x * RS_TILE;
   const int64_t base = tbase + (int64_t)warp * RS_WARP_ITEMS;
   const unsigned lt_mask = (1u << lane) - 1u;
-  uint64_t k[RS_ITEMS];
-  uint32_t v[RS_ITEMS];
-  int rank[RS_ITEMS];
-  int dig[RS_ITEMS];
+  uint64_t k[RS_ITEMS];  // the values are read again (L2) when the tile is rearranged: fewer registers
+  unsigned rank2[RS_ITEMS / 2];  // in-warp ranks (< RS_WARP_ITEMS), two 16-bit halves per register
+  // digit of item it (256 = past the end); recomputed from the key instead of held in registers
+  auto digit = [&](int it) { return base + it * 32 + lane < n ? (int)((k[it] >> shift) & 255) : 256; };
 #pragma unroll
   for (int it = 0; it < RS_ITEMS; ++it) {
     int64_t idx = base + it * 32 + lane;
     bool valid = idx < n;
     k[it] = valid ? kin[idx] : 0;
-    v[it] = valid ? vin[idx] : 0;
-    dig[it] = valid ? (int)((k[it] >> shift) & 255) : 256;
   }
 #pragma unroll
   for (int it = 0; it < RS_ITEMS; ++it) {
-    unsigned peers = __match_any_sync(0xffffffffu, dig[it]);
-    int before = whist[warp][dig[it]];
+    const int d = digit(it);
+    unsigned peers = __match_any_sync(0xffffffffu, d);
+    int before = whist[warp][d];
     __syncwarp();
     int leader = __ffs(peers) - 1;
-    if (lane == leader) whist[warp][dig[it]] = before + __popc(peers);
+    if (lane == leader) whist[warp][d] = before + __popc(peers);
     __syncwarp();
-    rank[it] = before + __popc(peers & lt_mask);
+    const unsigned rk = (unsigned)(before + __popc(peers & lt_mask));
+    if (it % 2 == 0) rank2[it / 2] = rk;
+    else rank2[it / 2] |= rk << 16;
   }
   __syncthreads();
   {  // exclusive prefix over warps for each digit; digit totals of the tile
@@ -227,10 +228,11 @@ __global__ void __launch_bounds__(RS_THREADS) k_rs_scatter(const uint64_t* __res
   __syncthreads();
 #pragma unroll
   for (int it = 0; it < RS_ITEMS; ++it) {
-    if (dig[it] < 256) {
-      const int pos = tstart[dig[it]] + whist[warp][dig[it]] + rank[it];
+    const int d = digit(it);
+    if (d < 256) {
+      const int pos = tstart[d] + whist[warp][d] + (int)((rank2[it / 2] >> (16 * (it % 2))) & 0xffffu);
       sk[pos] = k[it];
-      sv[pos] = v[it];
+      sv[pos] = vin[base + it * 32 + lane];
     }
   }
   __syncthreads();
