@@ -175,6 +175,7 @@ __global__ void __launch_bounds__(RS_THREADS, 3) k_rs_scatter(const uint64_t* __
   const int64_t tbase = (int64_t)blockIdx.x * RS_TILE;
   const int64_t base = tbase + (int64_t)warp * RS_WARP_ITEMS;
   const unsigned lt_mask = (1u << lane) - 1u;
+  const bool full = tbase + RS_TILE <= n;  // CTA-uniform: no past-the-end items in this tile
   uint64_t k[RS_ITEMS];  // the values are read again (L2) when the tile is rearranged: fewer registers
   unsigned rank2[RS_ITEMS / 2];  // in-warp ranks (< RS_WARP_ITEMS), two 16-bit halves per register
   // digit of item it (256 = past the end); recomputed from the key instead of held in registers
@@ -188,7 +189,18 @@ __global__ void __launch_bounds__(RS_THREADS, 3) k_rs_scatter(const uint64_t* __
 #pragma unroll
   for (int it = 0; it < RS_ITEMS; ++it) {
     const int d = digit(it);
-    unsigned peers = __match_any_sync(0xffffffffu, d);
+    // peers = lanes with the same digit, from one ballot per digit bit (VOTE on the ALU pipe instead of
+    // MATCH on the address-divergence unit, which bounded this kernel); bit 8 marks past-the-end items
+    unsigned peers = 0xffffffffu;
+#pragma unroll
+    for (int b = 0; b < 8; ++b) {
+      const unsigned bb = __ballot_sync(0xffffffffu, (d >> b) & 1);
+      peers &= ((d >> b) & 1) ? bb : ~bb;
+    }
+    if (!full) {
+      const unsigned bb = __ballot_sync(0xffffffffu, d >> 8);
+      peers &= (d >> 8) ? bb : ~bb;
+    }
     int before = whist[warp][d];
     __syncwarp();
     int leader = __ffs(peers) - 1;
