@@ -146,11 +146,16 @@ __global__ void __launch_bounds__(RS_THREADS) k_rs_hist(const uint64_t* __restri
   hist[threadIdx.x] = 0;
   __syncthreads();
   const int64_t base = (int64_t)blockIdx.x * RS_TILE;
-#pragma unroll 4
+  // all 16 loads in flight before the first shared-memory atomic
+  uint32_t d[RS_ITEMS];
+#pragma unroll
   for (int i = 0; i < RS_ITEMS; ++i) {
-    int64_t idx = base + (int64_t)i * RS_THREADS + threadIdx.x;
-    if (idx < n) atomicAdd(&hist[(keys[idx] >> shift) & 255], 1);
+    const int64_t idx = base + (int64_t)i * RS_THREADS + threadIdx.x;
+    d[i] = idx < n ? (uint32_t)((__ldg(keys + idx) >> shift) & 255) : 256u;
   }
+#pragma unroll
+  for (int i = 0; i < RS_ITEMS; ++i)
+    if (d[i] < 256u) atomicAdd(&hist[d[i]], 1);
   __syncthreads();
   counts[(int64_t)threadIdx.x * nblk + blockIdx.x] = hist[threadIdx.x];
 }
