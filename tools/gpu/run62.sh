@@ -1,3 +1,3 @@
 mkdir -p gpurun_out
 export PYTHONUNBUFFERED=1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"^k_rs_scatter$" -c 1 -o gpurun_out/rs_v92 -f python tools/run_build.py --config 5 --reps 1 > gpurun_out/ncu_rs_v92.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"^k_rs_scatter$" -c 1 -o gpurun_out/rs_v94 -f python tools/run_build.py --config 5 --reps 1 > gpurun_out/ncu_rs_v94.log 2>&1
