@@ -23,6 +23,7 @@
 #include <algorithm>
 #include <vector>
 
+#include <cstdlib>
 #include "fmi_internal.cuh"
 
 namespace fmi {
@@ -88,15 +89,17 @@ struct K5Shape {
   static constexpr size_t SMEM = ((size_t)K + 4 * L + (size_t)PN + 8) * sizeof(double) + 3 * L + 16;
 };
 
-template <int P>
-__global__ void __launch_bounds__(k5_threads<P>(), k5_threads<P>() == 256 ? 2 : (k5_threads<P>() == 128 ? 3 : 6))
+// NT = threads per node: k5_threads<P>() for full levels; 256 for levels with fewer nodes than CTA slots
+// (the top levels of every build are latency-bound: one node per SM)
+template <int P, int NT = k5_threads<P>()>
+__global__ void __launch_bounds__(NT, NT == 256 ? 2 : (NT == 128 ? 3 : 6))
     k_solve(const double* __restrict__ mom, int mode, const double* __restrict__ segrhs, double* __restrict__ delta,
             NodeTable nt, int64_t first, int64_t count, double* __restrict__ fac,
             const __grid_constant__ BasisTab bt, double delta2, double refine2, double refine_fill,
             double mom_tol, int64_t n_root, double defer_tau, int64_t* __restrict__ nflag) {
   using S = K5Shape<P>;
   constexpr int Q = S::Q, K = S::K, L = S::L;
-  constexpr int K5_THREADS = k5_threads<P>(), K5_WARPS = K5_THREADS / 32;
+  constexpr int K5_THREADS = NT, K5_WARPS = K5_THREADS / 32;
   extern __shared__ __align__(16) double sm[];
   double* sM = sm;          // [K]
   double* dinv = sM + K;    // [L]
@@ -561,14 +564,31 @@ void level_solve(const LevelCtx& c, const double* mom, int mode, const double* s
                  double refine_fill, int64_t n_root, int64_t* nflag, double* fac, cudaStream_t s, double defer_tau) {
   using S = K5Shape<P>;
   static const BasisTab bt = make_basis<P>();
+  constexpr int NT = k5_threads<P>();
+  static int small_max = 0;         // levels with <= small_max nodes run 256 threads per node
   static std::once_flag attr_once;  // one opt-in per kernel instantiation (thread-safe)
   std::call_once(attr_once, [&] {
     FMI_CK(cudaFuncSetAttribute(
-        k_solve<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::SMEM));
+        k_solve<P, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::SMEM));
+    if constexpr (NT < 256) {
+      FMI_CK(cudaFuncSetAttribute(
+          k_solve<P, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::SMEM));
+      int dev = 0, sms = 0;
+      FMI_CK(cudaGetDevice(&dev));
+      FMI_CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+      const char* e = std::getenv("FMI_K5_SMALL");
+      small_max = e ? std::atoi(e) : 2 * sms;
+    }
   });
   const int64_t grid = std::min<int64_t>(c.count, 1 << 20);
   if (grid <= 0) return;
-  FMI_LAUNCH(mode == 1 ? KID_REFINE_SOLVE : KID_SOLVE, s, k_solve<P>, (unsigned)grid, k5_threads<P>(), S::SMEM, mom, mode,
+  if (NT < 256 && grid <= small_max) {
+    FMI_LAUNCH(mode == 1 ? KID_REFINE_SOLVE : KID_SOLVE, s, (k_solve<P, 256>), (unsigned)grid, 256, S::SMEM, mom,
+               mode, segrhs, delta, c.nt, c.first, c.count, fac, bt, kDelta * kDelta, refine2, refine_fill, kMomentTol,
+               n_root, defer_tau, nflag);
+    return;
+  }
+  FMI_LAUNCH(mode == 1 ? KID_REFINE_SOLVE : KID_SOLVE, s, (k_solve<P, NT>), (unsigned)grid, NT, S::SMEM, mom, mode,
              segrhs, delta, c.nt, c.first, c.count, fac, bt, kDelta * kDelta, refine2, refine_fill, kMomentTol, n_root,
              defer_tau, nflag);
 }
