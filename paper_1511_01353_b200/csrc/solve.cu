@@ -577,7 +577,7 @@ void level_solve(const LevelCtx& c, const double* mom, int mode, const double* s
       FMI_CK(cudaGetDevice(&dev));
       FMI_CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
       const char* e = std::getenv("FMI_K5_SMALL");
-      small_max = e ? std::atoi(e) : 2 * sms;
+      small_max = e ? std::atoi(e) : 6 * sms;
     }
   });
   const int64_t grid = std::min<int64_t>(c.count, 1 << 20);
