@@ -400,8 +400,11 @@ def main():
         e2e_step()
     barrier()
     t0 = time.perf_counter()
+    e2e_step_ms = []  # per-step host wall clock (visibility of host-side jitter on the short configs)
     for _ in range(args.steps):
+        ts = time.perf_counter()
         e2e_step()
+        e2e_step_ms.append(round((time.perf_counter() - ts) * 1e3, 3))
     barrier()
     e2e_s = (time.perf_counter() - t0) / args.steps
     if world > 1:
@@ -448,7 +451,8 @@ def main():
                              "points, values, queries and D2H of the values inside the call; the query upload "
                              "overlaps the fit), max over ranks") if world == 1 else
                             "host wall clock around K steps (H2D of points, values, queries and D2H of the values "
-                            "inside), max over ranks"},
+                            "inside), max over ranks",
+                    "step_ms": e2e_step_ms},
             "gpu_launches": int(launches),
             "clocks": clocks.summary(),
             "check": {"max_abs_out": gpu_out_max},
