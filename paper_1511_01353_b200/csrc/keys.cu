@@ -135,9 +135,9 @@ __global__ void __launch_bounds__(256) k_keys(const double* __restrict__ pts, in
 // ------------------------------------------------------------------------------------------------
 constexpr int RS_THREADS = 256;
 constexpr int RS_WARPS = RS_THREADS / 32;
-constexpr int RS_ITEMS = 16;
-constexpr int RS_TILE = RS_THREADS * RS_ITEMS;  // 4096
-constexpr int RS_WARP_ITEMS = RS_TILE / RS_WARPS; // 512
+constexpr int RS_ITEMS = 12;
+constexpr int RS_TILE = RS_THREADS * RS_ITEMS;  // 3072 (12 items/thread: 64 registers, 4 CTAs/SM)
+constexpr int RS_WARP_ITEMS = RS_TILE / RS_WARPS; // 384 (in-warp ranks fit 16 bits)
 constexpr size_t kScatterSmem = (size_t)RS_TILE * (sizeof(uint64_t) + sizeof(uint32_t));
 
 __global__ void __launch_bounds__(RS_THREADS) k_rs_hist(const uint64_t* __restrict__ keys, int64_t n, int shift,
@@ -163,7 +163,7 @@ __global__ void __launch_bounds__(RS_THREADS) k_rs_hist(const uint64_t* __restri
 // Downsweep: stable rank of every item of the tile (per-warp match.any ranking + prefix over warps and
 // digits), the tile is rearranged in shared memory in digit order, then written out so that
 // consecutive threads store consecutive positions of each digit's global run (coalesced).
-__global__ void __launch_bounds__(RS_THREADS, 3) k_rs_scatter(const uint64_t* __restrict__ kin,
+__global__ void __launch_bounds__(RS_THREADS, 4) k_rs_scatter(const uint64_t* __restrict__ kin,
                                                            const uint32_t* __restrict__ vin, int64_t n, int shift,
                                                            int64_t nblk, const int64_t* __restrict__ offs,
                                                            uint64_t* __restrict__ kout, uint32_t* __restrict__ vout) {
