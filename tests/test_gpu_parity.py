@@ -249,3 +249,36 @@ def test_k6_split_and_fused_match_the_oracle(split_min, monkeypatch):
     q = q[:50_000]
     ora, gpu, *_ = check_parity(pts, f, cfg.degree, cfg.tol, cfg.max_depth, q, erms_vs=workloads.franke3d)
     assert ora.node_count == 585
+
+
+# ---------------------------------------------------------------------------------------------
+# sort edge cases: query counts around the K2 tile (3072 items) and warp (32) boundaries, and
+# point sets of one, two and three points (p = 0: 𝓛 = 1)
+# ---------------------------------------------------------------------------------------------
+
+@pytest.fixture(scope="module")
+def _tile_tree():
+    rng = np.random.default_rng(21)
+    pts = rng.random((20_000, 3))
+    f = workloads.franke3d(pts)
+    ora = fo.build(pts, f, 4, 1e-8, 4)
+    tree = gpu_build(pts, f, 4, 1e-8, 4)
+    yield ora, tree, float(np.max(np.abs(f)))
+    tree.free()
+
+
+@pytest.mark.parametrize("M", [1, 2, 31, 33, 3071, 3072, 3073, 6145])
+def test_eval_query_counts_around_sort_tiles(_tile_tree, M):
+    ora, tree, scale = _tile_tree
+    q = np.random.default_rng(1000 + M).random((M, 3))
+    val = gpu_eval(tree, q)
+    ref = fo.evaluate(ora, q)
+    assert np.max(np.abs(val - ref)) <= EVAL_TOL * scale
+
+
+@pytest.mark.parametrize("N", [1, 2, 3])
+def test_degree0_one_to_three_points(N):
+    rng = np.random.default_rng(40 + N)
+    pts = rng.random((N, 3))
+    f = rng.standard_normal(N)
+    check_parity(pts, f, 0, 0.0, 3, rng.random((100, 3)))
