@@ -21,8 +21,11 @@ Parity status of each function (the pins live in tests/test_oracle.py):
   fit_node ............... pinned (polynomial reproduction, unisolvent interpolation,
                            brute-force lstsq with an independent basis, p=0 mean,
                            annihilation, coplanar rank truncation vs 2-D lstsq)
-  build .................. pinned (brute-force tree on tiny inputs, telescoping identity,
-                           non-increasing residual, constant/polynomial -> 1 node)
+  _qr_r, TSQR branch ..... pinned (R of a > 2^16-row matrix = LAPACK's up to row signs; fit_node
+                           streamed vs single-block and vs independent lstsq above 2^16 rows)
+  build, build_subtree ... pinned (brute-force tree on tiny inputs, telescoping identity,
+                           non-increasing residual, constant/polynomial -> 1 node; a restricted
+                           or node-started run reproduces the full run's nodes)
   evaluate ............... pinned (path-sum == per-leaf lstsq; polynomial reproduction)
 """
 from __future__ import annotations
@@ -104,12 +107,31 @@ def fit_node(u: np.ndarray, r: np.ndarray, p: int, delta: float = DELTA) -> Node
     u = np.asarray(u, dtype=np.float64).reshape(-1, 3)
     r = np.asarray(r, dtype=np.float64)
     L = rank(p)
-    lam = vandermonde(u, p)
-    d = np.sqrt(np.sum(lam * lam, axis=0))
-    nonzero = d > 0
-    a = np.zeros_like(lam)
-    a[:, nonzero] = lam[:, nonzero] / d[nonzero]
-    R = _qr_r(np.hstack([a, r[:, None]]))  # (L+1) x (L+1)
+    if u.shape[0] <= _TSQR_ROWS:
+        lam = vandermonde(u, p)
+        d = np.sqrt(np.sum(lam * lam, axis=0))
+        nonzero = d > 0
+        a = np.zeros_like(lam)
+        a[:, nonzero] = lam[:, nonzero] / d[nonzero]
+        R = _qr_r(np.hstack([a, r[:, None]]))  # (L+1) x (L+1)
+    else:
+        # The same two steps, streamed over row blocks so that Λ is never held whole (a node of
+        # 2e7 points at p = 6 would need 13 GB): first the column norms, then the row-streamed
+        # QR (TSQR) of the equilibrated [Λ D⁻¹ | r] block by block.
+        d2 = np.zeros(L)
+        for s in range(0, u.shape[0], _TSQR_ROWS):
+            lam = vandermonde(u[s:s + _TSQR_ROWS], p)
+            d2 += np.sum(lam * lam, axis=0)
+        d = np.sqrt(d2)
+        nonzero = d > 0
+        dd = np.where(nonzero, d, 1.0)
+        R = None
+        with threadpool_limits(limits=1, user_api="blas"):
+            for s in range(0, u.shape[0], _TSQR_ROWS):
+                lam = vandermonde(u[s:s + _TSQR_ROWS], p)
+                a = np.where(nonzero, lam / dd, 0.0)
+                blk = np.hstack([a, r[s:s + _TSQR_ROWS, None]])
+                R = np.linalg.qr(blk if R is None else np.vstack([R, blk]), mode="r")
     R = np.vstack([R, np.zeros((L + 1 - R.shape[0], L + 1))]) if R.shape[0] < L + 1 else R
     kept: list[int] = []
     diag_ok = np.abs(np.diag(R)[:L]) > delta
@@ -143,6 +165,16 @@ def fit_node(u: np.ndarray, r: np.ndarray, p: int, delta: float = DELTA) -> Node
     return NodeFit(coeffs=c, kept=mask, min_pivot=float(np.min(piv)) if len(kept) else 0.0)
 
 
+def apply_fit(u: np.ndarray, coeffs: np.ndarray, p: int) -> np.ndarray:
+    """Λ(u)·P_F (the update term of P:332 and the per-node term of f(r) = Λ(r)·F_p),
+    formed in row blocks so that Λ is never held whole for large nodes or query sets."""
+    u = np.asarray(u, dtype=np.float64).reshape(-1, 3)
+    out = np.empty(u.shape[0])
+    for s in range(0, u.shape[0], _TSQR_ROWS):
+        out[s:s + _TSQR_ROWS] = vandermonde(u[s:s + _TSQR_ROWS], p) @ coeffs
+    return out
+
+
 def morton_prefix(depth: int, cell: tuple[int, int, int]) -> int:
     """Label of a node: interleave the bits of its cell (i, j, k) at ``depth`` with x fastest, so that
     the digit of level t is o = bx + 2 by + 4 bz (S:324 octant numbering; reading G7).  Labels only."""
@@ -172,7 +204,7 @@ class Tree:
     residual_rms: np.ndarray     # (nodes,) post-fit RMS over the node's points
     child_rms: np.ndarray        # (nodes, 8) E_RMS of each octant block (nan if n_o == 0)
     child_count: np.ndarray      # (nodes, 8) n_o
-    child_index: np.ndarray      # (nodes, 8) index of the child node or -1
+    child_index: np.ndarray      # (nodes, 8) index of the child node, -1 none, -2 created but not expanded
     residual: np.ndarray         # (N,) final residual in INPUT order (bookkeeping)
 
     @property
@@ -218,19 +250,11 @@ def octant(ul: np.ndarray) -> np.ndarray:
 
 
 def build(points: np.ndarray, f: np.ndarray, p: int, tau: float, max_depth: int,
-          delta: float = DELTA) -> Tree:
-    """FMT_Mesh_to_Tree (Algorithm 1), run depth-first exactly as printed.
-
-    For the node P holding points x(j:k) and residual f(j:k):
-      line 2  map to the node frame (P:299)                  -> local_coords
-      line 3  FMT_Mesh_to_Moments: fit, f <- f - Λ P_F (Alg. 2)  -> fit_node
-      line 4  FMT_Ordered_by_Octant: stable partition into 8 blocks (P:301)
-      lines 6-12 for each octant o with n_o points:
-              E_RMS = sqrt(sum_block f^2 / n_o) on the post-fit residual (P:305, G3)
-              recurse iff E_RMS > tau and n_o >= 𝓛 (P:306, G4) and depth+1 <= max_depth (G5)
-              block bounds: running start j, end j + n_o (G2, S:378)
-    The caller's arrays are not modified (the paper overwrites x and f in place).
-    """
+          delta: float = DELTA, descend=None) -> Tree:
+    """FMT_Mesh_to_Tree (Algorithm 1) called on the root node: the root cube (G6), then
+    ``build_subtree`` from depth 0.  The caller's arrays are not modified (the paper overwrites x and
+    f in place).  ``descend`` (test harness only) restricts which created children are expanded;
+    see ``build_subtree``."""
     pts = np.asarray(points, dtype=np.float64).reshape(-1, 3)
     f = np.asarray(f, dtype=np.float64).reshape(-1)
     N = pts.shape[0]
@@ -239,23 +263,53 @@ def build(points: np.ndarray, f: np.ndarray, p: int, tau: float, max_depth: int,
         raise ValueError(f"N={N} < 𝓛={L}: the root fit is underdetermined (S:348)")
     lo, width = root_cube(pts)
     u = to_unit(pts, lo, width)
+    tree = build_subtree(u, f, p, tau, max_depth, 0, (0, 0, 0), delta, descend)
+    tree.lo, tree.width = lo, width
+    return tree
+
+
+def build_subtree(u: np.ndarray, f: np.ndarray, p: int, tau: float, max_depth: int, depth0: int,
+                  cell0: tuple[int, int, int], delta: float = DELTA, descend=None) -> Tree:
+    """FMT_Mesh_to_Tree (Algorithm 1) called on the node P of depth ``depth0`` and cell
+    ``cell0`` (Alg. 1 is stated for any node P: its recursion calls itself on each created octant,
+    P:308-309).  ``u``: root-cube coordinates of P's points (all inside P's box); ``f``: the residual
+    P receives (the original values when P is the root).  Run depth-first exactly as printed:
+
+      line 2  map to the node frame (P:299)                  -> local_coords
+      line 3  FMT_Mesh_to_Moments: fit, f <- f - Λ P_F (Alg. 2)  -> fit_node, apply_fit
+      line 4  FMT_Ordered_by_Octant: stable partition into 8 blocks (P:301)
+      lines 6-12 for each octant o with n_o points:
+              E_RMS = sqrt(sum_block f^2 / n_o) on the post-fit residual (P:305, G3)
+              recurse iff E_RMS > tau and n_o >= 𝓛 (P:306, G4) and depth+1 <= max_depth (G5)
+              block bounds: running start j, end j + n_o (G2, S:378)
+
+    ``descend(depth, cell) -> bool`` (None = always) is a test-harness restriction, not part of the
+    method: a child that Alg. 1 creates but ``descend`` rejects is recorded with child_index -2
+    ("created, not expanded in this run") and its subtree is skipped.  Subtrees are independent given
+    the residual they receive, so every expanded node is exactly the node of the unrestricted run.
+    Returned nodes are in creation (pre-)order; node 0 is P.  ``residual`` is the final residual in
+    the order of ``u`` (entries of skipped subtrees hold their received residual)."""
+    u = np.asarray(u, dtype=np.float64).reshape(-1, 3)
+    f = np.asarray(f, dtype=np.float64).reshape(-1)
+    N = u.shape[0]
+    L = rank(p)
     perm = np.arange(N)          # current order of the points (Alg. 1 permutes in place)
     res = f.copy()               # the residual, in 'perm' order
     nodes = []                   # dicts, in creation (pre-)order
 
     # explicit stack of (depth, cell, start, end, parent, octant-in-parent)
-    stack = [(0, (0, 0, 0), 0, N, -1, -1)]
+    stack = [(depth0, tuple(int(v) for v in cell0), 0, N, -1, -1)]
     while stack:
         depth, cell, j0, j1, parent, oct_in_parent = stack.pop()
         idx = perm[j0:j1]
         ul = local_coords(u[idx], depth, np.array(cell))
         fit = fit_node(ul, res[j0:j1], p, delta)
-        res[j0:j1] = res[j0:j1] - vandermonde(ul, p) @ fit.coeffs     # Alg. 2 last line
+        res[j0:j1] = res[j0:j1] - apply_fit(ul, fit.coeffs, p)              # Alg. 2 last line (P:332)
         n = j1 - j0
         me = len(nodes)
         node = dict(depth=depth, cell=cell, n=n, coeffs=fit.coeffs, kept=fit.kept,
                     min_pivot=fit.min_pivot,
-                    rms=float(np.sqrt(np.sum(res[j0:j1] ** 2) / n)),
+                    rms=float(np.sqrt(np.sum(res[j0:j1] ** 2) / n)) if n else 0.0,
                     child_rms=np.full(8, np.nan), child_count=np.zeros(8, dtype=np.int64),
                     child_index=np.full(8, -1, dtype=np.int64))
         nodes.append(node)
@@ -278,7 +332,10 @@ def build(points: np.ndarray, f: np.ndarray, p: int, tau: float, max_depth: int,
                 node["child_rms"][oc] = e_rms
                 if e_rms > tau and n_o >= L and depth + 1 <= max_depth:        # P:306 (+ G5)
                     ccell = (2 * cell[0] + (oc & 1), 2 * cell[1] + ((oc >> 1) & 1), 2 * cell[2] + ((oc >> 2) & 1))
-                    children.append((depth + 1, ccell, j, k, me, oc))          # FMT_New_Octant
+                    if descend is None or descend(depth + 1, ccell):
+                        children.append((depth + 1, ccell, j, k, me, oc))      # FMT_New_Octant
+                    else:
+                        node["child_index"][oc] = -2
             j = k                                                               # G2
         # push in reverse so that octant 1 is processed first (depth-first, as Alg. 1)
         stack.extend(reversed(children))
@@ -287,7 +344,7 @@ def build(points: np.ndarray, f: np.ndarray, p: int, tau: float, max_depth: int,
     residual[perm] = res
     T = len(nodes)
     return Tree(
-        p=p, tau=tau, max_depth=max_depth, lo=lo, width=width,
+        p=p, tau=tau, max_depth=max_depth, lo=np.zeros(3), width=1.0,
         depth=np.array([nd["depth"] for nd in nodes], dtype=np.int64),
         cell=np.array([nd["cell"] for nd in nodes], dtype=np.int64).reshape(T, 3),
         prefix=np.array([morton_prefix(nd["depth"], nd["cell"]) for nd in nodes], dtype=np.uint64),
@@ -322,12 +379,14 @@ def evaluate(tree: Tree, q: np.ndarray) -> np.ndarray:
         for nd in np.unique(nodes_here):
             sel = active[nodes_here == nd]
             ul = local_coords(u[sel], int(tree.depth[nd]), tree.cell[nd])
-            out[sel] += vandermonde(ul, tree.p) @ tree.coeffs[nd]
+            out[sel] += apply_fit(ul, tree.coeffs[nd], tree.p)
             sel_in = sel[inside[sel]]
             if sel_in.size == 0:
                 continue
             o = octant(local_coords(u[sel_in], int(tree.depth[nd]), tree.cell[nd]))
             ch = tree.child_index[nd][o]
+            if np.any(ch == -2):
+                raise ValueError("query reaches a node that this restricted run did not expand")
             go = ch >= 0
             node_of[sel_in[go]] = ch[go]
             nxt.append(sel_in[go])

@@ -392,3 +392,98 @@ def test_beats_prior_work_franke():
     q = workloads.uniform_points(n, 1)
     erms, einf = workloads.rms_and_max(fo.evaluate(tree, q) - workloads.franke3d(q))
     assert erms < float(erms_b) and einf < float(einf_b)
+
+
+# ---------------------------------------------------------------------------------------------
+# row-streamed QR (TSQR branch of _qr_r and of fit_node, nodes above 2^16 rows)
+# ---------------------------------------------------------------------------------------------
+
+def test_qr_r_tsqr_branch_equals_lapack():
+    """_qr_r above _TSQR_ROWS rows streams blocks (R <- qr([R; block])).  Householder R is unique up
+    to the signs of its rows: |R| must equal LAPACK's one-shot dgeqrf R of the same matrix, and RᵀR
+    must equal AᵀA."""
+    rng = np.random.default_rng(11)
+    n = fo._TSQR_ROWS + 4_321
+    A = rng.standard_normal((n, 24))
+    A[:, 5] *= 1e-3
+    R = fo._qr_r(A)
+    R0 = np.linalg.qr(A, mode="r")
+    assert R.shape == R0.shape == (24, 24)
+    s = np.sign(np.diag(R)) * np.sign(np.diag(R0))
+    assert np.max(np.abs(R * s[:, None] - R0)) <= 1e-10 * np.max(np.abs(R0))
+    G = A.T @ A
+    assert np.max(np.abs(R.T @ R - G)) <= 1e-11 * np.max(np.abs(G))
+
+
+@pytest.mark.parametrize("coplanar", [False, True])
+def test_fit_node_streamed_equals_single_block(coplanar, monkeypatch):
+    """fit_node on more than _TSQR_ROWS rows (column norms and TSQR streamed over row blocks) gives the
+    same fit as the single-block path on the same rows, including the rank-truncation walk."""
+    rng = np.random.default_rng(12)
+    u = rng.uniform(-1, 1, (3_000, 3))
+    if coplanar:
+        u[:, 2] = -0.25
+    f = workloads.franke3d((u + 1) / 2)
+    p = 4
+    one = fo.fit_node(u, f, p)
+    monkeypatch.setattr(fo, "_TSQR_ROWS", 700)
+    many = fo.fit_node(u, f, p)
+    assert np.array_equal(one.kept, many.kept)
+    V = fo.vandermonde(u, p)
+    assert np.max(np.abs(V @ one.coeffs - V @ many.coeffs)) <= 1e-12
+    assert np.max(np.abs(fo.apply_fit(u, many.coeffs, p) - V @ many.coeffs)) <= 1e-15
+
+
+def test_fit_node_above_tsqr_threshold_equals_independent_lstsq():
+    """A node with more than 2^16 points (the real streaming threshold): fitted values equal an SVD
+    least-squares fit in the Legendre product basis (independent basis and routine)."""
+    rng = np.random.default_rng(13)
+    u = rng.uniform(-1, 1, (fo._TSQR_ROWS + 3_777, 3))
+    f = workloads.franke3d((u + 1) / 2)
+    p = 3
+    fit = fo.fit_node(u, f, p)
+    assert fit.kept.all()
+    ours = fo.apply_fit(u, fit.coeffs, p)
+    ref = _ls_eval(_ls_fit((u + 1) / 2, f, p), (u + 1) / 2, p)
+    assert np.max(np.abs(ours - ref)) <= 1e-12
+
+
+def test_restricted_and_node_started_runs_reproduce_the_full_tree():
+    """Alg. 1 called on a node (build_subtree) with the residual that node receives, and a run whose
+    expansion is restricted to a few cells (descend), reproduce the unrestricted run's nodes exactly:
+    the recursion only reads the node's own block."""
+    pts = workloads.uniform_points(6_000, 3)
+    f = workloads.franke3d(pts)
+    p, tau, D = 2, 1e-5, 3
+    full = fo.build(pts, f, p, tau, D)
+    fk = {(int(full.depth[i]), tuple(int(v) for v in full.cell[i])): i for i in range(full.node_count)}
+    pick = {(2, (1, 2, 0)), (2, (3, 3, 3))}
+
+    def descend(d, cell):
+        return d < 2 or any(d >= dd and tuple(c >> (d - dd) for c in cell) == cc for dd, cc in pick)
+
+    part = fo.build(pts, f, p, tau, D, descend=descend)
+    assert 9 < part.node_count < full.node_count
+    for i in range(part.node_count):
+        key = (int(part.depth[i]), tuple(int(v) for v in part.cell[i]))
+        j = fk[key]
+        assert np.array_equal(part.coeffs[i], full.coeffs[j])
+        assert np.array_equal(part.child_count[i], full.child_count[j])
+        assert np.array_equal(part.child_index[i] != -1, full.child_index[j] >= 0)
+        if key[0] == 2 and key not in pick:
+            raise AssertionError("expanded a node outside the restriction")
+    # node-started run: depth-1 node (1,0,1) with the residual the root leaves on its points
+    cell = (1, 0, 1)
+    inside = np.all(np.minimum(np.floor(pts * 2), 1).astype(int) == cell, axis=1)
+    root_only = fo.build(pts, f, p, tau, D, descend=lambda d, c: False)
+    sub = fo.build_subtree(pts[inside], root_only.residual[inside], p, tau, D, 1, cell)
+    for i in range(sub.node_count):
+        j = fk[(int(sub.depth[i]), tuple(int(v) for v in sub.cell[i]))]
+        assert np.array_equal(sub.coeffs[i], full.coeffs[j])
+        assert sub.residual_rms[i] == full.residual_rms[j]
+    assert sub.node_count == sum(1 for k in fk if k[0] >= 1 and tuple(c >> (k[0] - 1) for c in k[1]) == cell)
+    # evaluation inside the subtree: same path sum as the full tree minus the root term
+    q = (np.array(cell) + workloads.uniform_points(300, 4)) / 2
+    ul0 = fo.local_coords(q, 0, np.zeros(3, dtype=np.int64))
+    got = fo.evaluate(sub, q) + fo.apply_fit(ul0, full.coeffs[0], p)
+    assert np.max(np.abs(got - fo.evaluate(full, q))) <= 1e-14
