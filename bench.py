@@ -27,6 +27,7 @@ import json
 import math
 import os
 import statistics
+import subprocess
 import sys
 import threading
 import time
@@ -133,24 +134,86 @@ class ClockSampler:
 # ------------------------------------------------------------------------------------------------
 # CPU baseline: the oracle as it stands on a bounded sample of the workload
 # ------------------------------------------------------------------------------------------------
-def oracle_sample_cfg(cfg: workloads.Config, target_points: int) -> workloads.Config:
-    n = min(cfg.n, target_points)
-    m = min(cfg.m, target_points)
-    return cfg.scaled(n=n, m=m)
+def host_cores() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
 
 
-def time_oracle(cfg: workloads.Config, sample_points: int):
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def _oracle_cell_job(args):
+    """One sampled subtree: Alg. 1 called on the cell's node with the original values (telescoping
+    start) + the interpolant at the config's queries inside the cell."""
+    u, f, q, p, tau, D, depth, cell = args
     from oracle import fmt_oracle
-    sc = oracle_sample_cfg(cfg, sample_points)
-    pts, f, q = workloads.make_inputs(sc)
     t0 = time.perf_counter()
-    tree = fmt_oracle.build(pts, f, sc.degree, sc.tol, sc.max_depth)
+    tree = fmt_oracle.build_subtree(u, f, p, tau, D, depth, cell)
     fmt_oracle.evaluate(tree, q)
+    return time.perf_counter() - t0, tree.node_count
+
+
+def time_oracle_sample(cfg: workloads.Config, pts, f, q, target_points: int, cells: int | None = None, seed: int = 0):
+    """The oracle (as it stands, never tuned) on a bounded sample of the SAME workload, on every host core.
+
+    If the config holds <= target_points points the sample is the whole workload (one process).  Else the
+    sample is ``cells`` (default: one per core) random octree cells of the shallowest depth d whose mean
+    cell holds <= target_points points (cells with >= 𝓛 points), each fitted as Alg. 1 called on that node
+    with the original values and evaluated at the config's queries inside it, one process per cell, all
+    cores busy.  value = (sampled points + sampled queries) / wall time."""
+    from oracle import fmt_oracle
+    cores = host_cores()
+    if cfg.n <= target_points:
+        t0 = time.perf_counter()
+        tree = fmt_oracle.build(pts, f, cfg.degree, cfg.tol, cfg.max_depth)
+        fmt_oracle.evaluate(tree, q)
+        dt = time.perf_counter() - t0
+        sample = (f"the whole {cfg.name} workload (N={cfg.n:,}, M={cfg.m:,}) -> {tree.node_count} nodes; "
+                  f"one process (numpy + single-threaded LAPACK QR)")
+        return (cfg.n + cfg.m) / dt, dt, 1, sample
+    d = 0
+    while cfg.n / 8 ** d > target_points:
+        d += 1
+    L = ranks(cfg.degree)[1]
+    cp = workloads.cell_of(pts, d)
+    lab = cp[:, 0] | (cp[:, 1] << d) | (cp[:, 2] << (2 * d))
+    cnt = np.bincount(lab, minlength=8 ** d)
+    cand = np.flatnonzero(cnt >= L)
+    k = min(len(cand), cells or cores)
+    pick = np.random.default_rng(seed).choice(cand, size=k, replace=False)
+    cq = workloads.cell_of(q, d)
+    qlab = cq[:, 0] | (cq[:, 1] << d) | (cq[:, 2] << (2 * d))
+    jobs, npts, nq = [], 0, 0
+    for c in pick:
+        cell = (int(c & (2 ** d - 1)), int((c >> d) & (2 ** d - 1)), int(c >> (2 * d)))
+        sel = lab == c
+        qsel = qlab == c
+        jobs.append((np.ascontiguousarray(pts[sel]), np.ascontiguousarray(f[sel]), np.ascontiguousarray(q[qsel]),
+                     cfg.degree, cfg.tol, cfg.max_depth, d, cell))
+        npts += int(sel.sum())
+        nq += int(qsel.sum())
+    import multiprocessing as mp
+    t0 = time.perf_counter()
+    with mp.get_context("spawn").Pool(min(cores, k)) as pool:
+        res = pool.map(_oracle_cell_job, jobs, chunksize=1)
     dt = time.perf_counter() - t0
-    sample = (f"{sc.name} recipe at N={sc.n:,}, M={sc.m:,} (same p={sc.degree}, tol={sc.tol:g}, "
-              f"max_depth={sc.max_depth}, generator) -> {tree.node_count} nodes; oracle = numpy + "
-              f"single-threaded LAPACK QR")
-    return (sc.n + sc.m) / dt, dt, sample
+    nodes = sum(r[1] for r in res)
+    sample = (f"{k} random depth-{d} cells of the {cfg.name} workload ({npts:,} points, {nq:,} queries, {nodes} nodes), "
+              f"each = Alg. 1 called on the cell's node with the original values (telescoping start) + the "
+              f"interpolant at the config's queries in it; {min(cores, k)} processes on {cores} cores "
+              f"({cpu_model()}), numpy + single-threaded LAPACK QR per process.  Only levels >= {d} are fitted, "
+              f"so this overstates the oracle's whole-workload throughput")
+    return (npts + nq) / dt, dt, min(cores, k), sample
 
 
 # ------------------------------------------------------------------------------------------------
@@ -175,33 +238,45 @@ def projected_points(t, L: int, max_depth: int) -> int:
     return int(proj.sum())
 
 
-def kernel_work(cfg, levels_points, depth_max: int, projected=None):
-    """Per-step algorithmic work of the main kernels: (unit, amount) — flops or bytes."""
+def kernel_work(cfg, levels_points, depth_max: int, projected=None, units=None):
+    """Per-step algorithmic work of the main kernels: (unit, amount) — flops or bytes.
+    ``units``: per-kernel work units the library counted in the timed region (fmi_profile_units),
+    divided by the number of steps — the sort passes and solved nodes actually executed."""
     K, L = ranks(cfg.degree)
     N, M = cfg.n, cfg.m
     pts = [int(x) for x in levels_points]
+    units = units or {}
     if projected is None:  # every point of every level projected (upper bound)
         projected = sum(pts)
-    return {
+    w = {
         # K4: one FMA per raw moment per point, once per build (owner pass)
         "moments": ("flop", 2 * K * N),
         # K6 per level: Horner (𝓛 FMA) + Σr² (1 FMA) per point, child projection (𝓛 FMA) per point
         # of a block that may become a child (deferred blocks: only those that did)
         "residual": ("flop", sum(n * (2 * L + 2) for n in pts) + 2 * L * projected),
-        # K6 root mode: projection of f onto the root frame (𝓛 FMA per point)
+        # K6 root mode (single GPU: fused with the Morton-order gather): projection of f onto the root
+        # frame (𝓛 FMA per point)
         "project": ("flop", 2 * L * N),
         # K7: one Horner of the pre-summed polynomial per query
         "eval": ("flop", 2 * L * M),
-        # K2: per 8-bit pass read key+index (12 B), write them (12 B), histogram read (8 B)
-        "sort": ("byte", 32 * (N * -(-3 * (cfg.max_depth + 1) // 8) + M * -(-3 * depth_max // 8))),
-        # gather: perm (4 B) + point (24 B) + value (8 B) read, 4 SoA doubles (32 B) written
+        # gather (sharded builds; fused into "project" on one GPU): perm (4 B) + record (32 B) read,
+        # 4 SoA doubles (32 B) written
         "gather": ("byte", 68 * N),
     }
+    if "sort" in units:   # 8-bit passes actually executed: 8 B (histogram) + 12 B read + 12 B written per item
+        w["sort"] = ("byte", 32 * units["sort"])
+    if "keys" in units:   # bytes counted per launch by the library (coordinates, values, keys, records)
+        w["keys"] = ("byte", units["keys"])
+    if "solve" in units:  # bordered Cholesky 𝓛³/3 + substitutions and assembly 3𝓛² per factored node
+        w["solve"] = ("flop", units["solve"] * (L ** 3 / 3 + 3 * L * L))
+    return w
 
 
-def rooflines(cfg, levels_points, depth_max, prof, steps, ms_per_step, hbm_peak, projected=None):
+def rooflines(cfg, levels_points, depth_max, prof, steps, ms_per_step, hbm_peak, projected=None, units=None,
+              traffic=None):
     out = {}
-    for name, (unit, work) in kernel_work(cfg, levels_points, depth_max, projected).items():
+    per_step_units = {k: v / steps for k, v in (units or {}).items() if v}
+    for name, (unit, work) in kernel_work(cfg, levels_points, depth_max, projected, per_step_units).items():
         ms, n = prof.get(name, (0.0, 0))
         if not n or ms <= 0:
             continue
@@ -215,36 +290,72 @@ def rooflines(cfg, levels_points, depth_max, prof, steps, ms_per_step, hbm_peak,
         out[name] = {"bound": bound, "achieved": achieved, "peak": peak, "unit": u, "frac": achieved / peak,
                      "traffic": None, "work_per_launch": per_launch, "launches_per_step": launches,
                      "mean_launch_ms": ms / n, "share_of_step": (ms / steps) / ms_per_step}
+        t = (traffic or {}).get(name)
+        if t:
+            out[name]["traffic"] = t["dram_bytes_per_launch"]
+            out[name]["traffic_note"] = t["source"]
     return out
 
 
+def load_traffic(cfg) -> dict:
+    """Per-kernel DRAM bytes per launch (dram__bytes_read.sum + dram__bytes_write.sum) from the committed
+    ncu capture of this config (profiles/traffic_cfg<c>.json, written by tools/ncu_traffic.py with the
+    capture file and commit it came from); {} if there is none."""
+    try:
+        with open(os.path.join(ROOT, "profiles", f"traffic_cfg{cfg.cfg}.json")) as fh:
+            return json.load(fh)
+    except Exception:
+        return {}
+
+
 def run_reference(args, cfg, rank, world):
+    """The base contract's reference arm for this tier: the oracle (oracle/fmt_oracle.py, CPU, as it stands)
+    timed on this host's cores, each step a bounded sample of the workload (time_oracle_sample)."""
     if rank != 0:
         return
-    sample_points = 50_000 if cfg.cfg >= 3 else min(cfg.n, 50_000)
-    times = []
+    pts, f, q = workloads.make_inputs(cfg)
+    target = 60_000
+    times, vals = [], []
     for i in range(args.warmup + args.steps):
-        v, dt, sample = time_oracle(cfg, sample_points)
+        v, dt, cores, sample = time_oracle_sample(cfg, pts, f, q, target, seed=i)
         if i >= args.warmup:
             times.append(dt)
-    sc = oracle_sample_cfg(cfg, sample_points)
+            vals.append(v)
+    value = statistics.median(vals)
     t = statistics.median(times)
-    value = (sc.n + sc.m) / t
     line = {
         "impl": "reference", "metric": "fp64 octree fit + eval points/sec", "value": value, "unit": "points/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": f"{cfg.name}: N={cfg.n:,} M={cfg.m:,} p={cfg.degree} max_depth={cfg.max_depth} "
-                               f"tol={cfg.tol:g} ({cfg.points}/{cfg.values})", "sample_n": sc.n, "sample_m": sc.m},
-        "cpu_baseline": {"value": value, "unit": "points/s", "cores": 1, "kind": "oracle", "sample": sample},
+                               f"tol={cfg.tol:g} ({cfg.points}/{cfg.values})"},
+        "cpu_baseline": {"value": value, "unit": "points/s", "cores": cores, "kind": "oracle", "sample": sample,
+                         "host_cores": host_cores(), "cpu_model": cpu_model()},
         "e2e": {"value": value, "unit": "points/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
+def self_launch(args) -> None:
+    """`bench.py --gpus N` outside torchrun: re-run this command under torch.distributed.run with N ranks
+    (the driver's own launch line), so that N processes, one per GPU, are always what is measured."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    sys.exit(subprocess.call(cmd))
+
+
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        self_launch(args)
     rank, world, local = dist_env()
+    if world != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr)
+        sys.exit(2)
     cfg = workloads.CONFIGS[args.config]
     if args.n or args.m:
         cfg = cfg.scaled(n=args.n, m=args.m)
@@ -274,6 +385,7 @@ def main():
     pts, f, q = workloads.make_inputs(cfg)
     gen_s = time.perf_counter() - t_gen
     N, M = cfg.n, cfg.m
+    pts_all, f_all, q_all = pts, f, q
     if world > 1:  # this rank's slice of the global workload (the sharded build exchanges by cell)
         pts, f = pts[rank * N // world:(rank + 1) * N // world], f[rank * N // world:(rank + 1) * N // world]
         q = q[rank * M // world:(rank + 1) * M // world]
@@ -347,6 +459,7 @@ def main():
     launches = fmi.launch_count() - launches0
     fmi.profile_enable(False)
     prof = fmi.profile_get()
+    units = fmi.profile_units()
     total_ms = ev0.elapsed_time(ev1)
     if world > 1:
         t = torch.tensor([total_ms], device=dev, dtype=torch.float64)
@@ -362,20 +475,13 @@ def main():
     pt_levels = int(np.sum(levels_points))
     hbm_peak = measured_hbm_peak()
     roofs = rooflines(cfg, levels_points, len(levels_points) - 1, prof, args.steps, ms_per_step, hbm_peak,
-                      proj_pts)
+                      proj_pts, units, load_traffic(cfg) if world == 1 else None)
     dominant = max(roofs, key=lambda k: roofs[k]["share_of_step"]) if roofs else None
-    # DRAM traffic per k_residual launch from an ncu capture of one cfg-5 build (tools/gpu/run48.sh,
-    # profiles/round1_k6_traffic_cfg5.csv): the step's 11 launches (6 Horner-only passes, 5 projection
-    # passes) move 63.45 GB = the algorithmic 40 B per point-level + 32 B per projected point (no re-reads)
-    if cfg.cfg == 5 and roofs.get("residual"):
-        roofs["residual"]["traffic"] = 63.45e9 / 11
-        roofs["residual"]["traffic_note"] = ("ncu dram__bytes_read+write summed over the 11 k_residual launches of a "
-                                             "cfg-5 build / 11; algorithmic 40 B/point-level + 32 B/projected point")
-    # k_moments (one launch per build): 4.82 GB read (= the algorithmic 24 B/point) + 2.90 GB of per-chunk
-    # partial sums written (profiles/round1_ncu_k4_traffic.txt)
-    if cfg.cfg == 5 and roofs.get("moments"):
-        roofs["moments"]["traffic"] = 7.71e9
-        roofs["moments"]["traffic_note"] = "ncu dram__bytes_read+write of the cfg-5 launch: 4.82 GB read + 2.90 GB written"
+    # correctness of the timed step's output: interpolation error against the analytic function on a
+    # sample of this rank's queries, next to the oracle-parity tests (tests/test_gpu_*.py)
+    out_host = d_out.cpu().numpy()
+    chk = np.random.default_rng(0).choice(q.shape[0], size=min(q.shape[0], 1_000_000), replace=False)
+    e_rms, e_inf = workloads.rms_and_max(out_host[chk] - workloads.exact_values(cfg, q[chk]))
     step_kernel_ms = sum(v[0] for v in prof.values()) / args.steps
 
     # ---- e2e through the C ABI with pinned host buffers -----------------------------------------
@@ -418,9 +524,9 @@ def main():
     if rank == 0:
         cpu = None
         if not args.no_cpu_baseline and world == 1:
-            v, dt, sample = time_oracle(cfg, 100_000)
-            cpu = {"value": v, "unit": "points/s", "cores": 1, "kind": "oracle", "sample": sample,
-                   "seconds": dt}
+            v, dt, cores, sample = time_oracle_sample(cfg, pts_all, f_all, q_all, 400_000)
+            cpu = {"value": v, "unit": "points/s", "cores": cores, "kind": "oracle", "sample": sample,
+                   "seconds": dt, "host_cores": host_cores(), "cpu_model": cpu_model()}
         line = {
             "metric": "fp64 octree fit + eval points/sec",
             "value": value, "unit": "points/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -455,7 +561,8 @@ def main():
                     "step_ms": e2e_step_ms},
             "gpu_launches": int(launches),
             "clocks": clocks.summary(),
-            "check": {"max_abs_out": gpu_out_max},
+            "check": {"queries": int(chk.size), "e_rms_vs_exact": e_rms, "e_inf_vs_exact": e_inf,
+                      "max_abs_out_e2e": gpu_out_max},
         }
         print(json.dumps(line), flush=True)
     if world > 1:

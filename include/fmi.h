@@ -223,8 +223,13 @@ int fmi_profile_enable(int on);
 int fmi_profile_reset(void);
 /* kernel names: "keys", "sort", "gather", "moments", "moments_reduce", "solve", "children",
  * "residual", "residual_reduce", "decide", "chunks", "scan", "eval", "misc", "project", "m2m",
- * "level_gather", "refine_solve", "refine", "presum", "unscoped_gram", "unscoped_solve" */
+ * "level_gather", "refine_solve", "refine", "presum", "unscoped_gram", "unscoped_solve", "solve_qr" */
 int fmi_profile_get(const char* kernel, double* total_ms, int64_t* launches);
+/* Algorithmic work units the kernel's launches processed since the last reset (while enabled):
+ * "keys" keyed points + queries, "sort" items summed over the 8-bit passes actually executed,
+ * "solve" nodes factored by the Gram solve (K5), "refine_solve" node substitutions (K5r).
+ * bench.py multiplies them by the per-unit bytes / flops of DESIGN.md §5.  0 / FMI_EINPUT. */
+int fmi_profile_units(const char* kernel, int64_t* units);
 /* Total kernel launches issued by the library since load (or since fmi_profile_reset). */
 int64_t fmi_launch_count(void);
 

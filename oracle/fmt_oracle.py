@@ -68,9 +68,11 @@ def basis(p: int) -> list[tuple[int, int, int]]:
 def vandermonde(u: np.ndarray, p: int) -> np.ndarray:
     """Λ(1:N, lmn) = x1^l x2^m x3^n / (l! m! n!) (§2 geometric moments; Alg. 2)."""
     u = np.asarray(u, dtype=np.float64).reshape(-1, 3)
+    # pw[a][k] = u_a ** k, each power formed once (the same `**` as inline, so the same bits)
+    pw = [[u[:, a] ** k for k in range(p + 1)] for a in range(3)]
     cols = []
     for (l, m, n) in basis(p):
-        cols.append(u[:, 0] ** l * u[:, 1] ** m * u[:, 2] ** n / (factorial(l) * factorial(m) * factorial(n)))
+        cols.append(pw[0][l] * pw[1][m] * pw[2][n] / (factorial(l) * factorial(m) * factorial(n)))
     return np.stack(cols, axis=1) if cols else np.zeros((u.shape[0], 0))
 
 

@@ -5,7 +5,9 @@
 //   moment tree + raw moments once per build (K4 + M2M: the Gram of Alg. 2)
 //   per level: K5 node solve -> fused K6 residual update + block energies + child
 //   projections (Qᵀf of the children) -> decisions + compaction.
-// The only host synchronisation per level is one 16-byte read of the next level's size.
+// Host synchronisations per fit level: two small counter reads (after K5: refinement / direct-moment /
+// deferral counts; after the decisions: the next level's size), plus two more on the rare levels with
+// nodes whose translated moments fail the rounding check; one per moment-tree level.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -155,6 +157,7 @@ std::vector<Pending> g_pending;
 std::vector<cudaEvent_t> g_event_pool;
 double g_prof_ms[KID_COUNT];
 int64_t g_prof_n[KID_COUNT];
+int64_t g_prof_units[KID_COUNT];
 thread_local cudaEvent_t tl_open = nullptr;
 
 cudaEvent_t get_event() {
@@ -171,7 +174,7 @@ const char* kNames[KID_COUNT] = {"keys",     "sort",     "gather", "moments", "m
                                  "solve",    "children", "residual", "residual_reduce",
                                  "decide",   "chunks",   "scan",   "eval",    "misc",
                                  "project",  "m2m",      "level_gather", "refine_solve", "refine", "presum",
-                                 "unscoped_gram", "unscoped_solve"};
+                                 "unscoped_gram", "unscoped_solve", "solve_qr"};
 }  // namespace
 
 const char* kernel_name(int kid) { return (kid >= 0 && kid < KID_COUNT) ? kNames[kid] : "?"; }
@@ -192,6 +195,12 @@ void prof_end(int kid, cudaStream_t s) {
   FMI_CK(cudaEventRecord(b, s));
   g_pending.push_back({kid, tl_open, b});
   tl_open = nullptr;
+}
+
+void prof_units(int kid, int64_t units) {
+  if (!g_prof.load(std::memory_order_relaxed) || kid < 0 || kid >= KID_COUNT) return;
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  g_prof_units[kid] += units;
 }
 
 void prof_collect() {
@@ -414,7 +423,7 @@ void fused_gather_root(const double4* packed, const uint32_t* perm, const double
 //     upward translation (M2M), deepest level first;
 //  C. root projection (one pass), then per fit level: gather [moments | projection] -> K5 solve
 //     (+ K5q QR re-fit of flagged nodes) -> fused K6 (residual, block energies, child projections)
-//     -> decisions + compaction.  One 16-byte D2H per level (the next level's size).
+//     -> decisions + compaction.  Small counter read-backs: after K5 and after the decisions.
 template <int P>
 void run_levels(fmi_tree* T, const uint64_t* keys, double* ux, double* uy, double* uz, double* r, cudaStream_t s,
                 const double* root_b, const LateValues* late) {
@@ -613,6 +622,8 @@ void run_levels(fmi_tree* T, const uint64_t* keys, double* ux, double* uy, doubl
       if (nref > 0) {
         T->refined_nodes += nref;
         delta.ensure((size_t)count * L, s);
+        // FMI_REFINE_STEPS=0: the K6_CHILD pass still reads δ of the flagged nodes — make it zero
+        if (T->refine_steps == 0) FMI_CK(cudaMemsetAsync(delta.p, 0, (size_t)count * L * sizeof(double), s));
         for (int it = 0; it < T->refine_steps; ++it) {
           level_residual<P>(c, K6_OWN, it, delta.p, chunks.p, dev_small.p + 1, max6, begin.p, count * 8, partial.p,
                             segsum.p, s);
@@ -1131,11 +1142,46 @@ void dump(FILE* fp, const T* dev, int64_t n, cudaStream_t s) {
   if (n && fwrite(h.data(), sizeof(T), (size_t)n, fp) != (size_t)n) fail(FMI_EINPUT, "short write");
 }
 template <typename T>
-void undump(FILE* fp, T* dev, int64_t n, cudaStream_t s) {
+std::vector<T> undump(FILE* fp, T* dev, int64_t n, cudaStream_t s) {
   std::vector<T> h((size_t)n);
   if (n && fread(h.data(), sizeof(T), (size_t)n, fp) != (size_t)n) fail(FMI_EVERSION, "truncated tree file");
   if (n) FMI_CK(cudaMemcpyAsync(dev, h.data(), (size_t)n * sizeof(T), cudaMemcpyHostToDevice, s));
   FMI_CK(cudaStreamSynchronize(s));
+  return h;
+}
+
+// A loaded file is untrusted input: the evaluation kernels follow child indices and the level
+// tables are indexed by depth, so every node record is checked before the tree is handed out
+// (FMI_EVERSION with the offending node index).
+void validate_nodes(const std::vector<int4>& cell, const std::vector<int32_t>& parent,
+                    const std::vector<int32_t>& child, const std::vector<int32_t>& rank, int depth_max, int D, int L) {
+  const int64_t n = (int64_t)cell.size();
+  auto bad = [](int64_t i, const char* what) {
+    fail(FMI_EVERSION, "corrupt tree file: node " + std::to_string(i) + ": " + what);
+  };
+  for (int64_t i = 0; i < n; ++i) {
+    const int d = cell[i].w;
+    if (d < 0 || d > depth_max || d > D) bad(i, "depth out of range");
+    if (i == 0 ? d != 0 : (d != cell[i - 1].w && d != cell[i - 1].w + 1)) bad(i, "depths not level-contiguous");
+    const int64_t side = int64_t(1) << d;
+    if (cell[i].x < 0 || cell[i].y < 0 || cell[i].z < 0 || cell[i].x >= side || cell[i].y >= side || cell[i].z >= side)
+      bad(i, "cell outside its level");
+    if (rank[i] < 0 || rank[i] > L) bad(i, "rank out of range");
+    const int32_t pa = parent[i];
+    if (i == 0) {
+      if (pa != -1) bad(i, "root has a parent");
+    } else if (pa < 0 || pa >= i || cell[pa].w != d - 1) {
+      bad(i, "parent index");
+    }
+    for (int o = 0; o < 8; ++o) {
+      const int32_t c = child[(size_t)i * 8 + o];
+      if (c == -1) continue;
+      if (c <= i || c >= n || parent[c] != i || cell[c].w != d + 1 || cell[c].x != 2 * cell[i].x + (o & 1) ||
+          cell[c].y != 2 * cell[i].y + ((o >> 1) & 1) || cell[c].z != 2 * cell[i].z + ((o >> 2) & 1))
+        bad(i, "child index");
+    }
+  }
+  if (n > 0 && cell[n - 1].w != depth_max) bad(n - 1, "deepest level differs from the header");
 }
 }  // namespace
 
@@ -1368,7 +1414,10 @@ fmi_tree* fmi_load(const char* path) {
       if (fread(&h, sizeof h, 1, fp) != 1 || std::memcmp(h.magic, kMagic, 8) != 0)
         fail(FMI_EVERSION, "not an fmi tree file");
       if (h.version != kFileVersion) fail(FMI_EVERSION, "unsupported tree file version");
-      if (h.p < 0 || h.p > FMI_MAX_DEGREE || h.nodes < 1 || h.depth_max < 0 || h.depth_max > FMI_MAX_DEPTH)
+      if (h.p < 0 || h.p > FMI_MAX_DEGREE || h.nodes < 1 || h.nodes > (int64_t(1) << 31) - 1 || h.depth_max < 0 ||
+          h.depth_max > FMI_MAX_DEPTH || h.D < 0 || h.D > FMI_MAX_DEPTH || h.depth_max > h.D ||
+          (h.p > FMI_MAX_LEVEL_DEGREE && h.D != 0) || !(h.width > 0) || !std::isfinite(h.width) ||
+          !std::isfinite(h.lo[0]) || !std::isfinite(h.lo[1]) || !std::isfinite(h.lo[2]) || !(h.tau >= 0) || h.N < 0)
         fail(FMI_EVERSION, "corrupt tree file header");
       T = new fmi_tree();
       T->p = h.p;
@@ -1387,20 +1436,19 @@ fmi_tree* fmi_load(const char* path) {
       ensure_table(T->nt, T->cap, h.nodes, T->L, true, s);
       T->nodes = h.nodes;
       const int64_t n = h.nodes, L = T->L;
-      undump(fp, T->nt.cell, n, s);
-      undump(fp, T->nt.parent, n, s);
-      undump(fp, T->nt.child, n * 8, s);
+      const std::vector<int4> cell = undump(fp, T->nt.cell, n, s);
+      const std::vector<int32_t> parent = undump(fp, T->nt.parent, n, s);
+      const std::vector<int32_t> child = undump(fp, T->nt.child, n * 8, s);
       undump(fp, T->nt.child_n, n * 8, s);
       undump(fp, T->nt.child_ss, n * 8, s);
       undump(fp, T->nt.coef, n * L, s);
       undump(fp, T->nt.pcoef, n * L, s);
       undump(fp, T->nt.rms, n, s);
       undump(fp, T->nt.minpiv, n, s);
-      undump(fp, T->nt.rank, n, s);
+      const std::vector<int32_t> rank = undump(fp, T->nt.rank, n, s);
       undump(fp, T->nt.flag, n, s);
+      validate_nodes(cell, parent, child, rank, h.depth_max, h.D, (int)L);
       // level bookkeeping from the (canonical, level-contiguous) depths
-      std::vector<int4> cell((size_t)n);
-      FMI_CK(cudaMemcpy(cell.data(), T->nt.cell, (size_t)n * sizeof(int4), cudaMemcpyDeviceToHost));
       for (int64_t i = 0; i < n; ++i) {
         const int d = cell[i].w;
         if (d >= (int)T->lvl_first.size()) {
@@ -1576,7 +1624,7 @@ int fmi_profile_enable(int on) {
 int fmi_profile_reset(void) {
   prof_collect();
   std::lock_guard<std::mutex> lk(g_prof_mu);
-  for (int k = 0; k < KID_COUNT; ++k) { g_prof_ms[k] = 0.0; g_prof_n[k] = 0; }
+  for (int k = 0; k < KID_COUNT; ++k) { g_prof_ms[k] = 0.0; g_prof_n[k] = 0; g_prof_units[k] = 0; }
   g_launches.store(0);
   return 0;
 }
@@ -1588,6 +1636,18 @@ int fmi_profile_get(const char* kernel, double* total_ms, int64_t* launches) {
     if (kernel && std::strcmp(kernel, kNames[k]) == 0) {
       if (total_ms) *total_ms = g_prof_ms[k];
       if (launches) *launches = g_prof_n[k];
+      return 0;
+    }
+  }
+  set_error(FMI_EINPUT, "unknown kernel name");
+  return FMI_EINPUT;
+}
+
+int fmi_profile_units(const char* kernel, int64_t* units) {
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  for (int k = 0; k < KID_COUNT; ++k) {
+    if (kernel && std::strcmp(kernel, kNames[k]) == 0) {
+      if (units) *units = g_prof_units[k];
       return 0;
     }
   }

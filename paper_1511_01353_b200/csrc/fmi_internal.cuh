@@ -48,12 +48,16 @@ enum KernelId {
   KID_KEYS = 0, KID_SORT, KID_GATHER, KID_MOMENTS, KID_MOMENTS_REDUCE, KID_SOLVE, KID_CHILDREN,
   KID_RESIDUAL, KID_RESIDUAL_REDUCE, KID_DECIDE, KID_CHUNKS, KID_SCAN, KID_EVAL, KID_MISC, KID_PROJECT,
   KID_M2M, KID_LEVEL_GATHER, KID_REFINE_SOLVE, KID_REFINE, KID_PRESUM, KID_UNSCOPED_GRAM, KID_UNSCOPED_SOLVE,
+  KID_SOLVE_QR,
   KID_COUNT
 };
 const char* kernel_name(int kid);
 void prof_begin(int kid, cudaStream_t s);
 void prof_end(int kid, cudaStream_t s);
 void prof_collect();  // after a stream sync: accumulate elapsed times of completed launches
+// algorithmic work units processed by the launches of a kernel (items per sort pass, keyed points,
+// solved nodes, ...), summed while profiling is on; bench.py turns them into bytes / flops
+void prof_units(int kid, int64_t units);
 
 #define FMI_LAUNCH(kid, stream, kernel, grid, block, smem, ...)                          \
   do {                                                                                   \

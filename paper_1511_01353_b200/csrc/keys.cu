@@ -387,6 +387,8 @@ void morton_keys(const double* pts, int64_t n, const double lo[3], double width,
                  uint32_t* idx, cudaStream_t s, const double* f, double4* packed) {
   if (n <= 0) return;
   unsigned grid = (unsigned)((n + 255) / 256);
+  // algorithmic bytes: coordinates read (24), key + index written (12), record written (32), value read (8)
+  prof_units(KID_KEYS, n * (36 + (packed ? 32 : 0) + (f ? 8 : 0)));
   FMI_LAUNCH(KID_KEYS, s, k_keys, grid, 256, 0, pts, n, lo[0], lo[1], lo[2], width, unit, D, keys, idx, f, packed);
 }
 
@@ -403,6 +405,7 @@ void radix_sort_pairs(uint64_t*& keys, uint32_t*& vals, uint64_t*& keys_tmp, uin
   uint64_t* ka = keys; uint32_t* va = vals; uint64_t* kb = keys_tmp; uint32_t* vb = vals_tmp;
   int passes = 0;
   for (int shift = bit_lo; shift < nbits; shift += 8, ++passes) {
+    prof_units(KID_SORT, n);  // items of this pass: 8 B key read (histogram) + 12 B read + 12 B written (scatter)
     FMI_LAUNCH(KID_SORT, s, k_rs_hist, (unsigned)nblk, RS_THREADS, 0, ka, n, shift, nblk, counts.p);
     exclusive_scan_i64(counts.p, counts.p, nblk * 256, nullptr, s);
     FMI_LAUNCH(KID_SORT, s, k_rs_scatter, (unsigned)nblk, RS_THREADS, kScatterSmem, ka, va, n, shift, nblk, counts.p,

@@ -582,6 +582,7 @@ void level_solve(const LevelCtx& c, const double* mom, int mode, const double* s
   });
   const int64_t grid = std::min<int64_t>(c.count, 1 << 20);
   if (grid <= 0) return;
+  if (mode != 1) prof_units(KID_SOLVE, c.count);  // nodes factored (𝓛³/3 + 3𝓛² flop each)
   if (NT < 256 && grid <= small_max) {
     FMI_LAUNCH(mode == 1 ? KID_REFINE_SOLVE : KID_SOLVE, s, (k_solve<P, 256>), (unsigned)grid, 256, S::SMEM, mom,
                mode, segrhs, delta, c.nt, c.first, c.count, fac, bt, kDelta * kDelta, refine2, refine_fill, kMomentTol,

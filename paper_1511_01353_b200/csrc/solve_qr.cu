@@ -220,7 +220,7 @@ void level_solve_qr(const LevelCtx& c, const double* mom, double* scratch, int64
   static const BasisTabQ bt = make_basis_q<P>();
   const int64_t grid = std::min<int64_t>(c.count, slots);
   if (grid <= 0) return;
-  FMI_LAUNCH(KID_SOLVE, s, k_solve_qr<P>, (unsigned)grid, KQ_THREADS, 0, c.ux, c.uy, c.uz, c.r, c.nt, c.first,
+  FMI_LAUNCH(KID_SOLVE_QR, s, k_solve_qr<P>, (unsigned)grid, KQ_THREADS, 0, c.ux, c.uy, c.uz, c.r, c.nt, c.first,
              c.count, mom, scratch, bt, kDelta);
 }
 

@@ -33,7 +33,7 @@ EXPORTED = (
     "fmi_export_nodes", "fmi_root_cube", "fmi_residual", "fmi_level_stats", "fmi_profile_enable",
     "fmi_profile_reset", "fmi_profile_get", "fmi_launch_count", "fmi_build_stats", "fmi_build_dist",
     "fmi_dist_xbuf_bytes", "fmi_bbox", "fmi_cell_counts", "fmi_partition", "fmi_scatter", "fmi_transfer",
-    "fmi_save", "fmi_load",
+    "fmi_save", "fmi_load", "fmi_profile_units",
 )
 
 # allreduce(ctx, n, dtype) -> int: in-place SUM of the first n elements of the exchange buffer
@@ -52,7 +52,7 @@ class FmiDist(ctypes.Structure):
 
 KERNELS = ("keys", "sort", "gather", "moments", "moments_reduce", "solve", "children", "residual",
            "residual_reduce", "decide", "chunks", "scan", "eval", "misc", "project", "m2m", "level_gather",
-           "refine_solve", "refine", "presum", "unscoped_gram", "unscoped_solve")
+           "refine_solve", "refine", "presum", "unscoped_gram", "unscoped_solve", "solve_qr")
 
 
 class FmiNode(ctypes.Structure):
@@ -111,6 +111,8 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.fmi_profile_reset.argtypes = []
     lib.fmi_profile_get.restype = I32
     lib.fmi_profile_get.argtypes = [ctypes.c_char_p, P(D), P(I64)]
+    lib.fmi_profile_units.restype = I32
+    lib.fmi_profile_units.argtypes = [ctypes.c_char_p, P(I64)]
     lib.fmi_build_dist.restype = VP
     lib.fmi_build_dist.argtypes = [VP, VP, I64, I32, D, I32, P(FmiDist)]
     lib.fmi_dist_xbuf_bytes.restype = I64
@@ -169,6 +171,23 @@ def _ptr(a, ncols: int | None, name: str):
     return ctypes.c_void_p(arr.ctypes.data), n, arr
 
 
+def _out_ptr(out, m: int):
+    """(pointer, keepalive) of a caller-provided result buffer of M doubles.  The library writes M
+    doubles through the pointer, so nothing may be converted (a converted copy would swallow the
+    result) and the length must be exactly M (a shorter buffer would be overrun)."""
+    if hasattr(out, "is_cuda") and hasattr(out, "data_ptr"):
+        import torch
+        if out.dtype != torch.float64 or not out.is_contiguous():
+            raise TypeError("out: tensors must be float64 and contiguous")
+    elif not (isinstance(out, np.ndarray) and out.dtype == np.float64 and out.flags.c_contiguous
+              and out.flags.writeable):
+        raise TypeError("out must be a writeable float64 C-contiguous numpy array or a float64 contiguous tensor")
+    if out.ndim != 1 or out.shape[0] != m:
+        raise ValueError(f"out must have shape ({m},)")
+    op, _, keep = _ptr(out, None, "out")
+    return op, keep
+
+
 def set_stream(stream) -> None:
     """Use a CUDA stream (torch.cuda.Stream, raw handle int, or None) for subsequent calls."""
     lib = load_library()
@@ -220,11 +239,7 @@ class Tree:
                 out = torch.empty(m, dtype=torch.float64, device=q.device)
             else:
                 out = np.empty(m, dtype=np.float64)
-        if isinstance(out, np.ndarray) and (out.dtype != np.float64 or not out.flags.c_contiguous):
-            raise TypeError("out must be a float64 C-contiguous array")
-        op, mo, ok = _ptr(out, None, "out")
-        if mo != m:
-            raise ValueError("out must have M entries")
+        op, ok = _out_ptr(out, m)
         rc = lib.fmi_eval(ctypes.c_void_p(self.handle), qp, m, op)
         if rc != 0:
             _raise_last(rc)
@@ -276,9 +291,7 @@ class Tree:
         lib = load_library()
         if out is None:
             out = np.empty(self.n, dtype=np.float64)
-        if isinstance(out, np.ndarray) and (out.dtype != np.float64 or not out.flags.c_contiguous):
-            raise TypeError("out must be a float64 C-contiguous array")
-        op, _, _ = _ptr(out, None, "out")
+        op, _ = _out_ptr(out, self.n)
         rc = lib.fmi_residual(ctypes.c_void_p(self.handle), op)
         if rc != 0:
             _raise_last(rc)
@@ -333,7 +346,7 @@ def transfer(pts, f, q, degree: int, tol: float, max_depth: int, out=None):
             out = torch.empty(m, dtype=torch.float64, device=q.device)
         else:
             out = np.empty(m, dtype=np.float64)
-    op, mo, ok = _ptr(out, None, "out")
+    op, ok = _out_ptr(out, m)
     rc = lib.fmi_transfer(pp, fp, n, qp, m, op, int(degree), float(tol), int(max_depth))
     if rc != 0:
         _raise_last(rc)
@@ -437,6 +450,17 @@ def profile_get() -> dict:
         n = ctypes.c_int64()
         if lib.fmi_profile_get(k.encode(), ctypes.byref(ms), ctypes.byref(n)) == 0:
             out[k] = (float(ms.value), int(n.value))
+    return out
+
+
+def profile_units() -> dict:
+    """Algorithmic work units per kernel since the last reset (include/fmi.h fmi_profile_units)."""
+    lib = load_library()
+    out = {}
+    for k in KERNELS:
+        u = ctypes.c_int64()
+        if lib.fmi_profile_units(k.encode(), ctypes.byref(u)) == 0:
+            out[k] = int(u.value)
     return out
 
 

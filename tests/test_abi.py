@@ -91,3 +91,16 @@ def test_oracle_is_not_imported_by_the_product():
             if fn.endswith((".py", ".cu", ".cuh", ".h")):
                 txt = open(os.path.join(dirpath, fn)).read()
                 assert "oracle" not in re.sub(r"#.*|//.*", "", txt).lower() or fn == "fmi.py" and "oracle" not in txt, fn
+
+
+def test_result_buffer_validation_without_gpu():
+    """transfer()/eval() write M doubles through `out`: a wrong dtype, layout or length is rejected before
+    the library is called (no silent converted copy, no overrun)."""
+    import paper_1511_01353_b200 as fmi
+    pts = np.random.default_rng(0).random((100, 3))
+    f = pts[:, 0].copy()
+    q = pts[:10].copy()
+    for bad, exc in [(np.empty(10, dtype=np.float32), TypeError), (np.empty(9), ValueError),
+                     (np.empty((10, 2))[:, 0], TypeError), (np.empty(11), ValueError), ([0.0] * 10, TypeError)]:
+        with pytest.raises(exc):
+            fmi.transfer(pts, f, q, 1, 1e-6, 1, out=bad)

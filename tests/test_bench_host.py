@@ -77,3 +77,54 @@ def test_reference_arm_line_contract():
         assert k in line, k
     assert line["impl"] == "reference" and line["cpu_baseline"]["kind"] == "oracle"
     assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["value"] > 0
+
+
+def test_kernel_work_uses_executed_units():
+    """Sort bytes come from the 8-bit passes the library actually ran, solve flops from the nodes it
+    factored, key bytes from the library's own per-launch count (fmi_profile_units)."""
+    cfg = workloads.CONFIGS[5]
+    K, L = bench.ranks(cfg.degree)
+    units = {"sort": 3 * cfg.n + 3 * cfg.m, "solve": 4880, "keys": 76 * cfg.n + 68 * cfg.m}
+    w = bench.kernel_work(cfg, [cfg.n], depth_max=0, projected=0, units=units)
+    assert w["sort"] == ("byte", 32 * (3 * cfg.n + 3 * cfg.m))
+    assert w["solve"] == ("flop", 4880 * (L ** 3 / 3 + 3 * L * L))
+    assert w["keys"] == ("byte", 76 * cfg.n + 68 * cfg.m)
+    # per-step units: the roofline divides the timed region's units by the step count
+    prof = {"sort": (14.6, 12)}   # 2 steps x (3 + 3 passes) x ... launches; 7.3 ms per step
+    r = bench.rooflines(cfg, [cfg.n], 0, prof, steps=2, ms_per_step=100.0, hbm_peak=6456.8,
+                        units={"sort": 2 * units["sort"]})
+    per_launch = 32 * units["sort"] / 6
+    assert r["sort"]["achieved"] == pytest.approx(per_launch / (14.6e-3 / 12) / 1e9)
+
+
+def test_self_launch_under_torchrun_reference_arm():
+    """`bench.py --gpus 2` outside torchrun re-launches itself with 2 ranks (the driver's launch line);
+    rank 0 alone prints the reference line."""
+    env = dict(os.environ)
+    for k in ("WORLD_SIZE", "RANK", "LOCAL_RANK", "MASTER_ADDR", "MASTER_PORT"):
+        env.pop(k, None)
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--config", "1",
+                          "--gpus", "2", "--steps", "1", "--warmup", "0"], capture_output=True, text=True,
+                         timeout=600, cwd=ROOT, env=env)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1
+    line = json.loads(lines[0])
+    assert line["n_gpus"] == 2 and line["impl"] == "reference"
+
+
+def test_world_size_must_match_gpus():
+    env = dict(os.environ, WORLD_SIZE="2", RANK="1", LOCAL_RANK="1")
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--config", "1",
+                          "--gpus", "1", "--steps", "1", "--warmup", "0"], capture_output=True, text=True,
+                         timeout=300, cwd=ROOT, env=env)
+    assert out.returncode == 2 and "WORLD_SIZE" in out.stderr
+
+
+def test_oracle_sample_uses_every_core_on_large_configs():
+    """The cpu_baseline sample of a large config: one process per core over random cells of the workload."""
+    cfg = workloads.CONFIGS[2].scaled(m=20_000)
+    pts, f, q = workloads.make_inputs(cfg)
+    v, dt, cores, sample = bench.time_oracle_sample(cfg, pts, f, q, target_points=15_000, cells=2)
+    assert v > 0 and cores == min(2, bench.host_cores())
+    assert "depth-1 cells" in sample

@@ -95,3 +95,39 @@ def test_pinned_host_values_uploaded_late():
     with pytest.raises(fmi.FmiError) as ei:
         fmi.build(hp.numpy(), hf.numpy(), cfg.degree, cfg.tol, cfg.max_depth)
     assert ei.value.code == -1
+
+
+@pytest.mark.parametrize("what", ["depth", "child", "parent", "cell", "header_D"])
+def test_load_rejects_corrupt_node_records(tmp_path, what):
+    """A tree file is untrusted input: a node record whose depth, parent, child index or cell is
+    inconsistent is rejected with FMI_EVERSION naming the node (before any kernel follows it)."""
+    import struct
+    import paper_1511_01353_b200 as fmi
+    from paper_1511_01353_b200 import fmi as f_
+    cfg = workloads.CONFIGS[1]
+    pts, f, q = workloads.make_inputs(cfg)
+    path = tmp_path / "tree.fmi"
+    with fmi.build(pts, f, cfg.degree, cfg.tol, cfg.max_depth) as t:
+        t.save(str(path))
+        n = t.node_count
+    raw = bytearray(path.read_bytes())
+    H = 88                                   # FileHeader: magic, 4 int32, 2 int64, 5 doubles, 2 int32
+    cell, parent, child = H, H + 16 * n, H + 20 * n
+    if what == "depth":
+        struct.pack_into("<i", raw, cell + 5 * 16 + 12, 7)
+    elif what == "child":
+        struct.pack_into("<i", raw, child + 4 * 3, 1_000_000)
+    elif what == "parent":
+        struct.pack_into("<i", raw, parent + 4 * (n - 1), n + 5)
+    elif what == "cell":
+        struct.pack_into("<i", raw, cell + 2 * 16, 9)
+    else:
+        struct.pack_into("<i", raw, 80, 99)
+    bad = tmp_path / "bad.fmi"
+    bad.write_bytes(bytes(raw))
+    with pytest.raises(f_.FmiError) as ei:
+        f_.load(str(bad))
+    assert ei.value.code == f_.FMI_EVERSION
+    assert ("node" in str(ei.value)) or what == "header_D"
+    # the untouched file still loads
+    fmi.load(str(path)).free()

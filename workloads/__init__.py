@@ -180,3 +180,17 @@ def rms_and_max(err: np.ndarray) -> tuple[float, float]:
     """E_rms and E_inf of an error vector (§4)."""
     err = np.asarray(err, dtype=np.float64)
     return float(math.sqrt(np.mean(err * err))) if err.size else 0.0, float(np.max(np.abs(err))) if err.size else 0.0
+
+
+def cell_queries(depth: int, cell, n: int, seed: int) -> np.ndarray:
+    """Uniform query points inside the octree cell ``cell`` = (i, j, k) at ``depth`` of the unit root
+    cube: (cell + U[0,1)^3) / 2^depth, ``default_rng(seed)``.  Used for the parity queries inside the
+    sampled subtrees of the full-size configs (tests/golden/oracle_cfg*.npz)."""
+    r = np.random.default_rng(seed).random((n, 3))
+    return (np.asarray(cell, dtype=np.float64) + r) / float(2 ** depth)
+
+
+def cell_of(points: np.ndarray, depth: int) -> np.ndarray:
+    """Integer cell (i, j, k) of unit-cube points at ``depth``: min(floor(x 2^depth), 2^depth - 1)
+    (selection of a subtree's points for the harness)."""
+    return np.minimum(np.floor(np.asarray(points) * float(2 ** depth)), 2 ** depth - 1).astype(np.int64)
