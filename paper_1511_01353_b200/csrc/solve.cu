@@ -580,7 +580,17 @@ void level_solve(const LevelCtx& c, const double* mom, int mode, const double* s
       small_max = e ? std::atoi(e) : 6 * sms;
     }
   });
-  const int64_t grid = std::min<int64_t>(c.count, 1 << 20);
+  static int64_t grid_cap = 1 << 20;  // FMI_K5_CTAS_PER_SM (experiments): persistent CTAs per SM
+  static std::once_flag cap_once;
+  std::call_once(cap_once, [&] {
+    if (const char* e = std::getenv("FMI_K5_CTAS_PER_SM")) {
+      int dev = 0, sms = 0;
+      FMI_CK(cudaGetDevice(&dev));
+      FMI_CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+      grid_cap = std::max<int64_t>(1, (int64_t)std::atoi(e) * sms);
+    }
+  });
+  const int64_t grid = std::min<int64_t>(c.count, grid_cap);
   if (grid <= 0) return;
   if (mode != 1) prof_units(KID_SOLVE, c.count);  // nodes factored (𝓛³/3 + 3𝓛² flop each)
   if (NT < 256 && grid <= small_max) {
