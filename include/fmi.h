@@ -82,6 +82,9 @@ fmi_tree* fmi_build(const double* pts, const double* f, int64_t N, int degree, d
  * caller-provided collective; every shard then holds identical global nodes (same solve, same
  * decisions).  Nodes of depth >= s are local to the shard holding their cell: no communication.
  * With s > max_depth every node is global and the points may be partitioned arbitrarily.
+ *   allreduce        NULL: the library-owned NCCL communicator (fmi_dist_init over the same world) sums
+ *                    in place on the device buffers, on the library stream — the multi-GPU path.
+ *                    Otherwise a caller collective (the single-GPU virtual-shard tests):
  *   xbuf/xbuf_bytes  device exchange buffer owned by the caller (>= fmi_dist_xbuf_bytes())
  *   allreduce        collective in-place SUM over all shards of the first n elements of xbuf
  *                    (dtype 0 = fp64, 1 = int64, 2 = fp32); called from the building thread, after
@@ -105,6 +108,26 @@ typedef struct {
 
 fmi_tree* fmi_build_dist(const double* pts, const double* f, int64_t N, int degree, double tol, int max_depth,
                          const fmi_dist* dist);
+
+/*
+ * Library-owned NCCL communicator (one per process, one process per GPU).
+ *   fmi_get_unique_id   rank 0: write the 128-byte NCCL unique id to out128 (host memory); the caller
+ *                       broadcasts it to the other ranks (e.g. torch.distributed).
+ *   fmi_dist_init       collective over the world ranks (current CUDA device): creates the communicator
+ *                       (replacing a previous one).  A sharded build whose fmi_dist has allreduce == NULL
+ *                       then sums its global-level quantities with ncclAllReduce in place on the device
+ *                       buffers, on the library stream (no exchange buffer, no host round trip).
+ *   fmi_dist_finalize   destroy the communicator (idempotent).
+ *   fmi_dist_allreduce  in-place SUM over the ranks of n elements at the DEVICE pointer dev (dtype 0 fp64,
+ *                       1 int64, 2 fp32) on the library stream; returns after it completed.
+ * NCCL is loaded at run time (libnccl.so.2, the one the process already has when torch is imported).
+ * All return 0, FMI_EINPUT (bad argument), FMI_ECUDA (no device) or FMI_ENCCL (NCCL missing / failed,
+ * or no communicator).
+ */
+int fmi_get_unique_id(void* out128);
+int fmi_dist_init(int rank, int world, const void* id128);
+int fmi_dist_finalize(void);
+int fmi_dist_allreduce(void* dev, int64_t n, int dtype);
 
 /* Exchange-buffer size (bytes) a sharded build needs for this degree and shard depth. */
 int64_t fmi_dist_xbuf_bytes(int degree, int shard_depth);

@@ -389,9 +389,12 @@ void reset_tree(fmi_tree* T, cudaStream_t s) {
 
 // Collective SUM over the shards of a sharded build (fmi_dist): stage through the caller's exchange
 // buffer, synchronise, call the caller's collective, copy back (stream-ordered).
-void dist_sum(const fmi_tree* T, void* dev, int64_t n, int dtype, cudaStream_t s) {
-  const fmi_dist* d = T->dist;
+void dist_sum_raw(const fmi_dist* d, void* dev, int64_t n, int dtype, cudaStream_t s) {
   if (!d || n <= 0) return;
+  if (!d->allreduce) {  // the library-owned NCCL communicator: in place, on the stream, no host round trip
+    dist_comm_allreduce(dev, n, dtype, s);
+    return;
+  }
   const int64_t bytes = n * (dtype == 2 ? 4 : 8);
   if (bytes > d->xbuf_bytes)
     fail(FMI_EINPUT, "fmi_dist exchange buffer too small: need " + std::to_string(bytes) + " bytes");
@@ -399,6 +402,10 @@ void dist_sum(const fmi_tree* T, void* dev, int64_t n, int dtype, cudaStream_t s
   FMI_CK(cudaStreamSynchronize(s));
   if (d->allreduce(d->ctx, n, dtype) != 0) fail(FMI_ENCCL, "sharded build: the allreduce callback failed");
   FMI_CK(cudaMemcpyAsync(dev, d->xbuf, bytes, cudaMemcpyDeviceToDevice, s));
+}
+
+void dist_sum(const fmi_tree* T, void* dev, int64_t n, int dtype, cudaStream_t s) {
+  dist_sum_raw(T->dist, dev, n, dtype, s);
 }
 
 // values still uploading when the level build starts (fmi_build with page-locked host f): the moment
@@ -445,8 +452,12 @@ void run_levels(fmi_tree* T, const uint64_t* keys, double* ux, double* uy, doubl
     set_root(mt, T->N, false, s);
     {
       int64_t first = 0, count = 1;
+      bool short_keys = false;  // this shard's moment tree reaches below the sorted key levels
       for (int depth = 0; count > 0; ++depth) {
-        if (depth >= T->Dsorted) throw KeysShort{};  // octant digits below this depth are not sorted
+        if (depth >= T->Dsorted) {  // octant digits below this depth are not sorted
+          short_keys = true;
+          break;
+        }
         mfirst.push_back(first);
         mcount.push_back(count);
         ensure_table(mt, mt_cap, first + count + 8 * count, L, false, s);
@@ -467,6 +478,20 @@ void run_levels(fmi_tree* T, const uint64_t* keys, double* ux, double* uy, doubl
         first += count;
         count = host_small[0];
       }
+      if (T->dist) {
+        // sharded: every shard re-sorts if any shard is short (the retry repeats the global levels'
+        // collectives, so all shards must take it together); Dsorted > shard_depth, so every shard has
+        // completed the same global-level collectives when it gets here
+        DBuf<int64_t> flag(1, s);
+        const int64_t one = short_keys ? 1 : 0;
+        FMI_CK(cudaMemcpyAsync(flag.p, &one, sizeof one, cudaMemcpyHostToDevice, s));
+        dist_sum(T, flag.p, 1, 1, s);
+        int64_t any = 0;
+        FMI_CK(cudaMemcpyAsync(&any, flag.p, sizeof any, cudaMemcpyDeviceToHost, s));
+        FMI_CK(cudaStreamSynchronize(s));
+        short_keys = any != 0;
+      }
+      if (short_keys) throw KeysShort{};
       T->mt_nodes = first;
     }
     tmark("mtree", s);
@@ -537,8 +562,12 @@ void run_levels(fmi_tree* T, const uint64_t* keys, double* ux, double* uy, doubl
     const size_t fac_per_node = solve_factor_per_node(P);
     const int64_t qr_slots = 148;
     DBuf<double> qr_scratch((size_t)qr_slots * solve_qr_scratch_per_cta(P) / sizeof(double), s);
+    bool short_fit = false;  // a fit node below the sorted key levels (fit nodes need only >= 𝓛 points)
     for (int depth = 0; count > 0; ++depth) {
-      if (depth >= T->Dsorted) throw KeysShort{};  // octant digits below this depth are not sorted
+      if (depth >= T->Dsorted) {  // octant digits below this depth are not sorted
+        short_fit = true;
+        break;
+      }
       T->lvl_first.push_back(first);
       T->lvl_count.push_back(count);
       T->lvl_points.push_back(points);
@@ -551,8 +580,10 @@ void run_levels(fmi_tree* T, const uint64_t* keys, double* ux, double* uy, doubl
       FMI_CK(cudaMemsetAsync(nflag.p, 0, 3 * sizeof(int64_t), s));
       scratch.ensure((size_t)count * fac_per_node, s);
       // deferral: single shard only; split mode defers every node (Horner-only K6 + K6_PROJ)
+      // split-K6 threshold on the whole-job level size (a shard holds ~1/world of it)
+      const bool big_level = points * (T->dist ? T->dist->world : 1) >= T->split_min;
       const double defer_tau =
-          global ? 0.0 : ((T->k6_split && points >= T->split_min) ? INFINITY : T->defer_theta * T->tau);
+          global ? 0.0 : ((T->k6_split && big_level) ? INFINITY : T->defer_theta * T->tau);
       level_solve<P>(c, lvlmom.p, 0, nullptr, nullptr, T->refine2, T->refine_fill, T->Ntot, nflag.p, scratch.p, s,
                      defer_tau);
       FMI_CK(cudaMemcpyAsync(&host_small[2], nflag.p, 3 * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
@@ -600,8 +631,8 @@ void run_levels(fmi_tree* T, const uint64_t* keys, double* ux, double* uy, doubl
       // deferred and the level runs the Horner-only K6 (more points in flight per thread, no projection
       // registers) followed by K6_PROJ for the children actually created
       // the split pays on big levels (cfg 5: 2e8 points); small adaptive levels keep the fused pass
-      bool horner_only = T->k6_split && !global && points >= T->split_min;
-      if (!global && !horner_only && points >= T->split_min && ndefer_nodes * 2 >= count && ndefer_nodes > 0) {
+      bool horner_only = T->k6_split && !global && big_level;
+      if (!global && !horner_only && big_level && ndefer_nodes * 2 >= count && ndefer_nodes > 0) {
         if (ndefer_nodes < count)
           FMI_LAUNCH(KID_MISC, s, k_defer_all, (unsigned)((count + 255) / 256), 256, 0, T->nt, first, count);
         horner_only = true;
@@ -671,6 +702,17 @@ void run_levels(fmi_tree* T, const uint64_t* keys, double* ux, double* uy, doubl
       count = nnew;
       points = npts;
     }
+    if (T->dist) {  // sharded: the re-sort is collective (see the moment tree)
+      DBuf<int64_t> flag(1, s);
+      const int64_t one = short_fit ? 1 : 0;
+      FMI_CK(cudaMemcpyAsync(flag.p, &one, sizeof one, cudaMemcpyHostToDevice, s));
+      dist_sum(T, flag.p, 1, 1, s);
+      int64_t any = 0;
+      FMI_CK(cudaMemcpyAsync(&any, flag.p, sizeof any, cudaMemcpyDeviceToHost, s));
+      FMI_CK(cudaStreamSynchronize(s));
+      short_fit = any != 0;
+    }
+    if (short_fit) throw KeysShort{};
     // pre-summed polynomials for the evaluation (f1), level by level from the root
     for (size_t d = 0; d < T->lvl_first.size(); ++d) presum_level<P>(T->nt, T->lvl_first[d], T->lvl_count[d], s);
     tmark("presum", s);
@@ -771,8 +813,11 @@ fmi_tree* build_impl(const double* pts, const double* f, int64_t N, int degree, 
   if (!(tol >= 0.0)) fail(FMI_EPRECOND, "tol must be >= 0 (and not NaN)");
   const int L = rank3(degree);
   if (dist) {
-    if (!dist->allreduce || !dist->xbuf || dist->world < 1 || dist->rank < 0 || dist->rank >= dist->world)
+    if (dist->world < 1 || dist->rank < 0 || dist->rank >= dist->world || (dist->allreduce && !dist->xbuf))
       fail(FMI_EINPUT, "invalid fmi_dist");
+    // no callback: the library-owned NCCL communicator (fmi_dist_init) must span the same ranks
+    if (!dist->allreduce && !dist_comm_ready(dist->world))
+      fail(FMI_ENCCL, "fmi_dist without an allreduce callback needs fmi_dist_init over the same world");
     if (dist->shard_depth < 0 || dist->shard_depth > 6) fail(FMI_EPRECOND, "shard_depth outside 0..6");
     if (!(dist->width > 0.0)) fail(FMI_EINPUT, "fmi_dist: root cube width must be > 0");
   } else if (N < L) {
@@ -835,10 +880,10 @@ fmi_tree* build_impl(const double* pts, const double* f, int64_t N, int degree, 
     int64_t* hs = host_staging();
     hs[0] = N;
     hs[1] = hb[6] != 0.0 ? 1 : 0;
-    FMI_CK(cudaMemcpyAsync(dist->xbuf, hs, 2 * sizeof(int64_t), cudaMemcpyHostToDevice, s));
-    FMI_CK(cudaStreamSynchronize(s));
-    if (dist->allreduce(dist->ctx, 2, 1) != 0) fail(FMI_ENCCL, "sharded build: the allreduce callback failed");
-    FMI_CK(cudaMemcpyAsync(hs, dist->xbuf, 2 * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    DBuf<int64_t> two(2, s);
+    FMI_CK(cudaMemcpyAsync(two.p, hs, 2 * sizeof(int64_t), cudaMemcpyHostToDevice, s));
+    dist_sum_raw(dist, two.p, 2, 1, s);
+    FMI_CK(cudaMemcpyAsync(hs, two.p, 2 * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
     FMI_CK(cudaStreamSynchronize(s));
     Ntot = hs[0];
     if (hs[1] != 0) fail(FMI_EINPUT, "non-finite coordinate or value (on some shard)");
@@ -891,7 +936,8 @@ fmi_tree* build_impl(const double* pts, const double* f, int64_t N, int degree, 
     // K1 keys + K2 sort + gather.  Only the top Dsort levels of the keys are sorted: no node is deeper
     // than the moment tree, whose depth is ~log8(N/𝓛) for space-filling data.  If the moment tree does
     // reach depth Dsort (clustered data), run_levels throws KeysShort and the sort is redone over all
-    // levels.  Sharded builds sort all levels (every shard must take the same path).
+    // levels.  Sharded builds take Dsort from the global point count, at least one level below the
+    // shard depth, and agree on the retry collectively (run_levels).
     DBuf<uint64_t> keys(N, s), ktmp(N, s);
     DBuf<uint32_t> perm(N, s), ptmp(N, s);
     DBuf<double4> packed(N, s);
@@ -899,9 +945,10 @@ fmi_tree* build_impl(const double* pts, const double* f, int64_t N, int degree, 
     // the unscoped QR path (f2): degrees 11..14, or any degree at max_depth = 0 with FMI_UNSCOPED_QR=1
     const bool unscoped = !dist && max_depth == 0 && (degree > FMI_MAX_LEVEL_DEGREE || std::getenv("FMI_UNSCOPED_QR"));
     int Dsort = T->Dk;
-    if (!dist && !std::getenv("FMI_FULL_SORT")) {
+    if (!unscoped && !std::getenv("FMI_FULL_SORT")) {
       const double fill = std::max(1.0, (double)std::max<int64_t>(Ntot, 1) / (double)L);
       Dsort = std::min(T->Dk, (int)std::ceil(std::log(fill) / std::log(8.0)) + 1);
+      if (dist) Dsort = std::min(T->Dk, std::max(Dsort, dist->shard_depth + 1));
     }
     DBuf<int> fbad;
     DBuf<double> rootb;  // the root projection from the fused gather
@@ -1205,6 +1252,41 @@ fmi_tree* fmi_build_dist(const double* pts, const double* f, int64_t N, int degr
     return 0;
   });
   return out;
+}
+
+int fmi_get_unique_id(void* out128) {
+  return guard([&] {
+    if (!out128) fail(FMI_EINPUT, "null id buffer");
+    dist_nccl_unique_id(out128);
+    return 0;
+  });
+}
+
+int fmi_dist_init(int rank, int world, const void* id128) {
+  return guard([&] {
+    if (!id128 || world < 1 || rank < 0 || rank >= world) fail(FMI_EINPUT, "invalid rank / world / id");
+    require_device();
+    dist_nccl_init(rank, world, id128);
+    return 0;
+  });
+}
+
+int fmi_dist_finalize(void) {
+  return guard([&] {
+    dist_nccl_finalize();
+    return 0;
+  });
+}
+
+int fmi_dist_allreduce(void* dev, int64_t n, int dtype) {
+  return guard([&] {
+    if (n < 0 || (n > 0 && !dev) || dtype < 0 || dtype > 2) fail(FMI_EINPUT, "invalid argument");
+    if (n > 0 && !is_device_ptr(dev)) fail(FMI_EINPUT, "fmi_dist_allreduce needs a device pointer");
+    cudaStream_t s = tl_stream;
+    dist_comm_allreduce(dev, n, dtype, s);
+    FMI_CK(cudaStreamSynchronize(s));
+    return 0;
+  });
 }
 
 int64_t fmi_dist_xbuf_bytes(int degree, int shard_depth) {

@@ -59,6 +59,13 @@ void prof_collect();  // after a stream sync: accumulate elapsed times of comple
 // solved nodes, ...), summed while profiling is on; bench.py turns them into bytes / flops
 void prof_units(int kid, int64_t units);
 
+// dist.cu: the library-owned NCCL communicator (fmi_dist_init); fail(FMI_ENCCL) on errors
+void dist_nccl_unique_id(void* out128);
+void dist_nccl_init(int rank, int world, const void* id128);
+void dist_nccl_finalize();
+bool dist_comm_ready(int world);
+void dist_comm_allreduce(void* dev, int64_t n, int dtype, cudaStream_t s);  // in place, SUM
+
 #define FMI_LAUNCH(kid, stream, kernel, grid, block, smem, ...)                          \
   do {                                                                                   \
     ::fmi::prof_begin((kid), (stream));                                                  \

@@ -23,7 +23,13 @@ namespace {
 
 constexpr int K4_THREADS = 256;
 constexpr int K4_WARPS = K4_THREADS / 32;
-constexpr int K4_LIM = 64;  // outputs per group (128 accumulator registers)
+#ifndef FMI_K4_LIM
+#define FMI_K4_LIM 64
+#endif
+#ifndef FMI_K4_MINB
+#define FMI_K4_MINB 1
+#endif
+constexpr int K4_LIM = FMI_K4_LIM;  // outputs per group (2·LIM accumulator registers)
 constexpr int K4_RING = 8;  // per-lane point ring (cp.async prefetch distance K4_RING - 1)
 
 __device__ __forceinline__ void cp_async8(double* dst, const double* src) {
@@ -93,7 +99,7 @@ __device__ __forceinline__ void k4_run(int gw, const double* __restrict__ ux, co
 // its outputs to partial[chunk][..].  No cross-lane reduction; the 8 warps of a CTA read the same
 // 32 chunks (L1 reuse).  Chunks are <= kMomentChunk points (make_chunks).
 template <int P>
-__global__ void __launch_bounds__(K4_THREADS, 1)
+__global__ void __launch_bounds__(K4_THREADS, FMI_K4_MINB)
     k_moments(const double* __restrict__ ux, const double* __restrict__ uy, const double* __restrict__ uz,
               const int4* __restrict__ cell, int shift, const Chunk* __restrict__ chunks,
               const int64_t* __restrict__ nchunks, double* __restrict__ partial) {

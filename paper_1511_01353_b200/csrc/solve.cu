@@ -92,7 +92,7 @@ struct K5Shape {
 // NT = threads per node: k5_threads<P>() for full levels; 256 for levels with fewer nodes than CTA slots
 // (the top levels of every build are latency-bound: one node per SM)
 template <int P, int NT = k5_threads<P>()>
-__global__ void __launch_bounds__(NT, NT == 256 ? 2 : (NT == 128 ? 3 : 6))
+__global__ void __launch_bounds__(NT, NT == 512 ? 1 : (NT == 256 ? 2 : (NT == 128 ? 3 : 6)))
     k_solve(const double* __restrict__ mom, int mode, const double* __restrict__ segrhs, double* __restrict__ delta,
             NodeTable nt, int64_t first, int64_t count, double* __restrict__ fac,
             const __grid_constant__ BasisTab bt, double delta2, double refine2, double refine_fill,
@@ -565,43 +565,39 @@ void level_solve(const LevelCtx& c, const double* mom, int mode, const double* s
   using S = K5Shape<P>;
   static const BasisTab bt = make_basis<P>();
   constexpr int NT = k5_threads<P>();
-  static int small_max = 0;         // levels with <= small_max nodes run 256 threads per node
-  static std::once_flag attr_once;  // one opt-in per kernel instantiation (thread-safe)
+  static int small_max = 0;  // levels with <= small_max nodes run 256 threads per node (p <= 8)
+  static int tiny_max = 0;   // levels with <= tiny_max nodes (at most one per SM) run 512 threads per node
+  static int64_t grid_cap = 1 << 20;  // FMI_K5_CTAS_PER_SM (experiments): persistent CTAs per SM
+  static std::once_flag attr_once;    // one opt-in per kernel instantiation (thread-safe)
   std::call_once(attr_once, [&] {
-    FMI_CK(cudaFuncSetAttribute(
-        k_solve<P, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::SMEM));
+    int dev = 0, sms = 0;
+    FMI_CK(cudaGetDevice(&dev));
+    FMI_CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    FMI_CK(cudaFuncSetAttribute(k_solve<P, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::SMEM));
+    FMI_CK(cudaFuncSetAttribute(k_solve<P, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::SMEM));
     if constexpr (NT < 256) {
-      FMI_CK(cudaFuncSetAttribute(
-          k_solve<P, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::SMEM));
-      int dev = 0, sms = 0;
-      FMI_CK(cudaGetDevice(&dev));
-      FMI_CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+      FMI_CK(cudaFuncSetAttribute(k_solve<P, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::SMEM));
       const char* e = std::getenv("FMI_K5_SMALL");
       small_max = e ? std::atoi(e) : 6 * sms;
     }
-  });
-  static int64_t grid_cap = 1 << 20;  // FMI_K5_CTAS_PER_SM (experiments): persistent CTAs per SM
-  static std::once_flag cap_once;
-  std::call_once(cap_once, [&] {
-    if (const char* e = std::getenv("FMI_K5_CTAS_PER_SM")) {
-      int dev = 0, sms = 0;
-      FMI_CK(cudaGetDevice(&dev));
-      FMI_CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-      grid_cap = std::max<int64_t>(1, (int64_t)std::atoi(e) * sms);
-    }
+    const char* t = std::getenv("FMI_K5_TINY");
+    tiny_max = t ? std::atoi(t) : sms;
+    if (const char* e = std::getenv("FMI_K5_CTAS_PER_SM")) grid_cap = std::max<int64_t>(1, (int64_t)std::atoi(e) * sms);
   });
   const int64_t grid = std::min<int64_t>(c.count, grid_cap);
   if (grid <= 0) return;
   if (mode != 1) prof_units(KID_SOLVE, c.count);  // nodes factored (𝓛³/3 + 3𝓛² flop each)
-  if (NT < 256 && grid <= small_max) {
-    FMI_LAUNCH(mode == 1 ? KID_REFINE_SOLVE : KID_SOLVE, s, (k_solve<P, 256>), (unsigned)grid, 256, S::SMEM, mom,
-               mode, segrhs, delta, c.nt, c.first, c.count, fac, bt, kDelta * kDelta, refine2, refine_fill, kMomentTol,
-               n_root, defer_tau, nflag);
-    return;
+  const int kid = mode == 1 ? KID_REFINE_SOLVE : KID_SOLVE;
+#define K5_ARGS mom, mode, segrhs, delta, c.nt, c.first, c.count, fac, bt, kDelta * kDelta, refine2, refine_fill, \
+                kMomentTol, n_root, defer_tau, nflag
+  if (grid <= tiny_max) {  // latency-bound levels (the top of every tree): more warps per node
+    FMI_LAUNCH(kid, s, (k_solve<P, 512>), (unsigned)grid, 512, S::SMEM, K5_ARGS);
+  } else if (NT < 256 && grid <= small_max) {
+    FMI_LAUNCH(kid, s, (k_solve<P, 256>), (unsigned)grid, 256, S::SMEM, K5_ARGS);
+  } else {
+    FMI_LAUNCH(kid, s, (k_solve<P, NT>), (unsigned)grid, NT, S::SMEM, K5_ARGS);
   }
-  FMI_LAUNCH(mode == 1 ? KID_REFINE_SOLVE : KID_SOLVE, s, (k_solve<P, NT>), (unsigned)grid, NT, S::SMEM, mom, mode,
-             segrhs, delta, c.nt, c.first, c.count, fac, bt, kDelta * kDelta, refine2, refine_fill, kMomentTol, n_root,
-             defer_tau, nflag);
+#undef K5_ARGS
 }
 
 // doubles of per-node factor storage (bordered packed lower triangle)

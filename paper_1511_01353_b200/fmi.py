@@ -34,6 +34,7 @@ EXPORTED = (
     "fmi_profile_reset", "fmi_profile_get", "fmi_launch_count", "fmi_build_stats", "fmi_build_dist",
     "fmi_dist_xbuf_bytes", "fmi_bbox", "fmi_cell_counts", "fmi_partition", "fmi_scatter", "fmi_transfer",
     "fmi_save", "fmi_load", "fmi_profile_units",
+    "fmi_get_unique_id", "fmi_dist_init", "fmi_dist_finalize", "fmi_dist_allreduce",
 )
 
 # allreduce(ctx, n, dtype) -> int: in-place SUM of the first n elements of the exchange buffer
@@ -111,6 +112,14 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.fmi_profile_reset.argtypes = []
     lib.fmi_profile_get.restype = I32
     lib.fmi_profile_get.argtypes = [ctypes.c_char_p, P(D), P(I64)]
+    lib.fmi_get_unique_id.restype = I32
+    lib.fmi_get_unique_id.argtypes = [VP]
+    lib.fmi_dist_init.restype = I32
+    lib.fmi_dist_init.argtypes = [I32, I32, VP]
+    lib.fmi_dist_finalize.restype = I32
+    lib.fmi_dist_finalize.argtypes = []
+    lib.fmi_dist_allreduce.restype = I32
+    lib.fmi_dist_allreduce.argtypes = [VP, I64, I32]
     lib.fmi_profile_units.restype = I32
     lib.fmi_profile_units.argtypes = [ctypes.c_char_p, P(I64)]
     lib.fmi_build_dist.restype = VP
@@ -451,6 +460,43 @@ def profile_get() -> dict:
         if lib.fmi_profile_get(k.encode(), ctypes.byref(ms), ctypes.byref(n)) == 0:
             out[k] = (float(ms.value), int(n.value))
     return out
+
+
+def get_unique_id() -> bytes:
+    """rank 0: a fresh 128-byte NCCL unique id for fmi_dist_init (fmi_get_unique_id)."""
+    buf = ctypes.create_string_buffer(128)
+    rc = load_library().fmi_get_unique_id(buf)
+    if rc != 0:
+        _raise_last(rc)
+    return buf.raw
+
+
+def dist_init(rank: int, world: int, uid: bytes) -> None:
+    """Create the library-owned NCCL communicator (collective over the ranks; fmi_dist_init)."""
+    if len(uid) != 128:
+        raise ValueError("the NCCL unique id is 128 bytes")
+    buf = ctypes.create_string_buffer(uid, 128)
+    rc = load_library().fmi_dist_init(int(rank), int(world), buf)
+    if rc != 0:
+        _raise_last(rc)
+
+
+def dist_finalize() -> None:
+    rc = load_library().fmi_dist_finalize()
+    if rc != 0:
+        _raise_last(rc)
+
+
+def dist_allreduce(t) -> None:
+    """In-place SUM over the ranks of a contiguous CUDA tensor (float64, int64 or float32) through the
+    library communicator (fmi_dist_allreduce)."""
+    import torch
+    codes = {torch.float64: 0, torch.int64: 1, torch.float32: 2}
+    if not (t.is_cuda and t.is_contiguous() and t.dtype in codes):
+        raise TypeError("dist_allreduce needs a contiguous CUDA float64/int64/float32 tensor")
+    rc = load_library().fmi_dist_allreduce(ctypes.c_void_p(t.data_ptr()), t.numel(), codes[t.dtype])
+    if rc != 0:
+        _raise_last(rc)
 
 
 def profile_units() -> dict:

@@ -39,6 +39,20 @@ class TorchComm:
         self.rank = dist.get_rank(group)
         self.world = dist.get_world_size(group)
         self.host_staged = dist.get_backend(group) == "gloo"
+        # NCCL process group: the sharded build's in-build sums go through the library-owned NCCL
+        # communicator (fmi_dist_init), created once from a unique id broadcast over this group
+        self.library_nccl = not self.host_staged
+        self._lib_ready = False
+
+    def ensure_library_comm(self, kernels):
+        if self._lib_ready:
+            return
+        import torch
+        uid = kernels.get_unique_id() if self.rank == 0 else bytes(128)
+        t = torch.tensor(list(uid), dtype=torch.uint8, device="cuda")
+        self.dist.broadcast(t, src=0, group=self.group)
+        kernels.dist_init(self.rank, self.world, bytes(t.cpu().tolist()))
+        self._lib_ready = True
 
     def _op(self, t, fn):
         if self.host_staged and t.is_cuda:
@@ -291,7 +305,19 @@ def build_sharded(pts, f, degree: int, tol: float, max_depth: int, comm, smax: i
         comm.all_to_all(f_loc, f_sorted, r_list, s_list)
     else:
         p_loc, f_loc = pts, f
-    # 4. the sharded build: global nodes summed through the callback
+    # 4. the sharded build: global nodes summed by the library's NCCL communicator (in place, on the
+    #    library stream), or — in-process / gloo communicators — through the callback
+    if getattr(comm, "library_nccl", False):
+        comm.ensure_library_comm(fmi)
+        d = fmi.FmiDist()
+        d.rank, d.world, d.shard_depth = rank, world, s
+        for a in range(3):
+            d.lo[a] = float(lo[a])
+        d.width = float(width)
+        tree = fmi.build_dist(p_loc, f_loc, degree, tol, max_depth, d)
+        st = ShardedTree(tree, comm, lo, width, s, owner, kernels)
+        st._keep = (p_loc, f_loc)
+        return st
     xbytes = fmi.dist_xbuf_bytes(degree, s)
     xbuf = torch.empty(xbytes, dtype=torch.uint8, device=dev)
     views = {0: torch.float64, 1: torch.int64, 2: torch.float32}

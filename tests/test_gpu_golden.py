@@ -3,7 +3,7 @@ tools/make_golden.py, which calls only oracle/ and workloads/).
 
   cfg3  the whole tree: every node, every decision, 1e5 queries.
   cfg4  every depth-0/1 node and decision, and 8 whole depth-2 subtrees (the oracle ran Alg. 1 from
-        the root, expanding only those subtrees); 1e5 queries inside them.
+        the root, expanding only those subtrees); the config's own queries (the same mixture) inside them.
   cfg5  8 whole depth-2 subtrees, each Alg. 1 called on the depth-2 node with the original values
         (telescoping start; the root fit of 2e8 points is beyond the CPU oracle): compared (a) inside
         the full-size GPU tree and (b) as stand-alone problems mapped exactly onto the unit cube.
@@ -43,6 +43,10 @@ def _golden(c):
 def _queries(gold, c):
     if str(gold["mode"]) == "full":
         return workloads.uniform_points(int(gold["q_n"]), int(gold["q_seed"]))
+    if "q_index" in gold:   # the config's own queries (cfg 4: the mixture) inside the sampled subtrees
+        cfg = workloads.CONFIGS[c]
+        q = workloads.mixture_points(cfg.m, 1, workloads.mixture_centres(0))
+        return np.ascontiguousarray(q[gold["q_index"]])
     per = int(gold["q_per_cell"])
     return np.concatenate([workloads.cell_queries(2, tuple(int(v) for v in cell), per, int(gold["q_seed0"]) + t)
                            for t, cell in enumerate(gold["pick"])])

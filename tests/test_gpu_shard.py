@@ -109,3 +109,39 @@ def test_virtual_shards_all_global_and_empty_shard():
         vals = np.concatenate([r[2] for r in res])
         ora = fo.build(pts, f, 3, 1e-9, D)
         assert np.max(np.abs(vals - fo.evaluate(ora, q))) <= 1e-9 * np.max(np.abs(f))
+
+
+def test_library_nccl_communicator_world1():
+    """The library-owned NCCL communicator (fmi_get_unique_id / fmi_dist_init): an in-place device
+    allreduce, and a sharded build at world 1 whose global levels (shard depth 2) are summed by NCCL on
+    the library stream (no callback, no exchange buffer) reproduces the single-GPU tree."""
+    from paper_1511_01353_b200 import fmi
+    fmi.load_library()
+    uid = fmi.get_unique_id()
+    assert len(uid) == 128
+    fmi.dist_init(0, 1, uid)
+    try:
+        t = torch.arange(10, dtype=torch.float64, device="cuda")
+        fmi.dist_allreduce(t)
+        assert torch.equal(t.cpu(), torch.arange(10, dtype=torch.float64))
+        cfg = workloads.CONFIGS[2]
+        pts, f, q = workloads.make_inputs(cfg)
+        q = q[:50_000]
+        dp, df, dq = (torch.from_numpy(a).cuda() for a in (pts, f, q))
+        d = fmi.FmiDist()
+        d.rank, d.world, d.shard_depth = 0, 1, 2
+        d.width = 1.0
+        with fmi.build_dist(dp, df, cfg.degree, cfg.tol, cfg.max_depth, d) as tn, \
+                fmi.build(dp, df, cfg.degree, cfg.tol, cfg.max_depth) as one:
+            a, b = tn.export(), one.export()
+            for k in ("depth", "cell", "n_points", "child_count", "child"):
+                assert np.array_equal(a[k], b[k]), k
+            va, vb = tn.eval(dq).cpu().numpy(), one.eval(dq).cpu().numpy()
+            assert np.max(np.abs(va - vb)) <= 1e-9 * np.max(np.abs(f))
+        # a communicator of another world size is refused
+        d.world = 2
+        with pytest.raises(fmi.FmiError) as ei:
+            fmi.build_dist(dp, df, cfg.degree, cfg.tol, cfg.max_depth, d)
+        assert ei.value.code == fmi.FMI_ENCCL
+    finally:
+        fmi.dist_finalize()

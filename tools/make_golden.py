@@ -147,11 +147,17 @@ def make_cfg4(jobs, k):
     _log(f"cfg4 created depth-2 cells: {len(created)}; picked {pick}")
     u = pts                                         # unit cube: root-cube coordinates = points (G6)
     c2 = workloads.cell_of(u, 2)
-    jobsl = []
+    # queries: the config's own (the same mixture, seed 1, BASELINE.json) that fall in the picked cells,
+    # the first NQ/len(pick) of each cell in query order — uniform queries in a cell would ask for the
+    # polynomials far outside their data (clustered points), where no fit is meaningful
+    qall = workloads.mixture_points(cfg.m, 1, workloads.mixture_centres(0))
+    qc2 = workloads.cell_of(qall, 2)
+    jobsl, qidx = [], []
     for t, cell in enumerate(pick):
         inside = np.all(c2 == np.array(cell), axis=1)
-        qs = workloads.cell_queries(2, cell, NQ // len(pick), 4000 + t)
-        jobsl.append((u[inside], top.residual[inside], p, tau, D, 2, cell, qs))
+        qi = np.flatnonzero(np.all(qc2 == np.array(cell), axis=1))[:NQ // len(pick)]
+        qidx.append(qi)
+        jobsl.append((u[inside], top.residual[inside], p, tau, D, 2, cell, np.ascontiguousarray(qall[qi])))
     with mp.get_context("fork").Pool(jobs) as pool:
         res = pool.map(_subtree_job, jobsl, chunksize=1)
     vals = []
@@ -161,11 +167,13 @@ def make_cfg4(jobs, k):
         vals.append(v + _top_terms(top, qs, p))
     table = _node_table([top] + [s for s, _ in res])
     # mark the picked subtrees' roots as expanded in their parents' child_state
+    qidx = np.concatenate(qidx)
     np.savez_compressed(os.path.join(GOLDEN, "oracle_cfg4.npz"), mode="top+subtrees", cfg=4,
-                        pick=np.array(pick, dtype=np.int64), q_seed0=4000, q_per_cell=NQ // len(pick),
+                        pick=np.array(pick, dtype=np.int64), q_index=qidx.astype(np.int64),
                         values=np.concatenate(vals), **table)
     _summary("cfg4", cfg, table, f"depth 0-1 complete + depth-2 subtrees {pick} (2 most populated + random seed 4); "
-                                 f"values at workloads.cell_queries(2, cell, {NQ // len(pick)}, 4000+t); {time.time() - t0:.0f}s")
+                                 f"values at the config's queries (mixture, seed 1) in those cells, up to "
+                                 f"{NQ // len(pick)} per cell ({qidx.size} in all); {time.time() - t0:.0f}s")
 
 
 def _top_terms(top, qs, p):
