@@ -10,6 +10,10 @@
 // Queries are processed in Morton order so that neighbouring threads use the same node (coefficient
 // loads are warp-broadcast, L1-resident); results are scattered back to the caller's order.  A query
 // outside the root cube gets the root polynomial only.
+#include <algorithm>
+#include <cstdlib>
+#include <mutex>
+
 #include "horner.cuh"
 
 namespace fmi {
@@ -193,6 +197,99 @@ __global__ void __launch_bounds__(256) k_eval(const double* __restrict__ q, cons
   if (i1 < M) out[qi1] = v1;
 }
 
+// Pipelined persistent variant (the default for sorted queries with records): CTAs loop over tiles of
+// 512 sorted queries; the random 32-byte query records of the tile two steps ahead are fetched into a
+// shared-memory ring by cp.async while the current tile is evaluated, so the latency of the random
+// reads overlaps the Horner work instead of stalling every CTA at its start (DESIGN.md §5 K7).
+constexpr int EV_TILE = 512;
+constexpr int EV_THREADS = 256;
+
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)), "l"(src)
+               : "memory");
+}
+
+template <int P>
+__global__ void __launch_bounds__(EV_THREADS, 3)
+    k_eval_pipe(const double4* __restrict__ qpk, const uint64_t* __restrict__ keys, const uint32_t* __restrict__ idx,
+                int64_t M, int Dk, NodeTable nt, double* __restrict__ out) {
+  constexpr int L = rank3(P);
+  constexpr int LA = (L + 1) & ~1;
+  // dynamic shared memory: the record ring [2][EV_TILE] then the per-warp coefficient rows [8][LA]
+  extern __shared__ __align__(16) double ev_smem[];
+  double4 (*rec)[EV_TILE] = reinterpret_cast<double4 (*)[EV_TILE]>(ev_smem);
+  double (*cs)[LA] = reinterpret_cast<double (*)[LA]>(ev_smem + 2 * EV_TILE * 4);
+  __shared__ long long cta_node[EV_THREADS / 32];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t ntiles = (M + EV_TILE - 1) / EV_TILE;
+  // thread tid owns tile positions tid and tid + 256 (the 64-query warp layout of k_eval below:
+  // warp w takes positions 64w .. 64w+63, lane l the positions 64w + l and 64w + 32 + l)
+  const int pos0 = warp * 64 + lane, pos1 = pos0 + 32;
+  auto issue = [&](int64_t t, int slot) {
+    if (t < ntiles) {
+      const int64_t i0 = t * EV_TILE + pos0, i1 = t * EV_TILE + pos1;
+      if (i0 < M) {
+        const double4* src = qpk + idx[i0];
+        cp_async16(&rec[slot][pos0], src);
+        cp_async16(reinterpret_cast<double2*>(&rec[slot][pos0]) + 1, reinterpret_cast<const double2*>(src) + 1);
+      }
+      if (i1 < M) {
+        const double4* src = qpk + idx[i1];
+        cp_async16(&rec[slot][pos1], src);
+        cp_async16(reinterpret_cast<double2*>(&rec[slot][pos1]) + 1, reinterpret_cast<const double2*>(src) + 1);
+      }
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  int64_t t = blockIdx.x;
+  issue(t, 0);
+  issue(t + gridDim.x, 1);
+  int slot = 0;
+  for (; t < ntiles; t += gridDim.x, slot ^= 1) {
+    asm volatile("cp.async.wait_group 1;" ::: "memory");  // this tile's records (the next one in flight)
+    const int64_t i0 = t * EV_TILE + pos0, i1 = t * EV_TILE + pos1;
+    const double4 r0 = rec[slot][pos0], r1 = rec[slot][pos1];  // each thread reads only its own records
+    const uint64_t k0 = i0 < M ? keys[i0] : 0, k1 = i1 < M ? keys[i1] : 0;
+    const int64_t qi0 = i0 < M ? (int64_t)idx[i0] : 0, qi1 = i1 < M ? (int64_t)idx[i1] : 0;
+    int64_t n0, n1;
+    double x0, y0, z0, x1, y1, z1;
+    eval_descend(i0, M, true, Dk, nt, r0.x, r0.y, r0.z, k0, n0, x0, y0, z0);
+    eval_descend(i1, M, true, Dk, nt, r1.x, r1.y, r1.z, k1, n1, x1, y1, z1);
+    const int64_t node0 = __shfl_sync(0xffffffffu, n0, 0);
+    const bool uniform = __all_sync(0xffffffffu, (i0 >= M || n0 == node0) && (i1 >= M || n1 == node0));
+    if (lane == 0) cta_node[warp] = uniform ? (long long)node0 : -1ll;
+    __syncthreads();
+    bool cta_uniform = true;
+#pragma unroll
+    for (int w8 = 0; w8 < EV_THREADS / 32; ++w8)
+      cta_uniform = cta_uniform && cta_node[w8] == cta_node[0] && cta_node[w8] >= 0;
+    double v0, v1;
+    if (cta_uniform) {
+      const double* a = nt.pcoef + node0 * L;
+      for (int k = tid; k < L; k += EV_THREADS) cs[0][k] = __ldg(a + k);
+      __syncthreads();
+      horner3x2<P>(SmemCoef(cs[0]), x0, y0, z0, x1, y1, z1, v0, v1);
+    } else if (uniform) {
+      const double* a = nt.pcoef + node0 * L;
+      for (int k = lane; k < L; k += 32) cs[warp][k] = __ldg(a + k);
+      __syncwarp();
+      horner3x2<P>(SmemCoef(cs[warp]), x0, y0, z0, x1, y1, z1, v0, v1);
+    } else {
+      const double* a0 = nt.pcoef + n0 * L;
+      const double* a1 = nt.pcoef + n1 * L;
+      auto c0 = [&](int k) { return __ldg(a0 + k); };
+      auto c1 = [&](int k) { return __ldg(a1 + k); };
+      v0 = horner3<P>(c0, x0, y0, z0);
+      v1 = horner3<P>(c1, x1, y1, z1);
+    }
+    if (i0 < M) out[qi0] = v0;
+    if (i1 < M) out[qi1] = v1;
+    __syncthreads();  // cs / cta_node reuse; this slot's records consumed
+    issue(t + 2 * (int64_t)gridDim.x, slot);
+  }
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+}
+
 }  // namespace
 
 template <int P>
@@ -206,6 +303,24 @@ void eval_sorted(const double* q, const double4* qpk, const uint64_t* keys, cons
                  const double lo[3], double width, bool unit, int Dk, const NodeTable& nt, double* out,
                  cudaStream_t s) {
   if (M <= 0) return;
+  static int pipe_ctas = -1;  // persistent CTAs of the pipelined kernel (FMI_EVAL_PIPE=0: the one-shot kernel)
+  static std::once_flag once;
+  constexpr size_t smem = ((size_t)2 * EV_TILE * 4 + (size_t)(EV_THREADS / 32) * ((rank3(P) + 1) & ~1)) * sizeof(double);
+  std::call_once(once, [] {
+    int dev = 0, sms = 0, per = 0;
+    FMI_CK(cudaGetDevice(&dev));
+    FMI_CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    FMI_CK(cudaFuncSetAttribute(k_eval_pipe<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    FMI_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_eval_pipe<P>, EV_THREADS, smem));
+    const char* e = std::getenv("FMI_EVAL_PIPE");
+    pipe_ctas = (e && std::atoi(e) == 0) ? 0 : sms * std::max(1, per);
+  });
+  if (qpk && keys && idx && pipe_ctas > 0) {
+    const int64_t ntiles = (M + EV_TILE - 1) / EV_TILE;
+    FMI_LAUNCH(KID_EVAL, s, k_eval_pipe<P>, (unsigned)std::min<int64_t>(ntiles, pipe_ctas), EV_THREADS, smem, qpk, keys,
+               idx, M, Dk, nt, out);
+    return;
+  }
   FMI_LAUNCH(KID_EVAL, s, k_eval<P>, (unsigned)((M + 511) / 512), 256, 0, q, qpk, keys, idx, M, lo[0], lo[1], lo[2],
              width, unit, Dk, nt, out);
 }

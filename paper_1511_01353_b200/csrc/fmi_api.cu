@@ -739,23 +739,42 @@ void fused_gather_root(const double4* packed, const uint32_t* perm, const double
                             root_b, s);
 }
 
-// the unscoped fit (max_depth = 0) through the QR of unscoped.cu — one node, the root
+// the QR path (unscoped.cu) — every node fitted by the paper's QR through
+// the Legendre basis, level by level (Alg. 1): degrees 11..14 (beyond the fp64 moment Gram),
+// any max_depth; the unscoped fit of Fig. 1 is its max_depth = 0 case (one level, the root)
 template <int P>
 void run_unscoped(fmi_tree* T, const uint64_t* keys, double* ux, double* uy, double* uz, double* r, cudaStream_t s) {
   constexpr int L = rank3(P);
-  DBuf<int64_t> dev_small(8, s), flags(8, s), scan(8, s);
+  DBuf<int64_t> dev_small(8, s), flags, scan;
+  int64_t* host_small = host_staging();
   ensure_table(T->nt, T->cap, 16, L, true, s);
   set_root(T->nt, T->N, true, s);
   T->nodes = 1;
-  T->lvl_first.push_back(0);
-  T->lvl_count.push_back(1);
-  T->lvl_points.push_back(T->N);
-  T->depth_max = 0;
-  LevelCtx c{keys, ux, uy, uz, r, T->nt, 0, 1, 0, T->D, T->Dk, P, L, rank3(2 * P), T->tau};
-  level_children(c, s);
-  unscoped_fit<P>(c, s);
-  level_decide(c, false, nullptr, nullptr, flags.p, scan.p, dev_small.p + 2, s);
-  tmark("unscoped", s);
+  int64_t first = 0, count = 1, points = T->N;
+  for (int depth = 0; count > 0; ++depth) {
+    if (depth >= T->Dsorted) throw KeysShort{};  // octant digits below this depth are not sorted
+    T->lvl_first.push_back(first);
+    T->lvl_count.push_back(count);
+    T->lvl_points.push_back(points);
+    T->depth_max = depth;
+    ensure_table(T->nt, T->cap, first + count + 8 * count, L, true, s);
+    LevelCtx c{keys, ux, uy, uz, r, T->nt, first, count, depth, T->D, T->Dk, P, L, rank3(2 * P), T->tau};
+    level_children(c, s);
+    unscoped_fit<P>(c, s);
+    flags.ensure(count * 8, s);
+    scan.ensure(count * 8, s);
+    FMI_CK(cudaMemsetAsync(dev_small.p + 4, 0, sizeof(int64_t), s));
+    level_decide(c, false, nullptr, nullptr, flags.p, scan.p, dev_small.p + 2, s);
+    FMI_CK(cudaMemcpyAsync(host_small, dev_small.p + 2, 2 * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    FMI_CK(cudaStreamSynchronize(s));
+    const int64_t nnew = host_small[0], npts = host_small[1];
+    first += count;
+    T->nodes = first + nnew;
+    count = nnew;
+    points = npts;
+  }
+  for (size_t d = 0; d < T->lvl_first.size(); ++d) presum_level<P>(T->nt, T->lvl_first[d], T->lvl_count[d], s);
+  tmark("qr levels", s);
 }
 
 template <int P>
@@ -807,8 +826,8 @@ fmi_tree* build_impl(const double* pts, const double* f, int64_t N, int degree, 
   if ((!pts || !f) && !(dist && N == 0)) fail(FMI_EINPUT, "null pointer argument");
   if (N < 0) fail(FMI_EINPUT, "N < 0");
   if (degree < 0 || degree > FMI_MAX_DEGREE) fail(FMI_EPRECOND, "degree outside 0..14");
-  if (degree > FMI_MAX_LEVEL_DEGREE && (max_depth != 0 || dist))
-    fail(FMI_EPRECOND, "degree > 10 needs max_depth = 0 (the unscoped fit, P:251-265) and no sharding");
+  if (degree > FMI_MAX_LEVEL_DEGREE && dist)
+    fail(FMI_EPRECOND, "degree > 10 (the QR path) is single-GPU only");
   if (max_depth < 0 || max_depth > FMI_MAX_DEPTH) fail(FMI_EPRECOND, "max_depth outside 0..20");
   if (!(tol >= 0.0)) fail(FMI_EPRECOND, "tol must be >= 0 (and not NaN)");
   const int L = rank3(degree);
@@ -943,9 +962,12 @@ fmi_tree* build_impl(const double* pts, const double* f, int64_t N, int degree, 
     DBuf<double4> packed(N, s);
     DBuf<double> ux(N, s), uy(N, s), uz(N, s), r(N, s);
     // the unscoped QR path (f2): degrees 11..14, or any degree at max_depth = 0 with FMI_UNSCOPED_QR=1
-    const bool unscoped = !dist && max_depth == 0 && (degree > FMI_MAX_LEVEL_DEGREE || std::getenv("FMI_UNSCOPED_QR"));
+    // the QR path (unscoped.cu): degrees 11..14, or any degree with FMI_QR_PATH=1 (FMI_UNSCOPED_QR=1:
+    // the same, max_depth = 0 only)
+    const bool unscoped = !dist && (degree > FMI_MAX_LEVEL_DEGREE || std::getenv("FMI_QR_PATH") ||
+                                    (max_depth == 0 && std::getenv("FMI_UNSCOPED_QR")));
     int Dsort = T->Dk;
-    if (!unscoped && !std::getenv("FMI_FULL_SORT")) {
+    if (!std::getenv("FMI_FULL_SORT")) {
       const double fill = std::max(1.0, (double)std::max<int64_t>(Ntot, 1) / (double)L);
       Dsort = std::min(T->Dk, (int)std::ceil(std::log(fill) / std::log(8.0)) + 1);
       if (dist) Dsort = std::min(T->Dk, std::max(Dsort, dist->shard_depth + 1));
@@ -1498,7 +1520,7 @@ fmi_tree* fmi_load(const char* path) {
       if (h.version != kFileVersion) fail(FMI_EVERSION, "unsupported tree file version");
       if (h.p < 0 || h.p > FMI_MAX_DEGREE || h.nodes < 1 || h.nodes > (int64_t(1) << 31) - 1 || h.depth_max < 0 ||
           h.depth_max > FMI_MAX_DEPTH || h.D < 0 || h.D > FMI_MAX_DEPTH || h.depth_max > h.D ||
-          (h.p > FMI_MAX_LEVEL_DEGREE && h.D != 0) || !(h.width > 0) || !std::isfinite(h.width) ||
+          !(h.width > 0) || !std::isfinite(h.width) ||
           !std::isfinite(h.lo[0]) || !std::isfinite(h.lo[1]) || !std::isfinite(h.lo[2]) || !(h.tau >= 0) || h.N < 0)
         fail(FMI_EVERSION, "corrupt tree file header");
       T = new fmi_tree();

@@ -42,7 +42,7 @@ __global__ void __launch_bounds__(UTHREADS)
     k_leg_rows(const double* __restrict__ ux, const double* __restrict__ uy, const double* __restrict__ uz,
                const double* __restrict__ f, int64_t r0, int64_t nr, const uint8_t* __restrict__ el,
                const uint8_t* __restrict__ em, const uint8_t* __restrict__ en, int L, int LDV,
-               double* __restrict__ V) {
+               double* __restrict__ V, double cx, double cy, double cz, double sc) {
   __shared__ double tp[3][32][P + 1];  // s_k P_k of the 32 rows' local coordinates, per axis
   const int64_t base = (int64_t)blockIdx.x * 32;
   if (threadIdx.x < 96) {
@@ -51,7 +51,7 @@ __global__ void __launch_bounds__(UTHREADS)
     double u = 0.0;
     if (base + row < nr) {
       const double* src = ax == 0 ? ux : (ax == 1 ? uy : uz);
-      u = to_local(src[i], 0.5, 2.0);  // root frame: centre 1/2, scale 2
+      u = to_local(src[i], ax == 0 ? cx : (ax == 1 ? cy : cz), sc);  // the node frame
     }
     double pm = 1.0, pk = u;  // Bonnet: (k+1) P_{k+1} = (2k+1) u P_k - k P_{k-1}
     tp[ax][row][0] = 1.0;
@@ -187,6 +187,8 @@ __global__ void __launch_bounds__(CTHREADS) k_chol_bordered(double* __restrict__
   extern __shared__ __align__(16) double Pn[];  // [CKB][LDP]
   __shared__ double sinv[CKB];
   const int LDP = chol_ldp(n);
+  G += (int64_t)blockIdx.x * LDV * LDV;  // batched: node blockIdx.x of the batch
+  diag0 += (int64_t)blockIdx.x * LDV;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   for (int j0 = 0; j0 < n; j0 += CKB) {
     const int bw = min(CKB, n - j0), R = n - j0;
@@ -307,6 +309,8 @@ __global__ void k_r_mono(const double* __restrict__ G, int L, int LDV, const uin
   const int LA = L + 1;
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= (int64_t)LA * LA) return;
+  G += (int64_t)blockIdx.y * LDV * LDV;  // batched: node blockIdx.y of the batch
+  A += (int64_t)blockIdx.y * LA * LA;
   const int j = (int)(e / LA), i = (int)(e % LA);  // column j, row i
   double v = 0.0;
   if (j == L) {
@@ -338,9 +342,16 @@ __device__ __forceinline__ double ublock_sum(double v, double* red) {
 
 // ---- 5. equilibration, column-rejection walk (G9) and back substitution (one CTA) ---------------------
 __global__ void __launch_bounds__(UTHREADS)
-    k_unscoped_solve(double* __restrict__ A, int L, double delta, double* __restrict__ dinv, int* __restrict__ kept,
-                     double* __restrict__ piv, double* __restrict__ sol, NodeTable nt) {
+    k_unscoped_solve(double* __restrict__ A, int L, double delta, double* __restrict__ work, int* __restrict__ kept,
+                     NodeTable nt, int64_t node0) {
   const int LA = L + 1;
+  // batched: node node0 + blockIdx.x, its R in A[blockIdx.x], 3L doubles and L ints of scratch
+  A += (int64_t)blockIdx.x * LA * LA;
+  double* dinv = work + (int64_t)blockIdx.x * 3 * L;
+  double* piv = dinv + L;
+  double* sol = dinv + 2 * L;
+  kept += (int64_t)blockIdx.x * L;
+  const int64_t node = node0 + blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nwarp = UTHREADS / 32;
   __shared__ double red[UTHREADS / 32];
@@ -406,17 +417,17 @@ __global__ void __launch_bounds__(UTHREADS)
   }
   for (int i = tid; i < L; i += UTHREADS) {
     const double a = sol[i] * dinv[i];
-    nt.coef[i] = a;
-    nt.pcoef[i] = a;
+    nt.coef[node * L + i] = a;
+    nt.pcoef[node * L + i] = a;
   }
   if (tid == 0) {
     int rk = 0;
     double mn = INFINITY;
     for (int i = 0; i < L; ++i)
       if (kept[i] >= 0) { ++rk; mn = fmin(mn, piv[i]); }
-    nt.rank[0] = rk;
-    nt.minpiv[0] = rk ? mn : 0.0;
-    nt.flag[0] = 0;
+    nt.rank[node] = rk;
+    nt.minpiv[node] = rk ? mn : 0.0;
+    nt.flag[node] = 1;  // fitted by the Householder-QR path
   }
 }
 
@@ -424,7 +435,7 @@ __global__ void __launch_bounds__(UTHREADS)
 template <int P>
 __global__ void __launch_bounds__(UTHREADS)
     k_unscoped_resid(const double* __restrict__ ux, const double* __restrict__ uy, const double* __restrict__ uz,
-                     double* __restrict__ r, const double* __restrict__ coef, const Chunk* __restrict__ chunks,
+                     double* __restrict__ r, NodeTable nt, int64_t first, const Chunk* __restrict__ chunks,
                      const int64_t* __restrict__ nchunks, double* __restrict__ partial) {
   constexpr int L = rank3(P);
   __shared__ __align__(16) double sa[(L + 1) & ~1];
@@ -432,14 +443,16 @@ __global__ void __launch_bounds__(UTHREADS)
   const int64_t cidx = blockIdx.x;
   if (cidx >= *nchunks) return;
   const Chunk ck = chunks[cidx];
-  for (int i = threadIdx.x; i < L; i += UTHREADS) sa[i] = coef[i];
+  const int64_t node = first + (ck.owner >> 3);  // chunks of octant segments node*8 + o
+  const Frame fr = node_frame(nt.cell[node]);
+  for (int i = threadIdx.x; i < L; i += UTHREADS) sa[i] = nt.coef[node * L + i];
   __syncthreads();
   const SmemCoefVolatile cf(sa);
   double ss = 0.0;
   for (int64_t i = ck.start + threadIdx.x; i < ck.end; i += UTHREADS) {
-    const double x = to_local(ux[i], 0.5, 2.0);
-    const double y = to_local(uy[i], 0.5, 2.0);
-    const double z = to_local(uz[i], 0.5, 2.0);
+    const double x = to_local(ux[i], fr.cx, fr.scale);
+    const double y = to_local(uy[i], fr.cy, fr.scale);
+    const double z = to_local(uz[i], fr.cz, fr.scale);
     const double v = r[i] - horner3<P>(cf, x, y, z);
     r[i] = v;
     ss = fma(v, v, ss);
@@ -448,15 +461,15 @@ __global__ void __launch_bounds__(UTHREADS)
   if (threadIdx.x == 0) partial[cidx] = t;
 }
 
-// octant energies of the root in chunk order -> child_ss[o]
+// octant energies of the level's nodes in chunk order -> child_ss[(first + node)*8 + o]
 __global__ void k_octant_ss(const double* __restrict__ partial, const int64_t* __restrict__ chunk_begin,
-                            const int64_t* __restrict__ nchunks, NodeTable nt) {
-  const int o = threadIdx.x;
-  if (o >= 8) return;
-  const int64_t c0 = chunk_begin[o], c1 = o + 1 < 8 ? chunk_begin[o + 1] : *nchunks;
+                            const int64_t* __restrict__ nchunks, NodeTable nt, int64_t first, int64_t nseg) {
+  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= nseg) return;
+  const int64_t c0 = chunk_begin[g], c1 = g + 1 < nseg ? chunk_begin[g + 1] : *nchunks;
   double s = 0.0;
   for (int64_t c = c0; c < c1; ++c) s += partial[c];
-  nt.child_ss[o] = s;
+  nt.child_ss[first * 8 + g] = s;
 }
 
 // host: x^a = Σ_k e[a][k] · s_k P_k(x) from the monomial coefficients of the Legendre polynomials
@@ -512,53 +525,76 @@ void unscoped_fit(const LevelCtx& c, cudaStream_t s) {
   DBuf<uint8_t> dex(3 * L, s);
   FMI_CK(cudaMemcpyAsync(dex.p, ex.data(), 3 * L, cudaMemcpyHostToDevice, s));
   const uint8_t *el = dex.p, *em = dex.p + L, *en = dex.p + 2 * L;
-  // the root's point range
-  int64_t se[2];
-  FMI_CK(cudaMemcpyAsync(se, c.nt.start, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
-  FMI_CK(cudaMemcpyAsync(se + 1, c.nt.end, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  // the level's point ranges and cells (host copies drive the per-node Gram launches)
+  const int64_t count = c.count;
+  std::vector<int64_t> st(count), en_(count);
+  std::vector<int4> cell(count);
+  FMI_CK(cudaMemcpyAsync(st.data(), c.nt.start + c.first, count * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  FMI_CK(cudaMemcpyAsync(en_.data(), c.nt.end + c.first, count * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  FMI_CK(cudaMemcpyAsync(cell.data(), c.nt.cell + c.first, count * sizeof(int4), cudaMemcpyDeviceToHost, s));
   FMI_CK(cudaStreamSynchronize(s));
-  const int64_t n = se[1] - se[0];
-  // 1-2. Legendre Gram over slabs of rows
-  const int64_t slab = std::min<int64_t>(n, std::max<int64_t>(4096, ((int64_t)1 << 28) / LDV));  // <= 2 GB
-  const int nsplit = (int)std::max<int64_t>(1, std::min<int64_t>(std::max(1, 148 * 3 / ntile), slab / 512 + 1));
-  DBuf<double> V((size_t)slab * LDV, s), part((size_t)nsplit * LDV * LDV, s), G((size_t)LDV * LDV, s);
-  for (int64_t r0 = 0; r0 < n; r0 += slab) {
-    const int64_t nr = std::min(slab, n - r0);
-    FMI_LAUNCH(KID_UNSCOPED_GRAM, s, k_leg_rows<P>, (unsigned)((nr + 31) / 32), UTHREADS, 0, c.ux + se[0],
-               c.uy + se[0], c.uz + se[0], c.r + se[0], r0, nr, el, em, en, L, LDV, V.p);
-    FMI_LAUNCH(KID_UNSCOPED_GRAM, s, k_syrk_dmma, dim3((unsigned)ntile, (unsigned)nsplit), SYD_THREADS, 0, V.p, nr, LDV,
-               nsplit, r0 > 0, part.p);
+  int64_t nmax = 0;
+  for (int64_t b = 0; b < count; ++b) nmax = std::max(nmax, en_[b] - st[b]);
+  // 1-2. per node: Legendre rows of the node frame over slabs of its rows, split-K DMMA SYRK; the
+  // nodes' Grams are solved in batches (3-5: one CTA per node)
+  const int64_t slab = std::min<int64_t>(std::max<int64_t>(nmax, 1),
+                                         std::max<int64_t>(4096, ((int64_t)1 << 28) / LDV));  // <= 2 GB
+  const int64_t batch = std::max<int64_t>(1, std::min<int64_t>(count, ((int64_t)1 << 28) / ((int64_t)LDV * LDV)));
+  const int nsplit_max = std::max(1, 148 * 3 / ntile);
+  DBuf<double> V((size_t)slab * LDV, s), part((size_t)nsplit_max * LDV * LDV, s);
+  DBuf<double> G((size_t)batch * LDV * LDV, s), diag0((size_t)batch * LDV, s);
+  DBuf<double> A((size_t)batch * LA * LA, s), work((size_t)batch * 3 * L, s);
+  DBuf<int> kept((size_t)batch * L, s), nonpd(1, s);
+  FMI_CK(cudaMemsetAsync(nonpd.p, 0, sizeof(int), s));
+  const size_t csmem = (size_t)CKB * chol_ldp(LA) * sizeof(double);
+  // k_chol_bordered is shared by every degree: opt in once for the largest (p = 14) panel
+  static std::once_flag attr_once;
+  std::call_once(attr_once, [] {
+    const size_t most = (size_t)CKB * chol_ldp(rank3(UMAXP) + 1) * sizeof(double);
+    FMI_CK(cudaFuncSetAttribute(k_chol_bordered, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)most));
+  });
+  for (int64_t b0 = 0; b0 < count; b0 += batch) {
+    const int64_t nb = std::min(batch, count - b0);
+    for (int64_t b = 0; b < nb; ++b) {
+      const int64_t node = b0 + b, s0 = st[node], n = en_[node] - s0;
+      const double h = std::ldexp(1.0, -(cell[node].w + 1)), sc = std::ldexp(1.0, cell[node].w + 1);
+      const double cx = (2.0 * cell[node].x + 1.0) * h, cy = (2.0 * cell[node].y + 1.0) * h,
+                   cz = (2.0 * cell[node].z + 1.0) * h;
+      const int nsplit = (int)std::max<int64_t>(1, std::min<int64_t>(nsplit_max, std::min(slab, n) / 512 + 1));
+      for (int64_t r0 = 0; r0 < n; r0 += slab) {
+        const int64_t nr = std::min(slab, n - r0);
+        FMI_LAUNCH(KID_UNSCOPED_GRAM, s, k_leg_rows<P>, (unsigned)((nr + 31) / 32), UTHREADS, 0, c.ux + s0,
+                   c.uy + s0, c.uz + s0, c.r + s0, r0, nr, el, em, en, L, LDV, V.p, cx, cy, cz, sc);
+        FMI_LAUNCH(KID_UNSCOPED_GRAM, s, k_syrk_dmma, dim3((unsigned)ntile, (unsigned)nsplit), SYD_THREADS, 0, V.p, nr,
+                   LDV, nsplit, r0 > 0, part.p);
+      }
+      FMI_LAUNCH(KID_UNSCOPED_GRAM, s, k_sum_splits, (unsigned)(((int64_t)LA * LA + 255) / 256), 256, 0, part.p,
+                 nsplit, LDV, LA, G.p + b * LDV * LDV, diag0.p + b * LDV);
+    }
+    // 3-5
+    FMI_LAUNCH(KID_UNSCOPED_SOLVE, s, k_chol_bordered, (unsigned)nb, CTHREADS, csmem, G.p, LA, LDV, diag0.p, nonpd.p);
+    FMI_LAUNCH(KID_UNSCOPED_SOLVE, s, k_r_mono, dim3((unsigned)(((int64_t)LA * LA + 255) / 256), (unsigned)nb), 256, 0,
+               G.p, L, LDV, el, em, en, P, A.p);
+    FMI_LAUNCH(KID_UNSCOPED_SOLVE, s, k_unscoped_solve, (unsigned)nb, UTHREADS, 0, A.p, L, kDelta, work.p, kept.p,
+               c.nt, c.first + b0);
   }
   V.release();
-  DBuf<double> diag0(LA, s);
-  FMI_LAUNCH(KID_UNSCOPED_GRAM, s, k_sum_splits, (unsigned)(((int64_t)LA * LA + 255) / 256), 256, 0, part.p, nsplit,
-             LDV, LA, G.p, diag0.p);
   part.release();
-  // 3-5
-  DBuf<int> nonpd(1, s);
-  FMI_CK(cudaMemsetAsync(nonpd.p, 0, sizeof(int), s));
+  // 6. residual and octant energies over the level's octant segments
   {
-    const size_t smem = (size_t)CKB * chol_ldp(LA) * sizeof(double);
-    FMI_CK(cudaFuncSetAttribute(k_chol_bordered, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    FMI_LAUNCH(KID_UNSCOPED_SOLVE, s, k_chol_bordered, 1, CTHREADS, smem, G.p, LA, LDV, diag0.p, nonpd.p);
-  }
-  DBuf<double> A((size_t)LA * LA, s), work((size_t)3 * L, s);
-  DBuf<int> kept(L, s);
-  FMI_LAUNCH(KID_UNSCOPED_SOLVE, s, k_r_mono, (unsigned)(((int64_t)LA * LA + 255) / 256), 256, 0, G.p, L, LDV, el, em,
-             en, P, A.p);
-  FMI_LAUNCH(KID_UNSCOPED_SOLVE, s, k_unscoped_solve, 1, UTHREADS, 0, A.p, L, kDelta, work.p, kept.p, work.p + L,
-             work.p + 2 * L, c.nt);
-  // 6. residual and octant energies
-  {
-    DBuf<int64_t> counts(8, s), begin(8, s), nch(1, s);
-    const int64_t ch = std::max<int64_t>(1024, (n + 148 * 4 - 1) / (148 * 4));
-    const int64_t maxc = n / ch + 9;
+    int64_t points = 0;
+    for (int64_t b = 0; b < count; ++b) points += en_[b] - st[b];
+    const int64_t nseg = count * 8;
+    DBuf<int64_t> counts(nseg, s), begin(nseg, s), nch(1, s);
+    const int64_t ch = std::max<int64_t>(1024, (points + 148 * 4 - 1) / (148 * 4));
+    const int64_t maxc = points / ch + nseg + 1;
     DBuf<Chunk> chunks(maxc, s);
     DBuf<double> partial(maxc, s);
-    make_chunks(c.nt.child_start, nullptr, 8, ch, counts.p, begin.p, nch.p, chunks.p, maxc, s);
-    FMI_LAUNCH(KID_RESIDUAL, s, k_unscoped_resid<P>, (unsigned)maxc, UTHREADS, 0, c.ux, c.uy, c.uz, c.r, c.nt.coef,
-               chunks.p, nch.p, partial.p);
-    FMI_LAUNCH(KID_RESIDUAL_REDUCE, s, k_octant_ss, 1, 32, 0, partial.p, begin.p, nch.p, c.nt);
+    make_chunks(c.nt.child_start + c.first * 9, nullptr, nseg, ch, counts.p, begin.p, nch.p, chunks.p, maxc, s);
+    FMI_LAUNCH(KID_RESIDUAL, s, k_unscoped_resid<P>, (unsigned)maxc, UTHREADS, 0, c.ux, c.uy, c.uz, c.r, c.nt,
+               c.first, chunks.p, nch.p, partial.p);
+    FMI_LAUNCH(KID_RESIDUAL_REDUCE, s, k_octant_ss, (unsigned)((nseg + 127) / 128), 128, 0, partial.p, begin.p, nch.p,
+               c.nt, c.first, nseg);
     FMI_CK(cudaStreamSynchronize(s));
   }
 }

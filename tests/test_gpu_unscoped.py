@@ -160,3 +160,63 @@ def test_coplanar_points_rank_truncation(p):
     assert int(ora.kept[0].sum()) == (p + 1) * (p + 2) // 2
     assert int(ex["rank"][0]) == int(ora.kept[0].sum())
     assert np.max(np.abs(val - ref)) <= EVAL_TOL * np.max(np.abs(f))
+
+
+# ---------------------------------------------------------------------------------------------
+# the QR path on the octree (max_depth > 0): SURVEY §8 f3 at L_max = 12
+# ---------------------------------------------------------------------------------------------
+
+def _tree_parity(pts, f, p, tau, D, q, env=None):
+    from parity import compare_trees
+    fmi = _fmi()
+    old = {k: os.environ.get(k) for k in (env or {})}
+    os.environ.update(env or {})
+    try:
+        with fmi.build(_dev(pts), _dev(f), p, tau, D) as tree:
+            gpu = tree.export()
+            val = tree.eval(_dev(q)).cpu().numpy()
+            res = tree.residual()
+    finally:
+        for k, v in old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+    ora = fo.build(pts, f, p, tau, D)
+    ref = fo.evaluate(ora, q)
+    g, o = compare_trees(gpu, ora, tau)
+    scale = float(np.max(np.abs(f)))
+    assert np.max(np.abs(val - ref)) <= EVAL_TOL * scale, float(np.max(np.abs(val - ref)))
+    for key, gi in g.items():
+        a, b = gpu["residual_rms"][gi], ora.residual_rms[o[key]]
+        assert abs(a - b) <= 1e-6 * b + 1e-12 * scale, (key, a, b)
+        assert gpu["rank"][gi] == int(ora.kept[o[key]].sum()), key
+    return gpu, ora, val, res
+
+
+@pytest.mark.parametrize("p,N,D,tau", [(12, 40_000, 2, 1e-9), (11, 30_000, 3, 1e-8)])
+def test_qr_levels_high_degree_octree_vs_oracle(p, N, D, tau):
+    """Degrees above the moment-Gram limit on the octree: every node by the QR path, level by level
+    (Alg. 1): identical topology, counts and ranks, values within 1e-9·max|f|."""
+    rng = np.random.default_rng(600 + p)
+    pts = rng.random((N, 3))
+    f = workloads.franke3d(pts)
+    q = rng.random((4000, 3))
+    gpu, ora, _, _ = _tree_parity(pts, f, p, tau, D, q)
+    assert ora.node_count > 9 and gpu["depth"].max() == 2
+
+
+@pytest.mark.parametrize("p", [3, 6])
+def test_qr_levels_low_degree_vs_oracle_and_level_path(p):
+    """FMI_QR_PATH=1 routes an octree build of any degree through the QR path: same tree as the oracle
+    and as the moment-Gram level path."""
+    rng = np.random.default_rng(700 + p)
+    pts = rng.random((30_000, 3))
+    f = workloads.franke3d(pts)
+    q = rng.random((3000, 3))
+    gpu, ora, val, _ = _tree_parity(pts, f, p, 1e-7, 4, q, env={"FMI_QR_PATH": "1"})
+    fmi = _fmi()
+    with fmi.build(_dev(pts), _dev(f), p, 1e-7, 4) as t:
+        lv = t.eval(_dev(q)).cpu().numpy()
+        assert t.node_count == gpu["depth"].shape[0]
+    assert np.max(np.abs(val - lv)) <= EVAL_TOL * np.max(np.abs(f))

@@ -1,4 +1,4 @@
-"""Write the oracle's golden node lists for the full-size parity tests (tests/test_gpu_fullsize.py).
+"""Write the oracle's golden node lists for the full-size parity tests (tests/test_gpu_golden.py).
 
 Calls only ``oracle/`` and ``workloads/`` (no product code): every stored value is the oracle's.
 
@@ -6,7 +6,8 @@ Calls only ``oracle/`` and ``workloads/`` (no product code): every stored value 
         interpolant at the first 1e5 queries of the config.
   cfg4  Alg. 1 from the root with every depth-0/1 node expanded and ``--subtrees`` depth-2
         subtrees expanded completely (the depth-2 nodes receive the residual of the real root
-        and depth-1 fits); the interpolant at 1e5 queries inside those subtrees.
+        and depth-1 fits); the interpolant at the config's own queries (the mixture) inside them,
+        up to 25,000 per subtree.
   cfg5  the root fit of 2e8 points is beyond this host (Λ alone is 459 GB, ~4 h of QR), so each
         sampled depth-2 subtree is Alg. 1 called on the depth-2 node with the ORIGINAL f: by the
         telescoping identity the depth-2 node's fit of f equals the root + depth-1 +
@@ -155,7 +156,7 @@ def make_cfg4(jobs, k):
     jobsl, qidx = [], []
     for t, cell in enumerate(pick):
         inside = np.all(c2 == np.array(cell), axis=1)
-        qi = np.flatnonzero(np.all(qc2 == np.array(cell), axis=1))[:NQ // len(pick)]
+        qi = np.flatnonzero(np.all(qc2 == np.array(cell), axis=1))[:2 * NQ // len(pick)]
         qidx.append(qi)
         jobsl.append((u[inside], top.residual[inside], p, tau, D, 2, cell, np.ascontiguousarray(qall[qi])))
     with mp.get_context("fork").Pool(jobs) as pool:
@@ -173,7 +174,7 @@ def make_cfg4(jobs, k):
                         values=np.concatenate(vals), **table)
     _summary("cfg4", cfg, table, f"depth 0-1 complete + depth-2 subtrees {pick} (2 most populated + random seed 4); "
                                  f"values at the config's queries (mixture, seed 1) in those cells, up to "
-                                 f"{NQ // len(pick)} per cell ({qidx.size} in all); {time.time() - t0:.0f}s")
+                                 f"{2 * NQ // len(pick)} per cell ({qidx.size} in all); {time.time() - t0:.0f}s")
 
 
 def _top_terms(top, qs, p):

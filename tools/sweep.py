@@ -7,7 +7,10 @@ The paper's figures are placeholders ([FIGURE]), so only the SHAPE can be compar
 (P:396), and its headline (< 10^3 nodes with E_rms < 1e-11, E_inf < 1e-8) — which this
 sweep reports for the (p, τ, N) that reach it.  One JSON line per run.
 
-  python tools/sweep.py [--degrees 4 6 8 10] [--taus 1e-6 1e-8 1e-10 1e-12] [--log8n 4 5 6 7 8]
+  python tools/sweep.py [--degrees 4 8 12] [--taus 1e-6 1e-8 1e-10 1e-12] [--log8n 4 5 6 7 8 9]
+
+Degrees above 10 run the QR path on the octree (csrc/unscoped.cu).  Sweep points are checked against the
+oracle by tests/test_gpu_sweep.py (this tool does not import it).
 """
 import argparse
 import json
@@ -24,9 +27,9 @@ import paper_1511_01353_b200 as fmi  # noqa: E402
 import workloads  # noqa: E402
 
 ap = argparse.ArgumentParser()
-ap.add_argument("--degrees", type=int, nargs="+", default=[4, 6, 8, 10])
+ap.add_argument("--degrees", type=int, nargs="+", default=[4, 8, 12])  # L_max of P:383
 ap.add_argument("--taus", type=float, nargs="+", default=[1e-6, 1e-8, 1e-10, 1e-12])
-ap.add_argument("--log8n", type=int, nargs="+", default=[4, 5, 6, 7, 8])
+ap.add_argument("--log8n", type=int, nargs="+", default=[4, 5, 6, 7, 8, 9])  # N_p = 8^4..8^9
 ap.add_argument("--max-depth", type=int, default=10)
 a = ap.parse_args()
 
@@ -51,7 +54,7 @@ for k in a.log8n:
             dt = time.perf_counter() - t0
             err = val.cpu().numpy() - truth
             erms, einf = workloads.rms_and_max(err)
-            rec = {"N": n, "log8N": k, "degree": p, "rank": L, "tau": tau, "max_depth": a.max_depth,
+            rec = {"path": "qr" if p > 10 else "moments", "N": n, "log8N": k, "degree": p, "rank": L, "tau": tau, "max_depth": a.max_depth,
                    "nodes": tr.node_count, "levels": int(len(tr.level_stats()[0])), "E_rms": erms, "E_inf": einf,
                    "build_eval_s": dt,
                    "paper_headline": bool(tr.node_count < 1000 and erms < 1e-11 and einf < 1e-8)}
