@@ -151,8 +151,11 @@ std::atomic<bool> g_prof{false};
 std::mutex g_prof_mu;
 struct Pending {
   int kid;
+  unsigned grid;
   cudaEvent_t a, b;
 };
+// FMI_PROF_LOG=1 (with profiling on): every timed launch (kernel, grid, ms) to stderr — diagnostics
+const bool g_prof_log = [] { const char* e = std::getenv("FMI_PROF_LOG"); return e && std::atoi(e) > 0; }();
 std::vector<Pending> g_pending;
 std::vector<cudaEvent_t> g_event_pool;
 double g_prof_ms[KID_COUNT];
@@ -188,12 +191,12 @@ void prof_begin(int kid, cudaStream_t s) {
   FMI_CK(cudaEventRecord(tl_open, s));
 }
 
-void prof_end(int kid, cudaStream_t s) {
+void prof_end(int kid, cudaStream_t s, unsigned grid) {
   if (!g_prof.load(std::memory_order_relaxed) || !tl_open) return;
   std::lock_guard<std::mutex> lk(g_prof_mu);
   cudaEvent_t b = get_event();
   FMI_CK(cudaEventRecord(b, s));
-  g_pending.push_back({kid, tl_open, b});
+  g_pending.push_back({kid, grid, tl_open, b});
   tl_open = nullptr;
 }
 
@@ -210,6 +213,7 @@ void prof_collect() {
     if (cudaEventElapsedTime(&ms, p.a, p.b) == cudaSuccess) {
       g_prof_ms[p.kid] += ms;
       g_prof_n[p.kid] += 1;
+      if (g_prof_log) fprintf(stderr, "[fmi launch] %s grid=%u %.4f ms\n", kNames[p.kid], p.grid, ms);
     }
     cudaGetLastError();
     g_event_pool.push_back(p.a);

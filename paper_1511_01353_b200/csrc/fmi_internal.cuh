@@ -53,7 +53,8 @@ enum KernelId {
 };
 const char* kernel_name(int kid);
 void prof_begin(int kid, cudaStream_t s);
-void prof_end(int kid, cudaStream_t s);
+void prof_end(int kid, cudaStream_t s, unsigned grid = 0);
+inline unsigned launch_blocks(dim3 g) { return g.x * g.y * g.z; }
 void prof_collect();  // after a stream sync: accumulate elapsed times of completed launches
 // algorithmic work units processed by the launches of a kernel (items per sort pass, keyed points,
 // solved nodes, ...), summed while profiling is on; bench.py turns them into bytes / flops
@@ -71,7 +72,7 @@ void dist_comm_allreduce(void* dev, int64_t n, int dtype, cudaStream_t s);  // i
     ::fmi::prof_begin((kid), (stream));                                                  \
     kernel<<<(grid), (block), (smem), (stream)>>>(__VA_ARGS__);                          \
     FMI_CK(cudaGetLastError());                                                          \
-    ::fmi::prof_end((kid), (stream));                                                    \
+    ::fmi::prof_end((kid), (stream), ::fmi::launch_blocks(dim3(grid)));                   \
   } while (0)
 
 // ---------------------------------------------------------------------------------------------

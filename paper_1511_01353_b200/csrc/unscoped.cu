@@ -19,6 +19,7 @@
 // Evaluation uses the ordinary K7 path (one node).
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <mutex>
 #include <vector>
 
@@ -181,15 +182,21 @@ __host__ __device__ inline int chol_ldp(int n) {
 // previous ones up to rounding (degenerate point sets, e.g. coplanar): it is set to 0 and its monomial
 // counterparts are then rejected by the G9 walk.
 constexpr double kZeroPivot = 1e-13;
+// CholeskyQR2 trigger: nodes with fewer than kCholQR2Fill·𝓛 points (near-interpolation leaves: κ(V) of
+// 1e5 at n ≈ 𝓛, p = 12) or a relative Schur pivot below kCholQR2Ratio get the second pass.  The smallest
+// relative pivot underestimates κ² by orders of magnitude (2e-4 at κ = 1.7e5), so it alone cannot decide.
+constexpr double kCholQR2Ratio = 1e-2;
+constexpr double kCholQR2Fill = 16.0;
 __global__ void __launch_bounds__(CTHREADS) k_chol_bordered(double* __restrict__ G, int n, int LDV,
                                                             const double* __restrict__ diag0,
-                                                            int* __restrict__ nonpd) {
+                                                            int* __restrict__ nonpd, double* __restrict__ minrat) {
   extern __shared__ __align__(16) double Pn[];  // [CKB][LDP]
   __shared__ double sinv[CKB];
   const int LDP = chol_ldp(n);
   G += (int64_t)blockIdx.x * LDV * LDV;  // batched: node blockIdx.x of the batch
   diag0 += (int64_t)blockIdx.x * LDV;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  double rmin = INFINITY;  // warp 0: smallest Schur pivot / column norm² (1/κ² estimate), ρ excluded
   for (int j0 = 0; j0 < n; j0 += CKB) {
     const int bw = min(CKB, n - j0), R = n - j0;
     for (int e = tid; e < R * bw; e += CTHREADS) {
@@ -212,6 +219,7 @@ __global__ void __launch_bounds__(CTHREADS) k_chol_bordered(double* __restrict__
           } else {
             const bool ok = d > kZeroPivot * diag0[j];
             p = ok ? sqrt(d) : 0.0;
+            if (ok) rmin = fmin(rmin, d / diag0[j]);
             if (lane == 0 && !ok) atomicAdd(nonpd, 1);
           }
           const double inv = p > 0.0 ? 1.0 / p : 0.0;
@@ -300,6 +308,70 @@ __global__ void __launch_bounds__(CTHREADS) k_chol_bordered(double* __restrict__
     }
     __syncthreads();
   }
+  if (tid == 0 && minrat) minrat[blockIdx.x] = rmin;
+}
+
+// ---- 3b. CholeskyQR2 second pass for ill-conditioned nodes ------------------------------------------
+// One Cholesky of the Gram carries an error ~κ(V)²·eps into R_V; nodes with few points per unknown
+// (n ≈ 𝓛 at leaves) reach κ(V)² ~ 1e8.  The second pass makes R_V as accurate as the Householder R of
+// the paper's QR whenever κ(V)² eps < 1: Q1 = V L1⁻ᵀ (row-wise forward substitution),
+// L2 = chol(Q1ᵀQ1) (≈ I), R_V = (L1 L2)ᵀ.  Zero pivots of L1 give zero Q1 columns and zero L2
+// columns, so a column in the span of its predecessors keeps its representation (row of L1).
+//
+// Q1 rows in place: x L1ᵀ = v, i.e. x_j = (v_j − Σ_{k<j} L1[j][k] x_k) / L1[j][j] (0 for a zero pivot);
+// warp = QRB rows sharing every L1 row load, x kept in shared memory.
+constexpr int QRB = 4, QWARPS = 4;
+__global__ void __launch_bounds__(QWARPS * 32)
+    k_rows_trsm(double* __restrict__ V, int64_t nr, int LDV, int n, const double* __restrict__ G) {
+  extern __shared__ __align__(16) double xs[];  // [QWARPS][QRB][n]
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t r0 = ((int64_t)blockIdx.x * QWARPS + warp) * QRB;
+  if (r0 >= nr) return;
+  double* x = xs + (int64_t)warp * QRB * n;
+  for (int e = lane; e < QRB * n; e += 32) {
+    const int q = e / n, c = e - q * n;
+    x[e] = r0 + q < nr ? V[(r0 + q) * LDV + c] : 0.0;
+  }
+  __syncwarp();
+  for (int j = 0; j < n; ++j) {
+    const double* Lj = G + (int64_t)j * LDV;
+    double acc[QRB];
+#pragma unroll
+    for (int q = 0; q < QRB; ++q) acc[q] = 0.0;
+    for (int k = lane; k < j; k += 32) {
+      const double l = Lj[k];
+#pragma unroll
+      for (int q = 0; q < QRB; ++q) acc[q] = fma(l, x[q * n + k], acc[q]);
+    }
+#pragma unroll
+    for (int q = 0; q < QRB; ++q)
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) acc[q] += __shfl_xor_sync(0xffffffffu, acc[q], o);
+    const double d = Lj[j];
+    if (lane < QRB) {
+      double a = acc[0];
+#pragma unroll
+      for (int q = 1; q < QRB; ++q) if (lane == q) a = acc[q];
+      x[lane * n + j] = d > 0.0 ? (x[lane * n + j] - a) / d : 0.0;
+    }
+    __syncwarp();
+  }
+  for (int e = lane; e < QRB * n; e += 32) {
+    const int q = e / n, c = e - q * n;
+    if (r0 + q < nr) V[(r0 + q) * LDV + c] = x[e];
+  }
+}
+
+// Lc[i][k] = Σ_{m=k..i} L1[i][m] L2[m][k] (lower, row-major, ld LDV)
+__global__ void k_tri_product(const double* __restrict__ L1, const double* __restrict__ L2, int n, int LDV,
+                              double* __restrict__ Lc) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= (int64_t)n * n) return;
+  const int i = (int)(e / n), k = (int)(e % n);
+  if (k > i) return;
+  double v = 0.0;
+  for (int m = k; m <= i; ++m) v = fma(L1[(int64_t)i * LDV + m], L2[(int64_t)m * LDV + k], v);
+  Lc[(int64_t)i * LDV + k] = v;
 }
 
 // ---- 4. R = R_V C, augmented with [y; ρ] as column L; column-major A[col * LA + row] -----------------
@@ -553,6 +625,20 @@ void unscoped_fit(const LevelCtx& c, cudaStream_t s) {
     const size_t most = (size_t)CKB * chol_ldp(rank3(UMAXP) + 1) * sizeof(double);
     FMI_CK(cudaFuncSetAttribute(k_chol_bordered, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)most));
   });
+  // CholeskyQR2 (3b): FMI_CHOLQR2_RATIO overrides the relative-pivot trigger (0 disables the pass)
+  static const double cholqr2_ratio = [] {
+    const char* e = std::getenv("FMI_CHOLQR2_RATIO");
+    return e ? std::atof(e) : kCholQR2Ratio;
+  }();
+  DBuf<double> minrat((size_t)batch, s), G2, Gc, diag2;
+  std::vector<double> hrat(batch);
+  const size_t tsmem = (size_t)QWARPS * QRB * LA * sizeof(double);
+  static std::once_flag trsm_once;
+  std::call_once(trsm_once, [] {
+    const size_t most = (size_t)QWARPS * QRB * (rank3(UMAXP) + 1) * sizeof(double);
+    FMI_CK(cudaFuncSetAttribute(k_rows_trsm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)most));
+  });
+  int64_t n_cholqr2 = 0;
   for (int64_t b0 = 0; b0 < count; b0 += batch) {
     const int64_t nb = std::min(batch, count - b0);
     for (int64_t b = 0; b < nb; ++b) {
@@ -572,7 +658,42 @@ void unscoped_fit(const LevelCtx& c, cudaStream_t s) {
                  nsplit, LDV, LA, G.p + b * LDV * LDV, diag0.p + b * LDV);
     }
     // 3-5
-    FMI_LAUNCH(KID_UNSCOPED_SOLVE, s, k_chol_bordered, (unsigned)nb, CTHREADS, csmem, G.p, LA, LDV, diag0.p, nonpd.p);
+    FMI_LAUNCH(KID_UNSCOPED_SOLVE, s, k_chol_bordered, (unsigned)nb, CTHREADS, csmem, G.p, LA, LDV, diag0.p, nonpd.p,
+               minrat.p);
+    // 3b. CholeskyQR2 pass for the nodes whose first factor may have lost digits (few points per unknown
+    // or a small relative pivot) and whose rows fit one slab
+    FMI_CK(cudaMemcpyAsync(hrat.data(), minrat.p, nb * sizeof(double), cudaMemcpyDeviceToHost, s));
+    FMI_CK(cudaStreamSynchronize(s));
+    for (int64_t b = 0; b < nb; ++b) {
+      const int64_t node = b0 + b, s0 = st[node], n = en_[node] - s0;
+      if (!(hrat[b] < cholqr2_ratio || (double)n < kCholQR2Fill * L) || cholqr2_ratio <= 0.0 || n > slab || n == 0)
+        continue;
+      if (!G2.p) {
+        G2 = DBuf<double>((size_t)LDV * LDV, s);
+        Gc = DBuf<double>((size_t)LDV * LDV, s);
+        diag2 = DBuf<double>((size_t)LDV, s);
+        FMI_CK(cudaMemsetAsync(Gc.p, 0, (size_t)LDV * LDV * sizeof(double), s));
+      }
+      const double h = std::ldexp(1.0, -(cell[node].w + 1)), sc = std::ldexp(1.0, cell[node].w + 1);
+      const double cx = (2.0 * cell[node].x + 1.0) * h, cy = (2.0 * cell[node].y + 1.0) * h,
+                   cz = (2.0 * cell[node].z + 1.0) * h;
+      const int nsplit = (int)std::max<int64_t>(1, std::min<int64_t>(nsplit_max, n / 512 + 1));
+      double* L1 = G.p + b * LDV * LDV;
+      FMI_LAUNCH(KID_UNSCOPED_GRAM, s, k_leg_rows<P>, (unsigned)((n + 31) / 32), UTHREADS, 0, c.ux + s0, c.uy + s0,
+                 c.uz + s0, c.r + s0, 0, n, el, em, en, L, LDV, V.p, cx, cy, cz, sc);
+      FMI_LAUNCH(KID_UNSCOPED_SOLVE, s, k_rows_trsm, (unsigned)((n + QWARPS * QRB - 1) / (QWARPS * QRB)), QWARPS * 32,
+                 tsmem, V.p, n, LDV, LA, L1);
+      FMI_LAUNCH(KID_UNSCOPED_GRAM, s, k_syrk_dmma, dim3((unsigned)ntile, (unsigned)nsplit), SYD_THREADS, 0, V.p, n,
+                 LDV, nsplit, false, part.p);
+      FMI_LAUNCH(KID_UNSCOPED_GRAM, s, k_sum_splits, (unsigned)(((int64_t)LA * LA + 255) / 256), 256, 0, part.p,
+                 nsplit, LDV, LA, G2.p, diag2.p);
+      FMI_LAUNCH(KID_UNSCOPED_SOLVE, s, k_chol_bordered, 1u, CTHREADS, csmem, G2.p, LA, LDV, diag2.p, nonpd.p,
+                 (double*)nullptr);
+      FMI_LAUNCH(KID_UNSCOPED_SOLVE, s, k_tri_product, (unsigned)(((int64_t)LA * LA + 255) / 256), 256, 0, L1, G2.p,
+                 LA, LDV, Gc.p);
+      FMI_CK(cudaMemcpyAsync(L1, Gc.p, (size_t)LDV * LDV * sizeof(double), cudaMemcpyDeviceToDevice, s));
+      ++n_cholqr2;
+    }
     FMI_LAUNCH(KID_UNSCOPED_SOLVE, s, k_r_mono, dim3((unsigned)(((int64_t)LA * LA + 255) / 256), (unsigned)nb), 256, 0,
                G.p, L, LDV, el, em, en, P, A.p);
     FMI_LAUNCH(KID_UNSCOPED_SOLVE, s, k_unscoped_solve, (unsigned)nb, UTHREADS, 0, A.p, L, kDelta, work.p, kept.p,
@@ -580,6 +701,7 @@ void unscoped_fit(const LevelCtx& c, cudaStream_t s) {
   }
   V.release();
   part.release();
+  prof_units(KID_UNSCOPED_SOLVE, n_cholqr2);
   // 6. residual and octant energies over the level's octant segments
   {
     int64_t points = 0;
