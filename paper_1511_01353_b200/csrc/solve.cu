@@ -117,7 +117,9 @@ __global__ void __launch_bounds__(NT, NT == 512 ? 1 : (NT == 256 ? 2 : (NT == 12
   __shared__ double errw[K5_WARPS];
   __shared__ double sinv[KB];  // inverse pivots of the current panel
   __shared__ double Dg[KB * KB];  // lookahead: the next panel's diagonal block (column-major, ld KB)
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  // warp index broadcast from lane 0: provably warp-uniform for the compiler, so the warp-specialised
+  // branches (diagonal block on warp 0) keep their shuffles and MMAs on the converged fast path
+  const int tid = threadIdx.x, lane = tid & 31, warp = __shfl_sync(0xffffffffu, tid >> 5, 0);
   for (int i = tid; i < L; i += K5_THREADS) { bl[i] = bt.l[i]; bm[i] = bt.m[i]; bn[i] = bt.n[i]; }
   __syncthreads();
 
@@ -255,19 +257,18 @@ __global__ void __launch_bounds__(NT, NT == 512 ? 1 : (NT == 256 ? 2 : (NT == 12
               if (dinv[j] > 0.0 && !(sjj >= smin_sh)) smin_sh = sjj;  // also catches NaN
             }
             row[c] = lane == c ? p : row[c] * inv;
-            if (p > 0.0) {
-              // L[c2][c] from lane c2, 8 shuffles in flight before their FMAs (a shuffle->FMA pair per
-              // column entry would serialise on the shuffle latency)
+            // L[c2][c] from lane c2, 8 shuffles in flight before their FMAs (a shuffle->FMA pair per
+            // column entry would serialise on the shuffle latency); branch-free: a rejected column has
+            // row[c] = 0 on every lane, so its update adds zeros
 #pragma unroll
-              for (int b0 = c + 1; b0 < KB; b0 += 8) {
-                double l2[8];
+            for (int b0 = c + 1; b0 < KB; b0 += 8) {
+              double l2[8];
 #pragma unroll
-                for (int k = 0; k < 8; ++k)
-                  if (b0 + k < KB) l2[k] = __shfl_sync(0xffffffffu, row[c], b0 + k);
+              for (int k = 0; k < 8; ++k)
+                if (b0 + k < KB) l2[k] = __shfl_sync(0xffffffffu, row[c], b0 + k);
 #pragma unroll
-                for (int k = 0; k < 8; ++k)
-                  if (b0 + k < KB && lane >= b0 + k) row[b0 + k] -= row[c] * l2[k];
-              }
+              for (int k = 0; k < 8; ++k)
+                if (b0 + k < KB) row[b0 + k] = fma(lane >= b0 + k ? -row[c] : 0.0, l2[k], row[b0 + k]);
             }
           }
         }
@@ -400,16 +401,14 @@ __global__ void __launch_bounds__(NT, NT == 512 ? 1 : (NT == 256 ? 2 : (NT == 12
               pb[u] = Pn + (k0 - j0) + fc + fr * LDP;
             }
 #pragma unroll
-            for (int c = 0; c < KB; c += 4) {
-              if (c < bw) {  // columns past bw (last panel) enter as zeros
-                const bool in = c + fr < bw;
+            for (int c = 0; c < KB; c += 4) {  // columns past bw (last panel) enter as zeros
+              const bool in = c + fr < bw;
 #pragma unroll
-                for (int u = 0; u < TPW; ++u) {
-                  const double a = in ? pa[u][c * LDP] : 0.0;
-                  const double b = in ? pb[u][c * LDP] : 0.0;
-                  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
-                               : "+d"(d0[u]), "+d"(d1[u]) : "d"(a), "d"(b));
-                }
+              for (int u = 0; u < TPW; ++u) {
+                const double a = in ? pa[u][c * LDP] : 0.0;
+                const double b = in ? pb[u][c * LDP] : 0.0;
+                asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+                             : "+d"(d0[u]), "+d"(d1[u]) : "d"(a), "d"(b));
               }
             }
 #pragma unroll
@@ -557,6 +556,409 @@ __global__ void __launch_bounds__(NT, NT == 512 ? 1 : (NT == 256 ? 2 : (NT == 12
   K5T_PRINT
 }
 
+// ---- K5 resident variant (p <= 9): the whole bordered packed factor lives in shared memory ---------------
+// Same arithmetic, order of updates, pivots and rejections as k_solve (so the same results up to the
+// summation order of the DMMA tiles), but no panel copy and no global round trips: the diagonal block,
+// the row solve and the DMMA trailing update all work in place on the packed rows in shared memory
+// (𝓛 = 165: 111 KB -> 2 CTAs per SM; 𝓛 = 84: 29 KB -> 7).  The factor is copied to global memory once,
+// coalesced, for the refinement solves (mode 1 copies it back).  To fit two 𝓛 = 165 factors per SM the
+// moments are read through L1 (the node's K values are the only gather) and the pivots are read back
+// from the factor's diagonal (a rejected column's diagonal entry is 0).
+template <int P>
+struct K5Res {
+  using S = K5Shape<P>;
+  static constexpr int L = S::L, K = S::K;
+  static constexpr int64_t NAB = S::NAB;
+  // dinv, sy [L each] | A[NAB] (16-byte aligned) | exponents
+  static constexpr size_t A_OFF = ((2 * (size_t)L) + 1) & ~size_t(1);
+  static constexpr size_t SMEM = (A_OFF + (size_t)NAB + 2) * sizeof(double) + 3 * L + 16;
+  static constexpr bool fits = SMEM <= 227 * 1024;
+};
+template <int P>
+constexpr int k5r_threads() { return rank3(P) >= 120 ? 256 : (rank3(P) >= 56 ? 128 : 64); }
+template <int P>
+constexpr int k5r_minb() {
+  constexpr size_t per = K5Res<P>::SMEM + 1024;
+  constexpr int bys = (int)((228 * 1024) / per);
+  constexpr int byt = 65536 / (k5r_threads<P>() * 128);  // >= 128 registers: the diagonal block row[32] unspilled
+  constexpr int b = bys < byt ? bys : byt;
+  return b < 1 ? 1 : (b > 8 ? 8 : b);
+}
+
+template <int P, int NT>
+__global__ void __launch_bounds__(NT, k5r_minb<P>())
+    k_solve_res(const double* __restrict__ mom, int mode, const double* __restrict__ segrhs,
+                double* __restrict__ delta, NodeTable nt, int64_t first, int64_t count, double* __restrict__ fac,
+                const __grid_constant__ BasisTab bt, double delta2, double refine2, double refine_fill,
+                double mom_tol, int64_t n_root, double defer_tau, int64_t* __restrict__ nflag) {
+  using R = K5Res<P>;
+  constexpr int Q = 2 * P, K = R::K, L = R::L;
+  constexpr int NW = NT / 32;
+  extern __shared__ __align__(16) double sm[];
+  double* dinv = sm;
+  double* sy = dinv + L;
+  double* A = sm + R::A_OFF;  // packed lower rows 0..L-1 (row i at tri(i)), RHS row L at tri(L)
+  uint8_t* bl = reinterpret_cast<uint8_t*>(A + R::NAB + 2);
+  uint8_t* bm = bl + L;
+  uint8_t* bn = bm + L;
+  __shared__ double smin_sh, ynorm_sh;
+  __shared__ double errw[NW];
+  __shared__ double sinv[KB];
+  // warp index broadcast from lane 0: provably warp-uniform for the compiler, so the warp-specialised
+  // branches (diagonal block on warp 0) keep their shuffles and MMAs on the converged fast path
+  const int tid = threadIdx.x, lane = tid & 31, warp = __shfl_sync(0xffffffffu, tid >> 5, 0);
+  for (int i = tid; i < L; i += NT) { bl[i] = bt.l[i]; bm[i] = bt.m[i]; bn[i] = bt.n[i]; }
+  __syncthreads();
+  auto tri = [](int i) { return i * (i + 1) / 2; };  // 32-bit row offsets (NAB < 2^31)
+  constexpr int K5_THREADS = NT;
+  (void)K5_THREADS;
+  K5T_DECL
+
+  for (int64_t node = blockIdx.x; node < count; node += gridDim.x) {
+    K5T(6)
+    if (mode == 1 && !(nt.flag[first + node] & 2)) continue;
+    if (mode == 2 && !(nt.flag[first + node] & 4)) continue;
+    double* Ag = fac + node * R::NAB;
+    const double* mp = mom + node * (int64_t)(2 * K + L);
+    const double* bndg = mp + K + L;
+    if (tid == 0) smin_sh = INFINITY;
+    const double m000 = __ldg(mp);
+    if (mode == 0 && !(m000 > 0.0)) {  // below the moment tree (M_000 = 0): accumulate directly
+      if (tid == 0) {
+        nt.flag[first + node] = 4;
+        atomicAdd(reinterpret_cast<unsigned long long*>(nflag + 1), 1ull);
+      }
+      __syncthreads();
+      continue;
+    }
+    for (int i = tid; i < L; i += NT) {
+      const double m2 = __ldg(mp + basis_index(Q, 2 * bl[i], 2 * bm[i], 2 * bn[i]));
+      const double di = m2 > 0.0 ? 1.0 / sqrt(m2) : 0.0;
+      dinv[i] = di;
+      double b;
+      if (mode == 1) {
+        b = 0.0;
+        for (int o = 0; o < 8; ++o) b += segrhs[(node * 8 + o) * (L + 1) + i];
+      } else {
+        b = mp[K + i];
+      }
+      sy[i] = b * di;
+    }
+    __syncthreads();
+
+    if (mode == 1) {
+      // ---- refinement: the stored factor back into shared memory, forward substitution ----------
+      for (int64_t e = tid; e < R::NAB; e += NT) A[e] = Ag[e];
+      __syncthreads();
+      for (int j0 = 0; j0 < L; j0 += KB) {
+        const int j1 = min(j0 + KB, L);
+        for (int i = j0 + warp; i < j1; i += NW) {
+          const double* Ai = A + tri(i);
+          double v = 0.0;
+          for (int k = lane; k < j0; k += 32) v = fma(Ai[k], sy[k], v);
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+          if (lane == 0) sy[i] -= v;
+        }
+        __syncthreads();
+        if (warp == 0) {
+          for (int i = j0; i < j1; ++i) {
+            const double* Ai = A + tri(i);
+            double v = 0.0;
+            for (int k = j0 + lane; k < i; k += 32) v = fma(Ai[k], sy[k], v);
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+            const double pi = A[tri(i) + i];
+            if (lane == 0) sy[i] = pi > 0.0 ? (sy[i] - v) / pi : 0.0;
+            __syncwarp();
+          }
+        }
+        __syncthreads();
+      }
+    } else {
+      // ---- assemble the equilibrated Gram + RHS row in shared memory; moments' rounding bound -------
+      double errl = 0.0;
+      for (int i = warp; i <= L; i += NW) {
+        double* Ai = A + tri(i);
+        if (i == L) {
+          for (int k = lane; k < L; k += 32) Ai[k] = sy[k];
+          continue;
+        }
+        const int li = bl[i], mi = bm[i], ni = bn[i];
+        const double di = dinv[i];
+        for (int k = lane; k <= i; k += 32) {
+          const int gi = basis_index(Q, li + bl[k], mi + bm[k], ni + bn[k]);
+          const double dd = di * dinv[k];
+          Ai[k] = __ldg(mp + gi) * dd;
+          if (mode == 0) errl = fmax(errl, __ldg(bndg + gi) * dd);
+        }
+      }
+      if (mode == 0) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) errl = fmax(errl, __shfl_xor_sync(0xffffffffu, errl, o));
+        if (lane == 0) errw[warp] = errl;
+      }
+      __syncthreads();
+      if (mode == 0) {
+        double em = 0.0;
+        for (int w = 0; w < NW; ++w) em = fmax(em, errw[w]);
+        if (!(em <= mom_tol)) {
+          if (tid == 0) {
+            nt.flag[first + node] = 4;
+            atomicAdd(reinterpret_cast<unsigned long long*>(nflag + 1), 1ull);
+          }
+          __syncthreads();
+          continue;
+        }
+      }
+      K5T(0)
+      // ---- blocked right-looking Cholesky in place, column rejection, RHS row carried along --------
+      // diagonal block of columns jb..jb+bwd-1: warp 0, lane = row, the row in registers (shuffles)
+      auto diag = [&](int jb, int bwd) {
+        double row[KB];
+        const double* Ar = A + tri(jb + lane) + jb;
+#pragma unroll
+        for (int c = 0; c < KB; ++c) row[c] = (c <= lane && lane < bwd) ? Ar[c] : 0.0;
+#pragma unroll
+        for (int c = 0; c < KB; ++c) {
+          if (c < bwd) {
+            const int j = jb + c;
+            const double sjj = __shfl_sync(0xffffffffu, row[c], c);
+            const bool keep = dinv[j] > 0.0 && sjj > delta2;
+            const double inv = keep ? rsqrt(sjj) : 0.0;
+            const double p = keep ? sjj * inv : 0.0;
+            if (lane == 0) {
+              sinv[c] = inv;
+              if (dinv[j] > 0.0 && !(sjj >= smin_sh)) smin_sh = sjj;
+            }
+            row[c] = lane == c ? p : row[c] * inv;
+#pragma unroll
+            for (int b0 = c + 1; b0 < KB; b0 += 8) {
+              double l2[8];
+#pragma unroll
+              for (int k = 0; k < 8; ++k)
+                if (b0 + k < KB) l2[k] = __shfl_sync(0xffffffffu, row[c], b0 + k);
+#pragma unroll
+              for (int k = 0; k < 8; ++k)
+                if (b0 + k < KB) row[b0 + k] = fma(lane >= b0 + k ? -row[c] : 0.0, l2[k], row[b0 + k]);
+            }
+          }
+        }
+        if (lane < bwd) {
+          double* Aw = A + tri(jb + lane) + jb;
+#pragma unroll
+          for (int c = 0; c < KB; ++c)
+            if (c <= lane) Aw[c] = row[c];
+        }
+      };
+      // DMMA update of 8x8 tiles t in [t_lo, t_hi) of the trailing lower triangle rows/cols >= j1 by the
+      // panel columns j0..j0+bw-1 (tile (ti, tk), tk <= ti, rows j1+8ti.., cols j1+8tk..)
+      constexpr int TPW = 4;
+      const int fr = lane & 3, fc = lane >> 2;
+      auto trailing = [&](int j0, int bw, int j1, int t_lo, int t_hi, int wid, int nwk, bool skip_next, int iend) {
+        for (int t0 = t_lo + wid * TPW; t0 < t_hi; t0 += nwk * TPW) {
+          int ci[TPW], ck0[TPW];
+          bool v0[TPW], v1[TPW];
+          double d0[TPW], d1[TPW];
+          const double* pa[TPW];
+          const double* pb[TPW];
+#pragma unroll
+          for (int u = 0; u < TPW; ++u) {
+            const int t = min(t0 + u, t_hi - 1);
+            int ti = (int)((sqrt(8.0 * (double)t + 1.0) - 1.0) * 0.5);
+            while ((ti + 1) * (ti + 2) / 2 <= t) ++ti;
+            while (ti * (ti + 1) / 2 > t) --ti;
+            const int tk = t - ti * (ti + 1) / 2;
+            const int i0 = j1 + 8 * ti, k0 = j1 + 8 * tk;
+            ci[u] = i0 + fc;
+            ck0[u] = k0 + 2 * fr;
+            const bool own = t0 + u < t_hi && !(skip_next && i0 + 7 < iend);
+            v0[u] = own && ci[u] <= L && ck0[u] < L && (ck0[u] <= ci[u] || ci[u] == L);
+            v1[u] = own && ci[u] <= L && ck0[u] + 1 < L && (ck0[u] + 1 <= ci[u] || ci[u] == L);
+            d0[u] = d1[u] = 0.0;
+            // fragment rows (clamped into the matrix; rows past L are masked at the store)
+            const int ra = min(i0 + fc, L), rb = min(k0 + fc, L);
+            pa[u] = A + tri(ra) + j0 + fr;
+            pb[u] = A + tri(rb) + j0 + fr;
+          }
+#pragma unroll
+          for (int c = 0; c < KB; c += 4) {  // columns past bw (last panel) enter as zeros
+            const bool in = c + fr < bw;
+#pragma unroll
+            for (int u = 0; u < TPW; ++u) {
+              const double a = in ? pa[u][c] : 0.0;
+              const double b = in ? pb[u][c] : 0.0;
+              asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+                           : "+d"(d0[u]), "+d"(d1[u]) : "d"(a), "d"(b));
+            }
+          }
+#pragma unroll
+          for (int u = 0; u < TPW; ++u) {
+            if (v0[u]) A[tri(ci[u]) + ck0[u]] -= d0[u];
+            if (v1[u]) A[tri(ci[u]) + ck0[u] + 1] -= d1[u];
+          }
+        }
+      };
+      constexpr bool kLook = NW >= 4;
+      bool dg_ready = false;
+      for (int j0 = 0; j0 < L; j0 += KB) {
+        const int bw = min(KB, L - j0), j1 = j0 + bw;
+        if (!dg_ready && warp == 0) diag(j0, bw);  // else: factored by the lookahead (sinv set)
+        __syncthreads();
+        K5T(2)
+        // rows below the diagonal block (RHS row included): x = A_r L_diag⁻ᵀ, thread per row
+        for (int r = j1 + tid; r <= L; r += NT) {
+          double* Ar = A + tri(r) + j0;
+          double x[KB];
+#pragma unroll
+          for (int c = 0; c < KB; ++c) x[c] = c < bw ? Ar[c] : 0.0;
+#pragma unroll
+          for (int c = 0; c < KB; ++c) {
+            if (c < bw) {
+              const double inv = sinv[c];
+              const double lc = x[c] * inv;
+              x[c] = lc;
+              if (inv > 0.0) {
+#pragma unroll
+                for (int c2 = c + 1; c2 < KB; ++c2)
+                  if (c2 < bw) x[c2] -= lc * A[tri(j0 + c2) + j0 + c];
+              }
+            }
+          }
+#pragma unroll
+          for (int c = 0; c < KB; ++c)
+            if (c < bw) Ar[c] = x[c];
+        }
+        __syncthreads();
+        K5T(3)
+        if (j1 < L) {
+          const int R2 = L + 1 - j1;
+          const int nt8 = (R2 + 7) / 8;
+          const int ntile = nt8 * (nt8 + 1) / 2;
+          const int bw2 = min(KB, L - j1);
+          if (kLook) {
+            // the next diagonal block's tiles first (rows j1..j1+bw2-1: tiles ti < 4), then warp 0
+            // factors it while the other warps update the rest
+            const int nd8 = (bw2 + 7) / 8;
+            const int ndt = nd8 * (nd8 + 1) / 2;
+            trailing(j0, bw, j1, 0, ndt, warp, NW, false, 0);
+            __syncthreads();
+            if (warp == 0) diag(j1, bw2);
+            else trailing(j0, bw, j1, ndt, ntile, warp - 1, NW - 1, false, 0);
+          } else {
+            trailing(j0, bw, j1, 0, ntile, warp, NW, false, 0);
+          }
+          dg_ready = kLook;
+        }
+        __syncthreads();
+        K5T(4)
+      }
+      // y = row L of the factored bordered matrix; ‖y‖² = bᵀG⁻¹b
+      double yy = 0.0;
+      for (int i = tid; i < L; i += NT) {
+        const double v = A[tri(L) + i];
+        sy[i] = v;
+        yy = fma(v, v, yy);
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) yy += __shfl_xor_sync(0xffffffffu, yy, o);
+      if (lane == 0) errw[warp] = yy;
+      // the factor to global memory for the refinement solves (coalesced, off the critical path)
+      for (int64_t e = tid; e < R::NAB; e += NT) Ag[e] = A[e];
+      __syncthreads();
+      if (tid == 0) {
+        double t = 0.0;
+        for (int w = 0; w < NW; ++w) t += errw[w];
+        ynorm_sh = t;
+      }
+    }
+
+    // ---- back substitution R̃ c̃ = y in place (R̃ = factorᵀ), blocked from the bottom ------------------
+    {
+      auto solve_diag = [&](int j0, int bw) {
+        double yv = lane < bw ? sy[j0 + lane] : 0.0;
+        const double pd = lane < bw ? A[tri(j0 + lane) + j0 + lane] : 0.0;
+        const double pl = pd > 0.0 ? 1.0 / pd : 0.0;
+        for (int j = bw - 1; j >= 0; --j) {
+          const double cj = __shfl_sync(0xffffffffu, pl > 0.0 ? yv * pl : 0.0, j);
+          if (lane < j) yv -= A[tri(j0 + j) + j0 + lane] * cj;
+          if (lane == j) yv = cj;
+        }
+        if (lane < bw) sy[j0 + lane] = yv;
+      };
+      auto gemv = [&](int j0, int bw, int klo, int khi, int t, int T) {
+        for (int k = klo + t; k < khi; k += T) {
+          double v = 0.0;
+#pragma unroll
+          for (int q = 0; q < KB; ++q)
+            if (q < bw) v = fma(A[tri(j0 + q) + k], sy[j0 + q], v);
+          sy[k] -= v;
+        }
+      };
+      int j1 = L, j0 = max(0, L - KB);
+      if (warp == 0) solve_diag(j0, j1 - j0);
+      __syncthreads();
+      while (j0 > 0) {
+        const int bw = j1 - j0, jn0 = max(0, j0 - KB);
+        gemv(j0, bw, jn0, j0, tid, NT);  // the next block's rows first
+        __syncthreads();
+        if (NW > 1) {
+          if (warp == 0) solve_diag(jn0, j0 - jn0);
+          else gemv(j0, bw, 0, jn0, tid - 32, NT - 32);
+        } else {
+          solve_diag(jn0, j0 - jn0);
+          gemv(j0, bw, 0, jn0, tid, NT);
+        }
+        __syncthreads();
+        j1 = j0;
+        j0 = jn0;
+      }
+    }
+
+    K5T(5)
+    double* out = nt.coef + (first + node) * (int64_t)L;
+    if (mode == 1) {
+      for (int i = tid; i < L; i += NT) {
+        const double d = sy[i] * dinv[i];
+        delta[node * (int64_t)L + i] = d;
+        out[i] += d;
+      }
+      __syncthreads();
+      continue;
+    }
+    for (int i = tid; i < L; i += NT) out[i] = sy[i] * dinv[i];
+    if (tid == 0) {
+      int rk = 0;
+      double mn = INFINITY;
+      for (int i = 0; i < L; ++i) {
+        const double pi = A[tri(i) + i];
+        if (pi > 0.0) { ++rk; mn = fmin(mn, pi); }
+      }
+      nt.rank[first + node] = rk;
+      nt.minpiv[first + node] = rk ? mn : 0.0;
+      const int32_t par = nt.parent[first + node];
+      const int4 cc = nt.cell[first + node];
+      const double npts = par < 0 ? (double)n_root
+                                  : (double)nt.child_n[(int64_t)par * 8 + ((cc.x & 1) | ((cc.y & 1) << 1) | ((cc.z & 1) << 2))];
+      const bool refine = refine2 > 0.0 && (smin_sh < refine2 || npts < refine_fill * L);
+      const int fl = (smin_sh < kQrFlagPivot2) ? 1 : (refine ? 2 : 0);
+      int defer = 0;
+      if (isinf(defer_tau)) {
+        defer = 8;
+      } else if (par >= 0 && defer_tau > 0.0) {
+        const int oc = (cc.x & 1) | ((cc.y & 1) << 1) | ((cc.z & 1) << 2);
+        const double e_post2 = fmax(nt.child_ss[(int64_t)par * 8 + oc] - ynorm_sh, 0.0) / fmax(npts, 1.0);
+        defer = e_post2 < defer_tau * defer_tau ? 8 : 0;
+      }
+      nt.flag[first + node] = fl | defer;
+      if (fl == 2) atomicAdd(reinterpret_cast<unsigned long long*>(nflag), 1ull);
+      if (defer) atomicAdd(reinterpret_cast<unsigned long long*>(nflag + 2), 1ull);
+    }
+    __syncthreads();
+  }
+  K5T_PRINT
+}
+
 }  // namespace
 
 template <int P>
@@ -588,6 +990,22 @@ void level_solve(const LevelCtx& c, const double* mom, int mode, const double* s
   if (grid <= 0) return;
   if (mode != 1) prof_units(KID_SOLVE, c.count);  // nodes factored (𝓛³/3 + 3𝓛² flop each)
   const int kid = mode == 1 ? KID_REFINE_SOLVE : KID_SOLVE;
+  if constexpr (K5Res<P>::fits) {
+    // shared-memory-resident factor (p <= 9); FMI_K5_RES=0 selects the global-memory kernel
+    static const bool use_res = [] {
+      const char* e = std::getenv("FMI_K5_RES");
+      const bool on = !(e && std::atoi(e) == 0);
+      if (on) FMI_CK(cudaFuncSetAttribute(k_solve_res<P, k5r_threads<P>()>,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)K5Res<P>::SMEM));
+      return on;
+    }();
+    if (use_res) {
+      FMI_LAUNCH(kid, s, (k_solve_res<P, k5r_threads<P>()>), (unsigned)grid, k5r_threads<P>(), K5Res<P>::SMEM, mom,
+                 mode, segrhs, delta, c.nt, c.first, c.count, fac, bt, kDelta * kDelta, refine2, refine_fill,
+                 kMomentTol, n_root, defer_tau, nflag);
+      return;
+    }
+  }
 #define K5_ARGS mom, mode, segrhs, delta, c.nt, c.first, c.count, fac, bt, kDelta * kDelta, refine2, refine_fill, \
                 kMomentTol, n_root, defer_tau, nflag
   if (grid <= tiny_max) {  // latency-bound levels (the top of every tree): more warps per node
