@@ -556,6 +556,60 @@ __global__ void __launch_bounds__(NT, NT == 512 ? 1 : (NT == 256 ? 2 : (NT == 12
   K5T_PRINT
 }
 
+// 1/sqrt(x) for the Schur pivots (x in (delta², ~1]: no special operands): the hardware approximation
+// and one third-order Newton step, branch-free (the library rsqrt carries a slow-path call)
+__device__ __forceinline__ double rsqrt_pivot(double x) {
+  double r;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  const double e = fma(-x, r * r, 1.0);
+  return fma(fma(e, 0.375, 0.5), r * e, r);
+}
+
+// Cholesky with column rejection (G9) of a KR x KR diagonal block held one row per lane (row[c], c <= lane;
+// rows >= bwd and entries c > lane are zero), software-pipelined: right after column c is scaled, column
+// c+1 takes its update and its pivot (shuffle + reciprocal square root) is started, and the remaining
+// columns' updates are issued behind it; no branches and no stores inside the loop.  Each lane keeps the
+// pivot quantities of its own column (myinv: 1/p or 0; mys: the Schur pivot s_cc, for the minimum).
+template <int KR>
+__device__ __forceinline__ void chol_block(double (&row)[KR], int bwd, const double* __restrict__ dv, double delta2,
+                                           int lane, double& myinv, double& mys) {
+  auto pivot = [&](int c, double sjj, double& inv, double& p) {
+    const bool keep = c < bwd && dv[c] > 0.0 && sjj > delta2;
+    const double r = rsqrt_pivot(keep ? sjj : 1.0);
+    inv = keep ? r : 0.0;
+    p = keep ? sjj * r : 0.0;
+  };
+  double sjj = __shfl_sync(0xffffffffu, row[0], 0), inv, p;
+  pivot(0, sjj, inv, p);
+  myinv = 0.0;
+  mys = INFINITY;
+#pragma unroll
+  for (int c = 0; c < KR; ++c) {
+    if (lane == c) { myinv = inv; mys = sjj; }
+    row[c] = lane == c ? p : row[c] * inv;
+    double sjj_n = 0.0, inv_n = 0.0, p_n = 0.0;
+    if (c + 1 < KR) {
+      const double l = __shfl_sync(0xffffffffu, row[c], c + 1);
+      row[c + 1] = fma(lane >= c + 1 ? -row[c] : 0.0, l, row[c + 1]);
+      sjj_n = __shfl_sync(0xffffffffu, row[c + 1], c + 1);
+      pivot(c + 1, sjj_n, inv_n, p_n);
+    }
+#pragma unroll
+    for (int b0 = c + 2; b0 < KR; b0 += 8) {
+      double l2[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+        if (b0 + k < KR) l2[k] = __shfl_sync(0xffffffffu, row[c], b0 + k);
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+        if (b0 + k < KR) row[b0 + k] = fma(lane >= b0 + k ? -row[c] : 0.0, l2[k], row[b0 + k]);
+    }
+    sjj = sjj_n;
+    inv = inv_n;
+    p = p_n;
+  }
+}
+
 // ---- K5 resident variant (p <= 9): the whole bordered packed factor lives in shared memory ---------------
 // Same arithmetic, order of updates, pivots and rejections as k_solve (so the same results up to the
 // summation order of the DMMA tiles), but no panel copy and no global round trips: the diagonal block,
@@ -719,31 +773,17 @@ __global__ void __launch_bounds__(NT, k5r_minb<P>())
         const double* Ar = A + tri(jb + lane) + jb;
 #pragma unroll
         for (int c = 0; c < KB; ++c) row[c] = (c <= lane && lane < bwd) ? Ar[c] : 0.0;
+        double myinv, mys;
+        chol_block<KB>(row, bwd, dinv + jb, delta2, lane, myinv, mys);
+        // smallest Schur pivot of a non-zero column (NaN-propagating, as the unblocked rule)
+        double v = (lane < bwd && dinv[jb + lane] > 0.0) ? mys : INFINITY;
 #pragma unroll
-        for (int c = 0; c < KB; ++c) {
-          if (c < bwd) {
-            const int j = jb + c;
-            const double sjj = __shfl_sync(0xffffffffu, row[c], c);
-            const bool keep = dinv[j] > 0.0 && sjj > delta2;
-            const double inv = keep ? rsqrt(sjj) : 0.0;
-            const double p = keep ? sjj * inv : 0.0;
-            if (lane == 0) {
-              sinv[c] = inv;
-              if (dinv[j] > 0.0 && !(sjj >= smin_sh)) smin_sh = sjj;
-            }
-            row[c] = lane == c ? p : row[c] * inv;
-#pragma unroll
-            for (int b0 = c + 1; b0 < KB; b0 += 8) {
-              double l2[8];
-#pragma unroll
-              for (int k = 0; k < 8; ++k)
-                if (b0 + k < KB) l2[k] = __shfl_sync(0xffffffffu, row[c], b0 + k);
-#pragma unroll
-              for (int k = 0; k < 8; ++k)
-                if (b0 + k < KB) row[b0 + k] = fma(lane >= b0 + k ? -row[c] : 0.0, l2[k], row[b0 + k]);
-            }
-          }
+        for (int o = 16; o > 0; o >>= 1) {
+          const double w = __shfl_xor_sync(0xffffffffu, v, o);
+          v = (w < v || w != w) ? w : v;
         }
+        if (lane < bwd) sinv[lane] = myinv;
+        if (lane == 0 && !(v >= smin_sh)) smin_sh = v;
         if (lane < bwd) {
           double* Aw = A + tri(jb + lane) + jb;
 #pragma unroll
@@ -813,17 +853,16 @@ __global__ void __launch_bounds__(NT, k5r_minb<P>())
 #pragma unroll
           for (int c = 0; c < KB; ++c) x[c] = c < bw ? Ar[c] : 0.0;
 #pragma unroll
-          for (int c = 0; c < KB; ++c) {
-            if (c < bw) {
-              const double inv = sinv[c];
-              const double lc = x[c] * inv;
-              x[c] = lc;
-              if (inv > 0.0) {
+          for (int c2 = 0; c2 < KB; ++c2) {
+            // left-looking order of the same updates: x[c2] -= x[c] L[c2][c] for c = 0..c2-1 (the order of
+            // the right-looking loop), then the scaling; row c2 of the diagonal block is contiguous, so the
+            // loads share one base register (no per-row address registers, no spills); branch-free: a
+            // rejected column has inv = 0, x = 0
+            const double* Lr = A + tri(min(j0 + c2, L)) + j0;
+            double acc = x[c2];
 #pragma unroll
-                for (int c2 = c + 1; c2 < KB; ++c2)
-                  if (c2 < bw) x[c2] -= lc * A[tri(j0 + c2) + j0 + c];
-              }
-            }
+            for (int c = 0; c < c2; ++c) acc = fma(-x[c], Lr[c], acc);
+            x[c2] = c2 < bw ? acc * sinv[c2] : 0.0;
           }
 #pragma unroll
           for (int c = 0; c < KB; ++c)
