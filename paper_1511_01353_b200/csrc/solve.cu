@@ -72,6 +72,60 @@ __host__ __device__ constexpr int64_t tri(int i) { return (int64_t)i * (i + 1) /
 #define K5T_PRINT
 #endif
 
+// 1/sqrt(x) for the Schur pivots (x in (delta², ~1]: no special operands): the hardware approximation
+// and one third-order Newton step, branch-free (the library rsqrt carries a slow-path call)
+__device__ __forceinline__ double rsqrt_pivot(double x) {
+  double r;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  const double e = fma(-x, r * r, 1.0);
+  return fma(fma(e, 0.375, 0.5), r * e, r);
+}
+
+// Cholesky with column rejection (G9) of a KR x KR diagonal block held one row per lane (row[c], c <= lane;
+// rows >= bwd and entries c > lane are zero), software-pipelined: right after column c is scaled, column
+// c+1 takes its update and its pivot (shuffle + reciprocal square root) is started, and the remaining
+// columns' updates are issued behind it; no branches and no stores inside the loop.  Each lane keeps the
+// pivot quantities of its own column (myinv: 1/p or 0; mys: the Schur pivot s_cc, for the minimum).
+template <int KR>
+__device__ __forceinline__ void chol_block(double (&row)[KR], int bwd, const double* __restrict__ dv, double delta2,
+                                           int lane, double& myinv, double& mys) {
+  auto pivot = [&](int c, double sjj, double& inv, double& p) {
+    const bool keep = c < bwd && dv[c] > 0.0 && sjj > delta2;
+    const double r = rsqrt_pivot(keep ? sjj : 1.0);
+    inv = keep ? r : 0.0;
+    p = keep ? sjj * r : 0.0;
+  };
+  double sjj = __shfl_sync(0xffffffffu, row[0], 0), inv, p;
+  pivot(0, sjj, inv, p);
+  myinv = 0.0;
+  mys = INFINITY;
+#pragma unroll
+  for (int c = 0; c < KR; ++c) {
+    if (lane == c) { myinv = inv; mys = sjj; }
+    row[c] = lane == c ? p : row[c] * inv;
+    double sjj_n = 0.0, inv_n = 0.0, p_n = 0.0;
+    if (c + 1 < KR) {
+      const double l = __shfl_sync(0xffffffffu, row[c], c + 1);
+      row[c + 1] = fma(lane >= c + 1 ? -row[c] : 0.0, l, row[c + 1]);
+      sjj_n = __shfl_sync(0xffffffffu, row[c + 1], c + 1);
+      pivot(c + 1, sjj_n, inv_n, p_n);
+    }
+#pragma unroll
+    for (int b0 = c + 2; b0 < KR; b0 += 8) {
+      double l2[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+        if (b0 + k < KR) l2[k] = __shfl_sync(0xffffffffu, row[c], b0 + k);
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+        if (b0 + k < KR) row[b0 + k] = fma(lane >= b0 + k ? -row[c] : 0.0, l2[k], row[b0 + k]);
+    }
+    sjj = sjj_n;
+    inv = inv_n;
+    p = p_n;
+  }
+}
+
 template <int P>
 struct K5Shape {
   static constexpr int Q = 2 * P;
@@ -236,46 +290,27 @@ __global__ void __launch_bounds__(NT, NT == 512 ? 1 : (NT == 256 ? 2 : (NT == 12
       K5T(0)
       // ---- blocked right-looking Cholesky with column rejection, RHS row carried along ---------
       auto diag = [&](double* buf, int ld, int jb, int bwd) {
-        // diagonal block: unblocked Cholesky with column rejection by warp 0, lane = row, the row in
-        // registers; column entries travel by shuffles (no shared-memory round trips)
+        // diagonal block: Cholesky with column rejection by warp 0, lane = row, the row in registers
+        // (chol_block: software-pipelined pivots, shuffles, no shared-memory round trips)
         double row[KB];
 #pragma unroll
         for (int c = 0; c < KB; ++c) row[c] = (c <= lane && lane < bwd) ? buf[c * ld + lane] : 0.0;
+        double myinv, mys;
+        chol_block<KB>(row, bwd, dinv + jb, delta2, lane, myinv, mys);
+        double v = (lane < bwd && dinv[jb + lane] > 0.0) ? mys : INFINITY;
 #pragma unroll
-        for (int c = 0; c < KB; ++c) {
-          if (c < bwd) {
-            const int j = jb + c;
-            const double sjj = __shfl_sync(0xffffffffu, row[c], c);
-            const bool keep = dinv[j] > 0.0 && sjj > delta2;
-            // one reciprocal square root on the column-to-column critical path (p = sjj·rsqrt(sjj))
-            const double inv = keep ? rsqrt(sjj) : 0.0;
-            const double p = keep ? sjj * inv : 0.0;
-            if (lane == 0) {
-              piv[j] = p;
-              sinv[c] = inv;
-              pinv[j] = inv;
-              if (dinv[j] > 0.0 && !(sjj >= smin_sh)) smin_sh = sjj;  // also catches NaN
-            }
-            row[c] = lane == c ? p : row[c] * inv;
-            // L[c2][c] from lane c2, 8 shuffles in flight before their FMAs (a shuffle->FMA pair per
-            // column entry would serialise on the shuffle latency); branch-free: a rejected column has
-            // row[c] = 0 on every lane, so its update adds zeros
-#pragma unroll
-            for (int b0 = c + 1; b0 < KB; b0 += 8) {
-              double l2[8];
-#pragma unroll
-              for (int k = 0; k < 8; ++k)
-                if (b0 + k < KB) l2[k] = __shfl_sync(0xffffffffu, row[c], b0 + k);
-#pragma unroll
-              for (int k = 0; k < 8; ++k)
-                if (b0 + k < KB) row[b0 + k] = fma(lane >= b0 + k ? -row[c] : 0.0, l2[k], row[b0 + k]);
-            }
-          }
+        for (int o = 16; o > 0; o >>= 1) {
+          const double w = __shfl_xor_sync(0xffffffffu, v, o);
+          v = (w < v || w != w) ? w : v;
         }
+        if (lane == 0 && !(v >= smin_sh)) smin_sh = v;
         if (lane < bwd) {
 #pragma unroll
           for (int c = 0; c < KB; ++c)
             if (c <= lane) buf[c * ld + lane] = row[c];
+          sinv[lane] = myinv;
+          pinv[jb + lane] = myinv;
+          piv[jb + lane] = buf[lane * ld + lane];  // this lane's pivot p (its own store)
         }
       };
       bool dg_ready = false;  // Dg holds the factored diagonal block of the current panel
@@ -554,60 +589,6 @@ __global__ void __launch_bounds__(NT, NT == 512 ? 1 : (NT == 256 ? 2 : (NT == 12
     __syncthreads();
   }
   K5T_PRINT
-}
-
-// 1/sqrt(x) for the Schur pivots (x in (delta², ~1]: no special operands): the hardware approximation
-// and one third-order Newton step, branch-free (the library rsqrt carries a slow-path call)
-__device__ __forceinline__ double rsqrt_pivot(double x) {
-  double r;
-  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
-  const double e = fma(-x, r * r, 1.0);
-  return fma(fma(e, 0.375, 0.5), r * e, r);
-}
-
-// Cholesky with column rejection (G9) of a KR x KR diagonal block held one row per lane (row[c], c <= lane;
-// rows >= bwd and entries c > lane are zero), software-pipelined: right after column c is scaled, column
-// c+1 takes its update and its pivot (shuffle + reciprocal square root) is started, and the remaining
-// columns' updates are issued behind it; no branches and no stores inside the loop.  Each lane keeps the
-// pivot quantities of its own column (myinv: 1/p or 0; mys: the Schur pivot s_cc, for the minimum).
-template <int KR>
-__device__ __forceinline__ void chol_block(double (&row)[KR], int bwd, const double* __restrict__ dv, double delta2,
-                                           int lane, double& myinv, double& mys) {
-  auto pivot = [&](int c, double sjj, double& inv, double& p) {
-    const bool keep = c < bwd && dv[c] > 0.0 && sjj > delta2;
-    const double r = rsqrt_pivot(keep ? sjj : 1.0);
-    inv = keep ? r : 0.0;
-    p = keep ? sjj * r : 0.0;
-  };
-  double sjj = __shfl_sync(0xffffffffu, row[0], 0), inv, p;
-  pivot(0, sjj, inv, p);
-  myinv = 0.0;
-  mys = INFINITY;
-#pragma unroll
-  for (int c = 0; c < KR; ++c) {
-    if (lane == c) { myinv = inv; mys = sjj; }
-    row[c] = lane == c ? p : row[c] * inv;
-    double sjj_n = 0.0, inv_n = 0.0, p_n = 0.0;
-    if (c + 1 < KR) {
-      const double l = __shfl_sync(0xffffffffu, row[c], c + 1);
-      row[c + 1] = fma(lane >= c + 1 ? -row[c] : 0.0, l, row[c + 1]);
-      sjj_n = __shfl_sync(0xffffffffu, row[c + 1], c + 1);
-      pivot(c + 1, sjj_n, inv_n, p_n);
-    }
-#pragma unroll
-    for (int b0 = c + 2; b0 < KR; b0 += 8) {
-      double l2[8];
-#pragma unroll
-      for (int k = 0; k < 8; ++k)
-        if (b0 + k < KR) l2[k] = __shfl_sync(0xffffffffu, row[c], b0 + k);
-#pragma unroll
-      for (int k = 0; k < 8; ++k)
-        if (b0 + k < KR) row[b0 + k] = fma(lane >= b0 + k ? -row[c] : 0.0, l2[k], row[b0 + k]);
-    }
-    sjj = sjj_n;
-    inv = inv_n;
-    p = p_n;
-  }
 }
 
 // ---- K5 resident variant (p <= 9): the whole bordered packed factor lives in shared memory ---------------
