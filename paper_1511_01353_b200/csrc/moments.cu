@@ -146,6 +146,46 @@ __global__ void __launch_bounds__(256) k_moments_reduce(const double* __restrict
   }
 }
 
+// Few nodes (a huge root re-accumulated directly): the chunk range of each node is cut into KR_SLICES
+// fixed slices, CTA (node, slice, entry block) sums its slice in chunk order into slice partials, and
+// k_slices_reduce adds the slices in order — the same fixed summation order every run.
+constexpr int KR_SLICES = 64;
+__global__ void __launch_bounds__(256) k_moments_reduce_sliced(const double* __restrict__ partial,
+                                                               const int64_t* __restrict__ chunk_begin,
+                                                               const int64_t* __restrict__ nchunks, int64_t nodes,
+                                                               int rpn, int K, const int32_t* __restrict__ flag,
+                                                               int bit, double* __restrict__ slices) {
+  const int64_t node = blockIdx.x;
+  const int sl = blockIdx.y;
+  if (flag && !(flag[node] & bit)) return;
+  const int64_t c0 = chunk_begin[node * rpn];
+  const int64_t c1 = node + 1 < nodes ? chunk_begin[(node + 1) * rpn] : *nchunks;
+  const int64_t n = c1 - c0;
+  const int64_t a = c0 + n * sl / KR_SLICES, b = c0 + n * (sl + 1) / KR_SLICES;
+  const int e = blockIdx.z * blockDim.x + threadIdx.x;
+  if (e >= K) return;
+  double s[4] = {0, 0, 0, 0};
+  int64_t ci = a;
+  for (; ci + 4 <= b; ci += 4) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) s[k] += partial[(ci + k) * K + e];
+  }
+  for (; ci < b; ++ci) s[0] += partial[ci * K + e];
+  slices[(node * KR_SLICES + sl) * (int64_t)K + e] = (s[0] + s[1]) + (s[2] + s[3]);
+}
+
+__global__ void k_slices_reduce(const double* __restrict__ slices, int64_t nodes, int K,
+                                const int32_t* __restrict__ flag, int bit, double* __restrict__ out, int64_t stride) {
+  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= nodes * K) return;
+  const int64_t node = g / K;
+  const int e = (int)(g % K);
+  if (flag && !(flag[node] & bit)) return;
+  double t = 0.0;
+  for (int sl = 0; sl < KR_SLICES; ++sl) t += slices[(node * KR_SLICES + sl) * (int64_t)K + e];
+  out[node * stride + e] = t;
+}
+
 }  // namespace
 
 template <int P>
@@ -161,6 +201,15 @@ void direct_moments(const double* ux, const double* uy, const double* uz, const 
 void reduce_moments(const double* partial, const int64_t* chunk_begin, const int64_t* nchunks_dev, int64_t nodes,
                     int rpn, int K, const int32_t* flag, int bit, double* out, int64_t stride, cudaStream_t s) {
   if (nodes <= 0) return;
+  if (nodes <= 16) {  // too few CTAs for the per-node reduction: slice the chunk ranges (cfg 4 root: 1.6 ms)
+    DBuf<double> slices((size_t)nodes * KR_SLICES * K, s);
+    FMI_LAUNCH(KID_MOMENTS_REDUCE, s, k_moments_reduce_sliced,
+               dim3((unsigned)nodes, (unsigned)KR_SLICES, (unsigned)((K + 255) / 256)), 256, 0, partial, chunk_begin,
+               nchunks_dev, nodes, rpn, K, flag, bit, slices.p);
+    FMI_LAUNCH(KID_MOMENTS_REDUCE, s, k_slices_reduce, (unsigned)((nodes * K + 255) / 256), 256, 0, slices.p, nodes,
+               K, flag, bit, out, stride);
+    return;
+  }
   FMI_LAUNCH(KID_MOMENTS_REDUCE, s, k_moments_reduce, (unsigned)nodes, 256, 0, partial, chunk_begin, nchunks_dev, nodes,
              rpn, K, flag, bit, out, stride);
 }

@@ -13,6 +13,7 @@
 // One CTA per flagged node; the (𝓛+1) × (𝓛+1+QB) work matrix lives in a per-CTA global scratch slot
 // (L2-resident).  Non-flagged nodes exit immediately.
 #include <algorithm>
+#include <mutex>
 
 #include "horner.cuh"
 
@@ -21,7 +22,18 @@ namespace fmi {
 namespace {
 
 constexpr int KQ_THREADS = 256;
-constexpr int QB = 64;  // points per TSQR block
+// points per TSQR block: 128 when the shared-memory work matrix still fits (fewer, longer reflector
+// steps: the step cost is dominated by its reduction latency), else 64
+__host__ __device__ constexpr int qb_of(int p) {
+  return (size_t)(rank3(p) + 1) * (rank3(p) + 1 + 128) * sizeof(double) <= 200 * 1024 ? 128 : 64;
+}
+
+// dynamic shared memory of the work matrix (0: global scratch)
+__host__ __device__ constexpr size_t qr_smem_bytes(int p) {
+  return (size_t)(rank3(p) + 1) * (rank3(p) + 1 + qb_of(p)) * sizeof(double) <= 200 * 1024
+             ? (size_t)(rank3(p) + 1) * (rank3(p) + 1 + qb_of(p)) * sizeof(double)
+             : 0;
+}
 
 struct BasisTabQ {
   uint8_t l[286], m[286], n[286];
@@ -56,6 +68,7 @@ __global__ void __launch_bounds__(KQ_THREADS)
                const double* __restrict__ mom, double* __restrict__ scratch, const __grid_constant__ BasisTabQ bt,
                double delta) {
   constexpr int Q = 2 * P, K = rank3(Q), L = rank3(P), LA = L + 1;
+  constexpr int QB = qb_of(P);
   constexpr int LD = LA + QB;  // leading dimension (rows) of the column-major work matrix
   __shared__ double dinv[LA];
   __shared__ double v[LD];
@@ -63,7 +76,12 @@ __global__ void __launch_bounds__(KQ_THREADS)
   __shared__ int kept[L];
   __shared__ double piv[L];
   __shared__ double sol[L];
-  double* A = scratch + (int64_t)blockIdx.x * LA * LD;
+  // the work matrix in shared memory when it fits (p <= 7: 𝓛 = 84 -> 101 KB), else in the CTA's global
+  // scratch slot (L2-resident): every reflector step is a chain of dependent accesses, so the on-chip copy
+  // cuts its latency several-fold
+  constexpr bool kSmem = qr_smem_bytes(P) > 0;
+  extern __shared__ __align__(16) double qsm[];
+  double* A = kSmem ? qsm : scratch + (int64_t)blockIdx.x * LA * LD;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   constexpr int NWARP = KQ_THREADS / 32;
   __shared__ uint8_t bl[L], bm[L], bn[L];
@@ -126,16 +144,34 @@ __global__ void __launch_bounds__(KQ_THREADS)
         const double beta = 2.0 / vtv;
         for (int i = tid; i < QB; i += KQ_THREADS) v[i] = Aj[LA + i];
         __syncthreads();
-        for (int c = j + 1 + warp; c < LA; c += NWARP) {
-          double* Ac = A + (int64_t)c * LD;
-          double w = 0.0;
-          for (int i = lane; i < QB; i += 32) w += v[i] * Ac[LA + i];
+        // four columns per warp at a time: their dot products and shuffle reductions overlap
+        for (int c0 = j + 1 + warp; c0 < LA; c0 += 4 * NWARP) {
+          double w[4];
 #pragma unroll
-          for (int o = 16; o > 0; o >>= 1) w += __shfl_xor_sync(0xffffffffu, w, o);
-          w += v0 * Ac[j];
-          const double bw = beta * w;
-          for (int i = lane; i < QB; i += 32) Ac[LA + i] -= bw * v[i];
-          if (lane == 0) Ac[j] -= bw * v0;
+          for (int u = 0; u < 4; ++u) {
+            const int c = c0 + u * NWARP;
+            w[u] = 0.0;
+            if (c < LA) {
+              const double* Ac = A + (int64_t)c * LD;
+#pragma unroll
+              for (int i = lane; i < QB; i += 32) w[u] += v[i] * Ac[LA + i];
+            }
+          }
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+            for (int u = 0; u < 4; ++u) w[u] += __shfl_xor_sync(0xffffffffu, w[u], o);
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int c = c0 + u * NWARP;
+            if (c < LA) {
+              double* Ac = A + (int64_t)c * LD;
+              const double bw = beta * (w[u] + v0 * Ac[j]);
+#pragma unroll
+              for (int i = lane; i < QB; i += 32) Ac[LA + i] -= bw * v[i];
+              if (lane == 0) Ac[j] -= bw * v0;
+            }
+          }
         }
         __syncthreads();
         if (tid == 0) Aj[j] = alpha;
@@ -212,15 +248,20 @@ __global__ void __launch_bounds__(KQ_THREADS)
 
 size_t solve_qr_scratch_per_cta(int p) {
   const int L = rank3(p), LA = L + 1;
-  return (size_t)LA * (LA + QB) * sizeof(double);
+  return (size_t)LA * (LA + qb_of(p)) * sizeof(double);
 }
 
 template <int P>
 void level_solve_qr(const LevelCtx& c, const double* mom, double* scratch, int64_t slots, cudaStream_t s) {
   static const BasisTabQ bt = make_basis_q<P>();
+  constexpr size_t smem = qr_smem_bytes(P);
+  static std::once_flag attr_once;
+  std::call_once(attr_once, [] {
+    if (smem > 0) FMI_CK(cudaFuncSetAttribute(k_solve_qr<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  });
   const int64_t grid = std::min<int64_t>(c.count, slots);
   if (grid <= 0) return;
-  FMI_LAUNCH(KID_SOLVE_QR, s, k_solve_qr<P>, (unsigned)grid, KQ_THREADS, 0, c.ux, c.uy, c.uz, c.r, c.nt, c.first,
+  FMI_LAUNCH(KID_SOLVE_QR, s, k_solve_qr<P>, (unsigned)grid, KQ_THREADS, smem, c.ux, c.uy, c.uz, c.r, c.nt, c.first,
              c.count, mom, scratch, bt, kDelta);
 }
 
