@@ -26,6 +26,9 @@ constexpr int K4_WARPS = K4_THREADS / 32;
 #ifndef FMI_K4_LIM
 #define FMI_K4_LIM 64
 #endif
+#ifndef FMI_K4_PIPE
+#define FMI_K4_PIPE 1
+#endif
 #ifndef FMI_K4_MINB
 #define FMI_K4_MINB 1
 #endif
@@ -71,6 +74,26 @@ __device__ __forceinline__ void k4_loop(const double* __restrict__ ux, const dou
   };
 #pragma unroll
   for (int k = 0; k < PD; ++k) issue(ck.start + k, k);
+#if FMI_K4_PIPE
+  // the next point's local coordinates are read while the current point is accumulated (the ring-load
+  // and frame latency leave the FMA stream's critical path)
+  asm volatile("cp.async.wait_group %0;" ::"n"(PD - 1) : "memory");
+  double x = to_local(rg[lane], fr.cx, fr.scale), y = to_local(rg[32 + lane], fr.cy, fr.scale),
+         z = to_local(rg[64 + lane], fr.cz, fr.scale);
+  int t = 0;
+#pragma unroll 1
+  for (int64_t i = ck.start; i < ck.end; ++i) {
+    issue(i + PD, (t + PD) % R);
+    t = (t + 1 == R) ? 0 : t + 1;
+    asm volatile("cp.async.wait_group %0;" ::"n"(PD - 1) : "memory");
+    const double* sp = rg + t * 96 + lane;
+    const double xn = sp[0], yn = sp[32], zn = sp[64];
+    grp::accum<Q, K4_LIM, 0, g>(x, y, z, 1.0, acc);
+    x = to_local(xn, fr.cx, fr.scale);
+    y = to_local(yn, fr.cy, fr.scale);
+    z = to_local(zn, fr.cz, fr.scale);
+  }
+#else
   int t = 0;
 #pragma unroll 1
   for (int64_t i = ck.start; i < ck.end; ++i, t = (t + 1 == R) ? 0 : t + 1) {
@@ -82,6 +105,7 @@ __device__ __forceinline__ void k4_loop(const double* __restrict__ ux, const dou
     issue(i + PD, (t + PD) % R);
     grp::accum<Q, K4_LIM, 0, g>(x, y, z, 1.0, acc);
   }
+#endif
   double* o = out + grp::out_begin(Q, K4_LIM, 0, g);
 #pragma unroll
   for (int k = 0; k < n; ++k) o[k] = acc[k];
