@@ -263,8 +263,10 @@ def kernel_work(cfg, levels_points, depth_max: int, projected=None, units=None):
         # 4 SoA doubles (32 B) written
         "gather": ("byte", 68 * N),
     }
-    if "sort" in units:   # 8-bit passes actually executed: 8 B (histogram) + 12 B read + 12 B written per item
-        w["sort"] = ("byte", 32 * units["sort"])
+    if "sort" in units:   # bytes of the 8-bit passes actually executed, counted by the library: per item the key
+        # read by the histogram + key and index read and written by the scatter (32 B with 64-bit keys,
+        # 20 B with the 32-bit sort keys)
+        w["sort"] = ("byte", units["sort"])
     if "keys" in units:   # bytes counted per launch by the library (coordinates, values, keys, records)
         w["keys"] = ("byte", units["keys"])
     if "solve" in units:  # bordered Cholesky 𝓛³/3 + substitutions and assembly 3𝓛² per factored node

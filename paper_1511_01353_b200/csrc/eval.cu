@@ -160,8 +160,15 @@ __global__ void __launch_bounds__(256) k_eval(const double* __restrict__ q, cons
   uint64_t k0, k1;
   eval_fetch(q, qpk, keys, idx, i0, M, lo0, lo1, lo2, w, unit, qi0, ux0, uy0, uz0, k0);
   eval_fetch(q, qpk, keys, idx, i1, M, lo0, lo1, lo2, w, unit, qi1, ux1, uy1, uz1, k1);
-  eval_descend(i0, M, keys != nullptr, Dk, nt, ux0, uy0, uz0, k0, n0, x0, y0, z0);
-  eval_descend(i1, M, keys != nullptr, Dk, nt, ux1, uy1, uz1, k1, n1, x1, y1, z1);
+  // sorted queries without a key array (the sort moved 32-bit keys): the key from the record's
+  // root-cube coordinates, exactly as the key kernel formed it
+  if (!keys && qpk) {
+    k0 = morton_key(ux0, uy0, uz0, Dk);
+    k1 = morton_key(ux1, uy1, uz1, Dk);
+  }
+  const bool have_keys = keys != nullptr || qpk != nullptr;
+  eval_descend(i0, M, have_keys, Dk, nt, ux0, uy0, uz0, k0, n0, x0, y0, z0);
+  eval_descend(i1, M, have_keys, Dk, nt, ux1, uy1, uz1, k1, n1, x1, y1, z1);
   const int64_t node0 = __shfl_sync(0xffffffffu, n0, 0);
   const bool uniform = __all_sync(0xffffffffu, (i0 >= M || n0 == node0) && (i1 >= M || n1 == node0));
   // CTA-wide node (the usual case: a node holds thousands of sorted queries): one coefficient copy for
@@ -249,7 +256,8 @@ __global__ void __launch_bounds__(EV_THREADS, 3)
     asm volatile("cp.async.wait_group 1;" ::: "memory");  // this tile's records (the next one in flight)
     const int64_t i0 = t * EV_TILE + pos0, i1 = t * EV_TILE + pos1;
     const double4 r0 = rec[slot][pos0], r1 = rec[slot][pos1];  // each thread reads only its own records
-    const uint64_t k0 = i0 < M ? keys[i0] : 0, k1 = i1 < M ? keys[i1] : 0;
+    const uint64_t k0 = i0 < M ? (keys ? keys[i0] : morton_key(r0.x, r0.y, r0.z, Dk)) : 0;
+    const uint64_t k1 = i1 < M ? (keys ? keys[i1] : morton_key(r1.x, r1.y, r1.z, Dk)) : 0;
     const int64_t qi0 = i0 < M ? (int64_t)idx[i0] : 0, qi1 = i1 < M ? (int64_t)idx[i1] : 0;
     int64_t n0, n1;
     double x0, y0, z0, x1, y1, z1;
@@ -315,7 +323,7 @@ void eval_sorted(const double* q, const double4* qpk, const uint64_t* keys, cons
     const char* e = std::getenv("FMI_EVAL_PIPE");
     pipe_ctas = (e && std::atoi(e) > 0) ? sms * std::max(1, per) : 0;  // opt-in: measured slower (7.46 vs 6.83 ms, cfg 5)
   });
-  if (qpk && keys && idx && pipe_ctas > 0) {
+  if (qpk && idx && pipe_ctas > 0) {
     const int64_t ntiles = (M + EV_TILE - 1) / EV_TILE;
     FMI_LAUNCH(KID_EVAL, s, k_eval_pipe<P>, (unsigned)std::min<int64_t>(ntiles, pipe_ctas), EV_THREADS, smem, qpk, keys,
                idx, M, Dk, nt, out);

@@ -425,7 +425,8 @@ struct LateValues {
 
 template <int P>
 void fused_gather_root(const double4* packed, const uint32_t* perm, const double* f, int* bad, int64_t N,
-                       double* ux, double* uy, double* uz, double* r, double* root_b, cudaStream_t s);
+                       double* ux, double* uy, double* uz, double* r, double* root_b, cudaStream_t s,
+                       uint64_t* keys = nullptr, int D = 0);
 
 // Level-synchronous build:
 //  A. moment tree: every cell with >= 𝓛 points down to max_depth (integer guards of P:306 + G5,
@@ -730,7 +731,8 @@ void run_levels(fmi_tree* T, const uint64_t* keys, double* ux, double* uy, doubl
 // the gather of the sorted points fused with the root projection (single-GPU builds): chunks over [0, N)
 template <int P>
 void fused_gather_root(const double4* packed, const uint32_t* perm, const double* f, int* bad, int64_t N,
-                       double* ux, double* uy, double* uz, double* r, double* root_b, cudaStream_t s) {
+                       double* ux, double* uy, double* uz, double* r, double* root_b, cudaStream_t s, uint64_t* keys,
+                       int D) {
   constexpr int L = rank3(P);
   DBuf<int64_t> se(2, s), counts(1, s), begin(1, s), nch(1, s);
   FMI_LAUNCH(KID_MISC, s, k_fill_range, 1, 1, 0, se.p, N);
@@ -740,7 +742,7 @@ void fused_gather_root(const double4* packed, const uint32_t* perm, const double
   DBuf<double> partial((size_t)maxc * (L + 1), s);
   make_chunks(se.p, se.p + 1, 1, ch, counts.p, begin.p, nch.p, chunks.p, maxc, s);
   gather_root_projection<P>(packed, perm, f, bad, N, ux, uy, uz, r, chunks.p, nch.p, maxc, begin.p, partial.p,
-                            root_b, s);
+                            root_b, s, keys, D);
 }
 
 // the QR path (unscoped.cu) — every node fitted by the paper's QR through
@@ -961,7 +963,7 @@ fmi_tree* build_impl(const double* pts, const double* f, int64_t N, int degree, 
     // reach depth Dsort (clustered data), run_levels throws KeysShort and the sort is redone over all
     // levels.  Sharded builds take Dsort from the global point count, at least one level below the
     // shard depth, and agree on the retry collectively (run_levels).
-    DBuf<uint64_t> keys(N, s), ktmp(N, s);
+    DBuf<uint64_t> keys(N, s), ktmp;  // ktmp: the 64-bit sort only
     DBuf<uint32_t> perm(N, s), ptmp(N, s);
     DBuf<double4> packed(N, s);
     DBuf<double> ux(N, s), uy(N, s), uz(N, s), r(N, s);
@@ -983,9 +985,24 @@ fmi_tree* build_impl(const double* pts, const double* f, int64_t N, int degree, 
       FMI_CK(cudaMemsetAsync(fbad.p, 0, sizeof(int), s));
     }
     for (;;) {
-      morton_keys(dpts, N, T->lo, T->width, T->unit, T->Dk, keys.p, perm.p, s, late_f ? nullptr : df, packed.p);
-      tmark("keys", s);
-      radix_sort_pairs(keys.p, perm.p, ktmp.p, ptmp.p, N, 3 * T->Dk, s, 3 * (T->Dk - Dsort));
+      // the sorted key bits fit 32 bits (3·Dsort <= 32; every single-GPU and space-filling case): sort
+      // 32-bit keys (20 B per item and pass instead of 32) in the two halves of the key buffer, and let
+      // the gather recompute the full 64-bit keys from the gathered coordinates
+      const bool key32 = 3 * Dsort <= 32;
+      uint64_t* kout = key32 ? keys.p : nullptr;  // gathers write the full keys (sorted order)
+      if (key32) {
+        uint32_t* k32 = reinterpret_cast<uint32_t*>(keys.p);
+        uint32_t* k32tmp = k32 + N;
+        morton_keys(dpts, N, T->lo, T->width, T->unit, T->Dk, nullptr, perm.p, s, late_f ? nullptr : df, packed.p,
+                    k32, 3 * (T->Dk - Dsort));
+        tmark("keys", s);
+        radix_sort_pairs32(k32, perm.p, k32tmp, ptmp.p, N, 3 * Dsort, s);
+      } else {
+        morton_keys(dpts, N, T->lo, T->width, T->unit, T->Dk, keys.p, perm.p, s, late_f ? nullptr : df, packed.p);
+        tmark("keys", s);
+        ktmp.ensure(N, s);
+        radix_sort_pairs(keys.p, perm.p, ktmp.p, ptmp.p, N, 3 * T->Dk, s, 3 * (T->Dk - Dsort));
+      }
       T->Dsorted = Dsort;
       tmark("sort", s);
       // single-GPU level path: the gather fused with the root projection (it needs no tree)
@@ -994,19 +1011,20 @@ fmi_tree* build_impl(const double* pts, const double* f, int64_t N, int degree, 
       LateValues late{packed.p, perm.p, df, fbad.p, side.e_f};
       const bool late_levels = late_f && fuse_root;  // values join inside run_levels (after K4/M2M)
       if (late_levels) {
-        gather_points(packed.p, perm.p, N, ux.p, uy.p, uz.p, r.p, s);  // coordinates now (r: placeholder)
+        gather_points(packed.p, perm.p, N, ux.p, uy.p, uz.p, r.p, s, nullptr, nullptr, kout,
+                      T->Dk);  // coordinates now (r: placeholder)
       } else if (late_f) {
         FMI_CK(cudaStreamWaitEvent(s, side.e_f, 0));
-        gather_points(packed.p, perm.p, N, ux.p, uy.p, uz.p, r.p, s, df, fbad.p);
+        gather_points(packed.p, perm.p, N, ux.p, uy.p, uz.p, r.p, s, df, fbad.p, kout, T->Dk);
         int hbad = 0;
         FMI_CK(cudaMemcpyAsync(&hbad, fbad.p, sizeof(int), cudaMemcpyDeviceToHost, s));
         FMI_CK(cudaStreamSynchronize(s));
         if (hbad) fail(FMI_EINPUT, "non-finite coordinate or value");
       } else if (fuse_root) {
         FMI_DISPATCH(degree, fused_gather_root, packed.p, perm.p, nullptr, nullptr, N, ux.p, uy.p, uz.p, r.p, rootb.p,
-                     s);
+                     s, kout, T->Dk);
       } else {
-        gather_points(packed.p, perm.p, N, ux.p, uy.p, uz.p, r.p, s);
+        gather_points(packed.p, perm.p, N, ux.p, uy.p, uz.p, r.p, s, nullptr, nullptr, kout, T->Dk);
       }
       tmark("gather", s);
       try {
@@ -1053,12 +1071,21 @@ void eval_device(const fmi_tree* T, const double* dq, int64_t m, double* dout, c
   if (Dk == 0) {
     FMI_DISPATCH14(T->p, run_eval, T, dq, nullptr, nullptr, nullptr, m, 0, dout, s);
   } else {
-    DBuf<uint64_t> keys(m, s), ktmp(m, s);
     DBuf<uint32_t> idx(m, s), itmp(m, s);
     DBuf<double4> qpk(m, s);
-    morton_keys(dq, m, T->lo, T->width, T->unit, Dk, keys.p, idx.p, s, nullptr, qpk.p);
-    radix_sort_pairs(keys.p, idx.p, ktmp.p, itmp.p, m, 3 * Dk, s);
-    FMI_DISPATCH14(T->p, run_eval, T, dq, qpk.p, keys.p, idx.p, m, Dk, dout, s);
+    if (3 * Dk <= 32) {  // 32-bit sort keys; K7 recomputes each key from the query's record
+      DBuf<uint32_t> k32(m, s), k32tmp(m, s);
+      morton_keys(dq, m, T->lo, T->width, T->unit, Dk, nullptr, idx.p, s, nullptr, qpk.p, k32.p, 0);
+      radix_sort_pairs32(k32.p, idx.p, k32tmp.p, itmp.p, m, 3 * Dk, s);
+      k32.release();
+      k32tmp.release();
+      FMI_DISPATCH14(T->p, run_eval, T, dq, qpk.p, nullptr, idx.p, m, Dk, dout, s);
+    } else {
+      DBuf<uint64_t> keys(m, s), ktmp(m, s);
+      morton_keys(dq, m, T->lo, T->width, T->unit, Dk, keys.p, idx.p, s, nullptr, qpk.p);
+      radix_sort_pairs(keys.p, idx.p, ktmp.p, itmp.p, m, 3 * Dk, s);
+      FMI_DISPATCH14(T->p, run_eval, T, dq, qpk.p, keys.p, idx.p, m, Dk, dout, s);
+    }
   }
 }
 

@@ -76,6 +76,31 @@ void dist_comm_allreduce(void* dev, int64_t n, int dtype, cudaStream_t s);  // i
   } while (0)
 
 // ---------------------------------------------------------------------------------------------
+// Morton key of a root-cube unit coordinate (K1): q* = min(floor(u*·2^D), 2^D - 1) with an
+// exact power-of-two scaling (reading G7/G18), bits interleaved x fastest (octant o = bx + 2by + 4bz).
+// Shared by the key kernel and by the kernels that recompute keys from gathered coordinates.
+// ---------------------------------------------------------------------------------------------
+__device__ __forceinline__ uint64_t morton_spread3(uint64_t v) {
+  v &= 0x1fffffull;
+  v = (v | (v << 32)) & 0x1f00000000ffffull;
+  v = (v | (v << 16)) & 0x1f0000ff0000ffull;
+  v = (v | (v << 8)) & 0x100f00f00f00f00full;
+  v = (v | (v << 4)) & 0x10c30c30c30c30c3ull;
+  v = (v | (v << 2)) & 0x1249249249249249ull;
+  return v;
+}
+__device__ __forceinline__ uint64_t morton_quantize(double u, int D) {
+  const double scale = (double)(1ull << D);
+  double t = floor(__dmul_rn(u, scale));  // exact power-of-two scaling, no contraction
+  t = fmin(fmax(t, 0.0), scale - 1.0);    // u = 1 -> top cell; outside queries are clamped
+  return (uint64_t)t;
+}
+__device__ __forceinline__ uint64_t morton_key(double ux, double uy, double uz, int D) {
+  return morton_spread3(morton_quantize(ux, D)) | (morton_spread3(morton_quantize(uy, D)) << 1) |
+         (morton_spread3(morton_quantize(uz, D)) << 2);
+}
+
+// ---------------------------------------------------------------------------------------------
 // stream-ordered device buffers
 // ---------------------------------------------------------------------------------------------
 void* dmalloc(size_t bytes, cudaStream_t s);
@@ -145,16 +170,23 @@ void exclusive_scan_i64(const int64_t* in, int64_t* out, int64_t n, int64_t* tot
 void bbox_and_check(const double* pts, int64_t n, double* out8 /*device: min3,max3,nonfinite,unused*/,
                     const double* f, cudaStream_t s);
 // f/packed (fit points): also write the 32-byte records (u_x, u_y, u_z, f) read by gather_points
+// keys32 (optional): write the sort key (key >> bit_lo, < 2^32) instead of the 64-bit key (keys unused)
 void morton_keys(const double* pts, int64_t n, const double lo[3], double width, bool unit, int D, uint64_t* keys,
-                 uint32_t* idx, cudaStream_t s, const double* f = nullptr, double4* packed = nullptr);
+                 uint32_t* idx, cudaStream_t s, const double* f = nullptr, double4* packed = nullptr,
+                 uint32_t* keys32 = nullptr, int bit_lo = 0);
 // LSD radix sort of (keys, vals) by key bits [bit_lo, nbits), stable.  On return keys/vals point at the
 // sorted data and keys_tmp/vals_tmp at the scratch (the pointers may have been swapped).
 void radix_sort_pairs(uint64_t*& keys, uint32_t*& vals, uint64_t*& keys_tmp, uint32_t*& vals_tmp, int64_t n,
                       int nbits, cudaStream_t s, int bit_lo = 0);
+// the same over 32-bit sort keys (bits [0, nbits)): 20 B per item and pass instead of 32
+void radix_sort_pairs32(uint32_t*& keys, uint32_t*& vals, uint32_t*& keys_tmp, uint32_t*& vals_tmp, int64_t n,
+                        int nbits, cudaStream_t s);
 // f (optional): take the values from f[perm[i]] instead of the records (values uploaded after the keys
 // were built); *bad is set if one is non-finite
+// keys (optional): also write the 64-bit Morton keys (D levels) recomputed from the gathered coordinates
 void gather_points(const double4* packed, const uint32_t* perm, int64_t n, double* ux, double* uy, double* uz,
-                   double* r, cudaStream_t s, const double* f = nullptr, int* bad = nullptr);
+                   double* r, cudaStream_t s, const double* f = nullptr, int* bad = nullptr,
+                   uint64_t* keys = nullptr, int D = 0);
 
 // sharded build helpers (keys.cu): depth-s cell histogram, partition by owner shard, scatter
 void cell_counts(const double* pts, int64_t n, const double lo[3], double width, bool unit, int s, int64_t* counts,
@@ -256,7 +288,7 @@ template <int P> void gather_root_projection(const double4* packed, const uint32
                                              int64_t n, double* ux, double* uy, double* uz, double* r,
                                              const Chunk* chunks, const int64_t* nchunks_dev, int64_t max_chunks,
                                              const int64_t* chunk_begin, double* partial, double* segsum,
-                                             cudaStream_t s);
+                                             cudaStream_t s, uint64_t* keys = nullptr, int D = 0);
 // child projections of a node are deferred (flag bit 3) when its predicted post-fit RMS (pre-fit energy
 // minus the energy the fit removes) is below kDeferTheta·τ: its children are then unlikely to be
 // created, and the projection pass runs only for those that are

@@ -88,15 +88,8 @@ __global__ void __launch_bounds__(BB_THREADS) k_bbox_final(const double* __restr
 // ------------------------------------------------------------------------------------------------
 // K1 Morton keys
 // ------------------------------------------------------------------------------------------------
-__device__ __forceinline__ uint64_t spread3(uint64_t v) {
-  v &= 0x1fffffull;
-  v = (v | (v << 32)) & 0x1f00000000ffffull;
-  v = (v | (v << 16)) & 0x1f0000ff0000ffull;
-  v = (v | (v << 8)) & 0x100f00f00f00f00full;
-  v = (v | (v << 4)) & 0x10c30c30c30c30c3ull;
-  v = (v | (v << 2)) & 0x1249249249249249ull;
-  return v;
-}
+__device__ __forceinline__ uint64_t spread3(uint64_t v) { return morton_spread3(v); }
+__device__ __forceinline__ uint64_t quantize(double u, int D) { return morton_quantize(u, D); }
 
 // root-cube unit coordinate: (x - lo) / W, one IEEE subtraction and one division (same as the
 // oracle's to_unit); identity for the unit cube.
@@ -104,27 +97,22 @@ __device__ __forceinline__ double to_unit(double x, double lo, double w, bool un
   return unit ? x : __ddiv_rn(__dsub_rn(x, lo), w);
 }
 
-__device__ __forceinline__ uint64_t quantize(double u, int D) {
-  const double scale = (double)(1ull << D);
-  double t = floor(__dmul_rn(u, scale));       // exact power-of-two scaling, no contraction
-  const double top = scale - 1.0;
-  t = fmin(fmax(t, 0.0), top);                 // u = 1 -> top cell; outside queries are clamped
-  return (uint64_t)t;
-}
-
 // packed != nullptr (fit points): also write (u_x, u_y, u_z, f) as one 32-byte record, so that the
 // Morton-order gather reads ONE aligned sector per point instead of scattered pieces of pts and f.
+// keys32 != nullptr: the 32-bit sort key (the key bits from bit_lo up) instead of the 64-bit key.
 __global__ void __launch_bounds__(256) k_keys(const double* __restrict__ pts, int64_t n, double lo0, double lo1,
                                               double lo2, double w, bool unit, int D, uint64_t* __restrict__ keys,
                                               uint32_t* __restrict__ idx, const double* __restrict__ f,
-                                              double4* __restrict__ packed) {
+                                              double4* __restrict__ packed, uint32_t* __restrict__ keys32,
+                                              int bit_lo) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   double ux = to_unit(pts[3 * i + 0], lo0, w, unit);
   double uy = to_unit(pts[3 * i + 1], lo1, w, unit);
   double uz = to_unit(pts[3 * i + 2], lo2, w, unit);
-  uint64_t k = spread3(quantize(ux, D)) | (spread3(quantize(uy, D)) << 1) | (spread3(quantize(uz, D)) << 2);
-  keys[i] = k;
+  const uint64_t k = morton_key(ux, uy, uz, D);
+  if (keys32) keys32[i] = (uint32_t)(k >> bit_lo);
+  else keys[i] = k;
   idx[i] = (uint32_t)i;
   if (packed) packed[i] = make_double4(ux, uy, uz, f ? f[i] : 0.0);
 }
@@ -138,9 +126,12 @@ constexpr int RS_WARPS = RS_THREADS / 32;
 constexpr int RS_ITEMS = 12;
 constexpr int RS_TILE = RS_THREADS * RS_ITEMS;  // 3072 (12 items/thread: 64 registers, 4 CTAs/SM)
 constexpr int RS_WARP_ITEMS = RS_TILE / RS_WARPS; // 384 (in-warp ranks fit 16 bits)
-constexpr size_t kScatterSmem = (size_t)RS_TILE * (sizeof(uint64_t) + sizeof(uint32_t));
+template <typename KT>
+constexpr size_t scatter_smem() { return (size_t)RS_TILE * (sizeof(KT) + sizeof(uint32_t)); }
 
-__global__ void __launch_bounds__(RS_THREADS) k_rs_hist(const uint64_t* __restrict__ keys, int64_t n, int shift,
+// KT = uint64_t (full Morton keys) or uint32_t (the sorted key bits only: less traffic per pass)
+template <typename KT>
+__global__ void __launch_bounds__(RS_THREADS) k_rs_hist(const KT* __restrict__ keys, int64_t n, int shift,
                                                         int64_t nblk, int64_t* __restrict__ counts) {
   __shared__ int hist[256];
   hist[threadIdx.x] = 0;
@@ -163,16 +154,17 @@ __global__ void __launch_bounds__(RS_THREADS) k_rs_hist(const uint64_t* __restri
 // Downsweep: stable rank of every item of the tile (per-warp match.any ranking + prefix over warps and
 // digits), the tile is rearranged in shared memory in digit order, then written out so that
 // consecutive threads store consecutive positions of each digit's global run (coalesced).
-__global__ void __launch_bounds__(RS_THREADS, 4) k_rs_scatter(const uint64_t* __restrict__ kin,
+template <typename KT>
+__global__ void __launch_bounds__(RS_THREADS, 4) k_rs_scatter(const KT* __restrict__ kin,
                                                            const uint32_t* __restrict__ vin, int64_t n, int shift,
                                                            int64_t nblk, const int64_t* __restrict__ offs,
-                                                           uint64_t* __restrict__ kout, uint32_t* __restrict__ vout) {
+                                                           KT* __restrict__ kout, uint32_t* __restrict__ vout) {
   __shared__ int whist[RS_WARPS][257];
   __shared__ int tstart[257];           // exclusive prefix of the tile's digit counts
   __shared__ int64_t boff[256];
   extern __shared__ __align__(16) uint64_t rs_dyn[];
-  uint64_t* sk = rs_dyn;                                       // [RS_TILE]
-  uint32_t* sv = reinterpret_cast<uint32_t*>(rs_dyn + RS_TILE);  // [RS_TILE]
+  KT* sk = reinterpret_cast<KT*>(rs_dyn);                           // [RS_TILE]
+  uint32_t* sv = reinterpret_cast<uint32_t*>(sk + RS_TILE);         // [RS_TILE]
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   for (int t = threadIdx.x; t < RS_WARPS * 257; t += RS_THREADS) (&whist[0][0])[t] = 0;
   boff[threadIdx.x] = offs[(int64_t)threadIdx.x * nblk + blockIdx.x];
@@ -181,7 +173,7 @@ __global__ void __launch_bounds__(RS_THREADS, 4) k_rs_scatter(const uint64_t* __
   const int64_t base = tbase + (int64_t)warp * RS_WARP_ITEMS;
   const unsigned lt_mask = (1u << lane) - 1u;
   const bool full = tbase + RS_TILE <= n;  // CTA-uniform: no past-the-end items in this tile
-  uint64_t k[RS_ITEMS];  // the values are read again (L2) when the tile is rearranged: fewer registers
+  KT k[RS_ITEMS];  // the values are read again (L2) when the tile is rearranged: fewer registers
   unsigned rank2[RS_ITEMS / 2];  // in-warp ranks (< RS_WARP_ITEMS), two 16-bit halves per register
   // digit of item it (256 = past the end); recomputed from the key instead of held in registers
   auto digit = [&](int it) { return base + it * 32 + lane < n ? (int)((k[it] >> shift) & 255) : 256; };
@@ -255,7 +247,7 @@ __global__ void __launch_bounds__(RS_THREADS, 4) k_rs_scatter(const uint64_t* __
   __syncthreads();
   const int cnt = tstart[256];
   for (int pos = threadIdx.x; pos < cnt; pos += RS_THREADS) {
-    const uint64_t kk = sk[pos];
+    const KT kk = sk[pos];
     const int d = (int)((kk >> shift) & 255);
     const int64_t g = boff[d] + (pos - tstart[d]);
     kout[g] = kk;
@@ -268,7 +260,8 @@ __global__ void __launch_bounds__(RS_THREADS, 4) k_rs_scatter(const uint64_t* __
 // ------------------------------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) k_gather(const double4* __restrict__ packed, const uint32_t* __restrict__ perm,
                                                 int64_t n, double* __restrict__ ux, double* __restrict__ uy,
-                                                double* __restrict__ uz, double* __restrict__ r) {
+                                                double* __restrict__ uz, double* __restrict__ r,
+                                                uint64_t* __restrict__ keys, int D) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const double2* p = reinterpret_cast<const double2*>(packed + perm[i]);  // one 32-byte sector
@@ -277,6 +270,7 @@ __global__ void __launch_bounds__(256) k_gather(const double4* __restrict__ pack
   uy[i] = a.y;
   uz[i] = b.x;
   r[i] = b.y;
+  if (keys) keys[i] = morton_key(a.x, a.y, b.x, D);
 }
 
 // variant for values uploaded after the keys were built (fmi_build with page-locked host f): the value
@@ -284,7 +278,8 @@ __global__ void __launch_bounds__(256) k_gather(const double4* __restrict__ pack
 __global__ void __launch_bounds__(256) k_gather_f(const double4* __restrict__ packed, const uint32_t* __restrict__ perm,
                                                   const double* __restrict__ f, int64_t n, double* __restrict__ ux,
                                                   double* __restrict__ uy, double* __restrict__ uz,
-                                                  double* __restrict__ r, int* __restrict__ bad) {
+                                                  double* __restrict__ r, int* __restrict__ bad,
+                                                  uint64_t* __restrict__ keys, int D) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const uint32_t j = perm[i];
@@ -295,6 +290,7 @@ __global__ void __launch_bounds__(256) k_gather_f(const double4* __restrict__ pa
   uy[i] = a.y;
   uz[i] = b.x;
   r[i] = v;
+  if (keys) keys[i] = morton_key(a.x, a.y, b.x, D);
   if (!isfinite(v)) *bad = 1;
 }
 
@@ -384,32 +380,35 @@ void bbox_and_check(const double* pts, int64_t n, double* out8, const double* f,
 }
 
 void morton_keys(const double* pts, int64_t n, const double lo[3], double width, bool unit, int D, uint64_t* keys,
-                 uint32_t* idx, cudaStream_t s, const double* f, double4* packed) {
+                 uint32_t* idx, cudaStream_t s, const double* f, double4* packed, uint32_t* keys32, int bit_lo) {
   if (n <= 0) return;
   unsigned grid = (unsigned)((n + 255) / 256);
-  // algorithmic bytes: coordinates read (24), key + index written (12), record written (32), value read (8)
-  prof_units(KID_KEYS, n * (36 + (packed ? 32 : 0) + (f ? 8 : 0)));
-  FMI_LAUNCH(KID_KEYS, s, k_keys, grid, 256, 0, pts, n, lo[0], lo[1], lo[2], width, unit, D, keys, idx, f, packed);
+  // algorithmic bytes: coordinates read (24), key (8, or 4 for a sort key) + index (4) written, record
+  // written (32), value read (8)
+  prof_units(KID_KEYS, n * (24 + (keys32 ? 4 : 8) + 4 + (packed ? 32 : 0) + (f ? 8 : 0)));
+  FMI_LAUNCH(KID_KEYS, s, k_keys, grid, 256, 0, pts, n, lo[0], lo[1], lo[2], width, unit, D, keys, idx, f, packed,
+             keys32, bit_lo);
 }
 
-void radix_sort_pairs(uint64_t*& keys, uint32_t*& vals, uint64_t*& keys_tmp, uint32_t*& vals_tmp, int64_t n,
-                      int nbits, cudaStream_t s, int bit_lo) {
+template <typename KT>
+void radix_sort_impl(KT*& keys, uint32_t*& vals, KT*& keys_tmp, uint32_t*& vals_tmp, int64_t n, int nbits,
+                     cudaStream_t s, int bit_lo) {
   if (n <= 1 || nbits <= 0) return;
   static std::once_flag attr_once;  // one opt-in per kernel instantiation (thread-safe)
   std::call_once(attr_once, [&] {
-    FMI_CK(cudaFuncSetAttribute(
-        k_rs_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kScatterSmem));
+    FMI_CK(cudaFuncSetAttribute(k_rs_scatter<KT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)scatter_smem<KT>()));
   });
   const int64_t nblk = (n + RS_TILE - 1) / RS_TILE;
   DBuf<int64_t> counts((size_t)nblk * 256, s);
-  uint64_t* ka = keys; uint32_t* va = vals; uint64_t* kb = keys_tmp; uint32_t* vb = vals_tmp;
-  int passes = 0;
-  for (int shift = bit_lo; shift < nbits; shift += 8, ++passes) {
-    prof_units(KID_SORT, n);  // items of this pass: 8 B key read (histogram) + 12 B read + 12 B written (scatter)
-    FMI_LAUNCH(KID_SORT, s, k_rs_hist, (unsigned)nblk, RS_THREADS, 0, ka, n, shift, nblk, counts.p);
+  KT* ka = keys; uint32_t* va = vals; KT* kb = keys_tmp; uint32_t* vb = vals_tmp;
+  for (int shift = bit_lo; shift < nbits; shift += 8) {
+    // items of this pass: key read (histogram) + key and index read and written (scatter)
+    prof_units(KID_SORT, n * (int64_t)(3 * sizeof(KT) + 8));
+    FMI_LAUNCH(KID_SORT, s, k_rs_hist<KT>, (unsigned)nblk, RS_THREADS, 0, ka, n, shift, nblk, counts.p);
     exclusive_scan_i64(counts.p, counts.p, nblk * 256, nullptr, s);
-    FMI_LAUNCH(KID_SORT, s, k_rs_scatter, (unsigned)nblk, RS_THREADS, kScatterSmem, ka, va, n, shift, nblk, counts.p,
-               kb, vb);
+    FMI_LAUNCH(KID_SORT, s, k_rs_scatter<KT>, (unsigned)nblk, RS_THREADS, scatter_smem<KT>(), ka, va, n, shift, nblk,
+               counts.p, kb, vb);
     std::swap(ka, kb);
     std::swap(va, vb);
   }
@@ -417,14 +416,24 @@ void radix_sort_pairs(uint64_t*& keys, uint32_t*& vals, uint64_t*& keys_tmp, uin
   keys = ka; vals = va; keys_tmp = kb; vals_tmp = vb;
 }
 
+void radix_sort_pairs(uint64_t*& keys, uint32_t*& vals, uint64_t*& keys_tmp, uint32_t*& vals_tmp, int64_t n,
+                      int nbits, cudaStream_t s, int bit_lo) {
+  radix_sort_impl<uint64_t>(keys, vals, keys_tmp, vals_tmp, n, nbits, s, bit_lo);
+}
+
+void radix_sort_pairs32(uint32_t*& keys, uint32_t*& vals, uint32_t*& keys_tmp, uint32_t*& vals_tmp, int64_t n,
+                        int nbits, cudaStream_t s) {
+  radix_sort_impl<uint32_t>(keys, vals, keys_tmp, vals_tmp, n, nbits, s, 0);
+}
+
 void gather_points(const double4* packed, const uint32_t* perm, int64_t n, double* ux, double* uy, double* uz,
-                   double* r, cudaStream_t s, const double* f, int* bad) {
+                   double* r, cudaStream_t s, const double* f, int* bad, uint64_t* keys, int D) {
   if (n <= 0) return;
   unsigned grid = (unsigned)((n + 255) / 256);
   if (f)
-    FMI_LAUNCH(KID_GATHER, s, k_gather_f, grid, 256, 0, packed, perm, f, n, ux, uy, uz, r, bad);
+    FMI_LAUNCH(KID_GATHER, s, k_gather_f, grid, 256, 0, packed, perm, f, n, ux, uy, uz, r, bad, keys, D);
   else
-    FMI_LAUNCH(KID_GATHER, s, k_gather, grid, 256, 0, packed, perm, n, ux, uy, uz, r);
+    FMI_LAUNCH(KID_GATHER, s, k_gather, grid, 256, 0, packed, perm, n, ux, uy, uz, r, keys, D);
 }
 
 }  // namespace fmi

@@ -333,7 +333,7 @@ __global__ void __launch_bounds__(K6_THREADS, 2)
                   const double* __restrict__ f, int* __restrict__ bad, double* __restrict__ ux,
                   double* __restrict__ uy, double* __restrict__ uz, double* __restrict__ r,
                   const Chunk* __restrict__ chunks, const int64_t* __restrict__ nchunks,
-                  double* __restrict__ partial) {
+                  double* __restrict__ partial, uint64_t* __restrict__ keys, int D) {
   constexpr int L = rank3(P);
   constexpr int G = proj_groups(P);
   constexpr int SUB = K6_WARPS / G;
@@ -402,6 +402,7 @@ __global__ void __launch_bounds__(K6_THREADS, 2)
       const double R = f ? sval[(size_t)buf * BATCH + e] : rec[3];
       if (v) {
         ux[i] = X; uy[i] = Y; uz[i] = Z; r[i] = R;
+        if (keys) keys[i] = morton_key(X, Y, Z, D);  // the full key, recomputed (the sort moved 32-bit keys)
         if (f && !isfinite(R)) nbad = 1;
       }
       sx[e] = to_local(X, fc.cx, fc.scale);
@@ -520,7 +521,7 @@ template <int P>
 void gather_root_projection(const double4* packed, const uint32_t* perm, const double* f, int* bad, int64_t n,
                             double* ux, double* uy, double* uz, double* r, const Chunk* chunks,
                             const int64_t* nchunks_dev, int64_t max_chunks, const int64_t* chunk_begin,
-                            double* partial, double* segsum, cudaStream_t s) {
+                            double* partial, double* segsum, cudaStream_t s, uint64_t* keys, int D) {
   constexpr size_t smem = 2 * (size_t)(2 * K6_THREADS) * 5 * sizeof(double);
   static std::once_flag attr_once;
   std::call_once(attr_once, [&] {
@@ -528,7 +529,7 @@ void gather_root_projection(const double4* packed, const uint32_t* perm, const d
   });
   if (max_chunks > 0)
     FMI_LAUNCH(KID_PROJECT, s, k_gather_root<P>, (unsigned)max_chunks, K6_THREADS, smem, packed, perm, f, bad, ux, uy,
-               uz, r, chunks, nchunks_dev, partial);
+               uz, r, chunks, nchunks_dev, partial, keys, D);
   FMI_LAUNCH(KID_RESIDUAL_REDUCE, s, k_residual_reduce, dim3(1u, (unsigned)((rank3(P) + 1 + 31) / 32)), 256, 0,
              partial, chunk_begin, nchunks_dev, (int64_t)1, NodeTable{}, (int64_t)0, rank3(P), false, nullptr, segsum);
   (void)n;
@@ -539,7 +540,7 @@ void gather_root_projection(const double4* packed, const uint32_t* perm, const d
                                   const int64_t*, int64_t, double*, double*, cudaStream_t, const int32_t*, bool); \
   template void gather_root_projection<P>(const double4*, const uint32_t*, const double*, int*, int64_t, double*,    \
                                           double*, double*, double*, const Chunk*, const int64_t*, int64_t,           \
-                                          const int64_t*, double*, double*, cudaStream_t);
+                                          const int64_t*, double*, double*, cudaStream_t, uint64_t*, int);
 FMI_INST(0) FMI_INST(1) FMI_INST(2) FMI_INST(3) FMI_INST(4) FMI_INST(5)
 FMI_INST(6) FMI_INST(7) FMI_INST(8) FMI_INST(9) FMI_INST(10)
 #undef FMI_INST

@@ -84,16 +84,16 @@ def test_kernel_work_uses_executed_units():
     factored, key bytes from the library's own per-launch count (fmi_profile_units)."""
     cfg = workloads.CONFIGS[5]
     K, L = bench.ranks(cfg.degree)
-    units = {"sort": 3 * cfg.n + 3 * cfg.m, "solve": 4880, "keys": 76 * cfg.n + 68 * cfg.m}
+    units = {"sort": 20 * (3 * cfg.n + 2 * cfg.m), "solve": 4880, "keys": 76 * cfg.n + 68 * cfg.m}
     w = bench.kernel_work(cfg, [cfg.n], depth_max=0, projected=0, units=units)
-    assert w["sort"] == ("byte", 32 * (3 * cfg.n + 3 * cfg.m))
+    assert w["sort"] == ("byte", 20 * (3 * cfg.n + 2 * cfg.m))
     assert w["solve"] == ("flop", 4880 * (L ** 3 / 3 + 3 * L * L))
     assert w["keys"] == ("byte", 76 * cfg.n + 68 * cfg.m)
     # per-step units: the roofline divides the timed region's units by the step count
     prof = {"sort": (14.6, 12)}   # 2 steps x (3 + 3 passes) x ... launches; 7.3 ms per step
     r = bench.rooflines(cfg, [cfg.n], 0, prof, steps=2, ms_per_step=100.0, hbm_peak=6456.8,
                         units={"sort": 2 * units["sort"]})
-    per_launch = 32 * units["sort"] / 6
+    per_launch = units["sort"] / 6
     assert r["sort"]["achieved"] == pytest.approx(per_launch / (14.6e-3 / 12) / 1e9)
 
 
