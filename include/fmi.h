@@ -255,6 +255,11 @@ int fmi_profile_get(const char* kernel, double* total_ms, int64_t* launches);
 int fmi_profile_units(const char* kernel, int64_t* units);
 /* Total kernel launches issued by the library since load (or since fmi_profile_reset). */
 int64_t fmi_launch_count(void);
+/* Diagnostics (a stand-in for compute-sanitizer memcheck, which is closed on the GPU pool): with the
+ * environment variable FMI_GUARD=1 set before the first build, every library-owned device buffer gets
+ * 4 KiB guard bands (0xA5) before and after it, checked when the buffer is freed; returns the number of
+ * overwritten guard bands seen since load (each also reported on stderr).  0 when FMI_GUARD is off. */
+int64_t fmi_guard_violations(void);
 
 #ifdef __cplusplus
 }

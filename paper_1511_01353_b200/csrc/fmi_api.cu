@@ -19,6 +19,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
+#include <unordered_map>
 #include <string>
 #include <vector>
 
@@ -118,6 +119,19 @@ namespace {
 std::once_flag g_pool_once;
 }
 
+// FMI_GUARD=1 (diagnostics; compute-sanitizer is closed on the GPU pool): every library buffer gets
+// 4 KiB guard bands filled with 0xA5 before and after it; dfree checks them (an out-of-bounds write of
+// any kernel into a neighbouring allocation shows up there) and counts violations (fmi_guard_violations)
+namespace {
+constexpr size_t kGuardBytes = 4096;
+constexpr int kGuardByte = 0xA5;
+const bool g_guard = [] { const char* e = std::getenv("FMI_GUARD"); return e && std::atoi(e) > 0; }();
+std::mutex g_guard_mu;
+std::unordered_map<void*, size_t> g_guard_map;
+std::atomic<int64_t> g_guard_violations{0};
+}  // namespace
+int64_t guard_violations() { return g_guard_violations.load(); }
+
 void* dmalloc(size_t bytes, cudaStream_t s) {
   std::call_once(g_pool_once, [] {
     int dev = 0;
@@ -130,16 +144,49 @@ void* dmalloc(size_t bytes, cudaStream_t s) {
     cudaGetLastError();
   });
   void* p = nullptr;
-  cudaError_t e = cudaMallocAsync(&p, bytes, s);
+  const size_t g = g_guard ? kGuardBytes : 0;
+  cudaError_t e = cudaMallocAsync(&p, bytes + 2 * g, s);
   if (e != cudaSuccess) {
     cudaGetLastError();
     fail(FMI_ENOMEM, "device allocation of " + std::to_string(bytes) + " bytes failed: " + cudaGetErrorString(e));
   }
-  return p;
+  if (!g) return p;
+  // FMI_GUARD: guard bands before and after every library buffer, checked when it is freed
+  FMI_CK(cudaMemsetAsync(p, kGuardByte, g, s));
+  FMI_CK(cudaMemsetAsync(static_cast<char*>(p) + g + bytes, kGuardByte, g, s));
+  std::lock_guard<std::mutex> lk(g_guard_mu);
+  g_guard_map[static_cast<char*>(p) + g] = bytes;
+  return static_cast<char*>(p) + g;
 }
 
 void dfree(void* p, cudaStream_t s) {
-  if (p) cudaFreeAsync(p, s);
+  if (!p) return;
+  if (!g_guard) {
+    cudaFreeAsync(p, s);
+    return;
+  }
+  size_t bytes = 0;
+  {
+    std::lock_guard<std::mutex> lk(g_guard_mu);
+    auto it = g_guard_map.find(p);
+    if (it == g_guard_map.end()) return;  // not ours (cannot happen): leak rather than corrupt
+    bytes = it->second;
+    g_guard_map.erase(it);
+  }
+  char* base = static_cast<char*>(p) - kGuardBytes;
+  std::vector<unsigned char> h(2 * kGuardBytes);
+  cudaMemcpyAsync(h.data(), base, kGuardBytes, cudaMemcpyDeviceToHost, s);
+  cudaMemcpyAsync(h.data() + kGuardBytes, static_cast<char*>(p) + bytes, kGuardBytes, cudaMemcpyDeviceToHost, s);
+  cudaStreamSynchronize(s);
+  for (size_t i = 0; i < h.size(); ++i)
+    if (h[i] != (unsigned char)kGuardByte) {
+      g_guard_violations.fetch_add(1);
+      fprintf(stderr, "[fmi guard] %s guard of a %zu-byte buffer overwritten at byte %zd\n",
+              i < kGuardBytes ? "front" : "back", bytes,
+              i < kGuardBytes ? (ssize_t)i - (ssize_t)kGuardBytes : (ssize_t)(i - kGuardBytes));
+      break;
+    }
+  cudaFreeAsync(base, s);
 }
 
 // ------------------------------------------------------------------------------------------------
@@ -1791,5 +1838,7 @@ int fmi_profile_units(const char* kernel, int64_t* units) {
 }
 
 int64_t fmi_launch_count(void) { return g_launches.load(); }
+
+int64_t fmi_guard_violations(void) { return fmi::guard_violations(); }
 
 }  // extern "C"

@@ -104,6 +104,7 @@ __device__ __forceinline__ uint64_t morton_key(double ux, double uy, double uz, 
 // stream-ordered device buffers
 // ---------------------------------------------------------------------------------------------
 void* dmalloc(size_t bytes, cudaStream_t s);
+int64_t guard_violations();  // FMI_GUARD diagnostics (fmi_guard_violations)
 void dfree(void* p, cudaStream_t s);
 
 template <typename T>

@@ -25,6 +25,12 @@ namespace fmi {
 
 namespace {
 
+#ifndef FMI_K6_PLIM
+#define FMI_K6_PLIM 40
+#endif
+#ifndef FMI_K6_MINB
+#define FMI_K6_MINB 2
+#endif
 constexpr int K6_THREADS = 256;
 constexpr int K6_WARPS = K6_THREADS / 32;
 // points per thread in the Horner phase: 2 in the fused kernel (register budget shared with the
@@ -60,7 +66,7 @@ __host__ __device__ constexpr int pair_first(int P, int q) {  // basis index of 
 // number of output groups (a power of two dividing the warp count) with <= 40 outputs each
 __host__ __device__ constexpr int proj_groups(int P) {
   int g = 1;
-  while (g < K6_WARPS && (rank3(P) + g - 1) / g > 40) g *= 2;
+  while (g < K6_WARPS && (rank3(P) + g - 1) / g > FMI_K6_PLIM) g *= 2;
   return g;
 }
 // first pair of group g: greedy cut at cumulative outputs >= g * ceil(L/G)
@@ -149,7 +155,7 @@ __device__ __forceinline__ void proj_run(int gw, const double* sx, const double*
 // VAR: 0 = fused (Horner + Σr² + projections), 1 = Horner + Σr² only, 2 = projections only — the
 // specialised variants carry no registers for the part they skip
 template <int P, int VAR>
-__global__ void __launch_bounds__(K6_THREADS, 2)
+__global__ void __launch_bounds__(K6_THREADS, FMI_K6_MINB)
     k_residual(const double* __restrict__ ux, const double* __restrict__ uy, const double* __restrict__ uz,
                double* __restrict__ r, NodeTable nt, int64_t first, const Chunk* __restrict__ chunks,
                const int64_t* __restrict__ nchunks, int depth, int D, int mode, int iter,
@@ -328,7 +334,7 @@ __global__ void __launch_bounds__(K6_THREADS, 2)
 // ux, uy, uz, r of the later passes, and projected.  f (optional): values uploaded separately
 // (late-value path), taken from f[perm[i]] with the finiteness flag *bad.
 template <int P>
-__global__ void __launch_bounds__(K6_THREADS, 2)
+__global__ void __launch_bounds__(K6_THREADS, FMI_K6_MINB)
     k_gather_root(const double4* __restrict__ packed, const uint32_t* __restrict__ perm,
                   const double* __restrict__ f, int* __restrict__ bad, double* __restrict__ ux,
                   double* __restrict__ uy, double* __restrict__ uz, double* __restrict__ r,

@@ -31,7 +31,7 @@ MAX_DEPTH = 20
 EXPORTED = (
     "fmi_build", "fmi_eval", "fmi_free", "fmi_last_error", "fmi_set_stream", "fmi_node_count", "fmi_rank",
     "fmi_export_nodes", "fmi_root_cube", "fmi_residual", "fmi_level_stats", "fmi_profile_enable",
-    "fmi_profile_reset", "fmi_profile_get", "fmi_launch_count", "fmi_build_stats", "fmi_build_dist",
+    "fmi_profile_reset", "fmi_profile_get", "fmi_launch_count", "fmi_guard_violations", "fmi_build_stats", "fmi_build_dist",
     "fmi_dist_xbuf_bytes", "fmi_bbox", "fmi_cell_counts", "fmi_partition", "fmi_scatter", "fmi_transfer",
     "fmi_save", "fmi_load", "fmi_profile_units",
     "fmi_get_unique_id", "fmi_dist_init", "fmi_dist_finalize", "fmi_dist_allreduce",
@@ -144,6 +144,8 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.fmi_build_stats.argtypes = [VP, P(I64), I32]
     lib.fmi_launch_count.restype = I64
     lib.fmi_launch_count.argtypes = []
+    lib.fmi_guard_violations.restype = I64
+    lib.fmi_guard_violations.argtypes = []
     _lib = lib
     return lib
 
@@ -512,6 +514,11 @@ def profile_units() -> dict:
 
 def launch_count() -> int:
     return int(load_library().fmi_launch_count())
+
+
+def guard_violations() -> int:
+    """Overwritten guard bands seen under FMI_GUARD=1 (include/fmi.h fmi_guard_violations)."""
+    return int(load_library().fmi_guard_violations())
 
 
 def rank_of(degree: int) -> int:

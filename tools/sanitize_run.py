@@ -1,4 +1,5 @@
-"""Workload for compute-sanitizer runs (memcheck / racecheck / synccheck): every kernel family of the
+"""Workload for memory-safety runs — compute-sanitizer (memcheck / racecheck / synccheck) where the pool
+allows it, else the library's own guard bands (FMI_GUARD=1 python tools/sanitize_run.py): every kernel family of the
 hot path (keys, sort, gather, K4 moments, M2M TMA copies, K5 solve + refinement, K5q QR, K6 split and
 fused passes, decisions, presum, K7 eval, the unscoped f2 path) on BASELINE.json cfg 1 and a reduced
 cfg 2, through the C ABI.  Each phase checks its result against the oracle so a run that the
@@ -60,10 +61,18 @@ def main():
         rng = np.random.default_rng(5)
         x = rng.random((3000, 3))
         ok &= run(x, workloads.franke3d(x), rng.random((500, 3)), 10, 1e-12, 1, "p=10 D=1")
+    # the QR path on the octree (degrees 11-14 at depth > 0: Legendre Gram, CholeskyQR2 pass, walk)
+    rng = np.random.default_rng(9)
+    x = rng.random((8 ** 4, 3))
+    ok &= run(x, workloads.franke3d(x), rng.random((500, 3)), 11, 1e-6, 2, "QR path p=11 D=2")
     # unscoped f2 path (DMMA SYRK + single-CTA Cholesky + rejection walk)
     rng = np.random.default_rng(7)
     x = rng.random((4000, 3))
     ok &= run(x, workloads.franke3d(x), rng.random((500, 3)), 12, 0.0, 0, "unscoped p=12")
+    gv = fmi.guard_violations()
+    if os.environ.get("FMI_GUARD"):
+        print(f"guard bands overwritten: {gv}", flush=True)
+        ok &= gv == 0
     print("ALL OK" if ok else "FAILED", flush=True)
     sys.exit(0 if ok else 1)
 
