@@ -316,19 +316,15 @@ __global__ void __launch_bounds__(NT, NT == 512 ? 1 : (NT == 256 ? 2 : (NT == 12
       bool dg_ready = false;  // Dg holds the factored diagonal block of the current panel
       for (int j0 = 0; j0 < L; j0 += KB) {
         const int bw = min(KB, L - j0), R = L - j0 + 1;  // panel rows j0..L (row L = RHS)
-        // panel load: 8 independent L2 loads in flight per thread before their shared-memory stores
-        for (int e0 = tid; e0 < R * bw; e0 += 8 * K5_THREADS) {
-          double v[8];
-          int pos[8];
+        // panel load: warp per row, lane = column (one coalesced 256-byte row segment per load), 4 rows
+        // per warp in flight; rows of the lookahead's diagonal block come from Dg
+        for (int r0 = warp * 4; r0 < R; r0 += K5_WARPS * 4) {
+          double v[4];
 #pragma unroll
-          for (int k = 0; k < 8; ++k) {
-            const int e = e0 + k * K5_THREADS;
-            pos[k] = -1;
+          for (int k = 0; k < 4; ++k) {
+            const int r = r0 + k, i = j0 + r, c = lane;
             v[k] = 0.0;
-            if (e < R * bw) {
-              const int r = e / bw, c = e - r * bw;
-              const int i = j0 + r;
-              pos[k] = c * LDP + r;
+            if (r < R && c < bw) {
               if (r < bw && dg_ready) {
                 if (c <= r) v[k] = Dg[c * KB + r];
               } else if (i == L || c <= r) {
@@ -337,8 +333,8 @@ __global__ void __launch_bounds__(NT, NT == 512 ? 1 : (NT == 256 ? 2 : (NT == 12
             }
           }
 #pragma unroll
-          for (int k = 0; k < 8; ++k)
-            if (pos[k] >= 0) Pn[pos[k]] = v[k];
+          for (int k = 0; k < 4; ++k)
+            if (r0 + k < R && lane < bw) Pn[lane * LDP + r0 + k] = v[k];
         }
         __syncthreads();
         K5T(1)
@@ -609,8 +605,11 @@ struct K5Res {
   static constexpr size_t SMEM = (A_OFF + (size_t)NAB + 2) * sizeof(double) + 3 * L + 16;
   static constexpr bool fits = SMEM <= 227 * 1024;
 };
+#ifndef FMI_K5R_MID
+#define FMI_K5R_MID 64
+#endif
 template <int P>
-constexpr int k5r_threads() { return rank3(P) >= 120 ? 256 : (rank3(P) >= 56 ? 128 : 64); }
+constexpr int k5r_threads() { return rank3(P) >= 120 ? 256 : (rank3(P) >= 56 ? FMI_K5R_MID : 64); }
 template <int P>
 constexpr int k5r_minb() {
   constexpr size_t per = K5Res<P>::SMEM + 1024;
