@@ -282,3 +282,26 @@ def test_degree0_one_to_three_points(N):
     pts = rng.random((N, 3))
     f = rng.standard_normal(N)
     check_parity(pts, f, 0, 0.0, 3, rng.random((100, 3)))
+
+
+@pytest.mark.parametrize("eps", [1e-5, 3e-6, 3e-7, 1e-7])
+@pytest.mark.parametrize("p", [2, 4])
+def test_g9_near_threshold_sheet(p, eps):
+    """Column rejection near δ = 1e-6 (reading G9): points on the curved sheet z = x² + ε·w (root frame),
+    so the x²-type columns sit at distance ~1.25ε from the span of the columns before them.  The GPU
+    (K5 Gram pivots ~ε², hence the K5q Householder re-fit) keeps exactly the oracle's columns, and the
+    fitted values at the points agree within 1e-9·max|f|."""
+    rng = np.random.default_rng(11)
+    n = 2000
+    x, y, w = rng.uniform(-1, 1, (3, n))
+    u = np.stack([x, y, x * x + eps * w], axis=1)
+    pts = (u + 1.0) / 2.0
+    f = workloads.franke3d(pts)
+    ora = fo.build(pts, f, p, 0.0, 0)
+    with gpu_build(pts, f, p, 0.0, 0) as tree:
+        ex = tree.export()
+        got = gpu_eval(tree, pts)
+    ref = fo.evaluate(ora, pts)
+    assert int(ex["rank"][0]) == int(ora.kept[0].sum())
+    assert np.array_equal(ex["coeffs"][0] != 0, ora.kept[0])
+    assert np.max(np.abs(got - ref)) <= EVAL_TOL * np.max(np.abs(f))

@@ -487,3 +487,48 @@ def test_restricted_and_node_started_runs_reproduce_the_full_tree():
     ul0 = fo.local_coords(q, 0, np.zeros(3, dtype=np.int64))
     got = fo.evaluate(sub, q) + fo.apply_fit(ul0, full.coeffs[0], p)
     assert np.max(np.abs(got - fo.evaluate(full, q))) <= 1e-14
+
+
+def _walk_by_lstsq(u, p, delta):
+    """Reading G9 computed independently: walk the equilibrated Λ columns in Algorithm-2 order and keep
+    column j iff its distance from the span of the kept columns (SVD least squares, not the oracle's
+    Householder re-triangularisation) exceeds delta; returns the kept mask and every distance."""
+    lam = fo.vandermonde(u, p)
+    a = lam / np.linalg.norm(lam, axis=0)
+    kept, dist = [], []
+    for j in range(a.shape[1]):
+        if kept:
+            c, *_ = np.linalg.lstsq(a[:, kept], a[:, j], rcond=None)
+            d = float(np.linalg.norm(a[:, j] - a[:, kept] @ c))
+        else:
+            d = float(np.linalg.norm(a[:, j]))
+        dist.append(d)
+        if d > delta:
+            kept.append(j)
+    mask = np.zeros(a.shape[1], dtype=bool)
+    mask[kept] = True
+    return mask, np.array(dist)
+
+
+@pytest.mark.parametrize("eps", [1e-4, 1e-5, 3e-6, 1e-6, 3e-7, 1e-7, 1e-8])
+def test_g9_walk_near_threshold(eps):
+    """Column rejection near δ = 1e-6 (reading G9; PAPER.md P:330 is silent on rank deficiency): points
+    on the curved sheet z = x² + ε·w, so the column x² is at distance ~ε from the span of the columns
+    before it (z is one of them).  The oracle's kept set equals an independent SVD-least-squares walk
+    for every decision whose distance is not within 1% of δ, and the sheet's x²-type columns flip from
+    kept to dropped as ε crosses δ."""
+    rng = np.random.default_rng(11)
+    n = 400
+    x, y, w = rng.uniform(-1, 1, (3, n))
+    u = np.stack([x, y, x * x + eps * w], axis=1)
+    p = 2
+    fit = fo.fit_node(u, workloads.franke3d((u + 1) / 2), p)
+    mask, dist = _walk_by_lstsq(u, p, fo.DELTA)
+    clear = np.abs(dist / fo.DELTA - 1.0) > 1e-2
+    assert np.array_equal(fit.kept[clear], mask[clear])
+    j_x2 = fo.basis(p).index((2, 0, 0))
+    assert fit.kept[j_x2] == (dist[j_x2] > fo.DELTA)
+    if eps >= 1e-6:
+        assert fit.kept[j_x2]
+    if eps <= 3e-7:
+        assert not fit.kept[j_x2]
