@@ -104,7 +104,7 @@ __global__ void __launch_bounds__(PS_THREADS) k_presum(NodeTable nt, int64_t fir
 __device__ __forceinline__ void eval_fetch(const double* __restrict__ q, const double4* __restrict__ qpk,
                                            const uint64_t* __restrict__ keys, const uint32_t* __restrict__ idx,
                                            int64_t i, int64_t M, double lo0, double lo1, double lo2, double w,
-                                           bool unit, int64_t& qi, double& ux, double& uy, double& uz,
+                                           bool unit, int rec_idx, int64_t& qi, double& ux, double& uy, double& uz,
                                            uint64_t& key) {
   qi = 0;
   ux = uy = uz = 0.0;
@@ -116,6 +116,7 @@ __device__ __forceinline__ void eval_fetch(const double* __restrict__ q, const d
       const double2* p = reinterpret_cast<const double2*>(qpk + qi);
       const double2 a = __ldg(p), b = __ldg(p + 1);
       ux = a.x; uy = a.y; uz = b.x;
+      if (rec_idx) qi = (int64_t)b.y;  // bucketed records: idx is a bucket position, the input index is here
     } else {
       ux = to_unit_e(q[3 * qi + 0], lo0, w, unit);
       uy = to_unit_e(q[3 * qi + 1], lo1, w, unit);
@@ -148,7 +149,7 @@ template <int P>
 __global__ void __launch_bounds__(256) k_eval(const double* __restrict__ q, const double4* __restrict__ qpk,
                                               const uint64_t* __restrict__ keys, const uint32_t* __restrict__ idx,
                                               int64_t M, double lo0, double lo1, double lo2, double w, bool unit,
-                                              int Dk, NodeTable nt, double* __restrict__ out) {
+                                              int Dk, NodeTable nt, double* __restrict__ out, int rec_idx) {
   constexpr int L = rank3(P);
   constexpr int LA = (L + 1) & ~1;  // 16-byte aligned rows for pair loads
   __shared__ __align__(16) double cs[256 / 32][LA];
@@ -158,8 +159,8 @@ __global__ void __launch_bounds__(256) k_eval(const double* __restrict__ q, cons
   int64_t qi0, qi1, n0, n1;
   double x0, y0, z0, x1, y1, z1, ux0, uy0, uz0, ux1, uy1, uz1;
   uint64_t k0, k1;
-  eval_fetch(q, qpk, keys, idx, i0, M, lo0, lo1, lo2, w, unit, qi0, ux0, uy0, uz0, k0);
-  eval_fetch(q, qpk, keys, idx, i1, M, lo0, lo1, lo2, w, unit, qi1, ux1, uy1, uz1, k1);
+  eval_fetch(q, qpk, keys, idx, i0, M, lo0, lo1, lo2, w, unit, rec_idx, qi0, ux0, uy0, uz0, k0);
+  eval_fetch(q, qpk, keys, idx, i1, M, lo0, lo1, lo2, w, unit, rec_idx, qi1, ux1, uy1, uz1, k1);
   // sorted queries without a key array (the sort moved 32-bit keys): the key from the record's
   // root-cube coordinates, exactly as the key kernel formed it
   if (!keys && qpk) {
@@ -219,7 +220,7 @@ __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
 template <int P>
 __global__ void __launch_bounds__(EV_THREADS, 3)
     k_eval_pipe(const double4* __restrict__ qpk, const uint64_t* __restrict__ keys, const uint32_t* __restrict__ idx,
-                int64_t M, int Dk, NodeTable nt, double* __restrict__ out) {
+                int64_t M, int Dk, NodeTable nt, double* __restrict__ out, int rec_idx) {
   constexpr int L = rank3(P);
   constexpr int LA = (L + 1) & ~1;
   // dynamic shared memory: the record ring [2][EV_TILE] then the per-warp coefficient rows [8][LA]
@@ -258,7 +259,8 @@ __global__ void __launch_bounds__(EV_THREADS, 3)
     const double4 r0 = rec[slot][pos0], r1 = rec[slot][pos1];  // each thread reads only its own records
     const uint64_t k0 = i0 < M ? (keys ? keys[i0] : morton_key(r0.x, r0.y, r0.z, Dk)) : 0;
     const uint64_t k1 = i1 < M ? (keys ? keys[i1] : morton_key(r1.x, r1.y, r1.z, Dk)) : 0;
-    const int64_t qi0 = i0 < M ? (int64_t)idx[i0] : 0, qi1 = i1 < M ? (int64_t)idx[i1] : 0;
+    const int64_t qi0 = i0 < M ? (rec_idx ? (int64_t)r0.w : (int64_t)idx[i0]) : 0;
+    const int64_t qi1 = i1 < M ? (rec_idx ? (int64_t)r1.w : (int64_t)idx[i1]) : 0;
     int64_t n0, n1;
     double x0, y0, z0, x1, y1, z1;
     eval_descend(i0, M, true, Dk, nt, r0.x, r0.y, r0.z, k0, n0, x0, y0, z0);
@@ -309,7 +311,7 @@ void presum_level(const NodeTable& nt, int64_t first, int64_t count, cudaStream_
 template <int P>
 void eval_sorted(const double* q, const double4* qpk, const uint64_t* keys, const uint32_t* idx, int64_t M,
                  const double lo[3], double width, bool unit, int Dk, const NodeTable& nt, double* out,
-                 cudaStream_t s) {
+                 cudaStream_t s, bool rec_idx) {
   if (M <= 0) return;
   static int pipe_ctas = -1;  // persistent CTAs of the pipelined kernel (FMI_EVAL_PIPE=0: the one-shot kernel)
   static std::once_flag once;
@@ -326,16 +328,16 @@ void eval_sorted(const double* q, const double4* qpk, const uint64_t* keys, cons
   if (qpk && idx && pipe_ctas > 0) {
     const int64_t ntiles = (M + EV_TILE - 1) / EV_TILE;
     FMI_LAUNCH(KID_EVAL, s, k_eval_pipe<P>, (unsigned)std::min<int64_t>(ntiles, pipe_ctas), EV_THREADS, smem, qpk, keys,
-               idx, M, Dk, nt, out);
+               idx, M, Dk, nt, out, rec_idx ? 1 : 0);
     return;
   }
   FMI_LAUNCH(KID_EVAL, s, k_eval<P>, (unsigned)((M + 511) / 512), 256, 0, q, qpk, keys, idx, M, lo[0], lo[1], lo[2],
-             width, unit, Dk, nt, out);
+             width, unit, Dk, nt, out, rec_idx ? 1 : 0);
 }
 
 #define FMI_INST(P)                                                                                            \
   template void eval_sorted<P>(const double*, const double4*, const uint64_t*, const uint32_t*, int64_t,          \
-                               const double*, double, bool, int, const NodeTable&, double*, cudaStream_t);       \
+                               const double*, double, bool, int, const NodeTable&, double*, cudaStream_t, bool); \
   template void presum_level<P>(const NodeTable&, int64_t, int64_t, cudaStream_t);
 FMI_INST(0) FMI_INST(1) FMI_INST(2) FMI_INST(3) FMI_INST(4) FMI_INST(5)
 FMI_INST(6) FMI_INST(7) FMI_INST(8) FMI_INST(9) FMI_INST(10)

@@ -464,15 +464,16 @@ void dist_sum(const fmi_tree* T, void* dev, int64_t n, int dtype, cudaStream_t s
 // the upload event has completed
 struct LateValues {
   const double4* packed;
-  const uint32_t* perm;
+  uint32_t* perm;
+  const uint32_t* orig;  // bucketed keys: input index of each bucket position (else nullptr)
   const double* f;
   int* bad;
   cudaEvent_t ready;
 };
 
 template <int P>
-void fused_gather_root(const double4* packed, const uint32_t* perm, const double* f, int* bad, int64_t N,
-                       double* ux, double* uy, double* uz, double* r, double* root_b, cudaStream_t s,
+void fused_gather_root(const double4* packed, uint32_t* perm, const uint32_t* orig, const double* f, int* bad,
+                       int64_t N, double* ux, double* uy, double* uz, double* r, double* root_b, cudaStream_t s,
                        uint64_t* keys = nullptr, int D = 0);
 
 // Level-synchronous build:
@@ -584,7 +585,8 @@ void run_levels(fmi_tree* T, const uint64_t* keys, double* ux, double* uy, doubl
     if (late) {  // values uploaded meanwhile: gather them with the root projection, check finiteness
       FMI_CK(cudaStreamWaitEvent(s, late->ready, 0));
       segsum.ensure((size_t)(L + 1), s);
-      fused_gather_root<P>(late->packed, late->perm, late->f, late->bad, T->N, ux, uy, uz, r, segsum.p, s);
+      fused_gather_root<P>(late->packed, late->perm, late->orig, late->f, late->bad, T->N, ux, uy, uz, r, segsum.p,
+                           s);
       FMI_CK(cudaMemcpyAsync(host_small, late->bad, sizeof(int), cudaMemcpyDeviceToHost, s));
       FMI_CK(cudaStreamSynchronize(s));
       if (*reinterpret_cast<int*>(host_small)) fail(FMI_EINPUT, "non-finite coordinate or value");
@@ -777,10 +779,23 @@ void run_levels(fmi_tree* T, const uint64_t* keys, double* ux, double* uy, doubl
 
 // the gather of the sorted points fused with the root projection (single-GPU builds): chunks over [0, N)
 template <int P>
-void fused_gather_root(const double4* packed, const uint32_t* perm, const double* f, int* bad, int64_t N,
-                       double* ux, double* uy, double* uz, double* r, double* root_b, cudaStream_t s, uint64_t* keys,
-                       int D) {
+void fused_gather_root(const double4* packed, uint32_t* perm, const uint32_t* orig, const double* f, int* bad,
+                       int64_t N, double* ux, double* uy, double* uz, double* r, double* root_b, cudaStream_t s,
+                       uint64_t* keys, int D) {
   constexpr int L = rank3(P);
+  if (orig) {
+    // bucketed records: persistent CTAs striding over the batches in order (the window of positions in
+    // flight stays inside one bucket of records, L2-resident); one partial per CTA
+    constexpr int64_t kSpan = (int64_t)1 << 23;  // = kStrideSpan of gather_root_projection
+    const int64_t nl = (N + kSpan - 1) / kSpan;
+    const int64_t grid = std::max<int64_t>(1, std::min<int64_t>((std::min(N, kSpan) + 511) / 512, gather_root_ctas<P>()));
+    DBuf<int64_t> bn(2, s);
+    FMI_LAUNCH(KID_MISC, s, k_fill_range, 1, 1, 0, bn.p, nl * grid);  // chunk_begin = 0, nchunks = partial rows
+    DBuf<double> partial((size_t)(nl * grid) * (L + 1), s);
+    gather_root_projection<P>(packed, perm, orig, f, bad, N, ux, uy, uz, r, nullptr, bn.p + 1, nl * grid, bn.p,
+                              partial.p, root_b, s, keys, D, N);
+    return;
+  }
   DBuf<int64_t> se(2, s), counts(1, s), begin(1, s), nch(1, s);
   FMI_LAUNCH(KID_MISC, s, k_fill_range, 1, 1, 0, se.p, N);
   const int64_t ch = choose_chunk(N, 1024, 32);
@@ -788,7 +803,7 @@ void fused_gather_root(const double4* packed, const uint32_t* perm, const double
   DBuf<Chunk> chunks(maxc, s);
   DBuf<double> partial((size_t)maxc * (L + 1), s);
   make_chunks(se.p, se.p + 1, 1, ch, counts.p, begin.p, nch.p, chunks.p, maxc, s);
-  gather_root_projection<P>(packed, perm, f, bad, N, ux, uy, uz, r, chunks.p, nch.p, maxc, begin.p, partial.p,
+  gather_root_projection<P>(packed, perm, orig, f, bad, N, ux, uy, uz, r, chunks.p, nch.p, maxc, begin.p, partial.p,
                             root_b, s, keys, D);
 }
 
@@ -832,8 +847,8 @@ void run_unscoped(fmi_tree* T, const uint64_t* keys, double* ux, double* uy, dou
 
 template <int P>
 void run_eval(const fmi_tree* T, const double* q, const double4* qpk, const uint64_t* keys, const uint32_t* idx,
-              int64_t M, int Dk, double* out, cudaStream_t s) {
-  eval_sorted<P>(q, qpk, keys, idx, M, T->lo, T->width, T->unit, Dk, T->nt, out, s);
+              int64_t M, int Dk, double* out, cudaStream_t s, bool rec_idx = false) {
+  eval_sorted<P>(q, qpk, keys, idx, M, T->lo, T->width, T->unit, Dk, T->nt, out, s, rec_idx);
 }
 
 #define FMI_DISPATCH(p, FN, ...)                      \
@@ -1013,6 +1028,7 @@ fmi_tree* build_impl(const double* pts, const double* f, int64_t N, int degree, 
     DBuf<uint64_t> keys(N, s), ktmp;  // ktmp: the 64-bit sort only
     DBuf<uint32_t> perm(N, s), ptmp(N, s);
     DBuf<double4> packed(N, s);
+    DBuf<uint32_t> orig;  // bucketed keys: input index of every bucket position
     DBuf<double> ux(N, s), uy(N, s), uz(N, s), r(N, s);
     // the unscoped QR path (f2): degrees 11..14, or any degree at max_depth = 0 with FMI_UNSCOPED_QR=1
     // the QR path (unscoped.cu): degrees 11..14, or any degree with FMI_QR_PATH=1 (FMI_UNSCOPED_QR=1:
@@ -1037,7 +1053,20 @@ fmi_tree* build_impl(const double* pts, const double* f, int64_t N, int degree, 
       // the gather recompute the full 64-bit keys from the gathered coordinates
       const bool key32 = 3 * Dsort <= 32;
       uint64_t* kout = key32 ? keys.p : nullptr;  // gathers write the full keys (sorted order)
-      if (key32) {
+      // bucketed keys (FMI_BUCKET_SORT=2; measured slower for the build, whose gather is bound by the
+      // fused root projection): the top digit first, fused with the record write, so the gather reads
+      // the records bucket by bucket
+      const bool bucket_env = [] {  // FMI_BUCKET_SORT=2: also for the build's points
+        const char* e = std::getenv("FMI_BUCKET_SORT");
+        return e && std::atoi(e) >= 2;
+      }();
+      const bool bucket = key32 && bucket_env;
+      if (bucket) {
+        orig.ensure(N, s);
+        bucket_sort_keys(dpts, late_f ? nullptr : df, N, T->lo, T->width, T->unit, T->Dk, 3 * (T->Dk - Dsort),
+                         3 * Dsort, packed.p, orig.p, false, perm.p, s);
+        tmark("keys", s);
+      } else if (key32) {
         uint32_t* k32 = reinterpret_cast<uint32_t*>(keys.p);
         uint32_t* k32tmp = k32 + N;
         morton_keys(dpts, N, T->lo, T->width, T->unit, T->Dk, nullptr, perm.p, s, late_f ? nullptr : df, packed.p,
@@ -1055,23 +1084,24 @@ fmi_tree* build_impl(const double* pts, const double* f, int64_t N, int degree, 
       // single-GPU level path: the gather fused with the root projection (it needs no tree)
       const bool fuse_root = !unscoped && !dist;
       if (fuse_root) rootb.ensure((size_t)L + 1, s);
-      LateValues late{packed.p, perm.p, df, fbad.p, side.e_f};
+      const uint32_t* op = bucket ? orig.p : nullptr;  // bucket position -> input index
+      LateValues late{packed.p, perm.p, op, df, fbad.p, side.e_f};
       const bool late_levels = late_f && fuse_root;  // values join inside run_levels (after K4/M2M)
       if (late_levels) {
-        gather_points(packed.p, perm.p, N, ux.p, uy.p, uz.p, r.p, s, nullptr, nullptr, kout,
-                      T->Dk);  // coordinates now (r: placeholder)
+        gather_points(packed.p, perm.p, N, ux.p, uy.p, uz.p, r.p, s, nullptr, nullptr, kout, T->Dk, op,
+                      false);  // coordinates now (r: placeholder; perm still bucket positions)
       } else if (late_f) {
         FMI_CK(cudaStreamWaitEvent(s, side.e_f, 0));
-        gather_points(packed.p, perm.p, N, ux.p, uy.p, uz.p, r.p, s, df, fbad.p, kout, T->Dk);
+        gather_points(packed.p, perm.p, N, ux.p, uy.p, uz.p, r.p, s, df, fbad.p, kout, T->Dk, op, true);
         int hbad = 0;
         FMI_CK(cudaMemcpyAsync(&hbad, fbad.p, sizeof(int), cudaMemcpyDeviceToHost, s));
         FMI_CK(cudaStreamSynchronize(s));
         if (hbad) fail(FMI_EINPUT, "non-finite coordinate or value");
       } else if (fuse_root) {
-        FMI_DISPATCH(degree, fused_gather_root, packed.p, perm.p, nullptr, nullptr, N, ux.p, uy.p, uz.p, r.p, rootb.p,
-                     s, kout, T->Dk);
+        FMI_DISPATCH(degree, fused_gather_root, packed.p, perm.p, op, nullptr, nullptr, N, ux.p, uy.p, uz.p, r.p,
+                     rootb.p, s, kout, T->Dk);
       } else {
-        gather_points(packed.p, perm.p, N, ux.p, uy.p, uz.p, r.p, s, nullptr, nullptr, kout, T->Dk);
+        gather_points(packed.p, perm.p, N, ux.p, uy.p, uz.p, r.p, s, nullptr, nullptr, kout, T->Dk, op, true);
       }
       tmark("gather", s);
       try {
@@ -1089,6 +1119,7 @@ fmi_tree* build_impl(const double* pts, const double* f, int64_t N, int degree, 
     }
     ktmp.release();
     ptmp.release();
+    orig.release();
     packed.release();
     dpts_own.release();
     df_own.release();
@@ -1120,7 +1151,17 @@ void eval_device(const fmi_tree* T, const double* dq, int64_t m, double* dout, c
   } else {
     DBuf<uint32_t> idx(m, s), itmp(m, s);
     DBuf<double4> qpk(m, s);
-    if (3 * Dk <= 32) {  // 32-bit sort keys; K7 recomputes each key from the query's record
+    const bool bucket = [] {  // FMI_BUCKET_SORT=0: the plain LSD sort of the queries
+      const char* e = std::getenv("FMI_BUCKET_SORT");
+      return !(e && std::atoi(e) == 0);
+    }();
+    if (3 * Dk <= 32 && bucket) {
+      // bucketed records (top key digit first, the input index in each record): K7 reads the records of
+      // one bucket at a time; the keys are recomputed from the records
+      bucket_sort_keys(dq, nullptr, m, T->lo, T->width, T->unit, Dk, 0, 3 * Dk, qpk.p, nullptr, true, idx.p, s);
+      itmp.release();
+      FMI_DISPATCH14(T->p, run_eval, T, dq, qpk.p, nullptr, idx.p, m, Dk, dout, s, true);
+    } else if (3 * Dk <= 32) {  // 32-bit sort keys; K7 recomputes each key from the query's record
       DBuf<uint32_t> k32(m, s), k32tmp(m, s);
       morton_keys(dq, m, T->lo, T->width, T->unit, Dk, nullptr, idx.p, s, nullptr, qpk.p, k32.p, 0);
       radix_sort_pairs32(k32.p, idx.p, k32tmp.p, itmp.p, m, 3 * Dk, s);

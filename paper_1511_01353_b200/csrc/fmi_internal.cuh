@@ -185,9 +185,18 @@ void radix_sort_pairs32(uint32_t*& keys, uint32_t*& vals, uint32_t*& keys_tmp, u
 // f (optional): take the values from f[perm[i]] instead of the records (values uploaded after the keys
 // were built); *bad is set if one is non-finite
 // keys (optional): also write the 64-bit Morton keys (D levels) recomputed from the gathered coordinates
-void gather_points(const double4* packed, const uint32_t* perm, int64_t n, double* ux, double* uy, double* uz,
+// orig (bucketed keys): perm holds bucket positions and orig the input index of each; compose: replace
+// perm[i] by the input index once read
+void gather_points(const double4* packed, uint32_t* perm, int64_t n, double* ux, double* uy, double* uz,
                    double* r, cudaStream_t s, const double* f = nullptr, int* bad = nullptr,
-                   uint64_t* keys = nullptr, int D = 0);
+                   uint64_t* keys = nullptr, int D = 0, const uint32_t* orig = nullptr, bool compose = false);
+// Bucketed keys + sort (single-GPU 32-bit sort keys of nb = 3·levels bits): the top 8 key bits first,
+// fused with the record write (records in bucket order, orig[pos] = input index, or the input index in
+// the record's fourth slot with rec_idx), then the remaining bits sorted inside each bucket; perm[i] =
+// the bucket position of the i-th point in Morton order.  pts/f device pointers, n < 2^32.
+void bucket_sort_keys(const double* pts, const double* f, int64_t n, const double lo[3], double width, bool unit,
+                      int D, int bit_lo, int nb, double4* packed, uint32_t* orig, bool rec_idx, uint32_t* perm,
+                      cudaStream_t s);
 
 // sharded build helpers (keys.cu): depth-s cell histogram, partition by owner shard, scatter
 void cell_counts(const double* pts, int64_t n, const double lo[3], double width, bool unit, int s, int64_t* counts,
@@ -285,11 +294,16 @@ template <int P> void level_residual(const LevelCtx& c, int mode, int iter, cons
 // the gather of the sorted points (ux, uy, uz, r from packed[perm]) fused with the root projection
 // b = Λᵀf in the root frame -> segsum[0..𝓛] (chunks over [0, n)); f (optional): separately uploaded
 // values with the finiteness flag *bad
-template <int P> void gather_root_projection(const double4* packed, const uint32_t* perm, const double* f, int* bad,
+template <int P> void gather_root_projection(const double4* packed, uint32_t* perm, const uint32_t* orig,
+                                             const double* f, int* bad,
                                              int64_t n, double* ux, double* uy, double* uz, double* r,
                                              const Chunk* chunks, const int64_t* nchunks_dev, int64_t max_chunks,
                                              const int64_t* chunk_begin, double* partial, double* segsum,
-                                             cudaStream_t s, uint64_t* keys = nullptr, int D = 0);
+                                             cudaStream_t s, uint64_t* keys = nullptr, int D = 0,
+                                             int64_t n_stride = 0);
+// n_stride > 0: max_chunks persistent CTAs stride over batches of [0, n_stride) (chunks unused; one
+// partial per CTA); gather_root_ctas = the resident CTA count for that grid
+template <int P> int gather_root_ctas();
 // child projections of a node are deferred (flag bit 3) when its predicted post-fit RMS (pre-fit energy
 // minus the energy the fit removes) is below kDeferTheta·τ: its children are then unlikely to be
 // created, and the projection pass runs only for those that are
@@ -322,9 +336,11 @@ template <int P> void presum_level(const NodeTable& nt, int64_t first, int64_t c
 // c = the root level (count 1, child_start set); writes coef/pcoef/rank/minpiv/flag of the root, the
 // residual r (in place) and the root's octant energies child_ss.
 template <int P> void unscoped_fit(const LevelCtx& c, cudaStream_t s);
-// qpk (optional): the queries' root-cube coordinates as 32-byte records (from morton_keys)
+// qpk (optional): the queries' root-cube coordinates as 32-byte records (from morton_keys); rec_idx: the
+// records are in bucket order (bucket_sort_keys), idx holds bucket positions and each record's fourth slot
+// the query's input index (the output position)
 template <int P> void eval_sorted(const double* q, const double4* qpk, const uint64_t* keys, const uint32_t* idx,
                                   int64_t M, const double lo[3], double width, bool unit, int Dk, const NodeTable& nt,
-                                  double* out, cudaStream_t s);
+                                  double* out, cudaStream_t s, bool rec_idx = false);
 
 }  // namespace fmi

@@ -335,11 +335,11 @@ __global__ void __launch_bounds__(K6_THREADS, FMI_K6_MINB)
 // (late-value path), taken from f[perm[i]] with the finiteness flag *bad.
 template <int P>
 __global__ void __launch_bounds__(K6_THREADS, FMI_K6_MINB)
-    k_gather_root(const double4* __restrict__ packed, const uint32_t* __restrict__ perm,
+    k_gather_root(const double4* __restrict__ packed, uint32_t* __restrict__ perm, const uint32_t* __restrict__ orig,
                   const double* __restrict__ f, int* __restrict__ bad, double* __restrict__ ux,
                   double* __restrict__ uy, double* __restrict__ uz, double* __restrict__ r,
                   const Chunk* __restrict__ chunks, const int64_t* __restrict__ nchunks,
-                  double* __restrict__ partial, uint64_t* __restrict__ keys, int D) {
+                  double* __restrict__ partial, uint64_t* __restrict__ keys, int D, int64_t r0, int64_t n_stride) {
   constexpr int L = rank3(P);
   constexpr int G = proj_groups(P);
   constexpr int SUB = K6_WARPS / G;
@@ -353,9 +353,22 @@ __global__ void __launch_bounds__(K6_THREADS, FMI_K6_MINB)
   static_assert(SUB * L <= 4 * BATCH, "reduction buffer");
   double (*red)[L] = reinterpret_cast<double (*)[L]>(sbuf);
   extern __shared__ __align__(16) double stage[];  // [2][BATCH] records (4 doubles) + [2][BATCH] values
+  // chunk mode: CTA = one chunk of consecutive batches; stride mode (n_stride > 0, bucketed records):
+  // CTA b takes batches b, b + grid, ... of [r0, n_stride), so the CTAs in flight gather from a window of
+  // consecutive positions (a part of one bucket of records, L2-resident) instead of one chunk each
   const int64_t cidx = blockIdx.x;
-  if (cidx >= *nchunks) return;
-  const Chunk ck = chunks[cidx];
+  int64_t c0, c1, step;
+  if (n_stride > 0) {
+    c0 = r0 + cidx * BATCH;
+    c1 = n_stride;
+    step = (int64_t)gridDim.x * BATCH;
+  } else {
+    if (cidx >= *nchunks) return;
+    const Chunk ck = chunks[cidx];
+    c0 = ck.start;
+    c1 = ck.end;
+    step = BATCH;
+  }
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int gw = warp % G, sub = warp / G;
   double* out = partial + cidx * (int64_t)(L + 1);
@@ -365,15 +378,27 @@ __global__ void __launch_bounds__(K6_THREADS, FMI_K6_MINB)
   double* srec = stage;                    // [2][BATCH][4]
   double* sval = stage + 2 * BATCH * 4;    // [2][BATCH]
   uint32_t pn[PPT];                        // perm of the next batch (loaded one batch ahead)
+  uint32_t pi[PPT];                        // its input indices (bucketed keys: orig[perm]; else perm)
   auto load_perm = [&](int64_t base) {
 #pragma unroll
     for (int k = 0; k < PPT; ++k) {
       const int64_t i = base + tid + k * K6_THREADS;
-      pn[k] = i < ck.end ? perm[i] : perm[ck.start];
+      pn[k] = i < c1 ? perm[i] : 0u;
+    }
+    if (orig) {
+#pragma unroll
+      for (int k = 0; k < PPT; ++k) {
+        const int64_t i = base + tid + k * K6_THREADS;
+        pi[k] = orig[pn[k]];
+        if (i < c1) perm[i] = pi[k];  // the tree keeps input indices
+      }
+    } else {
+#pragma unroll
+      for (int k = 0; k < PPT; ++k) pi[k] = pn[k];
     }
   };
   auto issue = [&](int64_t base, int buf) {
-    if (base < ck.end) {
+    if (base < c1) {
 #pragma unroll
       for (int k = 0; k < PPT; ++k) {
         const int e = tid + k * K6_THREADS;
@@ -383,26 +408,26 @@ __global__ void __launch_bounds__(K6_THREADS, FMI_K6_MINB)
                      "l"(src) : "memory");
         asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(d + 2)),
                      "l"(src + 2) : "memory");
-        if (f) k6_cp8(sval + (size_t)buf * BATCH + e, f + pn[k]);
+        if (f) k6_cp8(sval + (size_t)buf * BATCH + e, f + pi[k]);
       }
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
   };
-  load_perm(ck.start);
-  issue(ck.start, 0);
-  load_perm(ck.start + BATCH);
+  load_perm(c0);
+  issue(c0, 0);
+  load_perm(c0 + step);
   int buf = 0;
   const Frame fc = node_frame(make_int4(0, 0, 0, 0));
   int nbad = 0;
-  for (int64_t base = ck.start; base < ck.end; base += BATCH, buf ^= 1) {
-    issue(base + BATCH, buf ^ 1);
-    load_perm(base + 2 * BATCH);
+  for (int64_t base = c0; base < c1; base += step, buf ^= 1) {
+    issue(base + step, buf ^ 1);
+    load_perm(base + 2 * step);
     asm volatile("cp.async.wait_group 1;" ::: "memory");
 #pragma unroll
     for (int k = 0; k < PPT; ++k) {
       const int e = tid + k * K6_THREADS;
       const int64_t i = base + e;
-      const bool v = i < ck.end;
+      const bool v = i < c1;
       const double* rec = srec + ((size_t)buf * BATCH + e) * 4;
       const double X = rec[0], Y = rec[1], Z = rec[2];
       const double R = f ? sval[(size_t)buf * BATCH + e] : rec[3];
@@ -417,7 +442,7 @@ __global__ void __launch_bounds__(K6_THREADS, FMI_K6_MINB)
       sr[e] = v ? R : 0.0;
     }
     __syncthreads();
-    const int nb = (int)min((int64_t)BATCH, ck.end - base);
+    const int nb = (int)min((int64_t)BATCH, c1 - base);
     proj_run<P>(gw, sx, sy, sz, sr, sub * 32 + lane, 32 * SUB, nb, acc, std::make_integer_sequence<int, G>{});
     __syncthreads();
   }
@@ -523,19 +548,48 @@ void level_residual(const LevelCtx& c, int mode, int iter, const double* delta, 
              segsum);
 }
 
+// resident CTAs of k_gather_root on the device (the stride-mode grid)
 template <int P>
-void gather_root_projection(const double4* packed, const uint32_t* perm, const double* f, int* bad, int64_t n,
+int gather_root_ctas() {
+  static int ctas = [] {
+    constexpr size_t smem = 2 * (size_t)(2 * K6_THREADS) * 5 * sizeof(double);
+    int dev = 0, sms = 0, per = 0;
+    FMI_CK(cudaGetDevice(&dev));
+    FMI_CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    FMI_CK(cudaFuncSetAttribute(k_gather_root<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    FMI_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_gather_root<P>, K6_THREADS, smem));
+    return sms * std::max(1, per);
+  }();
+  return ctas;
+}
+
+template <int P>
+void gather_root_projection(const double4* packed, uint32_t* perm, const uint32_t* orig, const double* f, int* bad,
+                            int64_t n,
                             double* ux, double* uy, double* uz, double* r, const Chunk* chunks,
                             const int64_t* nchunks_dev, int64_t max_chunks, const int64_t* chunk_begin,
-                            double* partial, double* segsum, cudaStream_t s, uint64_t* keys, int D) {
+                            double* partial, double* segsum, cudaStream_t s, uint64_t* keys, int D,
+                            int64_t n_stride) {
+  // stride mode: the range is cut into launches of <= kStrideSpan positions (a grid-wide step between
+  // them bounds how far the persistent CTAs drift apart, i.e. the window of records in flight); launch
+  // k writes partial rows [k·grid, (k+1)·grid)
+  constexpr int64_t kStrideSpan = (int64_t)1 << 23;
   constexpr size_t smem = 2 * (size_t)(2 * K6_THREADS) * 5 * sizeof(double);
   static std::once_flag attr_once;
   std::call_once(attr_once, [&] {
     FMI_CK(cudaFuncSetAttribute(k_gather_root<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   });
-  if (max_chunks > 0)
-    FMI_LAUNCH(KID_PROJECT, s, k_gather_root<P>, (unsigned)max_chunks, K6_THREADS, smem, packed, perm, f, bad, ux, uy,
-               uz, r, chunks, nchunks_dev, partial, keys, D);
+  if (n_stride > 0) {
+    const int64_t nl = (n_stride + kStrideSpan - 1) / kStrideSpan;
+    const int64_t grid = max_chunks / nl;  // CTAs per launch (max_chunks = nl · grid partial rows)
+    for (int64_t k = 0; k < nl; ++k)
+      FMI_LAUNCH(KID_PROJECT, s, k_gather_root<P>, (unsigned)grid, K6_THREADS, smem, packed, perm, orig, f, bad, ux,
+                 uy, uz, r, chunks, nchunks_dev, partial + k * grid * (rank3(P) + 1), keys, D, k * kStrideSpan,
+                 std::min(n_stride, (k + 1) * kStrideSpan));
+  } else if (max_chunks > 0) {
+    FMI_LAUNCH(KID_PROJECT, s, k_gather_root<P>, (unsigned)max_chunks, K6_THREADS, smem, packed, perm, orig, f, bad,
+               ux, uy, uz, r, chunks, nchunks_dev, partial, keys, D, (int64_t)0, (int64_t)0);
+  }
   FMI_LAUNCH(KID_RESIDUAL_REDUCE, s, k_residual_reduce, dim3(1u, (unsigned)((rank3(P) + 1 + 31) / 32)), 256, 0,
              partial, chunk_begin, nchunks_dev, (int64_t)1, NodeTable{}, (int64_t)0, rank3(P), false, nullptr, segsum);
   (void)n;
@@ -544,9 +598,12 @@ void gather_root_projection(const double4* packed, const uint32_t* perm, const d
 #define FMI_INST(P)                                                                                            \
   template void level_residual<P>(const LevelCtx&, int, int, const double*, const Chunk*, const int64_t*, int64_t, \
                                   const int64_t*, int64_t, double*, double*, cudaStream_t, const int32_t*, bool); \
-  template void gather_root_projection<P>(const double4*, const uint32_t*, const double*, int*, int64_t, double*,    \
+  template void gather_root_projection<P>(const double4*, uint32_t*, const uint32_t*, const double*, int*, int64_t,   \
+                                          double*,                                                                  \
                                           double*, double*, double*, const Chunk*, const int64_t*, int64_t,           \
-                                          const int64_t*, double*, double*, cudaStream_t, uint64_t*, int);
+                                          const int64_t*, double*, double*, cudaStream_t, uint64_t*, int,     \
+                                          int64_t);                                                           \
+  template int gather_root_ctas<P>();
 FMI_INST(0) FMI_INST(1) FMI_INST(2) FMI_INST(3) FMI_INST(4) FMI_INST(5)
 FMI_INST(6) FMI_INST(7) FMI_INST(8) FMI_INST(9) FMI_INST(10)
 #undef FMI_INST

@@ -605,6 +605,9 @@ struct K5Res {
   static constexpr size_t SMEM = (A_OFF + (size_t)NAB + 2) * sizeof(double) + 3 * L + 16;
   static constexpr bool fits = SMEM <= 227 * 1024;
 };
+#ifndef FMI_K5R_BLK2
+#define FMI_K5R_BLK2 1
+#endif
 #ifndef FMI_K5R_MID
 #define FMI_K5R_MID 64
 #endif
@@ -773,7 +776,56 @@ __global__ void __launch_bounds__(NT, k5r_minb<P>())
       };
       // DMMA update of 8x8 tiles t in [t_lo, t_hi) of the trailing lower triangle rows/cols >= j1 by the
       // panel columns j0..j0+bw-1 (tile (ti, tk), tk <= ti, rows j1+8ti.., cols j1+8tk..)
+#if FMI_K5R_BLK2
+      // DMMA update of 16x16 blocks b in [b_lo, b_hi) of the trailing lower triangle (rows/cols >= j1) by
+      // the panel columns j0..j0+bw-1: block (bi, bk), bk <= bi, rows j1+16bi.., cols j1+16bk.., as 2x2
+      // 8x8 tiles that share their fragments (two A and two B fragment loads per four m8n8k4 steps, half
+      // the shared-memory reads of independent tiles); the tile above the diagonal of a diagonal block is
+      // skipped.  Blocks are numbered row-major, so the blocks of the next diagonal block are a prefix.
+      const int fr = lane & 3, fc = lane >> 2;
+      auto trailing = [&](int j0, int bw, int j1, int t_lo, int t_hi, int wid, int nwk, bool, int) {
+        for (int t = t_lo + wid; t < t_hi; t += nwk) {
+          int bi = (int)((sqrt(8.0 * (double)t + 1.0) - 1.0) * 0.5);
+          while ((bi + 1) * (bi + 2) / 2 <= t) ++bi;
+          while (bi * (bi + 1) / 2 > t) --bi;
+          const int bk = t - bi * (bi + 1) / 2;
+          const bool dgb = bi == bk;
+          const int i0 = j1 + 16 * bi, k0 = j1 + 16 * bk;
+          // fragment rows (clamped into the matrix; rows past L are masked at the store)
+          const double* pa0 = A + tri(min(i0 + fc, L)) + j0 + fr;
+          const double* pa1 = A + tri(min(i0 + 8 + fc, L)) + j0 + fr;
+          const double* pb0 = A + tri(min(k0 + fc, L)) + j0 + fr;
+          const double* pb1 = A + tri(min(k0 + 8 + fc, L)) + j0 + fr;
+          double d[4][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
+#pragma unroll
+          for (int c = 0; c < KB; c += 4) {  // columns past bw (last panel) enter as zeros
+            const bool in = c + fr < bw;
+            const double a0 = in ? pa0[c] : 0.0, a1 = in ? pa1[c] : 0.0;
+            const double b0 = in ? pb0[c] : 0.0, b1 = in ? pb1[c] : 0.0;
+            asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+                         : "+d"(d[0][0]), "+d"(d[0][1]) : "d"(a0), "d"(b0));
+            if (!dgb)
+              asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+                           : "+d"(d[1][0]), "+d"(d[1][1]) : "d"(a0), "d"(b1));
+            asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+                         : "+d"(d[2][0]), "+d"(d[2][1]) : "d"(a1), "d"(b0));
+            asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+                         : "+d"(d[3][0]), "+d"(d[3][1]) : "d"(a1), "d"(b1));
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int ci = i0 + 8 * (u >> 1) + fc, ck = k0 + 8 * (u & 1) + 2 * fr;
+            if (ci > L || (u == 1 && dgb)) continue;
+            double* Ar = A + tri(ci);
+            if (ck < L && (ck <= ci || ci == L)) Ar[ck] -= d[u][0];
+            if (ck + 1 < L && (ck + 1 <= ci || ci == L)) Ar[ck + 1] -= d[u][1];
+          }
+        }
+      };
+      constexpr int TB = 16;  // rows per trailing work item
+#else
       constexpr int TPW = 4;
+      constexpr int TB = 8;  // rows per trailing work item
       const int fr = lane & 3, fc = lane >> 2;
       auto trailing = [&](int j0, int bw, int j1, int t_lo, int t_hi, int wid, int nwk, bool skip_next, int iend) {
         for (int t0 = t_lo + wid * TPW; t0 < t_hi; t0 += nwk * TPW) {
@@ -819,6 +871,7 @@ __global__ void __launch_bounds__(NT, k5r_minb<P>())
           }
         }
       };
+#endif
       constexpr bool kLook = NW >= 4;
       bool dg_ready = false;
       for (int j0 = 0; j0 < L; j0 += KB) {
@@ -852,13 +905,13 @@ __global__ void __launch_bounds__(NT, k5r_minb<P>())
         K5T(3)
         if (j1 < L) {
           const int R2 = L + 1 - j1;
-          const int nt8 = (R2 + 7) / 8;
+          const int nt8 = (R2 + TB - 1) / TB;
           const int ntile = nt8 * (nt8 + 1) / 2;
           const int bw2 = min(KB, L - j1);
           if (kLook) {
             // the next diagonal block's tiles first (rows j1..j1+bw2-1: tiles ti < 4), then warp 0
             // factors it while the other warps update the rest
-            const int nd8 = (bw2 + 7) / 8;
+            const int nd8 = (bw2 + TB - 1) / TB;
             const int ndt = nd8 * (nd8 + 1) / 2;
             trailing(j0, bw, j1, 0, ndt, warp, NW, false, 0);
             __syncthreads();

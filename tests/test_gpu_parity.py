@@ -251,8 +251,29 @@ def test_k6_split_and_fused_match_the_oracle(split_min, monkeypatch):
     assert ora.node_count == 585
 
 
+@pytest.mark.parametrize("mode", ["0", "2"])
+def test_bucket_sort_modes_match_the_oracle(mode, monkeypatch):
+    """Bucketed keys (top sort digit first, records in bucket order; keys.cu bucket_sort_keys): mode 2
+    also buckets the build's points (records gathered bucket by bucket, the root projection in stride
+    mode, perm composed back to input indices), mode 0 is the plain LSD sort for the queries too.  Both
+    give the oracle's tree and values (the default, queries only, is every other test); the residual
+    in input order checks the composed permutation."""
+    monkeypatch.setenv("FMI_BUCKET_SORT", mode)
+    cfg = workloads.CONFIGS[2]
+    pts, f, q = workloads.make_inputs(cfg)
+    q = q[:50_000]
+    ora, gpu, *_ = check_parity(pts, f, cfg.degree, cfg.tol, cfg.max_depth, q, erms_vs=workloads.franke3d)
+    assert ora.node_count == 585
+    with gpu_build(pts, f, cfg.degree, cfg.tol, cfg.max_depth) as tree:
+        res = tree.residual()
+    scale = float(np.max(np.abs(f)))
+    ref = f - fo.evaluate(ora, pts)
+    assert np.max(np.abs(res - ref)) <= EVAL_TOL * scale
+
+
 # ---------------------------------------------------------------------------------------------
-# sort edge cases: query counts around the K2 tile (3072 items) and warp (32) boundaries, and
+# sort edge cases: query counts around the K2 tile (3072 items), the bucket tile (1536) and warp (32)
+# boundaries, and
 # point sets of one, two and three points (p = 0: 𝓛 = 1)
 # ---------------------------------------------------------------------------------------------
 
@@ -267,7 +288,7 @@ def _tile_tree():
     tree.free()
 
 
-@pytest.mark.parametrize("M", [1, 2, 31, 33, 3071, 3072, 3073, 6145])
+@pytest.mark.parametrize("M", [1, 2, 31, 33, 1535, 1536, 1537, 3071, 3072, 3073, 4609, 6145])
 def test_eval_query_counts_around_sort_tiles(_tile_tree, M):
     ora, tree, scale = _tile_tree
     q = np.random.default_rng(1000 + M).random((M, 3))
