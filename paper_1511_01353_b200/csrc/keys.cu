@@ -733,9 +733,9 @@ void bucket_sort_keys(const double* pts, const double* f, int64_t n, const doubl
   DBuf<int32_t> tile0(257, s);
   DBuf<SegTile> seg((size_t)nblk2, s);
   DBuf<uint32_t> ka(n2, s), va(n2, s), kb(n2, s), vb(n2, s);
-  // the top digit: histogram (coordinates 24 B), then the scatter (coordinates + value 32 B read; record
+  // the top digit: histogram (coordinates 24 B), then the scatter (coordinates 24 B + value 8 B read; record
   // 32 B, orig 4 B, key and position 8 B written)
-  prof_units(KID_KEYS, n * (24 + 32 + (f ? 8 : 0) + 32 + (orig ? 4 : 0) + 8));
+  prof_units(KID_KEYS, n * (24 + 24 + (f ? 8 : 0) + 32 + (orig ? 4 : 0) + 8));
   FMI_LAUNCH(KID_KEYS, s, k_bk_hist, (unsigned)nblk, RS_THREADS, 0, pts, n, lo[0], lo[1], lo[2], width, unit, D,
              bit_lo, nb, nblk, counts.p);
   exclusive_scan_i64(counts.p, counts.p, nblk * 256, nullptr, s);
