@@ -9,7 +9,7 @@ import pytest
 
 import workloads
 from oracle import fmt_oracle as fo
-from parity import coeff_and_rms_errors, compare_trees
+from parity import coeff_and_rms_errors, compare_trees, rms_agreement
 
 torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
@@ -48,6 +48,7 @@ def check_parity(pts, f, p, tau, D, q, erms_vs=None):
     err = float(np.max(np.abs(val - ref))) if q.shape[0] else 0.0
     assert err <= EVAL_TOL * max(scale, 1e-300), f"max|gpu - oracle| = {err:.3e} > {EVAL_TOL * scale:.3e}"
     drms = coeff_and_rms_errors(gpu, ora, g, o)
+    rms_agreement(gpu, ora, g, o, scale)  # every common node's post-fit RMS (asserted per node)
     if erms_vs is not None:
         truth = erms_vs(q)
         e_gpu, _ = workloads.rms_and_max(val - truth)
