@@ -1158,9 +1158,14 @@ void eval_device(const fmi_tree* T, const double* dq, int64_t m, double* dout, c
     if (3 * Dk <= 32 && bucket) {
       // bucketed records (top key digit first, the input index in each record): K7 reads the records of
       // one bucket at a time; the keys are recomputed from the records
-      bucket_sort_keys(dq, nullptr, m, T->lo, T->width, T->unit, Dk, 0, 3 * Dk, qpk.p, nullptr, true, idx.p, s);
+      // the last sort pass writes the records themselves in Morton order: K7 reads them sequentially
+      // (no index array, no dependent gather), the input index rides in each record
+      idx.release();
       itmp.release();
-      FMI_DISPATCH14(T->p, run_eval, T, dq, qpk.p, nullptr, idx.p, m, Dk, dout, s, true);
+      DBuf<double4> qsorted(m, s);
+      const double4* rec = bucket_sort_keys(dq, nullptr, m, T->lo, T->width, T->unit, Dk, 0, 3 * Dk, qpk.p, nullptr,
+                                            true, nullptr, s, qsorted.p);
+      FMI_DISPATCH14(T->p, run_eval, T, dq, rec, nullptr, nullptr, m, Dk, dout, s, true);
     } else if (3 * Dk <= 32) {  // 32-bit sort keys; K7 recomputes each key from the query's record
       DBuf<uint32_t> k32(m, s), k32tmp(m, s);
       morton_keys(dq, m, T->lo, T->width, T->unit, Dk, nullptr, idx.p, s, nullptr, qpk.p, k32.p, 0);

@@ -193,10 +193,13 @@ void gather_points(const double4* packed, uint32_t* perm, int64_t n, double* ux,
 // Bucketed keys + sort (single-GPU 32-bit sort keys of nb = 3·levels bits): the top 8 key bits first,
 // fused with the record write (records in bucket order, orig[pos] = input index, or the input index in
 // the record's fourth slot with rec_idx), then the remaining bits sorted inside each bucket; perm[i] =
-// the bucket position of the i-th point in Morton order.  pts/f device pointers, n < 2^32.
-void bucket_sort_keys(const double* pts, const double* f, int64_t n, const double lo[3], double width, bool unit,
-                      int D, int bit_lo, int nb, double4* packed, uint32_t* orig, bool rec_idx, uint32_t* perm,
-                      cudaStream_t s);
+// the bucket position of the i-th point in Morton order.  pts/f device pointers, n < 2^32.  rec_sorted
+// (optional, n records): the last pass writes the records themselves in Morton order there instead of
+// perm.  Returns the array holding the records in Morton order when perm is not written (packed when the
+// top digit was the whole key, else rec_sorted), packed otherwise.
+const double4* bucket_sort_keys(const double* pts, const double* f, int64_t n, const double lo[3], double width,
+                                bool unit, int D, int bit_lo, int nb, double4* packed, uint32_t* orig, bool rec_idx,
+                                uint32_t* perm, cudaStream_t s, double4* rec_sorted = nullptr);
 
 // sharded build helpers (keys.cu): depth-s cell histogram, partition by owner shard, scatter
 void cell_counts(const double* pts, int64_t n, const double lo[3], double width, bool unit, int s, int64_t* counts,

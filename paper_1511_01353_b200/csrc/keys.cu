@@ -177,7 +177,9 @@ __global__ void __launch_bounds__(RS_THREADS, 4) k_rs_scatter(const KT* __restri
                                                            const uint32_t* __restrict__ vin, int64_t n, int shift,
                                                            int64_t nblk, const int64_t* __restrict__ offs,
                                                            KT* __restrict__ kout, uint32_t* __restrict__ vout,
-                                                           const SegTile* __restrict__ seg, int last) {
+                                                           const SegTile* __restrict__ seg, int last,
+                                                           const double4* __restrict__ rec_in,
+                                                           double4* __restrict__ rec_out) {
   __shared__ int whist[RS_WARPS][257];
   __shared__ int tstart[257];           // exclusive prefix of the tile's digit counts
   __shared__ int64_t boff[256];
@@ -272,7 +274,12 @@ __global__ void __launch_bounds__(RS_THREADS, 4) k_rs_scatter(const KT* __restri
     const int64_t g = boff[d] + (pos - tstart[d]);
     if (last) {  // last pass of a segmented sort: padding dropped, segments compacted, no keys
       const uint32_t v = sv[pos];
-      if (v != kPadVal) vout[g - sg.shift] = v;
+      // rec_out: the records themselves in sorted order (the value is a bucket position of rec_in; the
+      // reads stay inside the tile's bucket, L2-resident), so the consumer reads them sequentially
+      if (v != kPadVal) {
+        if (rec_out) rec_out[g - sg.shift] = rec_in[v];
+        else vout[g - sg.shift] = v;
+      }
     } else {
       kout[g] = kk;
       vout[g] = sv[pos];
@@ -698,7 +705,7 @@ void radix_sort_impl(KT*& keys, uint32_t*& vals, KT*& keys_tmp, uint32_t*& vals_
                (const SegTile*)nullptr);
     exclusive_scan_i64(counts.p, counts.p, nblk * 256, nullptr, s);
     FMI_LAUNCH(KID_SORT, s, k_rs_scatter<KT>, (unsigned)nblk, RS_THREADS, scatter_smem<KT>(), ka, va, n, shift, nblk,
-               counts.p, kb, vb, (const SegTile*)nullptr, 0);
+               counts.p, kb, vb, (const SegTile*)nullptr, 0, (const double4*)nullptr, (double4*)nullptr);
     std::swap(ka, kb);
     std::swap(va, vb);
   }
@@ -716,10 +723,10 @@ void radix_sort_pairs32(uint32_t*& keys, uint32_t*& vals, uint32_t*& keys_tmp, u
   radix_sort_impl<uint32_t>(keys, vals, keys_tmp, vals_tmp, n, nbits, s, 0);
 }
 
-void bucket_sort_keys(const double* pts, const double* f, int64_t n, const double lo[3], double width, bool unit,
-                      int D, int bit_lo, int nb, double4* packed, uint32_t* orig, bool rec_idx, uint32_t* perm,
-                      cudaStream_t s) {
-  if (n <= 0) return;
+const double4* bucket_sort_keys(const double* pts, const double* f, int64_t n, const double lo[3], double width,
+                                bool unit, int D, int bit_lo, int nb, double4* packed, uint32_t* orig, bool rec_idx,
+                                uint32_t* perm, cudaStream_t s, double4* rec_sorted) {
+  if (n <= 0) return packed;
   static std::once_flag attr_once;
   std::call_once(attr_once, [&] {
     FMI_CK(cudaFuncSetAttribute(k_rs_scatter<uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -746,24 +753,27 @@ void bucket_sort_keys(const double* pts, const double* f, int64_t n, const doubl
   // the remaining digits inside each bucket: segmented LSD passes over bits [0, nb - 8), the last one
   // writing the dense permutation (bucket positions in Morton order)
   const int npass = nb > 8 ? (nb - 8 + 7) / 8 : 0;
-  if (npass == 0) {
-    FMI_LAUNCH(KID_MISC, s, k_iota32, (unsigned)((n + 255) / 256), 256, 0, perm, n);
-    return;
+  if (npass == 0) {  // the bucket order is the sorted order
+    if (!rec_sorted) FMI_LAUNCH(KID_MISC, s, k_iota32, (unsigned)((n + 255) / 256), 256, 0, perm, n);
+    return packed;
   }
   uint32_t *k0 = ka.p, *v0 = va.p, *k1 = kb.p, *v1 = vb.p;
   for (int pass = 0; pass < npass; ++pass) {
     const int shift = 8 * pass;
     const bool last = pass + 1 == npass;
-    // key read (histogram) + key and value read, key and value written (the last pass: value only)
-    prof_units(KID_SORT, n * (int64_t)(last ? 16 : 20));
+    // key read (histogram) + key and value read, key and value written (the last pass: value only, or
+    // with rec_sorted the 32-byte record read and written instead)
+    prof_units(KID_SORT, n * (int64_t)(last ? (rec_sorted ? 76 : 16) : 20));
     FMI_LAUNCH(KID_SORT, s, k_rs_hist<uint32_t>, (unsigned)nblk2, RS_THREADS, 0, k0, n2, shift, nblk2, counts.p,
                (const SegTile*)seg.p);
     exclusive_scan_i64(counts.p, counts.p, nblk2 * 256, nullptr, s);
     FMI_LAUNCH(KID_SORT, s, k_rs_scatter<uint32_t>, (unsigned)nblk2, RS_THREADS, scatter_smem<uint32_t>(), k0, v0, n2,
-               shift, nblk2, counts.p, last ? nullptr : k1, last ? perm : v1, (const SegTile*)seg.p, last ? 1 : 0);
+               shift, nblk2, counts.p, last ? nullptr : k1, last ? perm : v1, (const SegTile*)seg.p, last ? 1 : 0,
+               (const double4*)packed, last ? rec_sorted : nullptr);
     std::swap(k0, k1);
     std::swap(v0, v1);
   }
+  return rec_sorted ? rec_sorted : packed;
 }
 
 void gather_points(const double4* packed, uint32_t* perm, int64_t n, double* ux, double* uy, double* uz, double* r,
