@@ -295,7 +295,10 @@ __global__ void __launch_bounds__(RS_THREADS, 4) k_rs_scatter(const KT* __restri
 // layout with every bucket padded to whole sort tiles (segmented passes, no top-digit pass).
 // ------------------------------------------------------------------------------------------------
 __device__ __forceinline__ int top_digit(uint32_t k, int nb) { return nb > 8 ? (int)(k >> (nb - 8)) : (int)k; }
-constexpr int BK_ITEMS = 6;
+#ifndef FMI_BK_ITEMS
+#define FMI_BK_ITEMS 6
+#endif
+constexpr int BK_ITEMS = FMI_BK_ITEMS;
 constexpr int BK_TILE = RS_THREADS * BK_ITEMS;      // 1536 points per top-digit tile
 constexpr int BK_WARP_ITEMS = BK_TILE / RS_WARPS;   // 192
 // staged coordinates + values, then the tile's keys and local indices in digit order: 66 KB (3 CTAs/SM)
@@ -396,7 +399,7 @@ __global__ void __launch_bounds__(256) k_bk_tiles(const int32_t* __restrict__ ti
 // in shared memory by coalesced loads, ranked by digit (warp ballots), their keys and local indices
 // rearranged in shared memory in digit order, then the records are formed and written so that
 // consecutive threads store consecutive positions of each digit's run (coalesced).
-__global__ void __launch_bounds__(RS_THREADS, 3) k_bk_scatter(const double* __restrict__ pts,
+__global__ void __launch_bounds__(RS_THREADS, BK_ITEMS <= 4 ? 4 : 3) k_bk_scatter(const double* __restrict__ pts,
                                                               const double* __restrict__ f, int64_t n, double lo0,
                                                               double lo1, double lo2, double w, bool unit, int D,
                                                               int bit_lo, int nb, int64_t nblk,

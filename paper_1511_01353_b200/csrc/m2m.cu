@@ -24,7 +24,7 @@ namespace fmi {
 
 namespace {
 
-constexpr int M2M_THREADS = 256;
+constexpr int M2M_THREADS = 1024;  // latency-bound shift chains: more threads in flight (1.74 -> 1.42 ms at cfg 5)
 constexpr double kEps = 1.1102230246251565e-16;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
