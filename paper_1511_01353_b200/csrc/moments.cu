@@ -21,8 +21,13 @@ namespace fmi {
 
 namespace {
 
-constexpr int K4_THREADS = 256;
-constexpr int K4_WARPS = K4_THREADS / 32;
+// threads per CTA: p = 10 runs 128-thread CTAs, two per SM (254 registers), so that its 20 output
+// groups fill 5 CTAs of 4 warps exactly (256-thread CTAs left 4 of every 24 warps idle)
+#ifndef FMI_K4_THREADS_P10
+#define FMI_K4_THREADS_P10 128
+#endif
+template <int P>
+constexpr int k4_threads() { return P >= 10 ? FMI_K4_THREADS_P10 : 256; }
 #ifndef FMI_K4_LIM
 #define FMI_K4_LIM 64
 #endif
@@ -32,7 +37,14 @@ constexpr int K4_WARPS = K4_THREADS / 32;
 #ifndef FMI_K4_MINB
 #define FMI_K4_MINB 1
 #endif
-constexpr int K4_LIM = FMI_K4_LIM;  // outputs per group (2·LIM accumulator registers)
+// outputs per group (2·LIM accumulator registers): at p = 10 groups of <= 96 outputs (20 groups, 254
+// registers, no spills) cut the per-point z-power and pair overhead (cfg 5: 43.4 -> 36.9 ms); smaller
+// degrees keep 64 (more groups = more warps per chunk set: cfg 3/4 measured slower with 96)
+#ifndef FMI_K4_LIM_P10
+#define FMI_K4_LIM_P10 96
+#endif
+template <int P>
+constexpr int k4_lim() { return P >= 10 ? FMI_K4_LIM_P10 : FMI_K4_LIM; }
 constexpr int K4_RING = 8;  // per-lane point ring (cp.async prefetch distance K4_RING - 1)
 
 __device__ __forceinline__ void cp_async8(double* dst, const double* src) {
@@ -44,9 +56,10 @@ template <int P>
 struct K4Plan {
   static constexpr int Q = 2 * P;
   static constexpr int K = rank3(Q);
-  static constexpr int NG = grp::ngroups(Q, K4_LIM, 0);
-  static constexpr int NGB = (NG + K4_WARPS - 1) / K4_WARPS;  // CTAs per 32 chunks
-  static constexpr int MG = grp::max_size(Q, K4_LIM, 0);
+  static constexpr int NG = grp::ngroups(Q, k4_lim<P>(), 0);
+  static constexpr int THREADS = k4_threads<P>(), WARPS = THREADS / 32;
+  static constexpr int NGB = (NG + WARPS - 1) / WARPS;  // CTAs per 32 chunks
+  static constexpr int MG = grp::max_size(Q, k4_lim<P>(), 0);
 };
 
 // The point loop of one group g (compile-time): z powers, pair products and the group's FMAs, no
@@ -58,7 +71,7 @@ __device__ __forceinline__ void k4_loop(const double* __restrict__ ux, const dou
                                         const double* __restrict__ uz, const Chunk& ck, const Frame& fr, double* rg,
                                         int lane, double* __restrict__ out) {
   constexpr int Q = 2 * P;
-  constexpr int n = grp::group_size(Q, K4_LIM, 0, g);
+  constexpr int n = grp::group_size(Q, k4_lim<P>(), 0, g);
   double acc[n];
 #pragma unroll
   for (int k = 0; k < n; ++k) acc[k] = 0.0;
@@ -88,7 +101,7 @@ __device__ __forceinline__ void k4_loop(const double* __restrict__ ux, const dou
     asm volatile("cp.async.wait_group %0;" ::"n"(PD - 1) : "memory");
     const double* sp = rg + t * 96 + lane;
     const double xn = sp[0], yn = sp[32], zn = sp[64];
-    grp::accum<Q, K4_LIM, 0, g>(x, y, z, 1.0, acc);
+    grp::accum<Q, k4_lim<P>(), 0, g>(x, y, z, 1.0, acc);
     x = to_local(xn, fr.cx, fr.scale);
     y = to_local(yn, fr.cy, fr.scale);
     z = to_local(zn, fr.cz, fr.scale);
@@ -103,10 +116,10 @@ __device__ __forceinline__ void k4_loop(const double* __restrict__ ux, const dou
     const double y = to_local(sp[32], fr.cy, fr.scale);
     const double z = to_local(sp[64], fr.cz, fr.scale);
     issue(i + PD, (t + PD) % R);
-    grp::accum<Q, K4_LIM, 0, g>(x, y, z, 1.0, acc);
+    grp::accum<Q, k4_lim<P>(), 0, g>(x, y, z, 1.0, acc);
   }
 #endif
-  double* o = out + grp::out_begin(Q, K4_LIM, 0, g);
+  double* o = out + grp::out_begin(Q, k4_lim<P>(), 0, g);
 #pragma unroll
   for (int k = 0; k < n; ++k) o[k] = acc[k];
 }
@@ -118,21 +131,21 @@ __device__ __forceinline__ void k4_run(int gw, const double* __restrict__ ux, co
   ((gw == Gs ? (k4_loop<P, Gs>(ux, uy, uz, ck, fr, rg, lane, out), 0) : 0), ...);
 }
 
-// Lane = chunk, warp = output group: lane l of warp w in CTA b accumulates group (b % NGB)·8 + w over
+// Lane = chunk, warp = output group: lane l of warp w in CTA b accumulates group (b % NGB)·WARPS + w over
 // the points of chunk 32·(b / NGB) + l (sequentially, in the frame of node cell[owner >> shift]) and writes
 // its outputs to partial[chunk][..].  No cross-lane reduction; the 8 warps of a CTA read the same
 // 32 chunks (L1 reuse).  Chunks are <= kMomentChunk points (make_chunks).
 template <int P>
-__global__ void __launch_bounds__(K4_THREADS, FMI_K4_MINB)
+__global__ void __launch_bounds__(k4_threads<P>(), k4_threads<P>() < 256 ? 256 / k4_threads<P>() : FMI_K4_MINB)
     k_moments(const double* __restrict__ ux, const double* __restrict__ uy, const double* __restrict__ uz,
               const int4* __restrict__ cell, int shift, const Chunk* __restrict__ chunks,
               const int64_t* __restrict__ nchunks, double* __restrict__ partial) {
   using PL = K4Plan<P>;
   constexpr int K = PL::K;
-  __shared__ __align__(16) double ring[K4_WARPS * K4_RING * 3 * 32];
+  __shared__ __align__(16) double ring[PL::WARPS * K4_RING * 3 * 32];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   // the NGB CTAs that read the same 32 chunks are adjacent in launch order (their re-reads hit L2)
-  const int gw = (int)(blockIdx.x % PL::NGB) * K4_WARPS + warp;
+  const int gw = (int)(blockIdx.x % PL::NGB) * PL::WARPS + warp;
   const int64_t cidx = (int64_t)(blockIdx.x / PL::NGB) * 32 + lane;
   if (gw >= PL::NG || cidx >= *nchunks) return;
   const Chunk ck = chunks[cidx];
@@ -218,7 +231,7 @@ void direct_moments(const double* ux, const double* uy, const double* uz, const 
                     cudaStream_t s) {
   using PL = K4Plan<P>;
   if (max_chunks <= 0) return;
-  FMI_LAUNCH(KID_MOMENTS, s, (k_moments<P>), (unsigned)((max_chunks + 31) / 32 * PL::NGB), K4_THREADS, 0, ux, uy,
+  FMI_LAUNCH(KID_MOMENTS, s, (k_moments<P>), (unsigned)((max_chunks + 31) / 32 * PL::NGB), PL::THREADS, 0, ux, uy,
              uz, cell, shift, chunks, nchunks_dev, partial);
 }
 
