@@ -34,6 +34,9 @@ namespace {
 template <int P>
 constexpr int k5_threads() { return rank3(P) >= 220 ? 256 : (rank3(P) >= 100 ? 128 : 64); }
 constexpr int KB = 32;
+#ifndef FMI_K5_PANEL_RB
+#define FMI_K5_PANEL_RB 18
+#endif
 
 struct BasisTab {
   uint8_t l[286], m[286], n[286];
@@ -316,12 +319,14 @@ __global__ void __launch_bounds__(NT, NT == 512 ? 1 : (NT == 256 ? 2 : (NT == 12
       bool dg_ready = false;  // Dg holds the factored diagonal block of the current panel
       for (int j0 = 0; j0 < L; j0 += KB) {
         const int bw = min(KB, L - j0), R = L - j0 + 1;  // panel rows j0..L (row L = RHS)
-        // panel load: warp per row, lane = column (one coalesced 256-byte row segment per load), 4 rows
-        // per warp in flight; rows of the lookahead's diagonal block come from Dg
-        for (int r0 = warp * 4; r0 < R; r0 += K5_WARPS * 4) {
-          double v[4];
+        // panel load: warp per row, lane = column (one coalesced 256-byte row segment per load), RB rows
+        // per warp in flight (the rows were just written by the trailing update: L2 latency per round);
+        // rows of the lookahead's diagonal block come from Dg
+        constexpr int RB = K5_WARPS >= 16 ? 4 : FMI_K5_PANEL_RB;
+        for (int r0 = warp * RB; r0 < R; r0 += K5_WARPS * RB) {
+          double v[RB];
 #pragma unroll
-          for (int k = 0; k < 4; ++k) {
+          for (int k = 0; k < RB; ++k) {
             const int r = r0 + k, i = j0 + r, c = lane;
             v[k] = 0.0;
             if (r < R && c < bw) {
@@ -333,7 +338,7 @@ __global__ void __launch_bounds__(NT, NT == 512 ? 1 : (NT == 256 ? 2 : (NT == 12
             }
           }
 #pragma unroll
-          for (int k = 0; k < 4; ++k)
+          for (int k = 0; k < RB; ++k)
             if (r0 + k < R && lane < bw) Pn[lane * LDP + r0 + k] = v[k];
         }
         __syncthreads();
