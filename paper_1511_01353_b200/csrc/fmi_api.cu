@@ -418,9 +418,15 @@ bool is_pinned_host(const void* p) {
   return a.type == cudaMemoryTypeHost;
 }
 
-int64_t choose_chunk(int64_t points, int64_t min_ch, int64_t per_sm_chunks) {
-  int64_t target = (points + 148 * per_sm_chunks - 1) / (148 * per_sm_chunks);
-  return std::max(min_ch, target);
+// chunk size for a pass over `points` points in `nseg` contiguous segments, aiming at per_sm_chunks
+// chunks per SM (whole waves of the 2-CTA/SM K6 kernels): every segment adds at most one partial chunk,
+// so the size is taken for per_sm_chunks·148 − nseg full chunks — the total then stays within the whole
+// waves instead of spilling a few CTAs into an extra, nearly empty wave (segments >= half the target:
+// many waves anyway, the plain size)
+int64_t choose_chunk(int64_t points, int64_t min_ch, int64_t per_sm_chunks, int64_t nseg) {
+  const int64_t tgt = 148 * per_sm_chunks;
+  const int64_t avail = 2 * nseg < tgt ? tgt - nseg : tgt;
+  return std::max(min_ch, (points + avail - 1) / avail);
 }
 
 // thrown by run_levels when the moment tree needs key digits below the sorted depth
@@ -599,7 +605,7 @@ void run_levels(fmi_tree* T, const uint64_t* keys, double* ux, double* uy, doubl
       gather_level(mtmom.p, mtbnd.p, T->nt.mtid, segsum.p, nullptr, 0, 1, K, KS, L, lvlmom.p, s);
     } else {  // root projection b = Λᵀf in the root frame
       LevelCtx c{keys, ux, uy, uz, r, T->nt, 0, 1, 0, T->D, T->Dk, P, L, K, T->tau};
-      const int64_t ch = choose_chunk(T->N, 1024, 32);
+      const int64_t ch = choose_chunk(T->N, 1024, 32, 1);
       const int64_t maxc = T->N / ch + 2;
       counts.ensure(8, s);
       begin.ensure(8, s);
@@ -693,7 +699,7 @@ void run_levels(fmi_tree* T, const uint64_t* keys, double* ux, double* uy, doubl
       }
       if (!global) level_solve_qr<P>(c, lvlmom.p, qr_scratch.p, qr_slots, s);
       // fused K6 over the level's octant segments
-      const int64_t ch6 = choose_chunk(points, 1024, 32);
+      const int64_t ch6 = choose_chunk(points, 1024, 32, count * 8);
       const int64_t max6 = points / ch6 + 8 * count + 1;
       counts.ensure(count * 8, s);
       begin.ensure(count * 8, s);
@@ -798,7 +804,7 @@ void fused_gather_root(const double4* packed, uint32_t* perm, const uint32_t* or
   }
   DBuf<int64_t> se(2, s), counts(1, s), begin(1, s), nch(1, s);
   FMI_LAUNCH(KID_MISC, s, k_fill_range, 1, 1, 0, se.p, N);
-  const int64_t ch = choose_chunk(N, 1024, 32);
+  const int64_t ch = choose_chunk(N, 1024, 32, 1);
   const int64_t maxc = N / ch + 2;
   DBuf<Chunk> chunks(maxc, s);
   DBuf<double> partial((size_t)maxc * (L + 1), s);
