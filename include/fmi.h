@@ -253,6 +253,12 @@ int fmi_profile_get(const char* kernel, double* total_ms, int64_t* launches);
  * "solve" nodes factored by the Gram solve (K5), "refine_solve" node substitutions (K5r).
  * bench.py multiplies them by the per-unit bytes / flops of DESIGN.md §5.  0 / FMI_EINPUT. */
 int fmi_profile_units(const char* kernel, int64_t* units);
+/* Restrict the event timing to the named kernels (comma-separated names from the list above, no spaces;
+ * NULL or "" = every kernel, the default).  bench.py times only the kernels it reports rooflines for
+ * inside its timed region: bracketing every one of the ~200 small launches of a step with events costs
+ * ~1.9 ms per cfg-5 step on the host launch path.  Launch and unit counters are not
+ * affected.  0 / FMI_EINPUT (unknown name; the selection is left unchanged). */
+int fmi_profile_select(const char* kernels);
 /* Total kernel launches issued by the library since load (or since fmi_profile_reset). */
 int64_t fmi_launch_count(void);
 /* Diagnostics (a stand-in for compute-sanitizer memcheck, which is closed on the GPU pool): with the

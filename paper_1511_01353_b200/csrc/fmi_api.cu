@@ -195,6 +195,8 @@ void dfree(void* p, cudaStream_t s) {
 namespace {
 std::atomic<int64_t> g_launches{0};
 std::atomic<bool> g_prof{false};
+std::atomic<uint32_t> g_prof_mask{~0u};  // kernel ids whose launches are timed (fmi_profile_select)
+static_assert(KID_COUNT <= 32, "g_prof_mask holds one bit per kernel id");
 std::mutex g_prof_mu;
 struct Pending {
   int kid;
@@ -230,9 +232,9 @@ const char* kNames[KID_COUNT] = {"keys",     "sort",     "gather", "moments", "m
 const char* kernel_name(int kid) { return (kid >= 0 && kid < KID_COUNT) ? kNames[kid] : "?"; }
 
 void prof_begin(int kid, cudaStream_t s) {
-  (void)kid;
   g_launches.fetch_add(1, std::memory_order_relaxed);
   if (!g_prof.load(std::memory_order_relaxed)) return;
+  if (!((g_prof_mask.load(std::memory_order_relaxed) >> kid) & 1u)) return;
   std::lock_guard<std::mutex> lk(g_prof_mu);
   tl_open = get_event();
   FMI_CK(cudaEventRecord(tl_open, s));
@@ -329,7 +331,18 @@ struct Trace {
   void flush(const char* tag) {
     if (!level) return;
     const double tot = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
-    fprintf(stderr, "[fmi trace] %s total=%.2f ms:%s\n", tag, tot, out.c_str());
+    // the stream-ordered pool's reserved bytes: growth between two identical builds = fresh physical memory
+    // mapped inside the build (a host-side stall of tens of ms)
+    int dev = 0;
+    cudaMemPool_t pool;
+    uint64_t reserved = 0, used = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &reserved);
+      cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemHigh, &used);
+    }
+    cudaGetLastError();
+    fprintf(stderr, "[fmi trace] %s total=%.2f ms pool_reserved=%.1f MB pool_used_high=%.1f MB:%s\n", tag, tot,
+            reserved / 1048576.0, used / 1048576.0, out.c_str());
   }
 };
 
@@ -633,12 +646,15 @@ void run_levels(fmi_tree* T, const uint64_t* keys, double* ux, double* uy, doubl
       T->lvl_points.push_back(points);
       T->depth_max = depth;
       ensure_table(T->nt, T->cap, first + count + 8 * count, L, true, s);
+      tmark("table", s);
       LevelCtx c{keys, ux, uy, uz, r, T->nt, first, count, depth, T->D, T->Dk, P, L, K, T->tau};
       level_children(c, s);
+      tmark("children", s);
       const bool global = T->dist && depth < T->shard_depth;  // nodes summed over the shards
       // K5: solve; nodes whose translated moments fail the rounding check are re-accumulated directly
       FMI_CK(cudaMemsetAsync(nflag.p, 0, 3 * sizeof(int64_t), s));
       scratch.ensure((size_t)count * fac_per_node, s);
+      tmark("scratch", s);
       // deferral: single shard only; split mode defers every node (Horner-only K6 + K6_PROJ)
       // split-K6 threshold on the whole-job level size (a shard holds ~1/world of it)
       const bool big_level = points * (T->dist ? T->dist->world : 1) >= T->split_min;
@@ -646,8 +662,10 @@ void run_levels(fmi_tree* T, const uint64_t* keys, double* ux, double* uy, doubl
           global ? 0.0 : ((T->k6_split && big_level) ? INFINITY : T->defer_theta * T->tau);
       level_solve<P>(c, lvlmom.p, 0, nullptr, nullptr, T->refine2, T->refine_fill, T->Ntot, nflag.p, scratch.p, s,
                      defer_tau);
+      tmark("k5", s);
       FMI_CK(cudaMemcpyAsync(&host_small[2], nflag.p, 3 * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
       FMI_CK(cudaStreamSynchronize(s));
+      tmark("k5sync", s);
       if (host_small[3] > 0) {
         // few flagged nodes, possibly huge (a root): longer chunks keep the chunk count (and the
         // per-node partial sums) bounded
@@ -1852,6 +1870,30 @@ int fmi_build_stats(const fmi_tree* T, int64_t* out, int cap) {
 
 int fmi_profile_enable(int on) {
   g_prof.store(on != 0);
+  return 0;
+}
+
+int fmi_profile_select(const char* kernels) {
+  if (!kernels || !*kernels) {
+    g_prof_mask.store(~0u);
+    return 0;
+  }
+  uint32_t mask = 0;
+  const char* b = kernels;
+  while (*b) {
+    const char* e = b;
+    while (*e && *e != ',') ++e;
+    int hit = -1;
+    for (int k = 0; k < KID_COUNT; ++k)
+      if (std::strlen(kNames[k]) == (size_t)(e - b) && std::strncmp(kNames[k], b, (size_t)(e - b)) == 0) hit = k;
+    if (hit < 0) {
+      set_error(FMI_EINPUT, "fmi_profile_select: unknown kernel name in '" + std::string(kernels) + "'");
+      return FMI_EINPUT;
+    }
+    mask |= 1u << hit;
+    b = *e ? e + 1 : e;
+  }
+  g_prof_mask.store(mask);
   return 0;
 }
 

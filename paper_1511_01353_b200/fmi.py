@@ -33,7 +33,7 @@ EXPORTED = (
     "fmi_export_nodes", "fmi_root_cube", "fmi_residual", "fmi_level_stats", "fmi_profile_enable",
     "fmi_profile_reset", "fmi_profile_get", "fmi_launch_count", "fmi_guard_violations", "fmi_build_stats", "fmi_build_dist",
     "fmi_dist_xbuf_bytes", "fmi_bbox", "fmi_cell_counts", "fmi_partition", "fmi_scatter", "fmi_transfer",
-    "fmi_save", "fmi_load", "fmi_profile_units",
+    "fmi_save", "fmi_load", "fmi_profile_units", "fmi_profile_select",
     "fmi_get_unique_id", "fmi_dist_init", "fmi_dist_finalize", "fmi_dist_allreduce",
 )
 
@@ -110,6 +110,8 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.fmi_profile_enable.argtypes = [I32]
     lib.fmi_profile_reset.restype = I32
     lib.fmi_profile_reset.argtypes = []
+    lib.fmi_profile_select.restype = I32
+    lib.fmi_profile_select.argtypes = [ctypes.c_char_p]
     lib.fmi_profile_get.restype = I32
     lib.fmi_profile_get.argtypes = [ctypes.c_char_p, P(D), P(I64)]
     lib.fmi_get_unique_id.restype = I32
@@ -447,6 +449,13 @@ def _data_ptr(a) -> int:
 
 def profile_enable(on: bool = True) -> None:
     load_library().fmi_profile_enable(1 if on else 0)
+
+
+def profile_select(kernels=None) -> None:
+    """Time only the named kernels (an iterable of names from KERNELS); None = every kernel."""
+    arg = ",".join(kernels).encode() if kernels else None
+    if load_library().fmi_profile_select(arg) != 0:
+        _raise_last(FMI_EINPUT)
 
 
 def profile_reset() -> None:

@@ -69,6 +69,22 @@ def test_argument_errors_without_gpu(lib):
     lib.fmi_free(None)  # NULL-safe
 
 
+def test_profile_select_names(lib):
+    """fmi_profile_select: every documented kernel name (and NULL / "" = all) is accepted; an unknown name is
+    FMI_EINPUT and leaves the selection alone (include/fmi.h)."""
+    import paper_1511_01353_b200 as fmi
+    assert lib.fmi_profile_select(None) == 0
+    assert lib.fmi_profile_select(b"") == 0
+    assert lib.fmi_profile_select(",".join(fmi.fmi.KERNELS).encode()) == 0
+    assert lib.fmi_profile_select(b"residual,moments") == 0
+    assert lib.fmi_profile_select(b"residual,nope") == fmi.fmi.FMI_EINPUT
+    assert "unknown kernel name" in fmi.last_error()[1]
+    assert lib.fmi_profile_select(b"resid") == fmi.fmi.FMI_EINPUT  # prefixes are not names
+    with pytest.raises(fmi.FmiError):
+        fmi.profile_select(["keys", "bogus"])
+    fmi.profile_select(None)
+
+
 def test_no_cpu_fallback_without_device(lib):
     """Valid arguments on a host without a GPU must fail loudly with FMI_ECUDA."""
     import paper_1511_01353_b200 as fmi

@@ -131,3 +131,32 @@ def test_load_rejects_corrupt_node_records(tmp_path, what):
     assert ("node" in str(ei.value)) or what == "header_D"
     # the untouched file still loads
     fmi.load(str(path)).free()
+
+
+def test_profile_select_times_only_the_named_kernels():
+    """fmi_profile_select (include/fmi.h): events only around the named kernels; launch and unit counters and
+    the results are unaffected (bench.py times its rooflined kernels this way inside the timed region)."""
+    import paper_1511_01353_b200 as fmi
+    cfg = workloads.CONFIGS[1]
+    pts, f, q = workloads.make_inputs(cfg)
+
+    def run(select):
+        fmi.profile_reset()
+        fmi.profile_select(select)
+        fmi.profile_enable(True)
+        n0 = fmi.launch_count()
+        with fmi.build(pts, f, cfg.degree, cfg.tol, cfg.max_depth) as t:
+            v = t.eval(q)
+        fmi.profile_enable(False)
+        timed = {k for k, (ms, n) in fmi.profile_get().items() if n}
+        return v, timed, fmi.launch_count() - n0, fmi.profile_units()
+
+    try:
+        v_all, timed_all, n_all, u_all = run(None)
+        v_sel, timed_sel, n_sel, u_sel = run(["residual", "solve"])
+    finally:
+        fmi.profile_select(None)
+    assert {"residual", "solve", "keys", "eval"} <= timed_all
+    assert timed_sel == {"residual", "solve"}
+    assert n_sel == n_all and u_sel == u_all
+    assert np.array_equal(v_all, v_sel)
